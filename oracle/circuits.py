@@ -1,0 +1,196 @@
+"""Oracle circuits: vec_mat (diagonal method), im2col conv, the paper's CNN.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+* vec_mat — PAPER.md:58-61 ("a variant of the encrypted vector-plain matrix
+  multiplication proposed by halevi", "replicating the input vector as many
+  times as possible into ciphertext slots and only left ciphertext
+  rotations"); layout = SURVEY C17.
+* im2col conv — PAPER.md:57, 64, 189-213 ("convolution windows as rows ...
+  flatten it as a vector via a vertical scan", "one multiplication operation
+  and log2(N) rotations and additions"); layout = SURVEY C18/C19.
+* CNN — PAPER.md:98: conv 7x7 stride 3, 4 kernels -> x^2 -> FC 256->64 -> x^2
+  -> FC 64->10; 6 multiplicative levels.
+
+Every slot-layout helper here is plain numpy indexing written from C17-C19;
+``tests/test_layouts.py`` pins them with a float slot simulator against numpy
+matmul and torch conv2d.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .oracle import OCt, OracleContext
+
+
+class ReplicationExhausted(ValueError):
+    pass
+
+
+# ------------------------------------------------------------ layouts ---
+def vecmat_diagonals(W: np.ndarray, ns: int, replicate_out: bool) -> np.ndarray:
+    """C17: D_k[j] = W[(j+k) mod n][j'] (W is in x out), j' = j mod m when the
+    output is replicated, else j' = j for j < m and 0 beyond."""
+    n, m = W.shape
+    if replicate_out and (ns % n or ns % m):
+        raise ValueError("replicated output needs n | slots and m | slots")
+    j = np.arange(ns)
+    span = (ns // n) * n
+    D = np.zeros((n, ns))
+    for k in range(n):
+        live = np.ones(ns, bool) if replicate_out else (j < m)
+        if ns % n and np.any(live & (j + k >= span)):
+            raise ReplicationExhausted(f"diagonal {k} reads past the replicated span")
+        jp = (j % m) if replicate_out else np.minimum(j, m - 1)
+        D[k] = np.where(live, W[(j + k) % n, jp], 0.0)
+    return D
+
+
+def vecmat_bias_slots(bias: np.ndarray, ns: int, replicate_out: bool) -> np.ndarray:
+    m = bias.shape[0]
+    j = np.arange(ns)
+    if replicate_out:
+        return bias[j % m].astype(np.float64)
+    out = np.zeros(ns)
+    out[:m] = bias
+    return out
+
+
+def replicate(x: np.ndarray, ns: int) -> np.ndarray:
+    """Client-side replication of an n-vector as many times as fits."""
+    n = x.shape[0]
+    out = np.zeros(ns)
+    r = ns // n
+    out[: r * n] = np.tile(x, r)
+    return out
+
+
+def conv_geometry(H: int, W: int, kh: int, kw: int, stride: int):
+    oh, ow = (H - kh) // stride + 1, (W - kw) // stride + 1
+    windows = oh * ow
+    chunk = 1 << (windows - 1).bit_length()
+    return oh, ow, windows, chunk
+
+
+def im2col_slots(img: np.ndarray, kh: int, kw: int, stride: int, ns: int) -> np.ndarray:
+    """C18: windows in row-major order of output positions, taps row-major;
+    slot = tap * chunk + window (vertical scan of the windows x taps matrix)."""
+    H, W = img.shape
+    oh, ow, windows, chunk = conv_geometry(H, W, kh, kw, stride)
+    if kh * kw * chunk > ns:
+        raise ValueError("im2col matrix does not fit the slots")
+    out = np.zeros(ns)
+    for r in range(oh):
+        for c in range(ow):
+            w = r * ow + c
+            patch = img[r * stride: r * stride + kh, c * stride: c * stride + kw].reshape(-1)
+            out[np.arange(kh * kw) * chunk + w] = patch
+    return out
+
+
+def conv_kernel_slots(kernel: np.ndarray, chunk: int, ns: int) -> np.ndarray:
+    """C18: K[tap * chunk + w] = kernel[tap] (kernel value replicated along its chunk)."""
+    taps = kernel.reshape(-1)
+    out = np.zeros(ns)
+    for t, v in enumerate(taps):
+        out[t * chunk:(t + 1) * chunk] = v
+    return out
+
+
+def conv_mask_slots(c: int, n_ch: int, chunk: int, ns: int) -> np.ndarray:
+    """C19: Mask_c = 1 on slots whose chunk index q satisfies q mod C_out = c."""
+    q = np.arange(ns) // chunk
+    return (q % n_ch == c).astype(np.float64)
+
+
+def conv_bias_slots(bias: np.ndarray, chunk: int, ns: int) -> np.ndarray:
+    q = np.arange(ns) // chunk
+    return bias[q % bias.shape[0]].astype(np.float64)
+
+
+def conv_fold_steps(chunk: int, ns: int) -> list:
+    """C19: fold by chunk * 2^r, r = 0 .. log2(ns/chunk) - 1."""
+    n_chunks = ns // chunk
+    return [chunk << r for r in range(n_chunks.bit_length() - 1)]
+
+
+# ------------------------------------------------------------ circuits ---
+def _shifted(q: int, shift: int) -> float:
+    """Plaintext scale q * 2^shift (exact in double for |shift| < 1000)."""
+    return float(q) * 2.0 ** shift
+
+
+def vec_mat(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | None,
+            replicate_out: bool, pt_scale_shift: int = 0) -> OCt:
+    """Step 11: acc = sum_k mul_plain(rot(x, k), D_k); rescale once; + bias.
+    D_k is encoded at scale q_l / 2^shift (l = ct level) so that the rescale by
+    q_l returns the ciphertext to its input scale / 2^shift (C14)."""
+    ns = ctx.slots
+    D = vecmat_diagonals(W, ns, replicate_out)
+    lvl = ct.level
+    pscale = _shifted(ctx.q[lvl], -pt_scale_shift)
+    acc = None
+    for k in range(W.shape[0]):
+        r = ct if k == 0 else ctx.rotate(ct, k)
+        t = ctx.mul_plain(r, ctx.encode(D[k], pscale, lvl))
+        acc = t if acc is None else ctx.add(acc, t)
+    acc = ctx.rescale(acc)
+    if bias is not None:
+        acc = ctx.add_plain(acc, ctx.encode(vecmat_bias_slots(bias, ns, replicate_out),
+                                            acc.scale, acc.level))
+    return acc
+
+
+def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarray | None,
+                chunk: int, kernel_shift: int = 0, mask_shift: int = 0) -> OCt:
+    """Steps 12 (C18/C19): per channel t_c = rescale(ct * K_c), log2(#chunks)
+    rounds t_c += rot(t_c, chunk 2^r); sum_c t_c * Mask_c; rescale; + bias."""
+    ns = ctx.slots
+    n_ch = kernels.shape[0]
+    lvl = ct.level
+    ts = []
+    for c in range(n_ch):
+        K = conv_kernel_slots(kernels[c], chunk, ns)
+        t = ctx.rescale(ctx.mul_plain(ct, ctx.encode(K, _shifted(ctx.q[lvl], kernel_shift), lvl)))
+        for step in conv_fold_steps(chunk, ns):
+            t = ctx.add(t, ctx.rotate(t, step))
+        ts.append(t)
+    lvl2 = ts[0].level
+    acc = None
+    for c in range(n_ch):
+        M = conv_mask_slots(c, n_ch, chunk, ns)
+        p = ctx.mul_plain(ts[c], ctx.encode(M, _shifted(ctx.q[lvl2], mask_shift), lvl2))
+        acc = p if acc is None else ctx.add(acc, p)
+    acc = ctx.rescale(acc)
+    if bias is not None:
+        acc = ctx.add_plain(acc, ctx.encode(conv_bias_slots(bias, chunk, ns), acc.scale,
+                                            acc.level))
+    return acc
+
+
+
+# Scale schedule of the CNN (R1/R2): log2 of the input scale and
+# the plaintext-scale shifts relative to the prime each following rescale drops.
+CNN_PLAN = dict(in_log2=30, conv_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=-4)
+
+
+def cnn_rotation_steps(ns: int = 4096, chunk: int = 64) -> list:
+    """A-rot: exactly the circuit's steps: FC1 1..255, FC2 1..63 and the conv fold."""
+    return sorted(set(range(1, 256)) | set(conv_fold_steps(chunk, ns)))
+
+
+def cnn_encrypt_input(ctx: OracleContext, img: np.ndarray, stream_id: int, plan=None) -> OCt:
+    plan = plan or CNN_PLAN
+    slots = im2col_slots(img, 7, 7, 3, ctx.slots)
+    return ctx.encrypt(ctx.encode(slots, 2.0 ** plan["in_log2"], ctx.L - 1), stream_id)
+
+
+def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None) -> OCt:
+    plan = plan or CNN_PLAN
+    x = im2col_conv(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64,
+                    plan["conv_shift"], plan["mask_shift"])
+    x = ctx.square(x)
+    x = vec_mat(ctx, x, w.fc1_w.T, w.fc1_b, replicate_out=True, pt_scale_shift=-plan["fc1_shift"])
+    x = ctx.square(x)
+    x = vec_mat(ctx, x, w.fc2_w.T, w.fc2_b, replicate_out=False, pt_scale_shift=-plan["fc2_shift"])
+    return x

@@ -1,0 +1,239 @@
+"""Pins of the oracle's scheme layer against exact algebraic identities
+(schoolbook products and big-int CRT on tiny N), a library Vandermonde solve, and
+homomorphism / rotation-group laws at realistic N.
+"""
+import numpy as np
+import pytest
+
+from conftest import negacyclic_mul
+from oracle.oracle import (OCt, OPt, OracleContext, sid, P_ENC_E0, P_ENC_E1, P_ENC_V, P_PK_A,
+                           P_PK_E)
+
+
+def crt(residues, qs):
+    Q = 1
+    for q in qs:
+        Q *= q
+    x = 0
+    for r, q in zip(residues, qs):
+        Qi = Q // q
+        x += int(r) * Qi * pow(Qi, -1, q)
+    return x % Q, Q
+
+
+def centered(x, Q):
+    return x - Q if 2 * x > Q else x
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    """N=32, 3 data primes + 2 special primes of 30 bits."""
+    c = OracleContext(5, (30, 30, 30, 30, 30), 2, 9)
+    c.keygen([1, 3, -1])
+    return c
+
+
+@pytest.fixture(scope="module")
+def mid():
+    c = OracleContext(12, (60, 40, 40, 60), 1, 0)
+    c.keygen([1, 2, 3, 5, -1, 2048])
+    return c
+
+
+# -------------------------------------------------------------- P6 encode ---
+@pytest.mark.parametrize("logN", [4, 5])
+def test_encode_matches_vandermonde_solve(logN):
+    """m is the unique real polynomial with m(zeta^{5^j}) = D z_j and m(zeta^{-5^j}) = D z_j
+    (C6); solve that linear system with numpy.linalg and compare the pre-rounding values."""
+    c = OracleContext(logN, (30, 30), 1, 0)
+    N, ns = c.N, c.N // 2
+    z = np.random.default_rng(logN).uniform(-1, 1, ns)
+    scale = 2.0 ** 20
+    pre, m = c.encode_coeffs(z, scale)
+    zeta = np.exp(1j * np.pi / N)
+    roots = [zeta ** pow(5, j, 2 * N) for j in range(ns)] + [zeta ** (-pow(5, j, 2 * N)) for j in range(ns)]
+    V = np.array([[r ** i for i in range(N)] for r in roots])
+    y = np.concatenate([scale * z, scale * z])
+    sol = np.linalg.solve(V, y)
+    assert np.max(np.abs(sol.imag)) < 1e-6
+    assert np.allclose(pre, sol.real, rtol=0, atol=1e-6)
+    assert np.array_equal(m, np.where(pre >= 0, np.floor(pre + 0.5), np.ceil(pre - 0.5)).astype(np.int64))
+
+
+def test_encode_decode_roundtrip_linearity_and_rotation(mid):
+    c = mid
+    rng = np.random.default_rng(4)
+    z1, z2 = rng.uniform(-1, 1, (2, c.slots))
+    D = 2.0 ** 40
+    p1, p2 = c.encode(z1, D, 2), c.encode(z2, D, 2)
+    assert np.max(np.abs(c.decode(p1) - z1)) < 2.0 ** -30
+    s = OPt(c._pw(0, p1.words[None], p2.words[None], 2)[0], 2, D)
+    assert np.max(np.abs(c.decode(s) - (z1 + z2))) < 2.0 ** -29
+    # decode(phi_{5^k}(m)) = roll(z, -k)  (C6 left rotation)
+    for k in (1, 3, c.slots - 1):
+        g = pow(5, k, 2 * c.N)
+        rw = np.stack([c.automorph_ntt(p1.words[t], t, g) for t in range(3)])
+        assert np.max(np.abs(c.decode(OPt(rw, 2, D)) - np.roll(z1, -k))) < 2.0 ** -30
+    # phi_{2N-1} conjugates the slots: real slots are unchanged
+    rw = np.stack([c.automorph_ntt(p1.words[t], t, 2 * c.N - 1) for t in range(3)])
+    assert np.max(np.abs(c.decode(OPt(rw, 2, D)) - z1)) < 2.0 ** -30
+
+
+# ------------------------------------------------------------- P7 encrypt ---
+def test_encrypt_exact_identity(tiny):
+    """c0 + c1 s - m = v e + e0 + e1 s (mod Q) exactly, with the oracle's own randomness."""
+    c = tiny
+    N = c.N
+    s_coef, _ = c.secret_key()
+    z = np.random.default_rng(1).uniform(-1, 1, c.slots)
+    pt = c.encode(z, 2.0 ** 20, 2)
+    sid_ = 77
+    ct = c.encrypt(pt, sid_)
+    v = c.sample_ternary(sid(P_ENC_V, sid_, 0))
+    e0 = c.sample_cdt(sid(P_ENC_E0, sid_, 0))
+    e1 = c.sample_cdt(sid(P_ENC_E1, sid_, 0))
+    e = c.sample_cdt(sid(P_PK_E, 0, 0))
+    ve = negacyclic_mul(v, e, N)
+    e1s = negacyclic_mul(e1, s_coef, N)
+    rhs = [ve[i] + int(e0[i]) + e1s[i] for i in range(N)]
+    s_ntt = c.secret_key()[1]
+    for i in range(3):
+        q = c.q[i]
+        lhs = [(int(a) + int(b) * int(s) - int(m)) % q
+               for a, b, s, m in zip(ct.words[0, i], ct.words[1, i], s_ntt[i], pt.words[i])]
+        assert [int(x) for x in c.intt(i, np.array(lhs, dtype=np.uint64))] == [r % q for r in rhs]
+    # the public key's uniform half is the C13 draw
+    assert np.array_equal(c.public_key()[1, 1], c.sample_uniform(sid(P_PK_A, 0, 1), 1))
+
+
+# -------------------------------------------------------------- P10 tensor ---
+def test_tensor_exact_identity(tiny):
+    c = tiny
+    N, lvl = c.N, 2
+    rng = np.random.default_rng(5)
+    x = OCt(np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in c.q[:3]]) for _ in range(2)]), lvl, 1.0)
+    y = OCt(np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in c.q[:3]]) for _ in range(2)]), lvl, 1.0)
+    d = c.tensor(x, y)
+    s_coef, _ = c.secret_key()
+    s2 = negacyclic_mul(s_coef, s_coef, N)
+    for i in range(3):
+        q = c.q[i]
+        co = lambda w: [int(t) for t in c.intt(i, w)]
+        X0, X1, Y0, Y1 = co(x.words[0, i]), co(x.words[1, i]), co(y.words[0, i]), co(y.words[1, i])
+        D0, D1, D2 = co(d.words[0, i]), co(d.words[1, i]), co(d.words[2, i])
+        lhs = [a + b + cc for a, b, cc in zip(D0, negacyclic_mul(D1, s_coef, N), negacyclic_mul(D2, s2, N))]
+        L1 = [a + b for a, b in zip(X0, negacyclic_mul(X1, s_coef, N))]
+        L2 = [a + b for a, b in zip(Y0, negacyclic_mul(Y1, s_coef, N))]
+        assert [t % q for t in lhs] == negacyclic_mul(L1, L2, N, q)
+
+
+# ------------------------------------------------------------ P8 keyswitch ---
+@pytest.mark.parametrize("which", ["relin", 1, -1])
+def test_keyswitch_noise_identity(tiny, which):
+    """u0 + u1 s = d s' + small, with |small| <= (K/2 + 1)(1 + ||s||_1) + sum_j |D_j e_j| / P."""
+    c = tiny
+    N, lvl = c.N, 2
+    rng = np.random.default_rng(6)
+    d = np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in c.q[:3]])
+    s_coef, s_ntt = c.secret_key()
+    if which == "relin":
+        u = c.keyswitch(d, lvl, None)
+        sp = [np.array([(int(a) * int(a)) % c.q[i] for a in s_ntt[i]], dtype=np.uint64) for i in range(3)]
+    else:
+        u = c.keyswitch(d, lvl, which)
+        g = c.galois_elt(which)
+        sp = [c.automorph_ntt(s_ntt[i], i, g) for i in range(3)]
+    res = []
+    for i in range(3):
+        q = c.q[i]
+        w = [(int(a) + int(b) * int(s) - int(dd) * int(t)) % q
+             for a, b, s, dd, t in zip(u[0, i], u[1, i], s_ntt[i], d[i], sp[i])]
+        res.append(c.intt(i, np.array(w, dtype=np.uint64)))
+    Q = c.q[0] * c.q[1] * c.q[2]
+    err = [abs(centered(crt([res[i][n] for i in range(3)], c.q[:3])[0], Q)) for n in range(N)]
+    P = c.q[3] * c.q[4]
+    bound = (c.K / 2 + 1) * (1 + N) + 3 * N * (max(c.q[:3]) // 2) * 19 / P
+    assert max(err) <= bound
+    assert max(err) < 2 ** 20  # far below any wrong-index/sign result (~q)
+
+
+# -------------------------------------------------------------- P9 rescale ---
+def test_rescale_is_exact_round_divide(tiny):
+    c = tiny
+    N, lvl = c.N, 2
+    rng = np.random.default_rng(8)
+    w = np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in c.q[:3]]) for _ in range(2)])
+    out = c.rescale(OCt(w, lvl, 2.0 ** 40))
+    assert out.level == 1 and out.scale == 2.0 ** 40 / c.q[2]
+    ql = c.q[2]
+    for p in range(2):
+        coeffs = [c.intt(i, w[p, i]) for i in range(3)]
+        expect = [[0] * N for _ in range(2)]
+        for n in range(N):
+            X, _ = crt([coeffs[i][n] for i in range(3)], c.q[:3])
+            r = (X + (ql - 1) // 2) // ql       # round(X / q_l), no ties (q_l odd)
+            for i in range(2):
+                expect[i][n] = r % c.q[i]
+        for i in range(2):
+            assert np.array_equal(out.words[p, i], c.ntt(i, np.array(expect[i], dtype=np.uint64)))
+
+
+def test_moddown_divround_two_primes(tiny):
+    """C15 with |B| = 2: out = floor((X + h) / B) - u, 0 <= u < 2, per coefficient."""
+    c = tiny
+    N = c.N
+    rng = np.random.default_rng(9)
+    keep, drop = [0, 1, 2], [3, 4]
+    xk = np.stack([rng.integers(0, c.q[i], N, dtype=np.uint64) for i in keep])
+    xd = np.stack([rng.integers(0, c.q[i], N, dtype=np.uint64) for i in drop])
+    out = c.divround(keep, drop, xk, xd)
+    B = c.q[3] * c.q[4]
+    qs = [c.q[i] for i in keep + drop]
+    us = set()
+    for n in range(N):
+        X, _ = crt([xk[0][n], xk[1][n], xk[2][n], xd[0][n], xd[1][n]], qs)
+        base = (X + (B - 1) // 2) // B
+        found = [u for u in range(2) if all((base - u) % c.q[i] == int(out[i][n]) for i in keep)]
+        assert found, f"coefficient {n}: not floor((X+h)/B) - u"
+        us.add(found[0])
+    assert 0 in us
+
+
+# ------------------------------------------------------- homomorphism laws ---
+def test_homomorphism_add_mul_rotate(mid):
+    c = mid
+    rng = np.random.default_rng(12)
+    D = 2.0 ** 40
+    for trial in range(3):
+        z1, z2 = rng.uniform(-1, 1, (2, c.slots))
+        a = c.encrypt(c.encode(z1, D, 2), 2 * trial)
+        b = c.encrypt(c.encode(z2, D, 2), 2 * trial + 1)
+        dec = lambda ct, n=None: c.decode(c.decrypt(ct), n)
+        assert np.max(np.abs(dec(a) - z1)) < 1e-6
+        assert np.max(np.abs(dec(c.add(a, b)) - (z1 + z2))) < 1e-6
+        assert np.max(np.abs(dec(c.sub(a, b)) - (z1 - z2))) < 1e-6
+        assert np.max(np.abs(dec(c.negate(a)) + z1)) < 1e-6
+        m = c.rescale(c.relinearize(c.tensor(a, b)))
+        assert m.level == 1 and np.max(np.abs(dec(m) - z1 * z2)) < 1e-6
+        pm = c.rescale(c.mul_plain(a, c.encode(z2, float(c.q[2]), 2)))
+        assert pm.scale == D and np.max(np.abs(dec(pm) - z1 * z2)) < 1e-6
+        for k in (1, 5, -1):
+            assert np.max(np.abs(dec(c.rotate(a, k)) - np.roll(z1, -k))) < 1e-6
+        # group action rot(rot(v,2),3) == rot(v,5); rotation by n_s is the identity
+        r23 = c.rotate(c.rotate(a, 2), 3)
+        assert np.max(np.abs(dec(r23) - dec(c.rotate(a, 5)))) < 1e-6
+        assert np.max(np.abs(dec(c.rotate(a, c.slots)) - z1)) < 1e-6
+
+
+def test_depth_accounting():
+    """A fresh ciphertext at an L-prime chain admits exactly L-1 rescaled squarings."""
+    c = OracleContext(11, (60, 40, 40, 40, 60), 1, 1)
+    c.keygen([])
+    x = np.random.default_rng(0).uniform(-1, 1, c.slots)
+    ct = c.encrypt(c.encode(x, 2.0 ** 40, c.L - 1), 0)
+    for i in range(c.L - 1):
+        ct = c.square(ct)
+    assert ct.level == 0
+    assert np.max(np.abs(c.decode(c.decrypt(ct)) - x ** (2 ** (c.L - 1)))) < 1e-4
+    with pytest.raises(ValueError):
+        c.square(ct)
