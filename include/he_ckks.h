@@ -1,0 +1,275 @@
+/*
+ * he_ckks.h — C-ABI boundary of the B200 CKKS hot path (arXiv 2104.03152,
+ * "TenSEAL: A Library for Encrypted Tensor Operations Using Homomorphic
+ * Encryption").
+ *
+ * The paper's encrypted-inference method evaluates CKKSVector operations
+ * on top of the CKKS scheme it takes from SEAL
+ * ("relies on the implementation of the CKKS scheme").  This
+ * header exposes exactly the calls of SURVEY.md §8(b): context/keygen
+ * (PAPER.md:35), encode/encrypt, the op catalogue
+ * (add, sub, negate, add_plain, mul_plain, mul, square),
+ * rotation, relinearize/rescale ("automatic
+ * relinearization and rescaling"), the im2col convolution (PAPER.md:57, 64,
+ * 189-213) and the vector-plain-matrix product, decrypt /
+ * decode; plus word import/export used by the parity tests.
+ *
+ * Every arithmetic step behind these calls runs in the library's own sm_100a
+ * kernels (paper_2104_03152_b200/csrc).  There is no CPU fallback: a call that
+ * needs the GPU and has none returns HE_CUDA_ERROR.
+ *
+ * Conventions (DESIGN.md §3 = SURVEY.md §8(c) C1-C20):
+ *   - N = 2^log2N, slots n_s = N/2.  Data primes q_0..q_{L-1}, special primes
+ *     p_0..p_{K-1} (the last K entries of he_params.bits), one uint64 word per
+ *     residue.  Prime selection C2, primitive root C4.
+ *   - A ciphertext handle is a BATCH of B ciphertexts sharing one level l,
+ *     scale (double) and size (2 or 3).  Device layout, limb-major:
+ *         words[b][poly][limb][n],  limb in 0..l, n in 0..N-1,
+ *     always in the NTT (evaluation) domain, bit-reversed order C5:
+ *         NTT(a)[j] = sum_i a_i psi^{(2 brv(j)+1) i}  (mod q_limb).
+ *     Plaintexts are words[b][limb][n] in the same domain.
+ *   - Rotation by k > 0 is a LEFT rotation of the slots, Galois
+ *     element 5^k mod 2N; k < 0 uses 5^{n_s+k} (C6).
+ *   - Hybrid key switching with one data prime per digit (dnum = L, C12),
+ *     centered digit lift (C16), rounding DivRound (C15).
+ *
+ * Ownership: every handle is created by the library and released by the
+ * caller with the matching he_free_* call.  Device memory is allocated
+ * stream-ordered on the context's stream (cudaMallocAsync pool); calls are
+ * asynchronous on that stream unless they read or write host memory, which
+ * they do synchronously (they return after the host buffer is consumed /
+ * filled).  Every operation is pure: it returns a fresh output handle and
+ * never modifies its inputs.
+ *
+ * Errors: every function returns he_status (0 = HE_OK).  On failure nothing
+ * is written to the output pointers and he_last_error() returns a
+ * thread-local message.  No C++ exception crosses this boundary.
+ */
+#ifndef HE_CKKS_H_
+#define HE_CKKS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: SPEC taxonomy mapped by SURVEY.md §8(b). */
+typedef int he_status;
+enum {
+  HE_OK = 0,
+  HE_INVALID_PARAMS = 1,        /* bad he_params */
+  HE_PARAM_MISMATCH = 2,        /* operands from different contexts */
+  HE_DOMAIN_MISMATCH = 3,       /* reserved: all handles are NTT-domain */
+  HE_LEVEL_MISMATCH = 4,        /* operand levels differ */
+  HE_SCALE_MISMATCH = 5,        /* additive operands' scales differ bitwise */
+  HE_LEVEL_EXHAUSTED = 6,       /* rescale at level 0 */
+  HE_SCALE_OVERFLOW = 7,        /* |scale * z| >= 2^62 in encode */
+  HE_MISSING_KEY = 8,           /* secret / relin key absent */
+  HE_MISSING_GALOIS_KEY = 9,    /* rotation step without a key */
+  HE_INVALID_ROTATION = 10,     /* step 0 or |step| >= n_s at keygen */
+  HE_TOO_MANY_VALUES = 11,      /* more than n_s values to encode */
+  HE_SHAPE_MISMATCH = 12,       /* batch sizes / ciphertext sizes disagree */
+  HE_LAYOUT_MISMATCH = 13,      /* im2col geometry does not fit the slots */
+  HE_REPLICATION_EXHAUSTED = 14,/* vec_mat diagonal reads past the replicated span */
+  HE_CUDA_ERROR = 15,           /* a CUDA call failed (includes: no GPU present) */
+  HE_OUT_OF_MEMORY = 16,        /* device allocation failed */
+  HE_INVALID_ARGUMENT = 17      /* null pointer, bad size, etc. */
+};
+
+typedef struct he_context he_context;
+typedef struct he_plaintext he_plaintext;
+typedef struct he_ciphertext he_ciphertext;
+
+/* Parameters (SURVEY.md §8(b) "Context/keys").
+ *   log2N      ring degree exponent, 10..15 (N = 1024..32768).
+ *   n_primes   total number of primes L + K (<= 64).
+ *   bits       n_primes prime bit sizes in [20, 60]; the LAST n_special are
+ *              the special key-switching primes (C1: SEAL convention,
+ *              PAPER.md:32).  Primes are chosen by rule C2.
+ *   n_special  K in 0..2 (K = 0 disables key switching).
+ *   scale_log2 informational default scale (encode takes an explicit scale).
+ *   dnum       number of key-switching digits; must equal L or 0 (= L), C12. */
+typedef struct he_params {
+  int log2N;
+  int n_primes;
+  const int* bits;
+  int n_special;
+  double scale_log2;
+  int dnum;
+} he_params;
+
+/* Last error message of the calling thread ("" if none). */
+const char* he_last_error(void);
+
+/* Create a context: prime search (C2), psi (C4), NTT twiddles with Shoup
+ * companions, RNS constants, CDT table (C11), all uploaded once.  `seed` is
+ * the Philox key of every draw the context makes (C9).  Fails with
+ * HE_CUDA_ERROR when no CUDA device is usable. */
+he_status he_context_create(const he_params* params, uint64_t seed, he_context** out);
+he_status he_context_free(he_context* ctx);
+
+/* Read back log2N, L (data primes), K (special primes). */
+he_status he_context_info(const he_context* ctx, int* log2N, int* L, int* K);
+/* Copy the L+K primes (data first, specials last) / psi values to host. */
+he_status he_context_primes(const he_context* ctx, uint64_t* primes_out, uint64_t* psi_out);
+/* Copy the C11 CDT table (20 words) to host. */
+he_status he_context_cdt(const he_context* ctx, uint64_t* table_out);
+
+/* Make all subsequent calls on ctx run on `stream` (a cudaStream_t, e.g. a
+ * torch.cuda.Stream's cuda_stream).  NULL selects the legacy default stream. */
+he_status he_set_stream(he_context* ctx, void* stream);
+/* Block until all work queued on the context's stream is done. */
+he_status he_sync(he_context* ctx);
+
+/* Key generation on the device: ternary
+ * secret s, public key (-a s + e, a) over the data limbs, relinearisation key
+ * for s^2 and one Galois key per distinct element of `rot_steps` (each step
+ * nonzero with |step| <= n_s; k = n_s gives the identity element, kept as a
+ * real key per C20).  May be called once per context. */
+he_status he_keygen(he_context* ctx, const int32_t* rot_steps, size_t n_steps);
+/* Drop the secret key (the "public" context of S:311-318): decrypt then fails
+ * with HE_MISSING_KEY. */
+he_status he_drop_secret_key(he_context* ctx);
+
+/* ---- encode / decode (C6/C7) -------------------------- */
+/* Encode B real vectors of n_per_item <= n_s values each (host array
+ * z[B][n_per_item], row-major) at `scale`, into a plaintext at `level`:
+ * m_i = round_half_away(scale (2/N) Re sum_j z_j zeta^{-i 5^j}), reduced into
+ * limbs 0..level and NTT'd.  Canonical-embedding IFFT in float64 on device. */
+he_status he_encode(he_context* ctx, const double* z, size_t n_per_item, size_t B, double scale,
+                    int level, he_plaintext** out);
+/* Same, with z already in device memory. */
+he_status he_encode_device(he_context* ctx, const double* z_dev, size_t n_per_item, size_t B,
+                           double scale, int level, he_plaintext** out);
+/* Decode the first n slots of every item into host out[B][n]: CRT compose,
+ * centre, float64, FFT, divide by the plaintext's scale (C6). */
+he_status he_decode(he_context* ctx, const he_plaintext* pt, double* out, size_t n);
+/* Same, writing device memory out_dev[B][n]. */
+he_status he_decode_device(he_context* ctx, const he_plaintext* pt, double* out_dev, size_t n);
+
+/* ---- encrypt / decrypt (C13) ----------------------------- */
+/* Public-key encryption of every item of pt; item b draws its randomness
+ * (v, e0, e1) from Philox stream `stream_id + b`.  Output scale/level = pt's. */
+he_status he_encrypt(he_context* ctx, const he_plaintext* pt, uint64_t stream_id,
+                     he_ciphertext** out);
+/* m = c0 + c1 s (+ c2 s^2).  Needs the secret key. */
+he_status he_decrypt(he_context* ctx, const he_ciphertext* ct, he_plaintext** out);
+
+/* ---- arithmetic ------------- */
+/* Binary ops require equal level, equal size and (for add/sub) bitwise-equal
+ * scale; B must match, or one side may have B = 1 (broadcast). */
+he_status he_add(he_context* ctx, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext** out);
+he_status he_sub(he_context* ctx, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext** out);
+he_status he_negate(he_context* ctx, const he_ciphertext* a, he_ciphertext** out);
+/* add_plain: level and scale must match the ciphertext's. */
+he_status he_add_plain(he_context* ctx, const he_ciphertext* a, const he_plaintext* p, he_ciphertext** out);
+/* mul_plain: level must match; output scale = scale_ct * scale_pt; no rescale (C14). */
+he_status he_mul_plain(he_context* ctx, const he_ciphertext* a, const he_plaintext* p, he_ciphertext** out);
+/* mul: tensor product, size-3 output, no relinearisation. */
+he_status he_mul(he_context* ctx, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext** out);
+/* square = tensor(a, a) -> relinearize -> rescale (C14). */
+he_status he_square(he_context* ctx, const he_ciphertext* a, he_ciphertext** out);
+/* relinearize a size-3 ciphertext with the s^2 key. */
+he_status he_relinearize(he_context* ctx, const he_ciphertext* a, he_ciphertext** out);
+/* rescale: exact round(X / q_l) on every limb, level l -> l-1, scale / q_l (C15). */
+he_status he_rescale(he_context* ctx, const he_ciphertext* a, he_ciphertext** out);
+/* rotate left by k (Galois automorphism 5^k + key switch). */
+he_status he_rotate(he_context* ctx, const he_ciphertext* a, int32_t k, he_ciphertext** out);
+
+/* ---- composite ops ----------------------------------- */
+/* Client-side im2col + vertical scan (C18), host only, float64: image
+ * img[H][W] -> slots[n_s] with slot = tap * chunk + window, chunk = next
+ * power of two >= #windows.  Writes *windows / *chunk if non-NULL. */
+he_status he_im2col_encode(const double* img, int H, int W, int kh, int kw, int stride,
+                           size_t n_slots, double* slots_out, int* windows, int* chunk);
+/* im2col convolution on the encrypted side (C18/C19): for every output
+ * channel c: t_c = rescale(ct * K_c); log2(n_s/chunk) rounds t_c += rot(t_c,
+ * chunk 2^r); then sum_c t_c * Mask_c, rescale, + bias.  kernels[C][kh*kw],
+ * bias[C] (may be NULL).  Kernel plaintexts are encoded at scale
+ * q_l * 2^kernel_shift, masks at q_{l-1} * 2^mask_shift.  Consumes 2 levels. */
+he_status he_im2col_conv(he_context* ctx, const he_ciphertext* ct, const double* kernels,
+                         int n_channels, int kh, int kw, const double* bias, int chunk,
+                         int kernel_shift, int mask_shift, he_ciphertext** out);
+/* Encrypted vector x plain matrix W[n][m] (in x out, row-major) by the
+ * diagonal method (C17): y = sum_{k<n} rot(x, k) * D_k, one
+ * rescale, + bias[m] (may be NULL).  The input must hold x replicated with
+ * period n.  replicate_out != 0 makes D_k periodic in m (output replicated
+ * with period m; needs n | n_s and m | n_s).  Diagonals are encoded at scale
+ * q_l * 2^(-pt_scale_shift).  Consumes 1 level; n-1 rotations, hoisted. */
+he_status he_vec_mat(he_context* ctx, const he_ciphertext* ct, const double* W, int n, int m,
+                     const double* bias, int replicate_out, int pt_scale_shift, he_ciphertext** out);
+/* Same with pre-encoded diagonals: diags is a plaintext batch of n items
+ * (item k = D_k) at the ciphertext's level; bias_pt (may be NULL) at the
+ * rescaled level and scale.  Used to inject oracle plaintexts (C7). */
+he_status he_vec_mat_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* diags,
+                        const he_plaintext* bias_pt, he_ciphertext** out);
+/* Same as he_im2col_conv with pre-encoded plaintexts: kernels (C items at
+ * the input level), masks (C items at level-1), bias_pt (may be NULL). */
+he_status he_im2col_conv_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* kernels,
+                            const he_plaintext* masks, const he_plaintext* bias_pt, int chunk,
+                            he_ciphertext** out);
+
+/* Encode-once forms of the two composite ops' plaintexts (weights stay
+ * resident on the device across batches; PAPER.md:98 excludes weight
+ * preparation from the timed forward).  `level` / `in_scale` describe the
+ * ciphertext the op will be applied to.  vec_mat: *diags = n items at
+ * `level`, *bias_pt (NULL if bias is NULL) at level-1 and the output scale.
+ * conv: *kernels_pt = C items at `level`, *masks_pt = C items at level-1,
+ * *bias_pt at level-2 and the output scale. */
+he_status he_vec_mat_encode(he_context* ctx, const double* W, int n, int m, const double* bias,
+                            int replicate_out, int pt_scale_shift, int level, double in_scale,
+                            he_plaintext** diags, he_plaintext** bias_pt);
+he_status he_im2col_conv_encode(he_context* ctx, const double* kernels, int n_channels, int kh, int kw,
+                                const double* bias, int chunk, int kernel_shift, int mask_shift,
+                                int level, double in_scale, he_plaintext** kernels_pt,
+                                he_plaintext** masks_pt, he_plaintext** bias_pt);
+
+/* ---- handles, import / export (test injection; not in the paper) ------ */
+he_status he_free_plaintext(he_plaintext* pt);
+he_status he_free_ciphertext(he_ciphertext* ct);
+he_status he_ct_info(const he_ciphertext* ct, size_t* B, int* size, int* level, double* scale);
+he_status he_pt_info(const he_plaintext* pt, size_t* B, int* level, double* scale);
+/* Device pointer of the words [B][size][level+1][N] (contiguous). */
+he_status he_ct_device_ptr(const he_ciphertext* ct, uint64_t** words);
+he_status he_pt_device_ptr(const he_plaintext* pt, uint64_t** words);
+/* Copy words between host (or device when `on_device` != 0) memory and a
+ * handle.  Import checks every word is < its prime (else HE_INVALID_ARGUMENT). */
+he_status he_ct_export_words(he_context* ctx, const he_ciphertext* ct, uint64_t* dst, int on_device);
+he_status he_ct_import_words(he_context* ctx, const uint64_t* src, int on_device, size_t B, int size,
+                             int level, double scale, he_ciphertext** out);
+he_status he_pt_export_words(he_context* ctx, const he_plaintext* pt, uint64_t* dst, int on_device);
+he_status he_pt_import_words(he_context* ctx, const uint64_t* src, int on_device, size_t B, int level,
+                             double scale, he_plaintext** out);
+/* Plaintext from signed integer coefficients m[B][N] (host): reduce per limb
+ * and NTT on device (C7 injection of an exactly-rounded encoding). */
+he_status he_pt_from_int_coeffs(he_context* ctx, const int64_t* m, size_t B, double scale, int level,
+                                he_plaintext** out);
+/* Export keys as NTT words: kind 0 = secret [L+K][N], 1 = public [2][L][N],
+ * 2 = relin [L][2][L+K][N], 3 = Galois key of rotation `step` (same shape). */
+he_status he_key_export(he_context* ctx, int kind, int32_t step, uint64_t* dst);
+/* Number of words he_key_export writes for `kind`. */
+size_t he_key_words(const he_context* ctx, int kind);
+
+/* ---- ring primitives (BASELINE config 2 microbench) ------ */
+/* In-place batched forward / inverse negacyclic NTT (C5) of device words
+ * d[B][n_limbs][N], limb i modulo prime i (n_limbs <= L+K). */
+he_status he_ntt_forward(he_context* ctx, uint64_t* d, size_t B, int n_limbs);
+he_status he_ntt_inverse(he_context* ctx, uint64_t* d, size_t B, int n_limbs);
+/* out = a (.) b pointwise mod prime of the limb, device words [B][n_limbs][N]. */
+he_status he_modmul(he_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t B,
+                    int n_limbs);
+/* Fused: out = INTT(NTT(a) (.) b) for coefficient-domain a and NTT-domain b
+ * (one kernel per limb: negacyclic ring product). */
+he_status he_ntt_mul_intt(he_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                          size_t B, int n_limbs);
+
+/* Number of kernels this library has launched on ctx (for the bench's
+ * gpu_launches claim). */
+uint64_t he_launch_count(const he_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HE_CKKS_H_ */

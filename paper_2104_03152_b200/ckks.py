@@ -1,0 +1,427 @@
+"""Thin Python binding of the C-ABI in include/he_ckks.h (argument marshalling only).
+
+Every function here is the C function of the same name: it converts numpy
+arrays / torch tensors to pointers, calls libhe_ckks.so and raises HEError on a
+non-zero status.  No arithmetic of the method happens in Python, and there is no
+CPU fallback: if the shared library or a CUDA device is missing, the calls fail.
+
+Small handle classes (Context, Plaintext, Ciphertext) own the C handles and free
+them on garbage collection.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhe_ckks.so")
+
+STATUS = {
+    0: "OK", 1: "INVALID_PARAMS", 2: "PARAM_MISMATCH", 3: "DOMAIN_MISMATCH", 4: "LEVEL_MISMATCH",
+    5: "SCALE_MISMATCH", 6: "LEVEL_EXHAUSTED", 7: "SCALE_OVERFLOW", 8: "MISSING_KEY",
+    9: "MISSING_GALOIS_KEY", 10: "INVALID_ROTATION", 11: "TOO_MANY_VALUES", 12: "SHAPE_MISMATCH",
+    13: "LAYOUT_MISMATCH", 14: "REPLICATION_EXHAUSTED", 15: "CUDA_ERROR", 16: "OUT_OF_MEMORY",
+    17: "INVALID_ARGUMENT",
+}
+
+
+class HEError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+
+
+class he_params(C.Structure):
+    _fields_ = [("log2N", C.c_int), ("n_primes", C.c_int), ("bits", C.POINTER(C.c_int)),
+                ("n_special", C.c_int), ("scale_log2", C.c_double), ("dnum", C.c_int)]
+
+
+VP = C.c_void_p
+VPP = C.POINTER(C.c_void_p)
+U64P = C.POINTER(C.c_uint64)
+I64P = C.POINTER(C.c_int64)
+DP = C.POINTER(C.c_double)
+SZ = C.c_size_t
+
+# name -> argtypes (restype he_status unless listed in _RESTYPES)
+_SIGS = {
+    "he_context_create": [C.POINTER(he_params), C.c_uint64, VPP],
+    "he_context_free": [VP],
+    "he_context_info": [VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "he_context_primes": [VP, U64P, U64P],
+    "he_context_cdt": [VP, U64P],
+    "he_set_stream": [VP, VP],
+    "he_sync": [VP],
+    "he_keygen": [VP, C.POINTER(C.c_int32), SZ],
+    "he_drop_secret_key": [VP],
+    "he_encode": [VP, DP, SZ, SZ, C.c_double, C.c_int, VPP],
+    "he_encode_device": [VP, VP, SZ, SZ, C.c_double, C.c_int, VPP],
+    "he_decode": [VP, VP, DP, SZ],
+    "he_decode_device": [VP, VP, VP, SZ],
+    "he_encrypt": [VP, VP, C.c_uint64, VPP],
+    "he_decrypt": [VP, VP, VPP],
+    "he_add": [VP, VP, VP, VPP],
+    "he_sub": [VP, VP, VP, VPP],
+    "he_negate": [VP, VP, VPP],
+    "he_add_plain": [VP, VP, VP, VPP],
+    "he_mul_plain": [VP, VP, VP, VPP],
+    "he_mul": [VP, VP, VP, VPP],
+    "he_square": [VP, VP, VPP],
+    "he_relinearize": [VP, VP, VPP],
+    "he_rescale": [VP, VP, VPP],
+    "he_rotate": [VP, VP, C.c_int32, VPP],
+    "he_im2col_encode": [DP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, SZ, DP, C.POINTER(C.c_int),
+                         C.POINTER(C.c_int)],
+    "he_im2col_conv": [VP, VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, VPP],
+    "he_vec_mat": [VP, VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, VPP],
+    "he_vec_mat_pt": [VP, VP, VP, VP, VPP],
+    "he_im2col_conv_pt": [VP, VP, VP, VP, VP, C.c_int, VPP],
+    "he_vec_mat_encode": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
+    "he_im2col_conv_encode": [VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_int,
+                              C.c_double, VPP, VPP, VPP],
+    "he_free_plaintext": [VP],
+    "he_free_ciphertext": [VP],
+    "he_ct_info": [VP, C.POINTER(SZ), C.POINTER(C.c_int), C.POINTER(C.c_int), DP],
+    "he_pt_info": [VP, C.POINTER(SZ), C.POINTER(C.c_int), DP],
+    "he_ct_device_ptr": [VP, C.POINTER(U64P)],
+    "he_pt_device_ptr": [VP, C.POINTER(U64P)],
+    "he_ct_export_words": [VP, VP, VP, C.c_int],
+    "he_ct_import_words": [VP, VP, C.c_int, SZ, C.c_int, C.c_int, C.c_double, VPP],
+    "he_pt_export_words": [VP, VP, VP, C.c_int],
+    "he_pt_import_words": [VP, VP, C.c_int, SZ, C.c_int, C.c_double, VPP],
+    "he_pt_from_int_coeffs": [VP, I64P, SZ, C.c_double, C.c_int, VPP],
+    "he_key_export": [VP, C.c_int, C.c_int32, U64P],
+    "he_key_words": [VP, C.c_int],
+    "he_ntt_forward": [VP, VP, SZ, C.c_int],
+    "he_ntt_inverse": [VP, VP, SZ, C.c_int],
+    "he_modmul": [VP, VP, VP, VP, SZ, C.c_int],
+    "he_ntt_mul_intt": [VP, VP, VP, VP, SZ, C.c_int],
+    "he_launch_count": [VP],
+    "he_last_error": [],
+}
+_RESTYPES = {"he_key_words": C.c_size_t, "he_launch_count": C.c_uint64, "he_last_error": C.c_char_p}
+
+_lib = None
+
+
+def lib():
+    """Load libhe_ckks.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2104_03152_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _RESTYPES.get(name, C.c_int)
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise HEError(rc, lib().he_last_error().decode())
+
+
+def _ptr(a):
+    """Raw data pointer of a numpy array or torch tensor."""
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _is_dev(a) -> int:
+    return int(hasattr(a, "is_cuda") and a.is_cuda)
+
+
+# ---------------------------------------------------------------- handles ---
+class Plaintext:
+    def __init__(self, ctx: "Context", h):
+        self.ctx, self.h = ctx, h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.he_free_plaintext(self.h)
+            self.h = None
+
+    def info(self):
+        B, lvl, sc = SZ(), C.c_int(), C.c_double()
+        _check(lib().he_pt_info(self.h, C.byref(B), C.byref(lvl), C.byref(sc)))
+        return B.value, lvl.value, sc.value
+
+    @property
+    def B(self): return self.info()[0]
+
+    @property
+    def level(self): return self.info()[1]
+
+    @property
+    def scale(self): return self.info()[2]
+
+    def words(self) -> np.ndarray:
+        B, lvl, _ = self.info()
+        out = np.zeros((B, lvl + 1, self.ctx.N), dtype=np.uint64)
+        _check(lib().he_pt_export_words(self.ctx.h, self.h, _ptr(out), 0))
+        return out
+
+
+class Ciphertext:
+    def __init__(self, ctx: "Context", h):
+        self.ctx, self.h = ctx, h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.he_free_ciphertext(self.h)
+            self.h = None
+
+    def info(self):
+        B, size, lvl, sc = SZ(), C.c_int(), C.c_int(), C.c_double()
+        _check(lib().he_ct_info(self.h, C.byref(B), C.byref(size), C.byref(lvl), C.byref(sc)))
+        return B.value, size.value, lvl.value, sc.value
+
+    @property
+    def B(self): return self.info()[0]
+
+    @property
+    def size(self): return self.info()[1]
+
+    @property
+    def level(self): return self.info()[2]
+
+    @property
+    def scale(self): return self.info()[3]
+
+    def words(self) -> np.ndarray:
+        B, size, lvl, _ = self.info()
+        out = np.zeros((B, size, lvl + 1, self.ctx.N), dtype=np.uint64)
+        _check(lib().he_ct_export_words(self.ctx.h, self.h, _ptr(out), 0))
+        return out
+
+    def device_ptr(self) -> int:
+        p = U64P()
+        _check(lib().he_ct_device_ptr(self.h, C.byref(p)))
+        return C.cast(p, C.c_void_p).value or 0
+
+
+class Context:
+    """he_context_create + the calls that take a context, under the C names."""
+
+    def __init__(self, logN: int, bits, n_special: int, seed: int, scale_log2: float = 0.0):
+        bits = [int(b) for b in bits]
+        arr = (C.c_int * len(bits))(*bits)
+        p = he_params(logN, len(bits), arr, n_special, scale_log2, 0)
+        h = C.c_void_p()
+        _check(lib().he_context_create(C.byref(p), seed, C.byref(h)))
+        self.h = h
+        lg, L, K = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().he_context_info(h, C.byref(lg), C.byref(L), C.byref(K)))
+        self.logN, self.L, self.K = lg.value, L.value, K.value
+        self.N = 1 << self.logN
+        pr = np.zeros(self.L + self.K, dtype=np.uint64)
+        ps = np.zeros(self.L + self.K, dtype=np.uint64)
+        _check(lib().he_context_primes(h, pr.ctypes.data_as(U64P), ps.ctypes.data_as(U64P)))
+        self.primes, self.psis = pr, ps
+        self.q = [int(x) for x in pr]
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.he_sync(self.h)
+            _lib.he_context_free(self.h)
+            self.h = None
+
+    @property
+    def slots(self) -> int:
+        return self.N // 2
+
+    # -- context ------------------------------------------------------------
+    def he_context_cdt(self) -> np.ndarray:
+        out = np.zeros(20, dtype=np.uint64)
+        _check(lib().he_context_cdt(self.h, out.ctypes.data_as(U64P)))
+        return out
+
+    def he_set_stream(self, stream) -> None:
+        """stream: a torch.cuda.Stream (or raw cudaStream_t int)."""
+        s = getattr(stream, "cuda_stream", stream)
+        _check(lib().he_set_stream(self.h, C.c_void_p(int(s) if s else 0)))
+
+    def he_sync(self) -> None:
+        _check(lib().he_sync(self.h))
+
+    def he_launch_count(self) -> int:
+        return int(lib().he_launch_count(self.h))
+
+    def he_keygen(self, steps=()) -> None:
+        steps = [int(s) for s in steps]
+        arr = (C.c_int32 * max(1, len(steps)))(*steps)
+        _check(lib().he_keygen(self.h, arr, len(steps)))
+
+    def he_drop_secret_key(self) -> None:
+        _check(lib().he_drop_secret_key(self.h))
+
+    def he_key_export(self, kind: int, step: int = 0) -> np.ndarray:
+        n = int(lib().he_key_words(self.h, kind))
+        out = np.zeros(n, dtype=np.uint64)
+        _check(lib().he_key_export(self.h, kind, step, out.ctypes.data_as(U64P)))
+        N, L, NP = self.N, self.L, self.L + self.K
+        shape = {0: (NP, N), 1: (2, L, N), 2: (L, 2, NP, N), 3: (L, 2, NP, N)}[kind]
+        return out.reshape(shape)
+
+    # -- encode / decode ------------------------------------------------------
+    def he_encode(self, z, scale: float, level: int) -> Plaintext:
+        """z: [B][n] (or [n]) float64 host array, or a CUDA float64 tensor."""
+        h = C.c_void_p()
+        if _is_dev(z):
+            z2 = z if z.dim() == 2 else z.reshape(1, -1)
+            z2 = z2.contiguous()
+            _check(lib().he_encode_device(self.h, _ptr(z2), z2.shape[1], z2.shape[0], float(scale), level,
+                                          C.byref(h)))
+        else:
+            z2 = np.ascontiguousarray(np.atleast_2d(np.asarray(z, dtype=np.float64)))
+            _check(lib().he_encode(self.h, z2.ctypes.data_as(DP), z2.shape[1], z2.shape[0], float(scale),
+                                   level, C.byref(h)))
+        return Plaintext(self, h)
+
+    def he_decode(self, pt: Plaintext, n: int | None = None, out=None):
+        n = self.slots if n is None else n
+        B = pt.B
+        if out is not None and _is_dev(out):
+            _check(lib().he_decode_device(self.h, pt.h, _ptr(out), n))
+            return out
+        res = np.zeros((B, n), dtype=np.float64)
+        _check(lib().he_decode(self.h, pt.h, res.ctypes.data_as(DP), n))
+        return res
+
+    def he_pt_from_int_coeffs(self, m, scale: float, level: int) -> Plaintext:
+        m2 = np.ascontiguousarray(np.atleast_2d(np.asarray(m, dtype=np.int64)))
+        h = C.c_void_p()
+        _check(lib().he_pt_from_int_coeffs(self.h, m2.ctypes.data_as(I64P), m2.shape[0], float(scale), level,
+                                           C.byref(h)))
+        return Plaintext(self, h)
+
+    def he_pt_import_words(self, w, level: int, scale: float) -> Plaintext:
+        h = C.c_void_p()
+        if _is_dev(w):
+            B = w.shape[0]
+            _check(lib().he_pt_import_words(self.h, _ptr(w), 1, B, level, float(scale), C.byref(h)))
+        else:
+            w2 = np.ascontiguousarray(w, dtype=np.uint64).reshape(-1, level + 1, self.N)
+            _check(lib().he_pt_import_words(self.h, _ptr(w2), 0, w2.shape[0], level, float(scale), C.byref(h)))
+        return Plaintext(self, h)
+
+    def he_ct_import_words(self, w, level: int, scale: float, size: int = 2) -> Ciphertext:
+        h = C.c_void_p()
+        if _is_dev(w):
+            B = w.shape[0]
+            _check(lib().he_ct_import_words(self.h, _ptr(w), 1, B, size, level, float(scale), C.byref(h)))
+        else:
+            w2 = np.ascontiguousarray(w, dtype=np.uint64).reshape(-1, size, level + 1, self.N)
+            _check(lib().he_ct_import_words(self.h, _ptr(w2), 0, w2.shape[0], size, level, float(scale),
+                                            C.byref(h)))
+        return Ciphertext(self, h)
+
+    # -- encrypt / decrypt ------------------------------------------------------
+    def he_encrypt(self, pt: Plaintext, stream_id: int = 0) -> Ciphertext:
+        h = C.c_void_p()
+        _check(lib().he_encrypt(self.h, pt.h, stream_id, C.byref(h)))
+        return Ciphertext(self, h)
+
+    def he_decrypt(self, ct: Ciphertext) -> Plaintext:
+        h = C.c_void_p()
+        _check(lib().he_decrypt(self.h, ct.h, C.byref(h)))
+        return Plaintext(self, h)
+
+    # -- arithmetic -------------------------------------------------------------
+    def _ct2(self, fn, *args) -> Ciphertext:
+        h = C.c_void_p()
+        _check(fn(self.h, *args, C.byref(h)))
+        return Ciphertext(self, h)
+
+    def he_add(self, a, b): return self._ct2(lib().he_add, a.h, b.h)
+    def he_sub(self, a, b): return self._ct2(lib().he_sub, a.h, b.h)
+    def he_negate(self, a): return self._ct2(lib().he_negate, a.h)
+    def he_add_plain(self, a, p): return self._ct2(lib().he_add_plain, a.h, p.h)
+    def he_mul_plain(self, a, p): return self._ct2(lib().he_mul_plain, a.h, p.h)
+    def he_mul(self, a, b): return self._ct2(lib().he_mul, a.h, b.h)
+    def he_square(self, a): return self._ct2(lib().he_square, a.h)
+    def he_relinearize(self, a): return self._ct2(lib().he_relinearize, a.h)
+    def he_rescale(self, a): return self._ct2(lib().he_rescale, a.h)
+    def he_rotate(self, a, k: int): return self._ct2(lib().he_rotate, a.h, int(k))
+
+    def he_vec_mat(self, ct, W, bias=None, replicate_out=False, pt_scale_shift=0) -> Ciphertext:
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        n, m = W.shape
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        return self._ct2(lib().he_vec_mat, ct.h, W.ctypes.data_as(DP), n, m,
+                         None if b is None else b.ctypes.data_as(DP), int(bool(replicate_out)),
+                         int(pt_scale_shift))
+
+    def he_vec_mat_encode(self, W, bias, replicate_out, pt_scale_shift, level, in_scale):
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        n, m = W.shape
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        d, bp = C.c_void_p(), C.c_void_p()
+        _check(lib().he_vec_mat_encode(self.h, W.ctypes.data_as(DP), n, m,
+                                       None if b is None else b.ctypes.data_as(DP), int(bool(replicate_out)),
+                                       int(pt_scale_shift), level, float(in_scale), C.byref(d), C.byref(bp)))
+        return Plaintext(self, d), (Plaintext(self, bp) if bp.value else None)
+
+    def he_im2col_conv_encode(self, kernels, bias, chunk, kernel_shift, mask_shift, level, in_scale):
+        k = np.ascontiguousarray(kernels, dtype=np.float64)
+        Cn, kh, kw = k.shape[0], k.shape[-2], k.shape[-1]
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        kp, mp, bp = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().he_im2col_conv_encode(self.h, k.ctypes.data_as(DP), Cn, kh, kw,
+                                           None if b is None else b.ctypes.data_as(DP), int(chunk),
+                                           int(kernel_shift), int(mask_shift), level, float(in_scale),
+                                           C.byref(kp), C.byref(mp), C.byref(bp)))
+        return Plaintext(self, kp), Plaintext(self, mp), (Plaintext(self, bp) if bp.value else None)
+
+    def he_vec_mat_pt(self, ct, diags: Plaintext, bias: Plaintext | None = None) -> Ciphertext:
+        return self._ct2(lib().he_vec_mat_pt, ct.h, diags.h, None if bias is None else bias.h)
+
+    def he_im2col_conv(self, ct, kernels, bias=None, chunk=64, kernel_shift=0, mask_shift=0) -> Ciphertext:
+        """kernels: [C][kh][kw] (or [C][1][kh][kw]) float64."""
+        k = np.ascontiguousarray(kernels, dtype=np.float64)
+        Cn, kh, kw = k.shape[0], k.shape[-2], k.shape[-1]
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        return self._ct2(lib().he_im2col_conv, ct.h, k.ctypes.data_as(DP), Cn, kh, kw,
+                         None if b is None else b.ctypes.data_as(DP), int(chunk), int(kernel_shift),
+                         int(mask_shift))
+
+    def he_im2col_conv_pt(self, ct, kernels: Plaintext, masks: Plaintext, bias: Plaintext | None,
+                          chunk: int) -> Ciphertext:
+        return self._ct2(lib().he_im2col_conv_pt, ct.h, kernels.h, masks.h, None if bias is None else bias.h,
+                         int(chunk))
+
+    # -- ring primitives (device tensors [B][nl][N] uint64 / int64) --------------
+    def he_ntt_forward(self, d, B: int, nl: int) -> None:
+        _check(lib().he_ntt_forward(self.h, _ptr(d), B, nl))
+
+    def he_ntt_inverse(self, d, B: int, nl: int) -> None:
+        _check(lib().he_ntt_inverse(self.h, _ptr(d), B, nl))
+
+    def he_modmul(self, a, b, out, B: int, nl: int) -> None:
+        _check(lib().he_modmul(self.h, _ptr(a), _ptr(b), _ptr(out), B, nl))
+
+    def he_ntt_mul_intt(self, a, b, out, B: int, nl: int) -> None:
+        _check(lib().he_ntt_mul_intt(self.h, _ptr(a), _ptr(b), _ptr(out), B, nl))
+
+
+def he_im2col_encode(img, kh: int, kw: int, stride: int, n_slots: int):
+    """Client-side im2col + vertical scan (C18). Returns (slots, windows, chunk)."""
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    H, W = img.shape
+    out = np.zeros(n_slots, dtype=np.float64)
+    w, ch = C.c_int(), C.c_int()
+    _check(lib().he_im2col_encode(img.ctypes.data_as(DP), H, W, kh, kw, stride, n_slots,
+                                  out.ctypes.data_as(DP), C.byref(w), C.byref(ch)))
+    return out, w.value, ch.value

@@ -1,0 +1,81 @@
+"""The paper's encrypted CNN driven through the C-ABI.
+
+conv 7x7 stride 3, 4 kernels (im2col) -> x^2 -> FC 256->64
+-> x^2 -> FC 64->10, one image per ciphertext, a batch of images per call.
+Every step is a C-ABI call (include/he_ckks.h); this module only sequences
+the calls and holds the resident weight plaintexts (encoded once).
+
+Scale schedule: input encoded at 2^30; conv
+kernels at q_l (shift 0), masks at q_{l-1} 2^-4, FC1 diagonals at q_l, FC2
+diagonals at q_l 2^-4.  Rotation keys: exactly the circuit's steps (A-rot).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .ckks import Context, he_im2col_encode
+
+PLAN = dict(in_log2=30, kernel_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=4)
+CHUNK = 64          # next power of two >= 64 windows (C18)
+KH = KW = 7
+STRIDE = 3
+
+
+def rotation_steps(ns: int = 4096, chunk: int = CHUNK) -> list:
+    """A-rot: FC1 diagonals 1..255 (FC2's 1..63 are a subset) and the conv fold chunk * 2^r."""
+    fold = []
+    s = chunk
+    while s < ns:
+        fold.append(s)
+        s <<= 1
+    return sorted(set(range(1, 256)) | set(fold))
+
+
+class EncryptedCNN:
+    """conv_w [4,1,7,7], conv_b [4], fc1_w [64,256], fc1_b [64], fc2_w [10,64], fc2_b [10] (PyTorch layouts)."""
+
+    def __init__(self, ctx: Context, w, plan=None):
+        self.ctx, self.plan = ctx, dict(plan or PLAN)
+        L = ctx.L
+        self.top = L - 1
+        in_scale = 2.0 ** self.plan["in_log2"]
+        k = np.asarray(w.conv_w, dtype=np.float64).reshape(w.conv_w.shape[0], KH, KW)
+        self.conv_k, self.conv_m, self.conv_b = ctx.he_im2col_conv_encode(
+            k, w.conv_b, CHUNK, self.plan["kernel_shift"], self.plan["mask_shift"], self.top, in_scale)
+        # scale after conv and square (tracked exactly like the library does)
+        s = in_scale * self.conv_k.scale / ctx.q[self.top]
+        s = s * self.conv_m.scale / ctx.q[self.top - 1]
+        lvl = self.top - 2
+        s = s * s / ctx.q[lvl]          # square: tensor, relin, rescale
+        lvl -= 1
+        self.fc1_d, self.fc1_b = ctx.he_vec_mat_encode(np.asarray(w.fc1_w).T, w.fc1_b, True,
+                                                       -self.plan["fc1_shift"], lvl, s)
+        s = s * self.fc1_d.scale / ctx.q[lvl]
+        lvl -= 1
+        s = s * s / ctx.q[lvl]
+        lvl -= 1
+        self.fc2_d, self.fc2_b = ctx.he_vec_mat_encode(np.asarray(w.fc2_w).T, w.fc2_b, False,
+                                                       self.plan["fc2_shift"], lvl, s)
+        self.n_out = int(np.asarray(w.fc2_w).shape[0])
+
+    def im2col(self, imgs: np.ndarray) -> np.ndarray:
+        return np.stack([he_im2col_encode(img, KH, KW, STRIDE, self.ctx.slots)[0] for img in imgs])
+
+    def encrypt(self, imgs: np.ndarray, stream_id: int = 0):
+        """Client side: im2col (host) -> encode -> encrypt, images [B][28][28]."""
+        slots = self.im2col(np.asarray(imgs, dtype=np.float64))
+        pt = self.ctx.he_encode(slots, 2.0 ** self.plan["in_log2"], self.top)
+        return self.ctx.he_encrypt(pt, stream_id)
+
+    def forward(self, ct):
+        """Server side: conv -> square -> FC1 -> square -> FC2."""
+        c = self.ctx
+        x = c.he_im2col_conv_pt(ct, self.conv_k, self.conv_m, self.conv_b, CHUNK)
+        x = c.he_square(x)
+        x = c.he_vec_mat_pt(x, self.fc1_d, self.fc1_b)
+        x = c.he_square(x)
+        return c.he_vec_mat_pt(x, self.fc2_d, self.fc2_b)
+
+    def decrypt(self, ct) -> np.ndarray:
+        """Client side: decrypt -> decode -> the first n_out slots per image."""
+        return self.ctx.he_decode(self.ctx.he_decrypt(ct), self.n_out)

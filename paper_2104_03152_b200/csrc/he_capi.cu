@@ -1,0 +1,760 @@
+// he_capi.cu — the C-ABI of include/he_ckks.h: argument validation, status
+// codes, host<->device marshalling and the host-side slot layouts of the
+// composite ops (C17-C19).  All arithmetic is in he_ops.cu's kernels.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "he_ops.h"
+
+using namespace he;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+he_status guard(F&& f) {
+  try {
+    f();
+    return HE_OK;
+  } catch (const HeError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return HE_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HE_INVALID_ARGUMENT;
+  }
+}
+
+void need(bool ok, he_status code, const char* msg) {
+  if (!ok) throw HeError(code, msg);
+}
+void need_ctx(const he_context* c) { need(c != nullptr, HE_INVALID_ARGUMENT, "null context"); }
+void need_ct(he_context* c, const he_ciphertext* a) {
+  need(a != nullptr, HE_INVALID_ARGUMENT, "null ciphertext");
+  need(a->ctx == c, HE_PARAM_MISMATCH, "ciphertext belongs to another context");
+}
+void need_pt(he_context* c, const he_plaintext* a) {
+  need(a != nullptr, HE_INVALID_ARGUMENT, "null plaintext");
+  need(a->ctx == c, HE_PARAM_MISMATCH, "plaintext belongs to another context");
+}
+void need_batch(int a, int b) {
+  need(a == b || a == 1 || b == 1, HE_SHAPE_MISMATCH, "batch sizes differ (and neither is 1)");
+}
+void need_out(void* p) { need(p != nullptr, HE_INVALID_ARGUMENT, "null output pointer"); }
+
+double shifted(u64 q, int shift) { return (double)q * std::ldexp(1.0, shift); }
+
+// Upload host doubles into a device scratch buffer.
+struct DevDoubles {
+  he_context* c;
+  double* d;
+  DevDoubles(he_context* c_, const double* h, size_t n) : c(c_), d(dalloc_t<double>(c_, n)) {
+    if (n) HE_CK(cudaMemcpyAsync(d, h, n * 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  ~DevDoubles() { dfree(c, d); }
+};
+
+struct PtGuard {
+  he_plaintext* p = nullptr;
+  ~PtGuard() { pt_free(p); }
+};
+
+// C17 diagonals: D_k[j] = W[(j+k) mod n][j'], j' = j mod m (replicated output)
+// or j for j < m (zero beyond).
+std::vector<double> vecmat_diagonals(const double* W, int n, int m, int ns, bool rep) {
+  need(n >= 1 && m >= 1 && n <= ns && m <= ns, HE_SHAPE_MISMATCH, "vec_mat: n, m must be in [1, n_s]");
+  if (rep) need(ns % n == 0 && ns % m == 0, HE_SHAPE_MISMATCH, "replicated output needs n | n_s and m | n_s");
+  const int span = (ns / n) * n;
+  std::vector<double> D((size_t)n * ns, 0.0);
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < ns; ++j) {
+      const bool live = rep || j < m;
+      if (!live) continue;
+      if (ns % n && j + k >= span)
+        throw HeError(HE_REPLICATION_EXHAUSTED, "vec_mat: diagonal reads past the replicated span");
+      const int jp = rep ? j % m : j;
+      D[(size_t)k * ns + j] = W[(size_t)((j + k) % n) * m + jp];
+    }
+  return D;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* he_last_error(void) { return g_err.c_str(); }
+
+he_status he_context_create(const he_params* p, uint64_t seed, he_context** out) {
+  return guard([&] {
+    need(p != nullptr && out != nullptr && p->bits != nullptr, HE_INVALID_ARGUMENT, "null argument");
+    need(p->n_primes >= 1 && p->n_primes <= 64, HE_INVALID_PARAMS, "n_primes out of range");
+    const int L = p->n_primes - p->n_special;
+    need(p->dnum == 0 || p->dnum == L, HE_INVALID_PARAMS, "only dnum = L (one prime per digit) is supported");
+    HostParams hp;
+    try {
+      hp = make_params(p->log2N, std::vector<int>(p->bits, p->bits + p->n_primes), p->n_special);
+    } catch (const std::runtime_error& e) {
+      throw HeError(HE_INVALID_PARAMS, e.what());
+    }
+    he_context* c = new he_context();
+    try {
+      context_init(c, hp, seed);
+    } catch (...) {
+      context_destroy(c);
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+he_status he_context_free(he_context* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    context_destroy(ctx);
+    delete ctx;
+  });
+}
+
+he_status he_context_info(const he_context* c, int* log2N, int* L, int* K) {
+  return guard([&] {
+    need_ctx(c);
+    if (log2N) *log2N = c->logN;
+    if (L) *L = c->L;
+    if (K) *K = c->K;
+  });
+}
+
+he_status he_context_primes(const he_context* c, uint64_t* primes_out, uint64_t* psi_out) {
+  return guard([&] {
+    need_ctx(c);
+    for (int t = 0; t < c->NP; ++t) {
+      if (primes_out) primes_out[t] = c->hp.q[t];
+      if (psi_out) psi_out[t] = c->hp.psi[t];
+    }
+  });
+}
+
+he_status he_context_cdt(const he_context* c, uint64_t* table_out) {
+  return guard([&] {
+    need_ctx(c);
+    need_out(table_out);
+    for (size_t k = 0; k < c->hp.cdt.size(); ++k) table_out[k] = c->hp.cdt[k];
+  });
+}
+
+he_status he_set_stream(he_context* c, void* stream) {
+  return guard([&] {
+    need_ctx(c);
+    c->stream = (cudaStream_t)stream;
+  });
+}
+
+he_status he_sync(he_context* c) {
+  return guard([&] {
+    need_ctx(c);
+    HE_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+uint64_t he_launch_count(const he_context* c) { return c ? c->launches : 0; }
+
+he_status he_keygen(he_context* c, const int32_t* steps, size_t n_steps) {
+  return guard([&] {
+    need_ctx(c);
+    need(!c->has_sk, HE_INVALID_ARGUMENT, "keys already generated for this context");
+    need(n_steps == 0 || steps != nullptr, HE_INVALID_ARGUMENT, "null rotation steps");
+    std::vector<int> st;
+    for (size_t i = 0; i < n_steps; ++i) {
+      need(steps[i] != 0 && std::abs(steps[i]) <= c->N / 2, HE_INVALID_ROTATION,
+           "rotation steps must be nonzero with |step| <= n_s");
+      st.push_back(steps[i]);
+    }
+    need(c->K > 0 || n_steps == 0, HE_INVALID_PARAMS, "rotation keys need at least one special prime");
+    keygen(c, st);
+  });
+}
+
+he_status he_drop_secret_key(he_context* c) {
+  return guard([&] {
+    need_ctx(c);
+    if (c->d_sk) {
+      HE_CK(cudaStreamSynchronize(c->stream));
+      cudaFree(c->d_sk);
+    }
+    c->d_sk = nullptr;
+    c->has_sk = false;
+  });
+}
+
+// ---------------------------------------------------------------- encode ---
+static void encode_common(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
+                          he_plaintext** out) {
+  need_ctx(c);
+  need_out(out);
+  need(B >= 1, HE_INVALID_ARGUMENT, "B must be >= 1");
+  need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+  need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
+  need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
+  *out = encode(c, z_dev, n, B, scale, level);
+}
+
+he_status he_encode(he_context* c, const double* z, size_t n, size_t B, double scale, int level,
+                    he_plaintext** out) {
+  return guard([&] {
+    need_ctx(c);
+    need(z != nullptr || n == 0, HE_INVALID_ARGUMENT, "null input");
+    DevDoubles d(c, z, n * B);
+    encode_common(c, d.d, n, B, scale, level, out);
+  });
+}
+
+he_status he_encode_device(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
+                           he_plaintext** out) {
+  return guard([&] { encode_common(c, z_dev, n, B, scale, level, out); });
+}
+
+he_status he_decode(he_context* c, const he_plaintext* pt, double* out, size_t n) {
+  return guard([&] {
+    need_ctx(c);
+    need_pt(c, pt);
+    need_out(out);
+    need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+    Scratch d(c, std::max<size_t>(1, (size_t)pt->B * n) * 8);
+    decode(c, pt, d.as<double>(), n);
+    HE_CK(cudaMemcpyAsync(out, d.p, (size_t)pt->B * n * 8, cudaMemcpyDeviceToHost, c->stream));
+    HE_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+he_status he_decode_device(he_context* c, const he_plaintext* pt, double* out_dev, size_t n) {
+  return guard([&] {
+    need_ctx(c);
+    need_pt(c, pt);
+    need_out(out_dev);
+    need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+    decode(c, pt, out_dev, n);
+  });
+}
+
+// -------------------------------------------------------- encrypt/decrypt ---
+he_status he_encrypt(he_context* c, const he_plaintext* pt, uint64_t stream_id, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c);
+    need_pt(c, pt);
+    need_out(out);
+    need(c->has_pk, HE_MISSING_KEY, "no public key (call he_keygen)");
+    *out = encrypt(c, pt, stream_id);
+  });
+}
+
+he_status he_decrypt(he_context* c, const he_ciphertext* ct, he_plaintext** out) {
+  return guard([&] {
+    need_ctx(c);
+    need_ct(c, ct);
+    need_out(out);
+    need(c->has_sk, HE_MISSING_KEY, "no secret key");
+    *out = decrypt(c, ct);
+  });
+}
+
+// ------------------------------------------------------------- arithmetic ---
+static void need_same(const he_ciphertext* a, const he_ciphertext* b, bool scale_too) {
+  need(a->level == b->level, HE_LEVEL_MISMATCH, "ciphertext levels differ");
+  need(a->size == b->size, HE_SHAPE_MISMATCH, "ciphertext sizes differ");
+  if (scale_too) need(a->scale == b->scale, HE_SCALE_MISMATCH, "ciphertext scales differ");
+  need_batch(a->B, b->B);
+}
+
+he_status he_add(he_context* c, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_ct(c, b); need_out(out);
+    need_same(a, b, true);
+    *out = ct_binop(c, 0, a, b);
+  });
+}
+
+he_status he_sub(he_context* c, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_ct(c, b); need_out(out);
+    need_same(a, b, true);
+    *out = ct_binop(c, 1, a, b);
+  });
+}
+
+he_status he_negate(he_context* c, const he_ciphertext* a, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    *out = ct_negate(c, a);
+  });
+}
+
+he_status he_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_pt(c, p); need_out(out);
+    need(a->level == p->level, HE_LEVEL_MISMATCH, "levels differ");
+    need(a->scale == p->scale, HE_SCALE_MISMATCH, "scales differ");
+    need_batch(a->B, p->B);
+    *out = ct_add_plain(c, a, p);
+  });
+}
+
+he_status he_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_pt(c, p); need_out(out);
+    need(a->level == p->level, HE_LEVEL_MISMATCH, "levels differ");
+    need_batch(a->B, p->B);
+    *out = ct_mul_plain(c, a, p);
+  });
+}
+
+he_status he_mul(he_context* c, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_ct(c, b); need_out(out);
+    need(a->size == 2 && b->size == 2, HE_SHAPE_MISMATCH, "mul needs size-2 ciphertexts");
+    need_same(a, b, false);
+    *out = ct_tensor(c, a, b);
+  });
+}
+
+he_status he_relinearize(he_context* c, const he_ciphertext* a, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    need(a->size == 3, HE_SHAPE_MISMATCH, "relinearize needs a size-3 ciphertext");
+    need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
+    *out = ct_relinearize(c, a);
+  });
+}
+
+he_status he_rescale(he_context* c, const he_ciphertext* a, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    need(a->level >= 1, HE_LEVEL_EXHAUSTED, "rescale at level 0");
+    *out = ct_rescale(c, a);
+  });
+}
+
+he_status he_square(he_context* c, const he_ciphertext* a, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    need(a->size == 2, HE_SHAPE_MISMATCH, "square needs a size-2 ciphertext");
+    need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
+    need(a->level >= 1, HE_LEVEL_EXHAUSTED, "square needs a level to rescale");
+    he_ciphertext* t = ct_tensor(c, a, a);
+    he_ciphertext* r = nullptr;
+    try {
+      r = ct_relinearize(c, t);
+    } catch (...) {
+      ct_free(t);
+      throw;
+    }
+    ct_free(t);
+    try {
+      *out = ct_rescale(c, r);
+    } catch (...) {
+      ct_free(r);
+      throw;
+    }
+    ct_free(r);
+  });
+}
+
+he_status he_rotate(he_context* c, const he_ciphertext* a, int32_t k, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    need(a->size == 2, HE_SHAPE_MISMATCH, "rotate needs a size-2 ciphertext");
+    const int ns = c->N / 2;
+    need(std::abs(k) <= ns, HE_INVALID_ROTATION, "|k| must be <= n_s");
+    u32 g;
+    if (k % ns == 0 && !galois_key(c, k == 0 ? ns : k, &g)) {  // identity without a key: copy
+      he_ciphertext* o = ct_new(c, a->B, a->size, a->level, a->scale);
+      HE_CK(cudaMemcpyAsync(o->d, a->d, ct_words(a) * 8, cudaMemcpyDeviceToDevice, c->stream));
+      *out = o;
+      return;
+    }
+    *out = ct_rotate(c, a, k, false);
+  });
+}
+
+// ------------------------------------------------------------- composite ---
+he_status he_im2col_encode(const double* img, int H, int W, int kh, int kw, int stride, size_t n_slots,
+                           double* slots_out, int* windows, int* chunk) {
+  return guard([&] {
+    need(img && slots_out, HE_INVALID_ARGUMENT, "null argument");
+    need(H >= kh && W >= kw && kh > 0 && kw > 0 && stride > 0, HE_SHAPE_MISMATCH, "bad conv geometry");
+    const ConvGeom g = conv_geometry(H, W, kh, kw, stride);
+    need((size_t)kh * kw * g.chunk <= n_slots, HE_LAYOUT_MISMATCH, "im2col matrix does not fit the slots");
+    std::fill(slots_out, slots_out + n_slots, 0.0);
+    for (int r = 0; r < g.oh; ++r)
+      for (int cc = 0; cc < g.ow; ++cc) {
+        const int w = r * g.ow + cc;
+        for (int a = 0; a < kh; ++a)
+          for (int b = 0; b < kw; ++b)
+            slots_out[(size_t)(a * kw + b) * g.chunk + w] = img[(size_t)(r * stride + a) * W + cc * stride + b];
+      }
+    if (windows) *windows = g.windows;
+    if (chunk) *chunk = g.chunk;
+  });
+}
+
+static void conv_checks(he_context* c, const he_ciphertext* ct, int C, int taps, int chunk) {
+  const int ns = c->N / 2;
+  need(ct->size == 2, HE_SHAPE_MISMATCH, "conv needs a size-2 ciphertext");
+  need(ct->level >= 2, HE_LEVEL_EXHAUSTED, "conv consumes two levels");
+  need(C >= 1, HE_SHAPE_MISMATCH, "need at least one channel");
+  need(chunk >= 1 && (chunk & (chunk - 1)) == 0 && chunk <= ns && ns % chunk == 0, HE_LAYOUT_MISMATCH,
+       "chunk must be a power of two dividing n_s");
+  need((size_t)taps * chunk <= (size_t)ns, HE_LAYOUT_MISMATCH, "taps x chunk exceeds the slots");
+  need(c->has_rlk || true, HE_MISSING_KEY, "");
+}
+
+he_status he_im2col_conv_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* kernels,
+                            const he_plaintext* masks, const he_plaintext* bias, int chunk, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_pt(c, kernels); need_pt(c, masks); need_out(out);
+    conv_checks(c, ct, kernels->B, 1, chunk);
+    need(masks->B == kernels->B, HE_SHAPE_MISMATCH, "one mask per kernel");
+    need(kernels->level == ct->level && masks->level == ct->level - 1, HE_LEVEL_MISMATCH,
+         "kernels at the input level, masks one below");
+    if (bias) {
+      need_pt(c, bias);
+      need(bias->B == 1, HE_SHAPE_MISMATCH, "bias is one plaintext");
+      need(bias->level == ct->level - 2, HE_LEVEL_MISMATCH, "bias at the output level");
+      const double s1 = ct->scale * kernels->scale / (double)c->hp.q[ct->level];
+      const double s2 = s1 * masks->scale / (double)c->hp.q[ct->level - 1];
+      need(bias->scale == s2, HE_SCALE_MISMATCH, "bias scale must equal the output scale");
+    }
+    for (int step = chunk; step < c->N / 2; step <<= 1) {
+      u32 g;
+      need(galois_key(c, step, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
+    }
+    *out = ct_conv(c, ct, kernels, masks, bias, chunk);
+  });
+}
+
+// C18/C19 plaintexts of the conv: kernels at q_l 2^kernel_shift (level l),
+// masks at q_{l-1} 2^mask_shift (level l-1), bias at the output scale (l-2).
+static void conv_encode(he_context* c, const double* kernels, int C, int kh, int kw, const double* bias,
+                        int chunk, int kernel_shift, int mask_shift, int l, double in_scale,
+                        he_plaintext** kp, he_plaintext** mp, he_plaintext** bp) {
+  const int ns = c->N / 2, taps = kh * kw;
+  need(kernels != nullptr, HE_INVALID_ARGUMENT, "null kernels");
+  need(l >= 2 && l < c->L, HE_LEVEL_EXHAUSTED, "conv consumes two levels");
+  need(C >= 1 && taps >= 1, HE_SHAPE_MISMATCH, "need at least one channel and tap");
+  need(chunk >= 1 && (chunk & (chunk - 1)) == 0 && ns % chunk == 0, HE_LAYOUT_MISMATCH,
+       "chunk must be a power of two dividing n_s");
+  need((size_t)taps * chunk <= (size_t)ns, HE_LAYOUT_MISMATCH, "taps x chunk exceeds the slots");
+  std::vector<double> K((size_t)C * ns, 0.0), M((size_t)C * ns, 0.0);
+  for (int ch = 0; ch < C; ++ch) {
+    for (int t = 0; t < taps; ++t)
+      for (int w = 0; w < chunk; ++w) K[(size_t)ch * ns + (size_t)t * chunk + w] = kernels[(size_t)ch * taps + t];
+    for (int s = 0; s < ns; ++s) M[(size_t)ch * ns + s] = ((s / chunk) % C == ch) ? 1.0 : 0.0;
+  }
+  PtGuard pk, pm, pb;
+  {
+    DevDoubles d(c, K.data(), K.size());
+    pk.p = encode(c, d.d, ns, C, shifted(c->hp.q[l], kernel_shift), l);
+  }
+  {
+    DevDoubles d(c, M.data(), M.size());
+    pm.p = encode(c, d.d, ns, C, shifted(c->hp.q[l - 1], mask_shift), l - 1);
+  }
+  if (bias) {
+    std::vector<double> bs(ns);
+    for (int s = 0; s < ns; ++s) bs[s] = bias[(s / chunk) % C];
+    const double s1 = in_scale * pk.p->scale / (double)c->hp.q[l];
+    const double s2 = s1 * pm.p->scale / (double)c->hp.q[l - 1];
+    DevDoubles d(c, bs.data(), bs.size());
+    pb.p = encode(c, d.d, ns, 1, s2, l - 2);
+  }
+  *kp = pk.p;
+  *mp = pm.p;
+  *bp = pb.p;
+  pk.p = pm.p = pb.p = nullptr;
+}
+
+he_status he_im2col_conv_encode(he_context* c, const double* kernels, int C, int kh, int kw, const double* bias,
+                                int chunk, int kernel_shift, int mask_shift, int level, double in_scale,
+                                he_plaintext** kp, he_plaintext** mp, he_plaintext** bp) {
+  return guard([&] {
+    need_ctx(c);
+    need(kp && mp && bp, HE_INVALID_ARGUMENT, "null output pointer");
+    conv_encode(c, kernels, C, kh, kw, bias, chunk, kernel_shift, mask_shift, level, in_scale, kp, mp, bp);
+  });
+}
+
+he_status he_im2col_conv(he_context* c, const he_ciphertext* ct, const double* kernels, int C, int kh, int kw,
+                         const double* bias, int chunk, int kernel_shift, int mask_shift, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(out);
+    conv_checks(c, ct, C, kh * kw, chunk);
+    for (int step = chunk; step < c->N / 2; step <<= 1) {
+      u32 g;
+      need(galois_key(c, step, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
+    }
+    PtGuard pk, pm, pb;
+    conv_encode(c, kernels, C, kh, kw, bias, chunk, kernel_shift, mask_shift, ct->level, ct->scale, &pk.p, &pm.p,
+                &pb.p);
+    *out = ct_conv(c, ct, pk.p, pm.p, pb.p, chunk);
+  });
+}
+
+he_status he_vec_mat_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags,
+                        const he_plaintext* bias_pt, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_pt(c, diags); need_out(out);
+    need(ct->size == 2, HE_SHAPE_MISMATCH, "vec_mat needs a size-2 ciphertext");
+    need(ct->level >= 1, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
+    need(diags->level == ct->level, HE_LEVEL_MISMATCH, "diagonals must be at the ciphertext level");
+    need(diags->B >= 1 && diags->B <= c->N / 2, HE_SHAPE_MISMATCH, "1 <= n <= n_s diagonals");
+    if (bias_pt) {
+      need_pt(c, bias_pt);
+      need(bias_pt->B == 1, HE_SHAPE_MISMATCH, "bias is one plaintext");
+      need(bias_pt->level == ct->level - 1, HE_LEVEL_MISMATCH, "bias at the rescaled level");
+      need(bias_pt->scale == ct->scale * diags->scale / (double)c->hp.q[ct->level], HE_SCALE_MISMATCH,
+           "bias scale must equal the output scale");
+    }
+    *out = ct_vec_mat(c, ct, diags, bias_pt);
+  });
+}
+
+static void vecmat_encode(he_context* c, const double* W, int n, int m, const double* bias, int replicate_out,
+                          int pt_scale_shift, int l, double in_scale, he_plaintext** dp, he_plaintext** bp) {
+  need(W != nullptr, HE_INVALID_ARGUMENT, "null matrix");
+  need(l >= 1 && l < c->L, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
+  const int ns = c->N / 2;
+  std::vector<double> D = vecmat_diagonals(W, n, m, ns, replicate_out != 0);
+  PtGuard pd, pb;
+  {
+    DevDoubles d(c, D.data(), D.size());
+    pd.p = encode(c, d.d, ns, n, shifted(c->hp.q[l], -pt_scale_shift), l);
+  }
+  if (bias) {
+    std::vector<double> bs(ns, 0.0);
+    for (int j = 0; j < ns; ++j)
+      if (replicate_out) bs[j] = bias[j % m];
+      else if (j < m) bs[j] = bias[j];
+    const double s = in_scale * pd.p->scale / (double)c->hp.q[l];
+    DevDoubles d(c, bs.data(), bs.size());
+    pb.p = encode(c, d.d, ns, 1, s, l - 1);
+  }
+  *dp = pd.p;
+  *bp = pb.p;
+  pd.p = pb.p = nullptr;
+}
+
+he_status he_vec_mat_encode(he_context* c, const double* W, int n, int m, const double* bias, int replicate_out,
+                            int pt_scale_shift, int level, double in_scale, he_plaintext** diags,
+                            he_plaintext** bias_pt) {
+  return guard([&] {
+    need_ctx(c);
+    need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
+    vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, level, in_scale, diags, bias_pt);
+  });
+}
+
+he_status he_vec_mat(he_context* c, const he_ciphertext* ct, const double* W, int n, int m, const double* bias,
+                     int replicate_out, int pt_scale_shift, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(out);
+    need(ct->size == 2, HE_SHAPE_MISMATCH, "vec_mat needs a size-2 ciphertext");
+    need(ct->level >= 1, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
+    for (int k = 1; k < n; ++k) {
+      u32 g;
+      need(galois_key(c, k, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a diagonal rotation");
+    }
+    PtGuard pd, pb;
+    vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, ct->level, ct->scale, &pd.p, &pb.p);
+    *out = ct_vec_mat(c, ct, pd.p, pb.p);
+  });
+}
+
+// ------------------------------------------------------ handles / words ---
+he_status he_free_plaintext(he_plaintext* pt) {
+  return guard([&] { pt_free(pt); });
+}
+he_status he_free_ciphertext(he_ciphertext* ct) {
+  return guard([&] { ct_free(ct); });
+}
+
+he_status he_ct_info(const he_ciphertext* ct, size_t* B, int* size, int* level, double* scale) {
+  return guard([&] {
+    need(ct != nullptr, HE_INVALID_ARGUMENT, "null ciphertext");
+    if (B) *B = ct->B;
+    if (size) *size = ct->size;
+    if (level) *level = ct->level;
+    if (scale) *scale = ct->scale;
+  });
+}
+
+he_status he_pt_info(const he_plaintext* pt, size_t* B, int* level, double* scale) {
+  return guard([&] {
+    need(pt != nullptr, HE_INVALID_ARGUMENT, "null plaintext");
+    if (B) *B = pt->B;
+    if (level) *level = pt->level;
+    if (scale) *scale = pt->scale;
+  });
+}
+
+he_status he_ct_device_ptr(const he_ciphertext* ct, uint64_t** words) {
+  return guard([&] {
+    need(ct && words, HE_INVALID_ARGUMENT, "null argument");
+    *words = ct->d;
+  });
+}
+
+he_status he_pt_device_ptr(const he_plaintext* pt, uint64_t** words) {
+  return guard([&] {
+    need(pt && words, HE_INVALID_ARGUMENT, "null argument");
+    *words = pt->d;
+  });
+}
+
+static void copy_out(he_context* c, const u64* src, size_t words, uint64_t* dst, int on_device) {
+  HE_CK(cudaMemcpyAsync(dst, src, words * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        c->stream));
+  if (!on_device) HE_CK(cudaStreamSynchronize(c->stream));
+}
+
+he_status he_ct_export_words(he_context* c, const he_ciphertext* ct, uint64_t* dst, int on_device) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(dst);
+    copy_out(c, ct->d, ct_words(ct), dst, on_device);
+  });
+}
+
+he_status he_pt_export_words(he_context* c, const he_plaintext* pt, uint64_t* dst, int on_device) {
+  return guard([&] {
+    need_ctx(c); need_pt(c, pt); need_out(dst);
+    copy_out(c, pt->d, pt_words(pt), dst, on_device);
+  });
+}
+
+he_status he_ct_import_words(he_context* c, const uint64_t* src, int on_device, size_t B, int size, int level,
+                             double scale, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_out(out);
+    need(src != nullptr && B >= 1, HE_INVALID_ARGUMENT, "bad source");
+    need(size == 2 || size == 3, HE_SHAPE_MISMATCH, "size must be 2 or 3");
+    need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
+    he_ciphertext* ct = ct_new(c, (int)B, size, level, scale);
+    try {
+      HE_CK(cudaMemcpyAsync(ct->d, src, ct_words(ct) * 8,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+      need(!check_words(c, ct->d, B * size, level + 1), HE_INVALID_ARGUMENT, "word not reduced mod its prime");
+    } catch (...) {
+      ct_free(ct);
+      throw;
+    }
+    *out = ct;
+  });
+}
+
+he_status he_pt_import_words(he_context* c, const uint64_t* src, int on_device, size_t B, int level, double scale,
+                             he_plaintext** out) {
+  return guard([&] {
+    need_ctx(c); need_out(out);
+    need(src != nullptr && B >= 1, HE_INVALID_ARGUMENT, "bad source");
+    need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
+    he_plaintext* pt = pt_new(c, (int)B, level, scale);
+    try {
+      HE_CK(cudaMemcpyAsync(pt->d, src, pt_words(pt) * 8,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+      need(!check_words(c, pt->d, B, level + 1), HE_INVALID_ARGUMENT, "word not reduced mod its prime");
+    } catch (...) {
+      pt_free(pt);
+      throw;
+    }
+    *out = pt;
+  });
+}
+
+he_status he_pt_from_int_coeffs(he_context* c, const int64_t* m, size_t B, double scale, int level,
+                                he_plaintext** out) {
+  return guard([&] {
+    need_ctx(c); need_out(out);
+    need(m != nullptr && B >= 1, HE_INVALID_ARGUMENT, "bad source");
+    need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
+    Scratch d(c, B * c->N * 8);
+    HE_CK(cudaMemcpyAsync(d.p, m, B * c->N * 8, cudaMemcpyHostToDevice, c->stream));
+    *out = pt_from_int(c, d.as<i64>(), B, scale, level);
+  });
+}
+
+size_t he_key_words(const he_context* c, int kind) {
+  if (!c) return 0;
+  const size_t N = c->N;
+  switch (kind) {
+    case 0: return (size_t)c->NP * N;
+    case 1: return (size_t)2 * c->L * N;
+    case 2:
+    case 3: return (size_t)c->L * 2 * c->NP * N;
+    default: return 0;
+  }
+}
+
+he_status he_key_export(he_context* c, int kind, int32_t step, uint64_t* dst) {
+  return guard([&] {
+    need_ctx(c); need_out(dst);
+    const u64* src = nullptr;
+    switch (kind) {
+      case 0: src = c->d_sk; break;
+      case 1: src = c->d_pk; break;
+      case 2: src = c->d_rlk; break;
+      case 3: {
+        u32 g;
+        src = galois_key(c, step, &g);
+        need(src != nullptr, HE_MISSING_GALOIS_KEY, "no Galois key for that step");
+        break;
+      }
+      default: throw HeError(HE_INVALID_ARGUMENT, "unknown key kind");
+    }
+    need(src != nullptr, HE_MISSING_KEY, "key not present");
+    copy_out(c, src, he_key_words(c, kind), dst, 0);
+  });
+}
+
+// ------------------------------------------------------------ ring prims ---
+static void ring_checks(he_context* c, const void* p, size_t B, int nl) {
+  need_ctx(c);
+  need(p != nullptr, HE_INVALID_ARGUMENT, "null buffer");
+  need(B >= 1 && nl >= 1 && nl <= c->NP, HE_SHAPE_MISMATCH, "bad batch / limb count");
+  need(B * nl < (1u << 31), HE_SHAPE_MISMATCH, "too many limbs in one call");
+}
+
+he_status he_ntt_forward(he_context* c, uint64_t* d, size_t B, int nl) {
+  return guard([&] {
+    ring_checks(c, d, B, nl);
+    ntt_rows(c, d, d, B, nl, (size_t)nl * c->N, (size_t)nl * c->N, false);
+  });
+}
+
+he_status he_ntt_inverse(he_context* c, uint64_t* d, size_t B, int nl) {
+  return guard([&] {
+    ring_checks(c, d, B, nl);
+    ntt_rows(c, d, d, B, nl, (size_t)nl * c->N, (size_t)nl * c->N, true);
+  });
+}
+
+he_status he_modmul(he_context* c, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t B, int nl) {
+  return guard([&] {
+    ring_checks(c, a, B, nl);
+    need(b && out, HE_INVALID_ARGUMENT, "null buffer");
+    modmul_rows(c, a, b, out, B, nl);
+  });
+}
+
+he_status he_ntt_mul_intt(he_context* c, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t B, int nl) {
+  return guard([&] {
+    ring_checks(c, a, B, nl);
+    need(b && out, HE_INVALID_ARGUMENT, "null buffer");
+    ring_mul(c, a, b, out, B, nl);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// he_internal.cuh — context / handle structs and launch helpers shared by the
+// kernel translation units of the B200 CKKS library.  Product code.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/he_ckks.h"
+#include "he_common.cuh"
+#include "he_host.h"
+#include "he_ntt.cuh"
+
+namespace he {
+
+struct HeError : std::runtime_error {
+  he_status code;
+  HeError(he_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define HE_CK(call)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::he::HeError(e_ == cudaErrorMemoryAllocation ? HE_OUT_OF_MEMORY : HE_CUDA_ERROR, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+}  // namespace he
+
+struct he_context {
+  he::HostParams hp;
+  int logN = 0, N = 0, L = 0, K = 0, NP = 0;
+  uint64_t seed = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // device tables
+  he::PrimeD* d_primes = nullptr;
+  he::u64 *d_tw = nullptr, *d_twsh = nullptr, *d_itw = nullptr, *d_itwsh = nullptr;
+  he::u64* d_cdt = nullptr;
+  he::u64 *d_P_mod = nullptr, *d_Pinv_mod = nullptr, *d_Ph_mod = nullptr;
+  he::u64 *d_Phat_inv = nullptr, *d_Phat_mod = nullptr;
+  he::u64 *d_rs_qinv = nullptr, *d_rs_h = nullptr, *d_crt = nullptr;
+  he::u64* d_q = nullptr;
+  int* d_slot_index = nullptr;
+  double *d_fft_w = nullptr, *d_zeta = nullptr;
+  // keys (NTT words)
+  bool has_sk = false, has_pk = false, has_rlk = false;
+  he::u64* d_sk = nullptr;   // [NP][N]
+  he::u64* d_pk = nullptr;   // [2][L][N]
+  he::u64* d_rlk = nullptr;  // [L][2][NP][N]
+  std::map<he::u64, he::u64*> gk;  // Galois element -> [L][2][NP][N]
+  std::vector<void*> owned;        // device allocations freed with the context
+};
+
+struct he_ciphertext {
+  he_context* ctx;
+  int B, size, level;
+  double scale;
+  he::u64* d;  // [B][size][level+1][N]
+};
+
+struct he_plaintext {
+  he_context* ctx;
+  int B, level;
+  double scale;
+  he::u64* d;  // [B][level+1][N]
+};
+
+namespace he {
+
+// ---- memory (stream-ordered pool on the context stream) -----------------
+void* dalloc(he_context* c, size_t bytes);
+void dfree(he_context* c, void* p);
+template <class T>
+T* dalloc_t(he_context* c, size_t n) { return (T*)dalloc(c, n * sizeof(T)); }
+
+// RAII scratch buffer
+struct Scratch {
+  he_context* c;
+  void* p;
+  Scratch(he_context* c_, size_t bytes) : c(c_), p(dalloc(c_, bytes)) {}
+  ~Scratch() { dfree(c, p); }
+  template <class T> T* as() const { return (T*)p; }
+};
+
+inline void check_launch(he_context* c) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw HeError(HE_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+// ---- NTT launch with per-instantiation smem opt-in -----------------------
+template <int LOGN, int CL, bool INV, class Job>
+void launch_ntt_t(he_context* c, const Job& job, int nblk) {
+  typedef NttGeom<LOGN, CL> G;
+  static bool configured = false;
+  auto kern = k_ntt<LOGN, CL, INV, Job>;
+  if (!configured) {
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+    if (CL == 2) HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  if (nblk <= 0) return;
+  const u64* tw = INV ? c->d_itw : c->d_tw;
+  const u64* twsh = INV ? c->d_itwsh : c->d_twsh;
+  if (CL == 1) {
+    kern<<<nblk, G::T, G::SMEM, c->stream>>>(job, c->d_primes, tw, twsh);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk * CL);
+    cfg.blockDim = dim3(G::T);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HE_CK(cudaLaunchKernelEx(&cfg, kern, job, (const PrimeD*)c->d_primes, tw, twsh));
+  }
+  check_launch(c);
+}
+
+template <bool INV, class Job>
+void launch_ntt(he_context* c, const Job& job, int nblk) {
+  switch (c->logN) {
+    case 10: launch_ntt_t<10, 1, INV>(c, job, nblk); break;
+    case 11: launch_ntt_t<11, 1, INV>(c, job, nblk); break;
+    case 12: launch_ntt_t<12, 1, INV>(c, job, nblk); break;
+    case 13: launch_ntt_t<13, 1, INV>(c, job, nblk); break;
+    case 14: launch_ntt_t<14, 1, INV>(c, job, nblk); break;
+    case 15: launch_ntt_t<15, 2, INV>(c, job, nblk); break;
+    default: throw HeError(HE_INVALID_PARAMS, "unsupported log2N");
+  }
+}
+
+// Grid for row-wise pointwise kernels: x covers N, y covers rows.
+inline dim3 rows_grid(he_context* c, size_t rows, int threads = 256) {
+  unsigned gx = (unsigned)((c->N + threads - 1) / threads);
+  unsigned gy = (unsigned)std::min<size_t>(rows, 65535);
+  return dim3(gx, gy ? gy : 1);
+}
+
+}  // namespace he

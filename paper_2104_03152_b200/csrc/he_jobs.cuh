@@ -1,0 +1,229 @@
+// he_jobs.cuh — load/store functors that fuse each CKKS step into the NTT
+// kernels of he_ntt.cuh (SURVEY.md §8(a) kernels K1-K7).  Product code.
+#pragma once
+#include "he_common.cuh"
+
+namespace he {
+
+// Plain transform of limbs: blk -> (item = blk / nl, limb = blk % nl), limb l
+// modulo prime l; items at strides src_bs / dst_bs words.
+struct JobLimbs {
+  const u64* src;
+  u64* dst;
+  int N, nl;
+  size_t src_bs, dst_bs;
+  __device__ int prime(int blk) const { return blk % nl; }
+  __device__ u64 load(int blk, u32 i, const PrimeD&) const {
+    return src[(size_t)(blk / nl) * src_bs + (size_t)(blk % nl) * N + i];
+  }
+  __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
+    dst[(size_t)(blk / nl) * dst_bs + (size_t)(blk % nl) * N + i] = v;
+  }
+};
+
+// Fused ring product out = INTT(NTT(a) (.) b) (config 2 "fwd -> modmul -> inv").
+struct JobRingMul {
+  const u64* a;
+  const u64* b;
+  u64* out;
+  int N, nl;
+  __device__ int prime(int blk) const { return blk % nl; }
+  __device__ u64 load(int blk, u32 i, const PrimeD&) const { return a[(size_t)blk * N + i]; }
+  __device__ u64 factor(int blk, u32 i, const PrimeD&) const { return b[(size_t)blk * N + i]; }
+  __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const { out[(size_t)blk * N + i] = v; }
+};
+
+// Signed small polynomials -> NTT words (encode injection, encryption noise,
+// key generation): blk -> (item = blk / nl, limb = blk % nl); reads
+// poly[item * src_bs + i] (int64), writes dst[item * dst_bs + limb * N + i].
+struct JobSignedToNtt {
+  const i64* poly;
+  u64* dst;
+  int N, nl;
+  size_t src_bs, dst_bs;
+  __device__ int prime(int blk) const { return blk % nl; }
+  __device__ u64 load(int blk, u32 i, const PrimeD& P) const {
+    return from_signed(poly[(size_t)(blk / nl) * src_bs + i], P);
+  }
+  __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
+    dst[(size_t)(blk / nl) * dst_bs + (size_t)(blk % nl) * N + i] = v;
+  }
+};
+
+// ModUp (a9, first half): digit j's coefficient residues [d]_{q_j} (already
+// INTT'd), centered lift (C16) into target t != j, NTT_t.
+//   coef: [B][Lc][N]; ext: [B][Lc][Lc+K][N] (t < Lc data, t >= Lc special).
+struct JobModUp {
+  const u64* coef;
+  u64* ext;
+  const u64* qtab;   // device table of all primes
+  int N, Lc, K, L;
+  __device__ void dec(int blk, int& b, int& j, int& t) const {
+    const int nt = Lc + K - 1;
+    b = blk / (Lc * nt);
+    const int r = blk % (Lc * nt);
+    j = r / nt;
+    const int tt = r % nt;
+    t = tt < j ? tt : tt + 1;
+  }
+  __device__ int prime(int blk) const {
+    int b, j, t;
+    dec(blk, b, j, t);
+    return t < Lc ? t : L + (t - Lc);
+  }
+  __device__ u64 load(int blk, u32 i, const PrimeD& P) const {
+    int b, j, t;
+    dec(blk, b, j, t);
+    return lift_centered(coef[((size_t)b * Lc + j) * N + i], __ldg(qtab + j), P);
+  }
+  __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
+    int b, j, t;
+    dec(blk, b, j, t);
+    ext[(((size_t)b * Lc + j) * (Lc + K) + t) * N + i] = v;
+  }
+};
+
+constexpr int KS_KB_MAX = 32;
+
+// Everything the key-switch inner product + ModDown jobs need (a9/a10, C15).
+struct KsArgs {
+  int N, logN, Lc, L, K, NP, B, KB;
+  const u64* ext;          // [B][Lc][Lc+K][N]
+  const u64* dsrc;         // digit source (NTT words): item b at dsrc + b*dsrc_bs, limb j at +j*N
+  size_t dsrc_bs;
+  const u64* keys[KS_KB_MAX];  // per rotation of this launch: [L][2][NP][N]
+  u32 gal[KS_KB_MAX];          // Galois element per rotation (1 = identity)
+  u64* tb;                 // [KB][B][2][K][N] ModDown intermediates (coefficient domain)
+  const u64* Ph_mod;       // floor(P/2) mod q_t  [NP]
+  const u64* Pinv_mod;     // P^{-1} mod q_i     [NP]
+  const u64* Phat_inv;     // (P/p_k)^{-1} mod p_k [K]
+  const u64* Phat_mod;     // (P/p_k) mod q_t   [K][NP]
+  // epilogue (KsData only): out_p = acc_in_p[n] + D (.) (u_p + [p < add_parts] addsrc_p[pi?(n)])
+  u64* out;                // item b at out + kk*out_ks + b*out_bs + p*Lc*N + i*N
+  size_t out_bs, out_ks;
+  const u64* acc_in;       // nullable, same strides as out (may alias out)
+  const u64* addsrc;       // nullable, item stride add_bs
+  size_t add_bs;
+  int add_parts;           // 0, 1 or 2
+  int add_gather;          // apply pi_g to the addsrc index
+  const u64* D;            // nullable plaintext factor: D + kk*D_ks + i*N
+  size_t D_ks;
+};
+
+// Inner product over digits at target limb t for source position sn.
+__device__ __forceinline__ u64 ks_inner(const KsArgs& a, int kk, int b, int part, int t, int tprime,
+                                        u32 sn, u32 n, const PrimeD& P) {
+  const u64* key = a.keys[kk];
+  u64 acc = 0;
+  for (int j = 0; j < a.Lc; ++j) {
+    const u64 x = (t == j) ? a.dsrc[(size_t)b * a.dsrc_bs + (size_t)j * a.N + sn]
+                           : a.ext[(((size_t)b * a.Lc + j) * (a.Lc + a.K) + t) * a.N + sn];
+    const u64 k = key[(((size_t)j * 2 + part) * a.NP + tprime) * a.N + n];
+    acc = add_mod(acc, mul_mod(x, k, P), P.q);
+  }
+  return acc;
+}
+
+// a9 special limbs: inner product at p_k, INTT, then
+// tb = [ (x + [P/2]_{p_k}) (P/p_k)^{-1} ]_{p_k}    (C15 y_k and its CRT weight)
+struct JobKsSpecial {
+  KsArgs a;
+  __device__ void dec(int blk, int& kk, int& b, int& part, int& k) const {
+    k = blk % a.K;
+    int r = blk / a.K;
+    part = r & 1;
+    r >>= 1;
+    b = r % a.B;
+    kk = r / a.B;
+  }
+  __device__ int prime(int blk) const { return a.L + blk % a.K; }
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
+    int kk, b, part, k;
+    dec(blk, kk, b, part, k);
+    const u32 g = a.gal[kk];
+    const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
+    return ks_inner(a, kk, b, part, a.Lc + k, a.L + k, sn, n, P);
+  }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
+    int kk, b, part, k;
+    dec(blk, kk, b, part, k);
+    const u64 y = add_mod(v, __ldg(a.Ph_mod + a.L + k), P.q);
+    a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n] = mul_mod(y, __ldg(a.Phat_inv + k), P);
+  }
+};
+
+// a9 data limbs: conv_i = sum_k tb_k [P/p_k]_{q_i} (coefficient domain), NTT,
+// then u = (IP_i + [P/2]_{q_i} - NTT(conv_i)) P^{-1} and the epilogue.
+struct JobKsData {
+  KsArgs a;
+  __device__ void dec(int blk, int& kk, int& b, int& part, int& i) const {
+    i = blk % a.Lc;
+    int r = blk / a.Lc;
+    part = r & 1;
+    r >>= 1;
+    b = r % a.B;
+    kk = r / a.B;
+  }
+  __device__ int prime(int blk) const { return blk % a.Lc; }
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
+    int kk, b, part, i;
+    dec(blk, kk, b, part, i);
+    u64 conv = 0;
+    for (int k = 0; k < a.K; ++k) {
+      const u64 t = a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n];
+      conv = add_mod(conv, mul_mod(reduce64(t, P), __ldg(a.Phat_mod + (size_t)k * a.NP + i), P), P.q);
+    }
+    return conv;
+  }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
+    int kk, b, part, i;
+    dec(blk, kk, b, part, i);
+    const u32 g = a.gal[kk];
+    const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
+    const u64 ip = ks_inner(a, kk, b, part, i, i, sn, n, P);
+    u64 u = sub_mod(add_mod(ip, __ldg(a.Ph_mod + i), P.q), v, P.q);
+    u = mul_mod(u, __ldg(a.Pinv_mod + i), P);
+    const size_t LN = (size_t)a.Lc * a.N;
+    if (part < a.add_parts)
+      u = add_mod(u, a.addsrc[(size_t)b * a.add_bs + part * LN + (size_t)i * a.N + (a.add_gather ? sn : n)], P.q);
+    if (a.D) u = mul_mod(u, a.D[(size_t)kk * a.D_ks + (size_t)i * a.N + n], P);
+    const size_t o = (size_t)kk * a.out_ks + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N + n;
+    if (a.acc_in) u = add_mod(u, a.acc_in[o], P.q);
+    a.out[o] = u;
+  }
+};
+
+// a11 rescale, step 1: INTT of the last limb l, y = [x_l + (q_l-1)/2]_{q_l}.
+struct JobRescaleLast {
+  const u64* x;     // [R][Lc][N] (R = B*size rows of polynomials)
+  u64* y;           // [R][N]
+  int N, Lc;
+  __device__ int prime(int) const { return Lc - 1; }
+  __device__ u64 load(int blk, u32 n, const PrimeD&) const {
+    return x[((size_t)blk * Lc + Lc - 1) * N + n];
+  }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
+    y[(size_t)blk * N + n] = add_mod(v, (P.q - 1) >> 1, P.q);
+  }
+};
+// a11 rescale, step 2: out_i = (x_i + [h]_{q_i} - NTT_i([y]_{q_i})) [q_l^{-1}]_{q_i}.
+struct JobRescaleData {
+  const u64* x;
+  const u64* y;
+  u64* out;         // [R][Lc-1][N]
+  const u64* h;     // [Lc-1] (q_l-1)/2 mod q_i   (row l of rs_h)
+  const u64* qinv;  // [Lc-1] q_l^{-1} mod q_i
+  int N, Lc;
+  __device__ int prime(int blk) const { return blk % (Lc - 1); }
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
+    return reduce64(y[(size_t)(blk / (Lc - 1)) * N + n], P);
+  }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
+    const int r = blk / (Lc - 1), i = blk % (Lc - 1);
+    const u64 xi = x[((size_t)r * Lc + i) * N + n];
+    const u64 t = sub_mod(add_mod(xi, __ldg(h + i), P.q), v, P.q);
+    out[((size_t)r * (Lc - 1) + i) * N + n] = mul_mod(t, __ldg(qinv + i), P);
+  }
+};
+
+}  // namespace he

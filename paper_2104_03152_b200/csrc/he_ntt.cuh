@@ -1,0 +1,214 @@
+// he_ntt.cuh — batched negacyclic NTT / INTT for sm_100a (SURVEY.md §8(a) a6,
+// kernels K1/K2), templated on load / store functors so that every producer
+// and consumer of a transform (digit lift, key inner product, ModDown,
+// rescale, encode, decrypt, ...) is fused into the transform's single pass
+// over HBM.
+//
+// Transform (C5): NTT(a)[j] = sum_i a_i psi^{(2 brv(j)+1) i} mod q, computed
+// by the merged-psi Cooley-Tukey network (twiddle of stage s, butterfly group
+// i: psi^{brv(2^s + i)}), output in bit-reversed order; the inverse is the
+// Gentleman-Sande network with psi^{-brv(.)} followed by N^{-1}.
+//
+// Layout: one CTA (or a 2-CTA cluster for N = 32768) owns one limb of N
+// words in shared memory (padded one word per 16 against bank conflicts).
+// Each thread owns 2^R words per pass and runs R radix-2 stages in registers
+// (Harvey lazy butterflies, Shoup twiddle products, values kept in [0, 4q)),
+// so a 2^13 transform makes 4 passes over shared memory and exactly one
+// coalesced read and one coalesced write of the limb in HBM.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "he_common.cuh"
+
+namespace he {
+
+template <int LOGN, int CL>
+struct NttGeom {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int LOGNL = LOGN - (CL == 2 ? 1 : 0);  // bits owned by one CTA
+  static constexpr int NL = 1 << LOGNL;
+  static constexpr int R = LOGNL - 9 > 4 ? LOGNL - 9 : 4;  // log2 words per thread
+  static constexpr int T = NL >> R;                          // threads per CTA
+  static constexpr int NPASS = (LOGNL + R - 1) / R;
+  static constexpr int SMEM = (NL + NL / 16) * 8;
+};
+
+__device__ __forceinline__ u32 spad(u32 i) { return i + (i >> 4); }
+
+// Cooley-Tukey butterfly, inputs/outputs in [0, 4q).
+__device__ __forceinline__ void ct_bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q, u64 two_q) {
+  u64 X = x >= two_q ? x - two_q : x;
+  u64 T = mul_shoup_lazy(y, w, wsh, q);
+  x = X + T;
+  y = X - T + two_q;
+}
+// Gentleman-Sande butterfly, inputs/outputs in [0, 2q).
+__device__ __forceinline__ void gs_bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q, u64 two_q) {
+  u64 U = x + y;
+  U = U >= two_q ? U - two_q : U;
+  u64 V = x - y + two_q;
+  x = U;
+  y = mul_shoup_lazy(V, w, wsh, q);
+}
+
+// One pass over local bits [LO, LO+NB): each thread loads 2^NB words per
+// group (2^(R-NB) groups), runs NB stages in registers, writes them back.
+template <int LOGN, int CL, bool INV, int LO, int NB>
+__device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const u64* __restrict__ tw,
+                                         const u64* __restrict__ twsh, u64 q, u64 two_q) {
+  typedef NttGeom<LOGN, CL> G;
+  constexpr int NG = 1 << (G::R - NB);
+  constexpr int E = 1 << NB;
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    const u32 g = tid + gi * G::T;
+    const u32 base = ((g >> LO) << (LO + NB)) | (g & ((1u << LO) - 1u));
+    u64 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = sm[spad(base + (k << LO))];
+    if (!INV) {
+#pragma unroll
+      for (int ss = 0; ss < NB; ++ss) {
+        const int b = LO + NB - 1 - ss;   // local == global bit being paired
+        const int s = LOGN - 1 - b;       // stage index
+        const int half = 1 << (NB - 1 - ss);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (k & half) continue;
+          const u32 j = gbase + base + (k << LO);
+          const u32 ti = (1u << s) + (j >> (LOGN - s));
+          ct_bfly(x[k], x[k + half], __ldg(tw + ti), __ldg(twsh + ti), q, two_q);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int ss = 0; ss < NB; ++ss) {
+        const int b = LO + ss;
+        const int s = LOGN - 1 - b;
+        const int half = 1 << ss;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (k & half) continue;
+          const u32 j = gbase + base + (k << LO);
+          const u32 ti = (1u << s) + (j >> (LOGN - s));
+          gs_bfly(x[k], x[k + half], __ldg(tw + ti), __ldg(twsh + ti), q, two_q);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) sm[spad(base + (k << LO))] = x[k];
+  }
+}
+
+// Passes over the local problem: group p covers local bits [pR, min(pR+R, LOGNL)).
+template <int LOGN, int CL, bool INV, int P>
+__device__ __forceinline__ void ntt_passes(u64* sm, u32 tid, u32 gbase, const u64* tw,
+                                           const u64* twsh, u64 q, u64 two_q) {
+  typedef NttGeom<LOGN, CL> G;
+  constexpr int GP = INV ? P : G::NPASS - 1 - P;  // forward runs top-down
+  constexpr int LO = GP * G::R;
+  constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+  ntt_pass<LOGN, CL, INV, LO, NB>(sm, tid, gbase, tw, twsh, q, two_q);
+  __syncthreads();
+  if constexpr (P + 1 < G::NPASS) ntt_passes<LOGN, CL, INV, P + 1>(sm, tid, gbase, tw, twsh, q, two_q);
+}
+
+// Cross-CTA stage (bit LOGN-1) of the 2-CTA cluster transform, through DSMEM.
+template <int LOGN, bool INV>
+__device__ __forceinline__ void ntt_cross_stage(u64* sm, u32 tid, const u64* tw, const u64* twsh,
+                                                u64 q, u64 two_q) {
+  namespace cg = cooperative_groups;
+  typedef NttGeom<LOGN, 2> G;
+  cg::cluster_group cl = cg::this_cluster();
+  const u32 rank = cl.block_rank();
+  u64* s0 = cl.map_shared_rank(sm, 0);
+  u64* s1 = cl.map_shared_rank(sm, 1);
+  const u64 w = __ldg(tw + 1), wsh = __ldg(twsh + 1);
+  for (u32 i = rank * (G::NL / 2) + tid; i < (rank + 1) * (G::NL / 2); i += G::T) {
+    u64 x = s0[spad(i)], y = s1[spad(i)];
+    if (!INV) ct_bfly(x, y, w, wsh, q, two_q);
+    else gs_bfly(x, y, w, wsh, q, two_q);
+    s0[spad(i)] = x;
+    s1[spad(i)] = y;
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  namespace cg = cooperative_groups;
+  cg::this_cluster().sync();
+}
+
+// Generic batched transform.  Job provides:
+//   int  prime(int blk)                           absolute prime index of limb blk
+//   u64  load(int blk, u32 i, const PrimeD&)      canonical input word i (natural index)
+//   void store(int blk, u32 i, u64 v, const PrimeD&)  canonical output word i
+// blk = blockIdx.x / CL.
+template <int LOGN, int CL, bool INV, class Job>
+__global__ void __launch_bounds__(NttGeom<LOGN, CL>::T)
+k_ntt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict__ tw_all,
+      const u64* __restrict__ twsh_all) {
+  typedef NttGeom<LOGN, CL> G;
+  extern __shared__ u64 sm[];
+  const u32 tid = threadIdx.x;
+  const int blk = blockIdx.x / CL;
+  const u32 rank = CL == 2 ? (blockIdx.x & 1) : 0;
+  const u32 gbase = rank * G::NL;
+  const int pi = job.prime(blk);
+  const PrimeD P = load_prime(primes, pi);
+  const u64* tw = tw_all + (size_t)pi * G::N;
+  const u64* twsh = twsh_all + (size_t)pi * G::N;
+  for (u32 i = tid; i < G::NL; i += G::T) sm[spad(i)] = job.load(blk, gbase + i, P);
+  if (CL == 2) cluster_sync_all(); else __syncthreads();
+  if (CL == 2 && !INV) {
+    ntt_cross_stage<LOGN, false>(sm, tid, tw, twsh, P.q, P.two_q);
+    cluster_sync_all();
+  }
+  ntt_passes<LOGN, CL, INV, 0>(sm, tid, gbase, tw, twsh, P.q, P.two_q);
+  if (CL == 2 && INV) {
+    cluster_sync_all();
+    ntt_cross_stage<LOGN, true>(sm, tid, tw, twsh, P.q, P.two_q);
+    cluster_sync_all();
+  }
+  for (u32 i = tid; i < G::NL; i += G::T) {
+    u64 v = sm[spad(i)];
+    if (!INV) {
+      v = v >= P.two_q ? v - P.two_q : v;
+      v = v >= P.q ? v - P.q : v;
+    } else {
+      v = mul_shoup(v, P.ninv, P.ninvsh, P.q);
+    }
+    job.store(blk, gbase + i, v, P);
+  }
+}
+
+// Fused ring product: out = INTT(NTT(a) (.) b), one CTA per limb (CL = 1).
+// Job provides prime(blk), load(blk,i,P) (coefficient-domain a),
+// factor(blk,i,P) (NTT-domain b at bit-reversed position i) and store.
+template <int LOGN, class Job>
+__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T)
+k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict__ tw_all,
+               const u64* __restrict__ twsh_all, const u64* __restrict__ itw_all,
+               const u64* __restrict__ itwsh_all) {
+  typedef NttGeom<LOGN, 1> G;
+  extern __shared__ u64 sm[];
+  const u32 tid = threadIdx.x;
+  const int blk = blockIdx.x;
+  const int pi = job.prime(blk);
+  const PrimeD P = load_prime(primes, pi);
+  for (u32 i = tid; i < G::NL; i += G::T) sm[spad(i)] = job.load(blk, i, P);
+  __syncthreads();
+  ntt_passes<LOGN, 1, false, 0>(sm, tid, 0, tw_all + (size_t)pi * G::N, twsh_all + (size_t)pi * G::N,
+                                P.q, P.two_q);
+  for (u32 i = tid; i < G::NL; i += G::T) {
+    u64 v = sm[spad(i)];
+    v = v >= P.two_q ? v - P.two_q : v;
+    v = v >= P.q ? v - P.q : v;
+    sm[spad(i)] = mul_mod(v, job.factor(blk, i, P), P);
+  }
+  __syncthreads();
+  ntt_passes<LOGN, 1, true, 0>(sm, tid, 0, itw_all + (size_t)pi * G::N, itwsh_all + (size_t)pi * G::N,
+                               P.q, P.two_q);
+  for (u32 i = tid; i < G::NL; i += G::T) job.store(blk, i, mul_shoup(sm[spad(i)], P.ninv, P.ninvsh, P.q), P);
+}
+
+}  // namespace he

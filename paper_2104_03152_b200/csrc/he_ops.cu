@@ -1,0 +1,1002 @@
+// he_ops.cu — kernels and internal operations of the B200 CKKS hot path
+// (SURVEY.md §8(a) a1-a16).  Product code: shares nothing with oracle/.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "he_internal.cuh"
+#include "he_jobs.cuh"
+#include "he_ops.h"
+
+namespace he {
+
+// ======================================================== memory / setup ===
+void* dalloc(he_context* c, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, c->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw HeError(e == cudaErrorMemoryAllocation ? HE_OUT_OF_MEMORY : HE_CUDA_ERROR,
+                  std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+  }
+  return p;
+}
+void dfree(he_context* c, void* p) {
+  if (p) cudaFreeAsync(p, c->stream);
+}
+
+template <class T>
+static T* upload(he_context* c, const std::vector<T>& v) {
+  T* d = nullptr;
+  HE_CK(cudaMalloc(&d, std::max<size_t>(1, v.size()) * sizeof(T)));
+  if (!v.empty()) HE_CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  c->owned.push_back(d);
+  return d;
+}
+
+void context_init(he_context* c, const HostParams& hp, u64 seed) {
+  c->hp = hp;
+  c->logN = hp.logN;
+  c->N = hp.N;
+  c->L = hp.L;
+  c->K = hp.K;
+  c->NP = hp.L + hp.K;
+  c->seed = seed;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw HeError(HE_CUDA_ERROR, "no CUDA device available (the library has no CPU fallback)");
+  }
+  HE_CK(cudaGetDevice(&c->device));
+  // keep freed blocks cached in the stream-ordered pool
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+    u64 thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  std::vector<PrimeD> pd(c->NP);
+  for (int t = 0; t < c->NP; ++t) {
+    PrimeD& p = pd[t];
+    memset(&p, 0, sizeof(p));
+    p.q = hp.q[t];
+    p.two_q = 2 * hp.q[t];
+    p.mu = hp.mu[t];
+    p.ninv = hp.ninv[t];
+    p.ninvsh = hp.ninvsh[t];
+    p.k = (u32)hp.kbits[t];
+    p.mu64 = (u64)((~(u128)0 >> 64) / hp.q[t]);  // floor((2^64 - 1) / q) == floor(2^64 / q) for odd q
+    p.r64 = (u64)((((u128)1) << 64) % hp.q[t]);
+  }
+  c->d_primes = upload(c, pd);
+  c->d_tw = upload(c, hp.tw);
+  c->d_twsh = upload(c, hp.twsh);
+  c->d_itw = upload(c, hp.itw);
+  c->d_itwsh = upload(c, hp.itwsh);
+  c->d_cdt = upload(c, hp.cdt);
+  c->d_P_mod = upload(c, hp.P_mod);
+  c->d_Pinv_mod = upload(c, hp.Pinv_mod);
+  c->d_Ph_mod = upload(c, hp.Ph_mod);
+  c->d_Phat_inv = upload(c, hp.Phat_inv);
+  c->d_Phat_mod = upload(c, hp.Phat_mod);
+  c->d_rs_qinv = upload(c, hp.rs_qinv);
+  c->d_rs_h = upload(c, hp.rs_h);
+  c->d_crt = upload(c, hp.crt_words);
+  c->d_slot_index = upload(c, hp.slot_index);
+  c->d_fft_w = upload(c, hp.fft_w);
+  c->d_zeta = upload(c, hp.zeta_pow);
+  c->d_q = upload(c, hp.q);
+}
+
+void context_destroy(he_context* c) {
+  cudaStreamSynchronize(c->stream);
+  for (void* p : c->owned) cudaFree(p);
+  for (auto& kv : c->gk) cudaFree(kv.second);
+  if (c->d_sk) cudaFree(c->d_sk);
+  if (c->d_pk) cudaFree(c->d_pk);
+  if (c->d_rlk) cudaFree(c->d_rlk);
+}
+
+// ============================================================== handles ===
+he_ciphertext* ct_new(he_context* c, int B, int size, int level, double scale) {
+  he_ciphertext* ct = new he_ciphertext{c, B, size, level, scale, nullptr};
+  try {
+    ct->d = dalloc_t<u64>(c, ct_words(ct));
+  } catch (...) {
+    delete ct;
+    throw;
+  }
+  return ct;
+}
+he_plaintext* pt_new(he_context* c, int B, int level, double scale) {
+  he_plaintext* pt = new he_plaintext{c, B, level, scale, nullptr};
+  try {
+    pt->d = dalloc_t<u64>(c, pt_words(pt));
+  } catch (...) {
+    delete pt;
+    throw;
+  }
+  return pt;
+}
+void ct_free(he_ciphertext* ct) {
+  if (!ct) return;
+  dfree(ct->ctx, ct->d);
+  delete ct;
+}
+void pt_free(he_plaintext* pt) {
+  if (!pt) return;
+  dfree(pt->ctx, pt->d);
+  delete pt;
+}
+
+// ===================================================== pointwise kernels ===
+// Rows of N words; row r of a [B][size][Lc][N] array is limb r % Lc.
+enum BinOp { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2 };
+
+template <int OP>
+__global__ void k_binop(const u64* __restrict__ a, const u64* __restrict__ b, u64* __restrict__ out,
+                        const PrimeD* __restrict__ primes, int N, int Lc, size_t rows, size_t a_bs,
+                        size_t b_bs, size_t item_rows, size_t b_limb_bs, size_t o_bs) {
+  // a_bs / b_bs: item strides in words (0 = broadcast); item_rows = size*Lc.
+  // b_limb_bs: stride between b's polys inside an item (0 = same poly for every part).
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const size_t item = r / item_rows, ir = r % item_rows;
+    const int limb = (int)(ir % Lc);
+    const size_t part = ir / Lc;
+    const PrimeD P = load_prime(primes, limb);
+    const u64* pa = a + item * a_bs + ir * N;
+    const u64* pb = b + item * b_bs + part * b_limb_bs + (size_t)limb * N;
+    u64* po = out + item * o_bs + ir * N;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const u64 x = pa[n], y = pb[n];
+      po[n] = OP == OP_ADD ? add_mod(x, y, P.q) : OP == OP_SUB ? sub_mod(x, y, P.q) : mul_mod(x, y, P);
+    }
+  }
+}
+
+__global__ void k_negate(const u64* __restrict__ a, u64* __restrict__ out, const PrimeD* __restrict__ primes,
+                         int N, int Lc, size_t rows) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const u64 q = load_prime(primes, (int)(r % Lc)).q;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+      out[r * N + n] = neg_mod(a[r * N + n], q);
+  }
+}
+
+// (c0 c0', c0 c1' + c1 c0', c1 c1')  (SURVEY a7 tensor)
+__global__ void k_tensor(const u64* __restrict__ x, const u64* __restrict__ y, u64* __restrict__ out,
+                         const PrimeD* __restrict__ primes, int N, int Lc, size_t rows, size_t x_bs,
+                         size_t y_bs) {
+  // rows = B * Lc
+  const size_t LN = (size_t)Lc * N;
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const size_t b = r / Lc;
+    const int i = (int)(r % Lc);
+    const PrimeD P = load_prime(primes, i);
+    const u64* x0 = x + b * x_bs + (size_t)i * N;
+    const u64* y0 = y + b * y_bs + (size_t)i * N;
+    u64* o = out + b * 3 * LN + (size_t)i * N;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const u64 a0 = x0[n], a1 = x0[LN + n], b0 = y0[n], b1 = y0[LN + n];
+      o[n] = mul_mod(a0, b0, P);
+      o[LN + n] = add_mod(mul_mod(a0, b1, P), mul_mod(a1, b0, P), P.q);
+      o[2 * LN + n] = mul_mod(a1, b1, P);
+    }
+  }
+}
+
+// m = c0 + c1 s (+ c2 s^2)
+__global__ void k_decrypt(const u64* __restrict__ ct, const u64* __restrict__ sk, u64* __restrict__ out,
+                          const PrimeD* __restrict__ primes, int N, int Lc, int size, size_t rows) {
+  const size_t LN = (size_t)Lc * N;
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const size_t b = r / Lc;
+    const int i = (int)(r % Lc);
+    const PrimeD P = load_prime(primes, i);
+    const u64* c = ct + b * size * LN + (size_t)i * N;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const u64 s = sk[(size_t)i * N + n];
+      u64 acc = c[n], sp = s;
+      for (int p = 1; p < size; ++p) {
+        acc = add_mod(acc, mul_mod(c[p * LN + n], sp, P), P.q);
+        sp = mul_mod(sp, s, P);
+      }
+      out[r * N + n] = acc;
+    }
+  }
+}
+
+// c0 = v b + e0 + m, c1 = v a + e1 (C13). noise: [B][3][Lc][N] NTT words (v, e0, e1).
+__global__ void k_encrypt_combine(const u64* __restrict__ noise, const u64* __restrict__ pk,
+                                  const u64* __restrict__ pt, size_t pt_bs, u64* __restrict__ out,
+                                  const PrimeD* __restrict__ primes, int N, int Lc, int L, size_t rows) {
+  const size_t LN = (size_t)Lc * N;
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const size_t b = r / Lc;
+    const int i = (int)(r % Lc);
+    const PrimeD P = load_prime(primes, i);
+    const u64* v = noise + b * 3 * LN + (size_t)i * N;
+    const u64* pb = pk + (size_t)i * N;
+    const u64* pa = pk + ((size_t)L + i) * N;
+    const u64* m = pt + b * pt_bs + (size_t)i * N;
+    u64* o = out + b * 2 * LN + (size_t)i * N;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const u64 vv = v[n];
+      o[n] = add_mod(add_mod(mul_mod(vv, pb[n], P), v[LN + n], P.q), m[n], P.q);
+      o[LN + n] = add_mod(mul_mod(vv, pa[n], P), v[2 * LN + n], P.q);
+    }
+  }
+}
+
+// Small-coefficient sampling (C10 ternary / C11 CDT): row r uses stream
+// (pur << 56) | ((obj0 + r) << 16).
+__global__ void k_sample_small(i64* __restrict__ out, int N, int rows, u64 seed, u64 pur, u64 obj0, int kind,
+                               const u64* __restrict__ cdt) {
+  __shared__ u64 T[20];
+  if (threadIdx.x < 20) T[threadIdx.x] = cdt[threadIdx.x];
+  __syncthreads();
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+    const u64 sid = stream_sid(pur, obj0 + (u64)r, 0);
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+      out[(size_t)r * N + n] = kind == 0 ? sample_ternary(seed, sid, n) : sample_cdt(seed, sid, n, T);
+  }
+}
+
+// Uniform residues drawn as NTT words (C13): row (j, t) for j < nj, t < nt
+// writes out + j*j_stride + t*N with stream (pur<<56)|((obj0+j)<<16)|t.
+__global__ void k_sample_uniform(u64* __restrict__ out, size_t j_stride, int nj, int nt, int N, u64 seed,
+                                 u64 pur, u64 obj0, const PrimeD* __restrict__ primes) {
+  for (int r = blockIdx.y; r < nj * nt; r += gridDim.y) {
+    const int j = r / nt, t = r % nt;
+    const PrimeD P = load_prime(primes, t);
+    const u64 sid = stream_sid(pur, obj0 + (u64)j, (u64)t);
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+      out[(size_t)j * j_stride + (size_t)t * N + n] = sample_uniform(seed, sid, n, P);
+  }
+}
+
+// pk: b_i = -a_i s_i + e_i over data limbs (a already in pk[1]).
+__global__ void k_pk_combine(u64* __restrict__ pk, const u64* __restrict__ e_ntt, const u64* __restrict__ sk,
+                             const PrimeD* __restrict__ primes, int N, int L) {
+  for (int i = blockIdx.y; i < L; i += gridDim.y) {
+    const PrimeD P = load_prime(primes, i);
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const size_t o = (size_t)i * N + n;
+      const u64 a = pk[(size_t)L * N + o];
+      pk[o] = add_mod(neg_mod(mul_mod(a, sk[o], P), P.q), e_ntt[o], P.q);
+    }
+  }
+}
+
+// ksk_j = (b_j, a_j): b_j[t] = -a_j[t] s_t + e_j[t] + [t == j] [P]_{q_j} s'_t  (C12).
+// key: [L][2][NP][N] with a_j already in part 1; e_ntt: [L][NP][N].
+// s' = s^2 (gal == 0) or phi_g(s) in the NTT domain (gal = g).
+__global__ void k_ksk_combine(u64* __restrict__ key, const u64* __restrict__ e_ntt, const u64* __restrict__ sk,
+                              const u64* __restrict__ P_mod, const PrimeD* __restrict__ primes, int N, int logN,
+                              int L, int NP, u32 gal) {
+  for (int r = blockIdx.y; r < L * NP; r += gridDim.y) {
+    const int j = r / NP, t = r % NP;
+    const PrimeD P = load_prime(primes, t);
+    const u64 Pq = P_mod[t];
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const size_t sn = (size_t)t * N + n;
+      const u64 a = key[(((size_t)j * 2 + 1) * NP + t) * N + n];
+      u64 b = add_mod(neg_mod(mul_mod(a, sk[sn], P), P.q), e_ntt[((size_t)j * NP + t) * N + n], P.q);
+      if (t == j) {
+        u64 sp;
+        if (gal == 0) sp = mul_mod(sk[sn], sk[sn], P);
+        else sp = sk[(size_t)t * N + galois_src(n, gal, logN)];
+        b = add_mod(b, mul_mod(Pq, sp, P), P.q);
+      }
+      key[(((size_t)j * 2 + 0) * NP + t) * N + n] = b;
+    }
+  }
+}
+
+// Sum over kk of tmp[kk][item] into acc (vec_mat rotation chunks).
+__global__ void k_accumulate(u64* __restrict__ acc, const u64* __restrict__ tmp, int KB, size_t chunk_words,
+                             const PrimeD* __restrict__ primes, int N, int Lc, size_t rows) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const u64 q = load_prime(primes, (int)(r % Lc)).q;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      u64 s = acc[r * N + n];
+      for (int kk = 0; kk < KB; ++kk) s = add_mod(s, tmp[kk * chunk_words + r * N + n], q);
+      acc[r * N + n] = s;
+    }
+  }
+}
+
+// conv (C18): T[b*C + c] = ct_b (.) K_c
+__global__ void k_mul_plain_outer(const u64* __restrict__ ct, const u64* __restrict__ K, u64* __restrict__ out,
+                                  const PrimeD* __restrict__ primes, int N, int Lc, int C, size_t rows) {
+  // rows = B * C * 2 * Lc
+  const size_t LN = (size_t)Lc * N;
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int i = (int)(r % Lc);
+    const int part = (int)((r / Lc) & 1);
+    const size_t bc = r / (2 * Lc);
+    const int c = (int)(bc % C);
+    const size_t b = bc / C;
+    const PrimeD P = load_prime(primes, i);
+    const u64* x = ct + b * 2 * LN + part * LN + (size_t)i * N;
+    const u64* k = K + c * LN + (size_t)i * N;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+      out[r * N + n] = mul_mod(x[n], k[n], P);
+  }
+}
+
+// conv (C19): out[b] = sum_c T[b*C + c] (.) M_c
+__global__ void k_mask_sum(const u64* __restrict__ T, const u64* __restrict__ M, u64* __restrict__ out,
+                           const PrimeD* __restrict__ primes, int N, int Lc, int C, size_t rows) {
+  // rows = B * 2 * Lc
+  const size_t LN = (size_t)Lc * N;
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int i = (int)(r % Lc);
+    const int part = (int)((r / Lc) & 1);
+    const size_t b = r / (2 * Lc);
+    const PrimeD P = load_prime(primes, i);
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      u64 s = 0;
+      for (int c = 0; c < C; ++c)
+        s = add_mod(s, mul_mod(T[((b * C + c) * 2 + part) * LN + (size_t)i * N + n], M[c * LN + (size_t)i * N + n], P),
+                    P.q);
+      out[r * N + n] = s;
+    }
+  }
+}
+
+__global__ void k_check_words(const u64* __restrict__ w, const PrimeD* __restrict__ primes, int N, int Lc,
+                              size_t rows, int* bad) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const u64 q = load_prime(primes, (int)(r % Lc)).q;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+      if (w[r * N + n] >= q) atomicOr(bad, 1);
+  }
+}
+
+// ======================================================== encode / decode ===
+// Canonical embedding (C6) with a length-M = N/2 complex FFT:
+//   encode  w_i = zeta^{-i} sum_r Z[r] omega^{-i r},  Z[r_j] = z_j,
+//           m_i = round(c Re w_i), m_{i+M} = round(c Im w_i), c = 2 scale / N;
+//   decode  y_i = (X_i + i X_{i+M}) zeta^i,  z_j = Re(sum_i y_i omega^{i r_j}) / scale,
+// with omega = exp(2 pi i / M), 5^j = 4 r_j + 1 (mod 2N).
+__device__ void fft_inplace(double2* buf, int M, const double* __restrict__ w, double sign) {
+  for (int len = 2; len <= M; len <<= 1) {
+    const int half = len >> 1, step = M / len;
+    for (int t = threadIdx.x; t < M / 2; t += blockDim.x) {
+      const int pos = t % half;
+      const int i0 = (t / half) * len + pos, i1 = i0 + half;
+      const double c = w[2 * pos * step], s = sign * w[2 * pos * step + 1];
+      const double2 u = buf[i0], v = buf[i1];
+      const double2 vw = make_double2(v.x * c - v.y * s, v.x * s + v.y * c);
+      buf[i0] = make_double2(u.x + vw.x, u.y + vw.y);
+      buf[i1] = make_double2(u.x - vw.x, u.y - vw.y);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_encode_fft(const double* __restrict__ z, size_t n, double scale, i64* __restrict__ m_out,
+                             int* overflow, const int* __restrict__ slot_index, const double* __restrict__ w,
+                             const double* __restrict__ zeta, int N, int logM, double2* gscratch) {
+  extern __shared__ double2 fbuf[];
+  const int M = N / 2;
+  const int b = blockIdx.x;
+  double2* buf = gscratch ? gscratch + (size_t)b * M : fbuf;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (size_t j = threadIdx.x; j < n; j += blockDim.x)
+    buf[__brev((unsigned)slot_index[j]) >> (32 - logM)] = make_double2(z[(size_t)b * n + j], 0.0);
+  __syncthreads();
+  fft_inplace(buf, M, w, -1.0);
+  const double c = 2.0 * scale / (double)N;
+  const double lim = 4611686018427387904.0;  // 2^62
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    const double zr = zeta[2 * i], zi = -zeta[2 * i + 1];  // zeta^{-i}
+    const double2 v = buf[i];
+    const double re = c * (v.x * zr - v.y * zi), im = c * (v.x * zi + v.y * zr);
+    if (!(fabs(re) < lim) || !(fabs(im) < lim)) {
+      atomicOr(overflow, 1);
+      m_out[(size_t)b * N + i] = 0;
+      m_out[(size_t)b * N + i + M] = 0;
+    } else {
+      m_out[(size_t)b * N + i] = llround(re);
+      m_out[(size_t)b * N + i + M] = llround(im);
+    }
+  }
+}
+
+__global__ void k_decode_fft(const double* __restrict__ X, size_t n, double scale, double* __restrict__ z,
+                             const int* __restrict__ slot_index, const double* __restrict__ w,
+                             const double* __restrict__ zeta, int N, int logM, double2* gscratch) {
+  extern __shared__ double2 fbuf[];
+  const int M = N / 2;
+  const int b = blockIdx.x;
+  double2* buf = gscratch ? gscratch + (size_t)b * M : fbuf;
+  const double* x = X + (size_t)b * N;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    const double a = x[i], c = x[i + M], zr = zeta[2 * i], zi = zeta[2 * i + 1];
+    buf[__brev((unsigned)i) >> (32 - logM)] = make_double2(a * zr - c * zi, a * zi + c * zr);
+  }
+  __syncthreads();
+  fft_inplace(buf, M, w, 1.0);
+  for (size_t j = threadIdx.x; j < n; j += blockDim.x) z[(size_t)b * n + j] = buf[slot_index[j]].x / scale;
+}
+
+// CRT compose (a13): X = sum_i [x_i Qhat_i^{-1}]_{q_i} Qhat_i mod Q, centred, to double.
+constexpr int CRT_MAXW = 40;
+__global__ void k_crt_compose(const u64* __restrict__ coef, double* __restrict__ X, const u64* __restrict__ crt,
+                              const PrimeD* __restrict__ primes, int N, int Lc, size_t total) {
+  const u64* Qhat_inv = crt;
+  const u64* Qhat = crt + Lc;
+  const u64* Q = Qhat + (size_t)Lc * Lc;
+  const u64* Qh = Q + Lc;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / N;
+    const int n = (int)(idx % N);
+    u64 acc[CRT_MAXW + 1];
+    for (int w = 0; w <= Lc; ++w) acc[w] = 0;
+    for (int i = 0; i < Lc; ++i) {
+      const PrimeD P = load_prime(primes, i);
+      const u64 a = mul_mod(coef[(b * Lc + i) * N + n], Qhat_inv[i], P);
+      u64 carry = 0;
+      for (int w = 0; w < Lc; ++w) {
+        const u64 m = Qhat[(size_t)i * Lc + w];
+        const u64 lo = a * m, hi = __umul64hi(a, m);
+        u64 s = acc[w] + lo;
+        u64 c1 = s < lo;
+        s += carry;
+        c1 += s < carry;
+        acc[w] = s;
+        carry = hi + c1;
+      }
+      for (int w = Lc; w <= Lc && carry; ++w) {
+        acc[w] += carry;
+        carry = 0;
+      }
+    }
+    // reduce mod Q: acc < Lc Q
+    for (int it = 0; it < Lc + 1; ++it) {
+      bool ge = acc[Lc] != 0;
+      if (!ge) {
+        ge = true;
+        for (int w = Lc - 1; w >= 0; --w) {
+          if (acc[w] != Q[w]) { ge = acc[w] > Q[w]; break; }
+        }
+      }
+      if (!ge) break;
+      u64 borrow = 0;
+      for (int w = 0; w < Lc; ++w) {
+        const u64 d = acc[w] - Q[w] - borrow;
+        borrow = (acc[w] < Q[w] + borrow) || (Q[w] + borrow < Q[w]) ? 1 : 0;
+        acc[w] = d;
+      }
+      acc[Lc] -= borrow;
+    }
+    // centre: X > floor(Q/2) -> X - Q
+    bool gt = false;
+    for (int w = Lc - 1; w >= 0; --w) {
+      if (acc[w] != Qh[w]) { gt = acc[w] > Qh[w]; break; }
+    }
+    double v = 0.0;
+    if (gt) {
+      u64 borrow = 0;
+      for (int w = 0; w < Lc; ++w) {  // mag = Q - acc
+        const u64 d = Q[w] - acc[w] - borrow;
+        borrow = (Q[w] < acc[w] + borrow) || (acc[w] + borrow < acc[w]) ? 1 : 0;
+        acc[w] = d;
+      }
+    }
+    for (int w = Lc - 1; w >= 0; --w) v = v * 18446744073709551616.0 + (double)acc[w];
+    X[idx] = gt ? -v : v;
+  }
+}
+
+// ======================================================== internal ops ===
+static dim3 rows_grid2(he_context* c, size_t rows) { return rows_grid(c, rows, 256); }
+
+void ntt_rows(he_context* c, const u64* src, u64* dst, size_t items, int nl, size_t src_bs, size_t dst_bs,
+              bool inverse) {
+  JobLimbs j{src, dst, c->N, nl, src_bs, dst_bs};
+  if (inverse) launch_ntt<true>(c, j, (int)(items * nl));
+  else launch_ntt<false>(c, j, (int)(items * nl));
+}
+
+void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl) {
+  JobRingMul j{a, b, out, c->N, nl};
+  const int nblk = (int)(items * nl);
+  auto run = [&](auto kern, int T, int smem) {
+    static_cast<void>(T);
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw, c->d_twsh, c->d_itw, c->d_itwsh);
+    check_launch(c);
+  };
+  switch (c->logN) {
+    case 10: run(k_ntt_mul_intt<10, JobRingMul>, NttGeom<10, 1>::T, NttGeom<10, 1>::SMEM); break;
+    case 11: run(k_ntt_mul_intt<11, JobRingMul>, NttGeom<11, 1>::T, NttGeom<11, 1>::SMEM); break;
+    case 12: run(k_ntt_mul_intt<12, JobRingMul>, NttGeom<12, 1>::T, NttGeom<12, 1>::SMEM); break;
+    case 13: run(k_ntt_mul_intt<13, JobRingMul>, NttGeom<13, 1>::T, NttGeom<13, 1>::SMEM); break;
+    case 14: run(k_ntt_mul_intt<14, JobRingMul>, NttGeom<14, 1>::T, NttGeom<14, 1>::SMEM); break;
+    default: {
+      // N = 32768: three passes (the fused single-CTA form needs 256 KB of smem)
+      Scratch t(c, items * nl * (size_t)c->N * 8);
+      const size_t bs = (size_t)nl * c->N;
+      ntt_rows(c, a, t.as<u64>(), items, nl, bs, bs, false);
+      modmul_rows(c, t.as<u64>(), b, t.as<u64>(), items, nl);
+      ntt_rows(c, t.as<u64>(), out, items, nl, bs, bs, true);
+    }
+  }
+}
+
+void modmul_rows(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl) {
+  const size_t rows = items * nl;
+  k_binop<OP_MUL><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a, b, out, c->d_primes, c->N, nl, rows,
+                                                              (size_t)nl * c->N, (size_t)nl * c->N, nl, 0,
+                                                              (size_t)nl * c->N);
+  check_launch(c);
+}
+
+void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int nl) {
+  JobSignedToNtt j{poly, dst, c->N, nl, (size_t)c->N, (size_t)nl * c->N};
+  launch_ntt<false>(c, j, (int)(items * nl));
+}
+
+// ---- arithmetic -----------------------------------------------------------
+he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b) {
+  const int B = std::max(a->B, b->B), Lc = a->level + 1;
+  he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale);
+  const size_t rows = (size_t)B * a->size * Lc, LN = (size_t)Lc * c->N;
+  const size_t a_bs = a->B == 1 ? 0 : a->size * LN, b_bs = b->B == 1 ? 0 : b->size * LN;
+  // b indexed like a: pass b_limb_bs = LN with b pointer per part
+  dim3 g = rows_grid2(c, rows);
+  if (op == OP_ADD)
+    k_binop<OP_ADD><<<g, 256, 0, c->stream>>>(a->d, b->d, o->d, c->d_primes, c->N, Lc, rows, a_bs, b_bs,
+                                              (size_t)a->size * Lc, LN, a->size * LN);
+  else
+    k_binop<OP_SUB><<<g, 256, 0, c->stream>>>(a->d, b->d, o->d, c->d_primes, c->N, Lc, rows, a_bs, b_bs,
+                                              (size_t)a->size * Lc, LN, a->size * LN);
+  check_launch(c);
+  return o;
+}
+
+he_ciphertext* ct_negate(he_context* c, const he_ciphertext* a) {
+  const int Lc = a->level + 1;
+  he_ciphertext* o = ct_new(c, a->B, a->size, a->level, a->scale);
+  const size_t rows = (size_t)a->B * a->size * Lc;
+  k_negate<<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, o->d, c->d_primes, c->N, Lc, rows);
+  check_launch(c);
+  return o;
+}
+
+he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p) {
+  const int Lc = a->level + 1;
+  const int B = std::max(a->B, p->B);
+  he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale * p->scale);
+  const size_t LN = (size_t)Lc * c->N, rows = (size_t)B * a->size * Lc;
+  k_binop<OP_MUL><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                              a->B == 1 ? 0 : a->size * LN, p->B == 1 ? 0 : LN,
+                                                              (size_t)a->size * Lc, 0, a->size * LN);
+  check_launch(c);
+  return o;
+}
+
+he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p) {
+  const int Lc = a->level + 1;
+  const int B = std::max(a->B, p->B);
+  he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale);
+  const size_t LN = (size_t)Lc * c->N;
+  // copy all polys, then add the plaintext into poly 0 of every item
+  for (int b = 0; b < B; ++b) {
+    const u64* src = a->d + (a->B == 1 ? 0 : (size_t)b * a->size * LN);
+    HE_CK(cudaMemcpyAsync(o->d + (size_t)b * a->size * LN, src, a->size * LN * 8, cudaMemcpyDeviceToDevice,
+                          c->stream));
+  }
+  const size_t rows = (size_t)B * Lc;
+  // treat items as size-1 rows at stride size*LN
+  k_binop<OP_ADD><<<rows_grid2(c, rows), 256, 0, c->stream>>>(o->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                              a->size * LN, p->B == 1 ? 0 : LN, Lc, 0,
+                                                              a->size * LN);
+  check_launch(c);
+  return o;
+}
+
+he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphertext* y) {
+  const int Lc = x->level + 1;
+  const int B = std::max(x->B, y->B);
+  he_ciphertext* o = ct_new(c, B, 3, x->level, x->scale * y->scale);
+  const size_t LN = (size_t)Lc * c->N, rows = (size_t)B * Lc;
+  k_tensor<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, y->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                       x->B == 1 ? 0 : 2 * LN, y->B == 1 ? 0 : 2 * LN);
+  check_launch(c);
+  return o;
+}
+
+// ---- rescale (a11, C15) ----------------------------------------------------
+he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a) {
+  const int Lc = a->level + 1, l = a->level;
+  he_ciphertext* o = ct_new(c, a->B, a->size, l - 1, a->scale / (double)c->hp.q[l]);
+  const size_t R = (size_t)a->B * a->size;
+  Scratch y(c, R * c->N * 8);
+  JobRescaleLast j1{a->d, y.as<u64>(), c->N, Lc};
+  launch_ntt<true>(c, j1, (int)R);
+  JobRescaleData j2{a->d, y.as<u64>(), o->d, c->d_rs_h + (size_t)l * c->L, c->d_rs_qinv + (size_t)l * c->L,
+                    c->N, Lc};
+  launch_ntt<false>(c, j2, (int)(R * (Lc - 1)));
+  return o;
+}
+
+// ---- key switching (a9/a10, C12/C15/C16) -------------------------------------
+// ModUp of the digit source (NTT words, item stride bs): returns ext [B][Lc][Lc+K][N].
+static u64* modup(he_context* c, const u64* dsrc, size_t bs, int B, int Lc) {
+  const size_t N = c->N;
+  Scratch coef(c, (size_t)B * Lc * N * 8);
+  ntt_rows(c, dsrc, coef.as<u64>(), B, Lc, bs, (size_t)Lc * N, true);
+  u64* ext = dalloc_t<u64>(c, (size_t)B * Lc * (Lc + c->K) * N);
+  JobModUp j{coef.as<u64>(), ext, c->d_q, c->N, Lc, c->K, c->L};
+  launch_ntt<false>(c, j, B * Lc * (Lc + c->K - 1));
+  return ext;
+}
+
+static KsArgs ks_base(he_context* c, int B, int Lc, const u64* ext, const u64* dsrc, size_t dsrc_bs) {
+  KsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.N = c->N;
+  a.logN = c->logN;
+  a.Lc = Lc;
+  a.L = c->L;
+  a.K = c->K;
+  a.NP = c->NP;
+  a.B = B;
+  a.KB = 1;
+  a.ext = ext;
+  a.dsrc = dsrc;
+  a.dsrc_bs = dsrc_bs;
+  a.Ph_mod = c->d_Ph_mod;
+  a.Pinv_mod = c->d_Pinv_mod;
+  a.Phat_inv = c->d_Phat_inv;
+  a.Phat_mod = c->d_Phat_mod;
+  return a;
+}
+
+static void ks_launch(he_context* c, KsArgs& a) {
+  Scratch tb(c, (size_t)a.KB * a.B * 2 * a.K * a.N * 8);
+  a.tb = tb.as<u64>();
+  JobKsSpecial js{a};
+  launch_ntt<true>(c, js, a.KB * a.B * 2 * a.K);
+  JobKsData jd{a};
+  launch_ntt<false>(c, jd, a.KB * a.B * 2 * a.Lc);
+}
+
+const u64* galois_key(he_context* c, int step, u32* gal_out) {
+  const u64 g = galois_element(c->N, step);
+  auto it = c->gk.find(g);
+  if (it == c->gk.end()) return nullptr;
+  *gal_out = (u32)g;
+  return it->second;
+}
+
+he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a) {
+  const int Lc = a->level + 1;
+  const size_t LN = (size_t)Lc * c->N;
+  he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
+  u64* ext = modup(c, a->d + 2 * LN, 3 * LN, a->B, Lc);
+  KsArgs k = ks_base(c, a->B, Lc, ext, a->d + 2 * LN, 3 * LN);
+  k.keys[0] = c->d_rlk;
+  k.gal[0] = 1;
+  k.out = o->d;
+  k.out_bs = 2 * LN;
+  k.addsrc = a->d;
+  k.add_bs = 3 * LN;
+  k.add_parts = 2;
+  try {
+    ks_launch(c, k);
+  } catch (...) {
+    dfree(c, ext);
+    throw;
+  }
+  dfree(c, ext);
+  return o;
+}
+
+// rotate (add_input = false) or x + rotate(x) (add_input = true)
+he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool add_input) {
+  const int Lc = a->level + 1;
+  const size_t LN = (size_t)Lc * c->N;
+  u32 g = 0;
+  const u64* key = galois_key(c, step, &g);
+  if (!key) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
+  he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
+  u64* ext = modup(c, a->d + LN, 2 * LN, a->B, Lc);
+  KsArgs k = ks_base(c, a->B, Lc, ext, a->d + LN, 2 * LN);
+  k.keys[0] = key;
+  k.gal[0] = g;
+  k.out = o->d;
+  k.out_bs = 2 * LN;
+  k.addsrc = a->d;
+  k.add_bs = 2 * LN;
+  k.add_parts = 1;
+  k.add_gather = 1;
+  if (add_input) k.acc_in = a->d;
+  try {
+    ks_launch(c, k);
+  } catch (...) {
+    dfree(c, ext);
+    throw;
+  }
+  dfree(c, ext);
+  return o;
+}
+
+// vec_mat with pre-encoded diagonals (a14, C17): acc = sum_k rot(x, k) (.) D_k
+// with all rotations hoisted (one ModUp of c1 shared by every k), then one
+// rescale and the bias.
+he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
+                          const he_plaintext* bias) {
+  const int Lc = x->level + 1, n = diags->B, B = x->B;
+  const size_t LN = (size_t)Lc * c->N;
+  std::vector<const u64*> keys(n);
+  std::vector<u32> gals(n);
+  for (int k = 1; k < n; ++k) {
+    keys[k] = galois_key(c, k, &gals[k]);
+    if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(k));
+  }
+  // k = 0 term
+  he_plaintext d0{c, 1, diags->level, diags->scale, diags->d};
+  he_ciphertext* acc = ct_mul_plain(c, x, &d0);
+  he_ciphertext* res = nullptr;
+  u64* ext = nullptr;
+  try {
+    if (n > 1) {
+      ext = modup(c, x->d + LN, 2 * LN, B, Lc);
+      const int per_rot = B * 2 * Lc;
+      int KB = (4 * 148 + per_rot - 1) / per_rot;
+      KB = std::max(1, std::min(KB, KS_KB_MAX));
+      Scratch tmp(c, KB > 1 ? (size_t)KB * B * 2 * LN * 8 : 8);
+      for (int k0 = 1; k0 < n; k0 += KB) {
+        const int kb = std::min(KB, n - k0);
+        KsArgs a = ks_base(c, B, Lc, ext, x->d + LN, 2 * LN);
+        a.KB = kb;
+        for (int kk = 0; kk < kb; ++kk) {
+          a.keys[kk] = keys[k0 + kk];
+          a.gal[kk] = gals[k0 + kk];
+        }
+        a.addsrc = x->d;
+        a.add_bs = 2 * LN;
+        a.add_parts = 1;
+        a.add_gather = 1;
+        a.D = diags->d + (size_t)k0 * LN;
+        a.D_ks = LN;
+        a.out_bs = 2 * LN;
+        if (KB == 1) {
+          a.out = acc->d;
+          a.acc_in = acc->d;
+          a.out_ks = 0;
+          ks_launch(c, a);
+        } else {
+          a.out = tmp.as<u64>();
+          a.out_ks = (size_t)B * 2 * LN;
+          ks_launch(c, a);
+          const size_t rows = (size_t)B * 2 * Lc;
+          k_accumulate<<<rows_grid2(c, rows), 256, 0, c->stream>>>(acc->d, tmp.as<u64>(), kb, (size_t)B * 2 * LN,
+                                                                   c->d_primes, c->N, Lc, rows);
+          check_launch(c);
+        }
+      }
+    }
+    res = ct_rescale(c, acc);
+  } catch (...) {
+    dfree(c, ext);
+    ct_free(acc);
+    throw;
+  }
+  dfree(c, ext);
+  ct_free(acc);
+  if (bias) {
+    he_ciphertext* r2 = ct_add_plain(c, res, bias);
+    ct_free(res);
+    res = r2;
+  }
+  return res;
+}
+
+// im2col conv on the encrypted side (a15, C18/C19).
+he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
+                       const he_plaintext* masks, const he_plaintext* bias, int chunk) {
+  const int Lc = x->level + 1, C = kernels->B, B = x->B;
+  const size_t LN = (size_t)Lc * c->N;
+  he_ciphertext* T = ct_new(c, B * C, 2, x->level, x->scale * kernels->scale);
+  const size_t rows = (size_t)B * C * 2 * Lc;
+  k_mul_plain_outer<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, kernels->d, T->d, c->d_primes, c->N, Lc, C,
+                                                                rows);
+  check_launch(c);
+  he_ciphertext* t = nullptr;
+  try {
+    t = ct_rescale(c, T);
+    ct_free(T);
+    T = nullptr;
+    const int ns = c->N / 2;
+    for (int step = chunk; step < ns; step <<= 1) {
+      he_ciphertext* t2 = ct_rotate(c, t, step, true);
+      ct_free(t);
+      t = t2;
+    }
+    const int Lc2 = t->level + 1;
+    he_ciphertext* acc = ct_new(c, B, 2, t->level, t->scale * masks->scale);
+    const size_t rows2 = (size_t)B * 2 * Lc2;
+    k_mask_sum<<<rows_grid2(c, rows2), 256, 0, c->stream>>>(t->d, masks->d, acc->d, c->d_primes, c->N, Lc2, C,
+                                                            rows2);
+    check_launch(c);
+    ct_free(t);
+    t = nullptr;
+    he_ciphertext* r = ct_rescale(c, acc);
+    ct_free(acc);
+    if (bias) {
+      he_ciphertext* r2 = ct_add_plain(c, r, bias);
+      ct_free(r);
+      r = r2;
+    }
+    return r;
+  } catch (...) {
+    ct_free(T);
+    ct_free(t);
+    throw;
+  }
+}
+
+// ---- keygen (a2/a3, C9-C12) --------------------------------------------------
+static void make_ksk(he_context* c, u64* key, u64 pur_a, u64 pur_e, u64 objbase, u32 gal) {
+  const int L = c->L, NP = c->NP, N = c->N;
+  // a_j[t] uniform (NTT words) straight into part 1
+  k_sample_uniform<<<dim3((N + 255) / 256, std::min(L * NP, 65535)), 256, 0, c->stream>>>(
+      key + (size_t)NP * N, (size_t)2 * NP * N, L, NP, N, c->seed, pur_a, objbase, c->d_primes);
+  check_launch(c);
+  // e_j: one CDT polynomial per digit, NTT into every limb
+  Scratch e(c, (size_t)L * N * 8), et(c, (size_t)L * NP * N * 8);
+  k_sample_small<<<dim3((N + 255) / 256, std::min(L, 65535)), 256, 0, c->stream>>>(e.as<i64>(), N, L, c->seed,
+                                                                                 pur_e, objbase, 1, c->d_cdt);
+  check_launch(c);
+  signed_to_ntt(c, e.as<i64>(), et.as<u64>(), L, NP);
+  k_ksk_combine<<<dim3((N + 255) / 256, std::min(L * NP, 65535)), 256, 0, c->stream>>>(
+      key, et.as<u64>(), c->d_sk, c->d_P_mod, c->d_primes, N, c->logN, L, NP, gal);
+  check_launch(c);
+}
+
+void keygen(he_context* c, const std::vector<int>& steps) {
+  const int L = c->L, NP = c->NP, N = c->N;
+  HE_CK(cudaMalloc(&c->d_sk, (size_t)NP * N * 8));
+  {
+    Scratch s(c, (size_t)N * 8);
+    k_sample_small<<<dim3((N + 255) / 256, 1), 256, 0, c->stream>>>(s.as<i64>(), N, 1, c->seed, PUR_S, 0, 0,
+                                                                   c->d_cdt);
+    check_launch(c);
+    signed_to_ntt(c, s.as<i64>(), c->d_sk, 1, NP);
+  }
+  c->has_sk = true;
+  HE_CK(cudaMalloc(&c->d_pk, (size_t)2 * L * N * 8));
+  {
+    k_sample_uniform<<<dim3((N + 255) / 256, L), 256, 0, c->stream>>>(c->d_pk + (size_t)L * N, 0, 1, L, N,
+                                                                      c->seed, PUR_PK_A, 0, c->d_primes);
+    check_launch(c);
+    Scratch e(c, (size_t)N * 8), et(c, (size_t)L * N * 8);
+    k_sample_small<<<dim3((N + 255) / 256, 1), 256, 0, c->stream>>>(e.as<i64>(), N, 1, c->seed, PUR_PK_E, 0, 1,
+                                                                   c->d_cdt);
+    check_launch(c);
+    signed_to_ntt(c, e.as<i64>(), et.as<u64>(), 1, L);
+    k_pk_combine<<<dim3((N + 255) / 256, L), 256, 0, c->stream>>>(c->d_pk, et.as<u64>(), c->d_sk, c->d_primes,
+                                                                  N, L);
+    check_launch(c);
+  }
+  c->has_pk = true;
+  if (c->K > 0) {
+    const size_t kw = (size_t)L * 2 * NP * N;
+    HE_CK(cudaMalloc(&c->d_rlk, kw * 8));
+    make_ksk(c, c->d_rlk, PUR_RLK_A, PUR_RLK_E, 0, 0);
+    c->has_rlk = true;
+    for (int st : steps) {
+      const u64 g = galois_element(N, st);
+      if (c->gk.count(g)) continue;
+      u64* key = nullptr;
+      HE_CK(cudaMalloc(&key, kw * 8));
+      c->gk[g] = key;
+      make_ksk(c, key, PUR_GK_A, PUR_GK_E, g << 8, (u32)g);
+    }
+  }
+  HE_CK(cudaStreamSynchronize(c->stream));
+}
+
+// ---- encode / decode / encrypt / decrypt --------------------------------------
+he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level) {
+  const int N = c->N, M = N / 2, logM = c->logN - 1;
+  Scratch m(c, B * N * 8), flag(c, 4);
+  HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
+  const bool in_smem = M <= 8192;
+  Scratch g(c, in_smem ? 8 : B * M * 16);
+  const int smem = in_smem ? M * 16 : 0;
+  if (smem > 48 * 1024)
+    HE_CK(cudaFuncSetAttribute(k_encode_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m.as<i64>(), flag.as<int>(), c->d_slot_index,
+                                                      c->d_fft_w, c->d_zeta, N, logM,
+                                                      in_smem ? nullptr : g.as<double2>());
+  check_launch(c);
+  int hflag = 0;
+  HE_CK(cudaMemcpyAsync(&hflag, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  HE_CK(cudaStreamSynchronize(c->stream));
+  if (hflag) throw HeError(HE_SCALE_OVERFLOW, "encode: |scale * z| >= 2^62");
+  he_plaintext* pt = pt_new(c, (int)B, level, scale);
+  signed_to_ntt(c, m.as<i64>(), pt->d, B, level + 1);
+  return pt;
+}
+
+he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level) {
+  he_plaintext* pt = pt_new(c, (int)B, level, scale);
+  signed_to_ntt(c, m_dev, pt->d, B, level + 1);
+  return pt;
+}
+
+void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n) {
+  const int N = c->N, M = N / 2, logM = c->logN - 1, Lc = pt->level + 1;
+  const size_t B = pt->B;
+  Scratch coef(c, B * Lc * N * 8), X(c, B * N * 8);
+  ntt_rows(c, pt->d, coef.as<u64>(), B, Lc, (size_t)Lc * N, (size_t)Lc * N, true);
+  const size_t total = B * N;
+  k_crt_compose<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, c->stream>>>(
+      coef.as<u64>(), X.as<double>(), c->d_crt + c->hp.crt_off[pt->level], c->d_primes, N, Lc, total);
+  check_launch(c);
+  const bool in_smem = M <= 8192;
+  Scratch g(c, in_smem ? 8 : B * M * 16);
+  const int smem = in_smem ? M * 16 : 0;
+  if (smem > 48 * 1024)
+    HE_CK(cudaFuncSetAttribute(k_decode_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_decode_fft<<<(unsigned)B, 512, smem, c->stream>>>(X.as<double>(), n, pt->scale, out_dev, c->d_slot_index,
+                                                      c->d_fft_w, c->d_zeta, N, logM,
+                                                      in_smem ? nullptr : g.as<double2>());
+  check_launch(c);
+}
+
+he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
+  const int N = c->N, Lc = pt->level + 1, B = pt->B;
+  // small polys [which][B][N]: v (C10 ternary), e0, e1 (C11 CDT); item b uses stream stream_id + b
+  Scratch small(c, (size_t)3 * B * N * 8), noise(c, (size_t)B * 3 * Lc * N * 8);
+  const dim3 g((N + 255) / 256, std::min(B, 65535));
+  const u64 pur[3] = {PUR_ENC_V, PUR_ENC_E0, PUR_ENC_E1};
+  for (int w = 0; w < 3; ++w) {
+    k_sample_small<<<g, 256, 0, c->stream>>>(small.as<i64>() + (size_t)w * B * N, N, B, c->seed, pur[w], stream_id,
+                                            w == 0 ? 0 : 1, c->d_cdt);
+    check_launch(c);
+    // NTT into noise [b][w][Lc][N]
+    JobSignedToNtt j{small.as<i64>() + (size_t)w * B * N, noise.as<u64>() + (size_t)w * Lc * N, N, Lc, (size_t)N,
+                     (size_t)3 * Lc * N};
+    launch_ntt<false>(c, j, B * Lc);
+  }
+  he_ciphertext* ct = ct_new(c, B, 2, pt->level, pt->scale);
+  const size_t rows = (size_t)B * Lc;
+  k_encrypt_combine<<<rows_grid2(c, rows), 256, 0, c->stream>>>(noise.as<u64>(), c->d_pk, pt->d,
+                                                               pt->B == 1 ? 0 : (size_t)Lc * N, ct->d, c->d_primes,
+                                                               N, Lc, c->L, rows);
+  check_launch(c);
+  return ct;
+}
+
+he_plaintext* decrypt(he_context* c, const he_ciphertext* ct) {
+  const int Lc = ct->level + 1;
+  he_plaintext* pt = pt_new(c, ct->B, ct->level, ct->scale);
+  const size_t rows = (size_t)ct->B * Lc;
+  k_decrypt<<<rows_grid2(c, rows), 256, 0, c->stream>>>(ct->d, c->d_sk, pt->d, c->d_primes, c->N, Lc, ct->size,
+                                                       rows);
+  check_launch(c);
+  return pt;
+}
+
+int check_words(he_context* c, const u64* w, size_t items, int Lc) {
+  Scratch flag(c, 4);
+  HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
+  const size_t rows = items * Lc;
+  k_check_words<<<rows_grid2(c, rows), 256, 0, c->stream>>>(w, c->d_primes, c->N, Lc, rows, flag.as<int>());
+  check_launch(c);
+  int h = 0;
+  HE_CK(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  HE_CK(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+}  // namespace he

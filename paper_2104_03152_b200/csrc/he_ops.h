@@ -1,0 +1,50 @@
+// he_ops.h — internal operations behind the C-ABI (he_capi.cu).  Product code.
+#pragma once
+#include <vector>
+
+#include "he_internal.cuh"
+
+namespace he {
+
+inline size_t ct_words(const he_ciphertext* c) { return (size_t)c->B * c->size * (c->level + 1) * c->ctx->N; }
+inline size_t pt_words(const he_plaintext* p) { return (size_t)p->B * (p->level + 1) * p->ctx->N; }
+
+void context_init(he_context* c, const HostParams& hp, u64 seed);
+void context_destroy(he_context* c);
+
+he_ciphertext* ct_new(he_context* c, int B, int size, int level, double scale);
+he_plaintext* pt_new(he_context* c, int B, int level, double scale);
+void ct_free(he_ciphertext* ct);
+void pt_free(he_plaintext* pt);
+
+// ring primitives on raw device words [items][nl][N]
+void ntt_rows(he_context* c, const u64* src, u64* dst, size_t items, int nl, size_t src_bs, size_t dst_bs,
+              bool inverse);
+void modmul_rows(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl);
+void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl);
+void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int nl);
+int check_words(he_context* c, const u64* w, size_t items, int Lc);
+
+// scheme
+void keygen(he_context* c, const std::vector<int>& steps);
+he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level);
+he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level);
+void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n);
+he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id);
+he_plaintext* decrypt(he_context* c, const he_ciphertext* ct);
+
+he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b);  // 0 add, 1 sub
+he_ciphertext* ct_negate(he_context* c, const he_ciphertext* a);
+he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p);
+he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p);
+he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphertext* y);
+he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a);
+he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a);
+he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool add_input);
+he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
+                          const he_plaintext* bias);
+he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
+                       const he_plaintext* masks, const he_plaintext* bias, int chunk);
+const u64* galois_key(he_context* c, int step, u32* gal_out);
+
+}  // namespace he
