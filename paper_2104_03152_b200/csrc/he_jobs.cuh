@@ -152,8 +152,8 @@ struct JobKsSpecial {
   }
 };
 
-// a9 data limbs: conv_i = sum_k tb_k [P/p_k]_{q_i} (coefficient domain), NTT,
-// then u = (IP_i + [P/2]_{q_i} - NTT(conv_i)) P^{-1} and the epilogue.
+// a9 data limbs: c_i = sum_k tb_k [P/p_k]_{q_i} - [P/2]_{q_i} (coefficient
+// domain), NTT, then u = (IP_i - NTT(c_i)) P^{-1} and the epilogue.
 struct JobKsData {
   KsArgs a;
   __device__ void dec(int blk, int& kk, int& b, int& part, int& i) const {
@@ -173,7 +173,9 @@ struct JobKsData {
       const u64 t = a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n];
       conv = add_mod(conv, mul_mod(reduce64(t, P), __ldg(a.Phat_mod + (size_t)k * a.NP + i), P), P.q);
     }
-    return conv;
+    // the +[P/2]_{q_i} of C15 is added to every COEFFICIENT, so it is folded
+    // here (coefficient domain) rather than after the transform
+    return sub_mod(conv, __ldg(a.Ph_mod + i), P.q);
   }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     int kk, b, part, i;
@@ -181,8 +183,7 @@ struct JobKsData {
     const u32 g = a.gal[kk];
     const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
     const u64 ip = ks_inner(a, kk, b, part, i, i, sn, n, P);
-    u64 u = sub_mod(add_mod(ip, __ldg(a.Ph_mod + i), P.q), v, P.q);
-    u = mul_mod(u, __ldg(a.Pinv_mod + i), P);
+    u64 u = mul_mod(sub_mod(ip, v, P.q), __ldg(a.Pinv_mod + i), P);
     const size_t LN = (size_t)a.Lc * a.N;
     if (part < a.add_parts)
       u = add_mod(u, a.addsrc[(size_t)b * a.add_bs + part * LN + (size_t)i * a.N + (a.add_gather ? sn : n)], P.q);
@@ -206,7 +207,7 @@ struct JobRescaleLast {
     y[(size_t)blk * N + n] = add_mod(v, (P.q - 1) >> 1, P.q);
   }
 };
-// a11 rescale, step 2: out_i = (x_i + [h]_{q_i} - NTT_i([y]_{q_i})) [q_l^{-1}]_{q_i}.
+// a11 rescale, step 2: out_i = (x_i - NTT_i([y]_{q_i} - [h]_{q_i})) [q_l^{-1}]_{q_i}.
 struct JobRescaleData {
   const u64* x;
   const u64* y;
@@ -216,12 +217,14 @@ struct JobRescaleData {
   int N, Lc;
   __device__ int prime(int blk) const { return blk % (Lc - 1); }
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
-    return reduce64(y[(size_t)(blk / (Lc - 1)) * N + n], P);
+    // [y]_{q_i} - [h]_{q_i}: h is added to every coefficient (C15), so it is
+    // folded in before the forward transform
+    return sub_mod(reduce64(y[(size_t)(blk / (Lc - 1)) * N + n], P), __ldg(h + blk % (Lc - 1)), P.q);
   }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
     const u64 xi = x[((size_t)r * Lc + i) * N + n];
-    const u64 t = sub_mod(add_mod(xi, __ldg(h + i), P.q), v, P.q);
+    const u64 t = sub_mod(xi, v, P.q);
     out[((size_t)r * (Lc - 1) + i) * N + n] = mul_mod(t, __ldg(qinv + i), P);
   }
 };
