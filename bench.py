@@ -1,0 +1,367 @@
+"""Benchmark of the B200 CKKS hot path (BASELINE.json metric).
+
+Headline workload (BASELINE config 5 = the config-4 network on a stream of
+seeded synthetic 28x28 images, sharded across GPUs): one STEP is, for a batch
+of B images per GPU, encode -> encrypt -> im2col conv -> square -> FC1 ->
+square -> FC2 -> decrypt -> decode, all in this library's sm_100a kernels.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+* value: encrypted CNN inferences/s of the whole job (all ranks), inputs (the
+  im2col'd slot vectors, float64) resident in HBM, CUDA events on the
+  library's stream, barrier + synchronize around K steps, max over ranks.
+* e2e: the same metric through the public API from pinned host images:
+  host im2col, H2D of the slot vectors inside he_encode, ..., D2H logits.
+* roofline: the dominant kernel (largest share of the step), its algorithmic
+  bytes / CUDA-event time against MEASURED_PEAKS.json HBM GB/s.
+* cpu_baseline (rank 0, N=1): the CPU oracle (oracle/, test infrastructure)
+  timed on a bounded sample of the same workload.
+* extra: key-switch rotations/s (config 3 shape) and NTT GB/s (config 2 shape).
+* --impl reference: the oracle (this tier's reference arm) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encrypted 28x28 CNN inferences/s/box"
+UNIT = "images/s"
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.stop = index, [], threading.Event()
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- ours ---
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2104_03152_b200 import Context, he_im2col_encode
+    from paper_2104_03152_b200.cnn import EncryptedCNN, rotation_steps
+    from synthetic import CFG4, cnn_weights, mnist_like_images
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    B = args.batch
+
+    ctx = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    ctx.he_set_stream(stream)
+    ctx.he_keygen(rotation_steps())
+    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed))
+    ns = ctx.slots
+
+    # this rank's shard of the image stream (image i depends only on (seed, i))
+    def shard(step):
+        start = (step * world + rank) * B
+        return mnist_like_images(B, 4, start=start)
+
+    n_batches = 2   # distinct input batches cycled through the steps
+    imgs_host = [shard(s) for s in range(n_batches)]
+    slots_host = [np.stack([he_im2col_encode(im, 7, 7, 3, ns)[0] for im in imgs]) for imgs in imgs_host]
+    slots_dev = [torch.from_numpy(s).to(dev) for s in slots_host]
+    logits_dev = torch.empty((B, net.n_out), dtype=torch.float64, device=dev)
+
+    def step_device(i):
+        x = slots_dev[i % n_batches]
+        pt = ctx.he_encode(x, 2.0 ** net.plan["in_log2"], net.top)
+        ct = ctx.he_encrypt(pt, 1_000_000 + i * B)
+        out = net.forward(ct)
+        ctx.he_decode(ctx.he_decrypt(out), net.n_out, out=logits_dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, K, W):
+        for i in range(W):
+            fn(i)
+        barrier()
+        l0 = ctx.he_launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(K):
+            fn(W + i)
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, ctx.he_launch_count() - l0
+
+    # --- device-resident timed region (headline value) ---
+    with ClockSampler(local_rank) as clk:
+        ms, launches = timed(step_device, args.steps, args.warmup)
+    value = world * B * args.steps / (ms / 1e3)
+
+    # --- kernel breakdown + roofline of the dominant kernel (profiled steps) ---
+    ctx.he_profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(2):
+        step_device(i)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    prof_step_ms = e0.elapsed_time(e1) / 2
+    prof = ctx.he_profile_read()
+    ctx.he_profile_enable(False)
+    tot = sum(v[1] for v in prof.values())
+    top = max(prof, key=lambda k: prof[k][1])
+    n_l, t_ms, alg_b, _ = prof[top]
+    peaks = load_peaks()
+    achieved = (alg_b / n_l) / (t_ms / n_l / 1e3) / 1e9 if t_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                "share_of_step": round(t_ms / 2 / prof_step_ms, 3),
+                "alg_bytes_per_launch": alg_b / n_l, "us_per_launch": round(t_ms / n_l * 1e3, 2),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+                if not peaks.get("_fallback") else "fallback 6650 GB/s"}
+    breakdown = {k: {"launches_per_step": v[0] / 2, "ms_per_step": round(v[1] / 2, 3),
+                     "share": round(v[1] / tot, 3)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+
+    # --- e2e through the public API from pinned host images ---
+    pinned = [torch.from_numpy(imgs).pin_memory() for imgs in imgs_host]
+    slot_buf = torch.empty((B, ns), dtype=torch.float64).pin_memory()
+    logits_host = np.zeros((B, net.n_out))
+
+    def step_e2e(i):
+        imgs = pinned[i % n_batches].numpy()
+        sb = slot_buf.numpy()
+        for b in range(B):
+            sb[b] = he_im2col_encode(imgs[b], 7, 7, 3, ns)[0]
+        pt = ctx.he_encode(sb, 2.0 ** net.plan["in_log2"], net.top)   # H2D inside the C call
+        ct = ctx.he_encrypt(pt, 2_000_000 + i * B)
+        logits_host[:] = ctx.he_decode(ctx.he_decrypt(net.forward(ct)), net.n_out)   # D2H inside
+
+    e2e_ms, _ = timed(step_e2e, args.steps, 1)
+    e2e = {"value": world * B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": B * ns * 8, "d2h_bytes_per_step": B * net.n_out * 8}
+
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        extra = micro_extra(ctx, stream, dev)
+
+    # result collection to rank 0 (outside the timed region): NCCL gather of logits
+    if world > 1:
+        gathered = [torch.empty_like(logits_dev) for _ in range(world)] if rank == 0 else None
+        dist.gather(logits_dev, gathered, dst=0)
+
+    return dict(value=value, ms=ms, launches=launches, clocks=clk.summary(), roofline=roofline,
+                breakdown=breakdown, e2e=e2e, extra=extra)
+
+
+def micro_extra(ctx_cnn, stream, dev):
+    """Config 2 (NTT GB/s) and config 3 (key-switch rotations/s) shapes, device-timed."""
+    import torch
+    from paper_2104_03152_b200 import Context
+    from synthetic import CFG2_PRIME_BITS, CFG3, messages
+    out = {}
+    # config 2: N=16384, L=8, B=256 forward / inverse / fused ring product
+    N, L, B = 1 << 14, 8, 256
+    c2 = Context(14, CFG2_PRIME_BITS(L), 0, 1)
+    c2.he_set_stream(stream)
+    q = torch.tensor([int(x) for x in c2.primes], dtype=torch.float64, device=dev)
+    a = (torch.rand((B, L, N), dtype=torch.float64, device=dev) * q[None, :, None]).to(torch.int64)
+    b = (torch.rand((B, L, N), dtype=torch.float64, device=dev) * q[None, :, None]).to(torch.int64)
+    o = torch.empty_like(a)
+
+    def t(fn, reps=5):
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    s_f = t(lambda: c2.he_ntt_forward(a, B, L))
+    s_i = t(lambda: c2.he_ntt_inverse(a, B, L))
+    s_m = t(lambda: c2.he_ntt_mul_intt(a, b, o, B, L))
+    nbytes = 16 * N * L * B
+    out["ntt_cfg2"] = {"shape": "N=16384 L=8 B=256 (4.3 GB/s basis: 16 N L B bytes)",
+                       "fwd_GBps": round(nbytes / s_f / 1e9, 1), "inv_GBps": round(nbytes / s_i / 1e9, 1),
+                       "fused_fwd_mul_inv_GBps": round(24 * N * L * B / s_m / 1e9, 1)}
+    del a, b, o
+    # config 3: N=16384, 8 data + 2 special 50-bit primes, 256 ciphertexts, rotations by 2^r and ct x ct
+    c3 = Context(CFG3.logN, CFG3.bits, CFG3.n_special, CFG3.seed)
+    c3.he_set_stream(stream)
+    steps = [1 << r for r in range(14)]
+    c3.he_keygen(steps)
+    Bc = 256
+    z = torch.from_numpy(messages(Bc, c3.slots, seed=CFG3.seed)).to(dev)
+    ct = c3.he_encrypt(c3.he_encode(z, 2.0 ** 50, c3.L - 1), 0)
+    s_rot = t(lambda: [c3.he_rotate(ct, s) for s in steps], reps=2)
+    s_mul = t(lambda: c3.he_rescale(c3.he_relinearize(c3.he_mul(ct, ct))), reps=3)
+    out["keyswitch_cfg3"] = {"shape": "N=16384, 8+2 x 50-bit primes, 256 ciphertexts, top level",
+                             "rotations_per_s": round(Bc * len(steps) / s_rot, 1),
+                             "mul_relin_rescale_per_s": round(Bc / s_mul, 1)}
+    return out
+
+
+# ------------------------------------------------------- oracle (CPU) ---
+def oracle_sample(images: int = 1):
+    """Oracle CNN (encrypt + forward + decrypt) on `images` images; returns (images/s, threads, note)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import circuits as OC
+    from oracle.oracle import OracleContext
+    from synthetic import CFG4, cnn_weights, mnist_like_images
+    o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    o.keygen(OC.cnn_rotation_steps())
+    w = cnn_weights(CFG4.seed)
+    imgs = mnist_like_images(images, 4, start=10_000)
+    cores = os.cpu_count() or 1
+
+    def one(i):
+        ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + i)
+        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w)), 10)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(images, cores)) as ex:
+        list(ex.map(one, range(images)))
+    dt = time.perf_counter() - t0
+    return images / dt, min(images, cores), dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    # each step: one full image through the oracle (encrypt + forward + decrypt), images
+    # processed in parallel over the host cores as the oracle allows (independent items)
+    per_step = 1
+    from oracle import circuits as OC  # noqa: F401  (import cost outside timing)
+    times = []
+    for i in range(args.warmup + args.steps):
+        v, cores, dt = oracle_sample(per_step)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = per_step / (ms / 1e3)
+    return dict(value=value, ms=ms, cores=1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+
+    config = {"workload": "BASELINE config 5 (config-4 CNN on seeded synthetic 28x28 images, sharded)",
+              "network": "conv7x7s3x4 -> x^2 -> fc256x64 -> x^2 -> fc64x10 (PAPER.md:98)",
+              "ckks": "N=8192, primes [31,26x6,31], scale 2^26 (input 2^30), 259 Galois keys",
+              "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+              "step": "encode+encrypt+conv+square+fc1+square+fc2+decrypt+decode",
+              "parallelism": f"dp{world} (independent images, no data-path collective)",
+              "l2": "inputs larger than L2 (1.9 GB of Galois keys read every step)"}
+
+    if args.impl == "reference":
+        r = run_reference(args, rank, world)
+        if rank == 0:
+            line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms"],
+                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                    "data": "synthetic", "config": dict(config, batch_per_gpu=1, global_batch=1,
+                                                        reference="CPU oracle (oracle/), 1 image per step"),
+                    "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                                     "sample": "1 image (encrypt + forward + decrypt) per step"},
+                    "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    r = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, dt = oracle_sample(1)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"1 image (encrypt + forward + decrypt) through the CPU oracle, {dt:.1f} s"}
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": config, "clocks": r["clocks"], "gpu_launches": r["launches"],
+                "e2e": r["e2e"], "roofline": r["roofline"], "cpu_baseline": cpu,
+                "breakdown": r["breakdown"], "extra": r["extra"],
+                "paper_context": "TenSEAL/SEAL CPU: 1456.29 ms/img (8 vCPU), 887.06 ms/img (16 vCPU), PAPER.md:113"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

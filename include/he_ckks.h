@@ -265,6 +265,15 @@ he_status he_modmul(he_context* ctx, const uint64_t* a, const uint64_t* b, uint6
 he_status he_ntt_mul_intt(he_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,
                           size_t B, int n_limbs);
 
+/* Opt-in profiler: with `on` != 0 every kernel launch of ctx is bracketed
+ * by CUDA events recorded on the context stream.  he_profile_read
+ * synchronises the stream and writes a JSON object into buf (NUL-terminated,
+ * truncated to len):  {"<kernel tag>": [launches, total_ms, alg_bytes,
+ * blocks], ...}  where alg_bytes are the algorithmic bytes of those launches
+ * (0 where not modelled).  Reading resets the records. */
+he_status he_profile_enable(he_context* ctx, int on);
+he_status he_profile_read(he_context* ctx, char* buf, size_t len);
+
 /* Number of kernels this library has launched on ctx (for the bench's
  * gpu_launches claim). */
 uint64_t he_launch_count(const he_context* ctx);

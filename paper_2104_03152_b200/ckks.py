@@ -100,6 +100,8 @@ _SIGS = {
     "he_modmul": [VP, VP, VP, VP, SZ, C.c_int],
     "he_ntt_mul_intt": [VP, VP, VP, VP, SZ, C.c_int],
     "he_launch_count": [VP],
+    "he_profile_enable": [VP, C.c_int],
+    "he_profile_read": [VP, C.c_char_p, SZ],
     "he_last_error": [],
 }
 _RESTYPES = {"he_key_words": C.c_size_t, "he_launch_count": C.c_uint64, "he_last_error": C.c_char_p}
@@ -258,6 +260,16 @@ class Context:
 
     def he_launch_count(self) -> int:
         return int(lib().he_launch_count(self.h))
+
+    def he_profile_enable(self, on: bool = True) -> None:
+        _check(lib().he_profile_enable(self.h, int(bool(on))))
+
+    def he_profile_read(self) -> dict:
+        """{kernel tag: [launches, total_ms, alg_bytes, blocks]} since the last read."""
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        _check(lib().he_profile_read(self.h, buf, len(buf)))
+        return json.loads(buf.value.decode())
 
     def he_keygen(self, steps=()) -> None:
         steps = [int(s) for s in steps]

@@ -164,6 +164,45 @@ he_status he_sync(he_context* c) {
 
 uint64_t he_launch_count(const he_context* c) { return c ? c->launches : 0; }
 
+he_status he_profile_enable(he_context* c, int on) {
+  return guard([&] {
+    need_ctx(c);
+    c->prof_on = on != 0;
+  });
+}
+
+he_status he_profile_read(he_context* c, char* buf, size_t len) {
+  return guard([&] {
+    need_ctx(c);
+    need(buf != nullptr && len > 0, HE_INVALID_ARGUMENT, "null buffer");
+    HE_CK(cudaStreamSynchronize(c->stream));
+    struct Acc { long n = 0; double ms = 0, bytes = 0, blocks = 0; };
+    std::map<std::string, Acc> acc;
+    for (auto& r : c->prof) {
+      float ms = 0;
+      HE_CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      Acc& a = acc[r.tag];
+      a.n++;
+      a.ms += ms;
+      a.bytes += r.bytes;
+      a.blocks += r.blocks;
+      c->ev_pool.push_back(r.a);
+      c->ev_pool.push_back(r.b);
+    }
+    c->prof.clear();
+    std::string js = "{";
+    for (auto& kv : acc) {
+      char tmp[256];
+      snprintf(tmp, sizeof(tmp), "%s\"%s\": [%ld, %.6f, %.1f, %.0f]", js.size() > 1 ? ", " : "", kv.first.c_str(),
+               kv.second.n, kv.second.ms, kv.second.bytes, kv.second.blocks);
+      js += tmp;
+    }
+    js += "}";
+    strncpy(buf, js.c_str(), len - 1);
+    buf[len - 1] = 0;
+  });
+}
+
 he_status he_keygen(he_context* c, const int32_t* steps, size_t n_steps) {
   return guard([&] {
     need_ctx(c);

@@ -12,6 +12,7 @@
 #include "../../include/he_ckks.h"
 #include "he_common.cuh"
 #include "he_host.h"
+#include "he_jobs.cuh"
 #include "he_ntt.cuh"
 
 namespace he {
@@ -55,6 +56,11 @@ struct he_context {
   he::u64* d_rlk = nullptr;  // [L][2][NP][N]
   std::map<he::u64, he::u64*> gk;  // Galois element -> [L][2][NP][N]
   std::vector<void*> owned;        // device allocations freed with the context
+  // opt-in profiler: CUDA events around every NTT-family launch
+  struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
 };
 
 struct he_ciphertext {
@@ -94,6 +100,37 @@ inline void check_launch(he_context* c) {
   if (e != cudaSuccess) throw HeError(HE_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
+inline cudaEvent_t prof_event(he_context* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  HE_CK(cudaEventCreate(&e));
+  return e;
+}
+
+// RAII profiling scope around one launch (no-op unless c->prof_on).
+struct ProfScope {
+  he_context* c;
+  he_context::ProfRec rec;
+  ProfScope(he_context* c_, const char* tag, double bytes, int blocks) : c(c_) {
+    rec = he_context::ProfRec{tag, nullptr, nullptr, bytes, blocks};
+    if (c->prof_on) {
+      rec.a = prof_event(c);
+      rec.b = prof_event(c);
+      HE_CK(cudaEventRecord(rec.a, c->stream));
+    }
+  }
+  ~ProfScope() {
+    if (c->prof_on && rec.b) {
+      cudaEventRecord(rec.b, c->stream);
+      c->prof.push_back(rec);
+    }
+  }
+};
+
 // ---- NTT launch with per-instantiation smem opt-in -----------------------
 template <int LOGN, int CL, bool INV, class Job>
 void launch_ntt_t(he_context* c, const Job& job, int nblk) {
@@ -108,6 +145,7 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
   if (nblk <= 0) return;
   const u64* tw = INV ? c->d_itw : c->d_tw;
   const u64* twsh = INV ? c->d_itwsh : c->d_twsh;
+  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk);
   if (CL == 1) {
     kern<<<nblk, G::T, G::SMEM, c->stream>>>(job, c->d_primes, tw, twsh);
   } else {

@@ -8,6 +8,7 @@ namespace he {
 // Plain transform of limbs: blk -> (item = blk / nl, limb = blk % nl), limb l
 // modulo prime l; items at strides src_bs / dst_bs words.
 struct JobLimbs {
+  static constexpr const char* kName = "ntt_limbs";
   const u64* src;
   u64* dst;
   int N, nl;
@@ -23,6 +24,7 @@ struct JobLimbs {
 
 // Fused ring product out = INTT(NTT(a) (.) b) (config 2 "fwd -> modmul -> inv").
 struct JobRingMul {
+  static constexpr const char* kName = "ntt_mul_intt";
   const u64* a;
   const u64* b;
   u64* out;
@@ -37,6 +39,7 @@ struct JobRingMul {
 // key generation): blk -> (item = blk / nl, limb = blk % nl); reads
 // poly[item * src_bs + i] (int64), writes dst[item * dst_bs + limb * N + i].
 struct JobSignedToNtt {
+  static constexpr const char* kName = "ntt_small";
   const i64* poly;
   u64* dst;
   int N, nl;
@@ -54,6 +57,7 @@ struct JobSignedToNtt {
 // INTT'd), centered lift (C16) into target t != j, NTT_t.
 //   coef: [B][Lc][N]; ext: [B][Lc][Lc+K][N] (t < Lc data, t >= Lc special).
 struct JobModUp {
+  static constexpr const char* kName = "ks_modup";
   const u64* coef;
   u64* ext;
   const u64* qtab;   // device table of all primes
@@ -127,6 +131,7 @@ __device__ __forceinline__ u64 ks_inner(const KsArgs& a, int kk, int b, int part
 // a9 special limbs: inner product at p_k, INTT, then
 // tb = [ (x + [P/2]_{p_k}) (P/p_k)^{-1} ]_{p_k}    (C15 y_k and its CRT weight)
 struct JobKsSpecial {
+  static constexpr const char* kName = "ks_special";
   KsArgs a;
   __device__ void dec(int blk, int& kk, int& b, int& part, int& k) const {
     k = blk % a.K;
@@ -155,6 +160,7 @@ struct JobKsSpecial {
 // a9 data limbs: c_i = sum_k tb_k [P/p_k]_{q_i} - [P/2]_{q_i} (coefficient
 // domain), NTT, then u = (IP_i - NTT(c_i)) P^{-1} and the epilogue.
 struct JobKsData {
+  static constexpr const char* kName = "ks_data";
   KsArgs a;
   __device__ void dec(int blk, int& kk, int& b, int& part, int& i) const {
     i = blk % a.Lc;
@@ -196,6 +202,7 @@ struct JobKsData {
 
 // a11 rescale, step 1: INTT of the last limb l, y = [x_l + (q_l-1)/2]_{q_l}.
 struct JobRescaleLast {
+  static constexpr const char* kName = "rescale_last";
   const u64* x;     // [R][Lc][N] (R = B*size rows of polynomials)
   u64* y;           // [R][N]
   int N, Lc;
@@ -209,6 +216,7 @@ struct JobRescaleLast {
 };
 // a11 rescale, step 2: out_i = (x_i - NTT_i([y]_{q_i} - [h]_{q_i})) [q_l^{-1}]_{q_i}.
 struct JobRescaleData {
+  static constexpr const char* kName = "rescale_data";
   const u64* x;
   const u64* y;
   u64* out;         // [R][Lc-1][N]
@@ -228,5 +236,36 @@ struct JobRescaleData {
     out[((size_t)r * (Lc - 1) + i) * N + n] = mul_mod(t, __ldg(qinv + i), P);
   }
 };
+
+// Algorithmic bytes of one launch of nblk blocks: every distinct input word
+// read once and every output word written once.
+inline double alg_bytes(const JobLimbs& j, int nblk) { return 16.0 * j.N * nblk; }
+inline double alg_bytes(const JobRingMul& j, int nblk) { return 24.0 * j.N * nblk; }
+inline double alg_bytes(const JobSignedToNtt& j, int nblk) { return 8.0 * j.N * (nblk + nblk / j.nl); }
+inline double alg_bytes(const JobModUp& j, int nblk) {
+  const int nt = j.Lc + j.K - 1;
+  return 8.0 * j.N * (nblk + (double)nblk / nt);
+}
+inline double alg_bytes(const JobKsSpecial& j, int) {
+  const KsArgs& a = j.a;
+  const double N8 = 8.0 * a.N;
+  return N8 * ((double)a.B * a.Lc * a.K + (double)a.KB * 2 * a.Lc * a.K + (double)a.KB * a.B * 2 * a.K);
+}
+inline double alg_bytes(const JobKsData& j, int) {
+  const KsArgs& a = j.a;
+  const double N8 = 8.0 * a.N;
+  double w = (double)a.KB * a.B * 2 * a.K                  // tb
+             + (double)a.B * a.Lc * a.Lc                   // ext data limbs (+ digit source diagonal)
+             + (double)a.KB * 2 * a.Lc * a.Lc              // key rows of the data limbs
+             + (double)a.KB * a.B * 2 * a.Lc;              // output
+  if (a.add_parts) w += (double)a.B * a.add_parts * a.Lc;
+  if (a.D) w += (double)a.KB * a.Lc;
+  if (a.acc_in) w += (double)a.KB * a.B * 2 * a.Lc;
+  return N8 * w;
+}
+inline double alg_bytes(const JobRescaleLast& j, int nblk) { return 16.0 * j.N * nblk; }
+inline double alg_bytes(const JobRescaleData& j, int nblk) {
+  return 8.0 * j.N * (2.0 * nblk + (double)nblk / (j.Lc - 1));
+}
 
 }  // namespace he

@@ -508,7 +508,10 @@ void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items,
   auto run = [&](auto kern, int T, int smem) {
     static_cast<void>(T);
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw, c->d_twsh, c->d_itw, c->d_itwsh);
+    {
+      ProfScope ps_(c, "ntt_mul_intt", alg_bytes(j, nblk), nblk);
+      kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw, c->d_twsh, c->d_itw, c->d_itwsh);
+    }
     check_launch(c);
   };
   switch (c->logN) {
@@ -530,9 +533,12 @@ void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items,
 
 void modmul_rows(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl) {
   const size_t rows = items * nl;
-  k_binop<OP_MUL><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a, b, out, c->d_primes, c->N, nl, rows,
-                                                              (size_t)nl * c->N, (size_t)nl * c->N, nl, 0,
-                                                              (size_t)nl * c->N);
+  {
+    ProfScope ps_(c, "pw_mul", 0.0, 0);
+    k_binop<OP_MUL><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a, b, out, c->d_primes, c->N, nl, rows,
+                                                                (size_t)nl * c->N, (size_t)nl * c->N, nl, 0,
+                                                                (size_t)nl * c->N);
+  }
   check_launch(c);
 }
 
@@ -550,11 +556,17 @@ he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_
   // b indexed like a: pass b_limb_bs = LN with b pointer per part
   dim3 g = rows_grid2(c, rows);
   if (op == OP_ADD)
-    k_binop<OP_ADD><<<g, 256, 0, c->stream>>>(a->d, b->d, o->d, c->d_primes, c->N, Lc, rows, a_bs, b_bs,
-                                              (size_t)a->size * Lc, LN, a->size * LN);
+    {
+      ProfScope ps_(c, "pw_add", 0.0, 0);
+      k_binop<OP_ADD><<<g, 256, 0, c->stream>>>(a->d, b->d, o->d, c->d_primes, c->N, Lc, rows, a_bs, b_bs,
+                                                (size_t)a->size * Lc, LN, a->size * LN);
+    }
   else
-    k_binop<OP_SUB><<<g, 256, 0, c->stream>>>(a->d, b->d, o->d, c->d_primes, c->N, Lc, rows, a_bs, b_bs,
-                                              (size_t)a->size * Lc, LN, a->size * LN);
+    {
+      ProfScope ps_(c, "pw_sub", 0.0, 0);
+      k_binop<OP_SUB><<<g, 256, 0, c->stream>>>(a->d, b->d, o->d, c->d_primes, c->N, Lc, rows, a_bs, b_bs,
+                                                (size_t)a->size * Lc, LN, a->size * LN);
+    }
   check_launch(c);
   return o;
 }
@@ -563,7 +575,10 @@ he_ciphertext* ct_negate(he_context* c, const he_ciphertext* a) {
   const int Lc = a->level + 1;
   he_ciphertext* o = ct_new(c, a->B, a->size, a->level, a->scale);
   const size_t rows = (size_t)a->B * a->size * Lc;
-  k_negate<<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, o->d, c->d_primes, c->N, Lc, rows);
+  {
+    ProfScope ps_(c, "pw_negate", 0.0, 0);
+    k_negate<<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, o->d, c->d_primes, c->N, Lc, rows);
+  }
   check_launch(c);
   return o;
 }
@@ -573,9 +588,12 @@ he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plai
   const int B = std::max(a->B, p->B);
   he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale * p->scale);
   const size_t LN = (size_t)Lc * c->N, rows = (size_t)B * a->size * Lc;
-  k_binop<OP_MUL><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
-                                                              a->B == 1 ? 0 : a->size * LN, p->B == 1 ? 0 : LN,
-                                                              (size_t)a->size * Lc, 0, a->size * LN);
+  {
+    ProfScope ps_(c, "pw_mul", 0.0, 0);
+    k_binop<OP_MUL><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                                a->B == 1 ? 0 : a->size * LN, p->B == 1 ? 0 : LN,
+                                                                (size_t)a->size * Lc, 0, a->size * LN);
+  }
   check_launch(c);
   return o;
 }
@@ -593,9 +611,12 @@ he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plai
   }
   const size_t rows = (size_t)B * Lc;
   // treat items as size-1 rows at stride size*LN
-  k_binop<OP_ADD><<<rows_grid2(c, rows), 256, 0, c->stream>>>(o->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
-                                                              a->size * LN, p->B == 1 ? 0 : LN, Lc, 0,
-                                                              a->size * LN);
+  {
+    ProfScope ps_(c, "pw_add", 0.0, 0);
+    k_binop<OP_ADD><<<rows_grid2(c, rows), 256, 0, c->stream>>>(o->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                                a->size * LN, p->B == 1 ? 0 : LN, Lc, 0,
+                                                                a->size * LN);
+  }
   check_launch(c);
   return o;
 }
@@ -605,8 +626,11 @@ he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphert
   const int B = std::max(x->B, y->B);
   he_ciphertext* o = ct_new(c, B, 3, x->level, x->scale * y->scale);
   const size_t LN = (size_t)Lc * c->N, rows = (size_t)B * Lc;
-  k_tensor<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, y->d, o->d, c->d_primes, c->N, Lc, rows,
-                                                       x->B == 1 ? 0 : 2 * LN, y->B == 1 ? 0 : 2 * LN);
+  {
+    ProfScope ps_(c, "pw_tensor", 0.0, 0);
+    k_tensor<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, y->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                         x->B == 1 ? 0 : 2 * LN, y->B == 1 ? 0 : 2 * LN);
+  }
   check_launch(c);
   return o;
 }
@@ -777,8 +801,11 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
           a.out_ks = (size_t)B * 2 * LN;
           ks_launch(c, a);
           const size_t rows = (size_t)B * 2 * Lc;
-          k_accumulate<<<rows_grid2(c, rows), 256, 0, c->stream>>>(acc->d, tmp.as<u64>(), kb, (size_t)B * 2 * LN,
-                                                                   c->d_primes, c->N, Lc, rows);
+          {
+            ProfScope ps_(c, "vecmat_accumulate", 0.0, 0);
+            k_accumulate<<<rows_grid2(c, rows), 256, 0, c->stream>>>(acc->d, tmp.as<u64>(), kb, (size_t)B * 2 * LN,
+                                                                     c->d_primes, c->N, Lc, rows);
+          }
           check_launch(c);
         }
       }
@@ -806,8 +833,11 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
   const size_t LN = (size_t)Lc * c->N;
   he_ciphertext* T = ct_new(c, B * C, 2, x->level, x->scale * kernels->scale);
   const size_t rows = (size_t)B * C * 2 * Lc;
-  k_mul_plain_outer<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, kernels->d, T->d, c->d_primes, c->N, Lc, C,
-                                                                rows);
+  {
+    ProfScope ps_(c, "conv_mul_plain", 0.0, 0);
+    k_mul_plain_outer<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, kernels->d, T->d, c->d_primes, c->N, Lc, C,
+                                                                  rows);
+  }
   check_launch(c);
   he_ciphertext* t = nullptr;
   try {
@@ -823,8 +853,11 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
     const int Lc2 = t->level + 1;
     he_ciphertext* acc = ct_new(c, B, 2, t->level, t->scale * masks->scale);
     const size_t rows2 = (size_t)B * 2 * Lc2;
-    k_mask_sum<<<rows_grid2(c, rows2), 256, 0, c->stream>>>(t->d, masks->d, acc->d, c->d_primes, c->N, Lc2, C,
-                                                            rows2);
+    {
+      ProfScope ps_(c, "conv_mask_sum", 0.0, 0);
+      k_mask_sum<<<rows_grid2(c, rows2), 256, 0, c->stream>>>(t->d, masks->d, acc->d, c->d_primes, c->N, Lc2, C,
+                                                              rows2);
+    }
     check_launch(c);
     ct_free(t);
     t = nullptr;
@@ -847,17 +880,26 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
 static void make_ksk(he_context* c, u64* key, u64 pur_a, u64 pur_e, u64 objbase, u32 gal) {
   const int L = c->L, NP = c->NP, N = c->N;
   // a_j[t] uniform (NTT words) straight into part 1
-  k_sample_uniform<<<dim3((N + 255) / 256, std::min(L * NP, 65535)), 256, 0, c->stream>>>(
-      key + (size_t)NP * N, (size_t)2 * NP * N, L, NP, N, c->seed, pur_a, objbase, c->d_primes);
+  {
+    ProfScope ps_(c, "sample_uniform", 0.0, 0);
+    k_sample_uniform<<<dim3((N + 255) / 256, std::min(L * NP, 65535)), 256, 0, c->stream>>>(
+        key + (size_t)NP * N, (size_t)2 * NP * N, L, NP, N, c->seed, pur_a, objbase, c->d_primes);
+  }
   check_launch(c);
   // e_j: one CDT polynomial per digit, NTT into every limb
   Scratch e(c, (size_t)L * N * 8), et(c, (size_t)L * NP * N * 8);
-  k_sample_small<<<dim3((N + 255) / 256, std::min(L, 65535)), 256, 0, c->stream>>>(e.as<i64>(), N, L, c->seed,
-                                                                                 pur_e, objbase, 1, c->d_cdt);
+  {
+    ProfScope ps_(c, "sample_small", 0.0, 0);
+    k_sample_small<<<dim3((N + 255) / 256, std::min(L, 65535)), 256, 0, c->stream>>>(e.as<i64>(), N, L, c->seed,
+                                                                                   pur_e, objbase, 1, c->d_cdt);
+  }
   check_launch(c);
   signed_to_ntt(c, e.as<i64>(), et.as<u64>(), L, NP);
-  k_ksk_combine<<<dim3((N + 255) / 256, std::min(L * NP, 65535)), 256, 0, c->stream>>>(
-      key, et.as<u64>(), c->d_sk, c->d_P_mod, c->d_primes, N, c->logN, L, NP, gal);
+  {
+    ProfScope ps_(c, "keygen_combine", 0.0, 0);
+    k_ksk_combine<<<dim3((N + 255) / 256, std::min(L * NP, 65535)), 256, 0, c->stream>>>(
+        key, et.as<u64>(), c->d_sk, c->d_P_mod, c->d_primes, N, c->logN, L, NP, gal);
+  }
   check_launch(c);
 }
 
@@ -866,24 +908,36 @@ void keygen(he_context* c, const std::vector<int>& steps) {
   HE_CK(cudaMalloc(&c->d_sk, (size_t)NP * N * 8));
   {
     Scratch s(c, (size_t)N * 8);
-    k_sample_small<<<dim3((N + 255) / 256, 1), 256, 0, c->stream>>>(s.as<i64>(), N, 1, c->seed, PUR_S, 0, 0,
-                                                                   c->d_cdt);
+    {
+      ProfScope ps_(c, "sample_small", 0.0, 0);
+      k_sample_small<<<dim3((N + 255) / 256, 1), 256, 0, c->stream>>>(s.as<i64>(), N, 1, c->seed, PUR_S, 0, 0,
+                                                                     c->d_cdt);
+    }
     check_launch(c);
     signed_to_ntt(c, s.as<i64>(), c->d_sk, 1, NP);
   }
   c->has_sk = true;
   HE_CK(cudaMalloc(&c->d_pk, (size_t)2 * L * N * 8));
   {
-    k_sample_uniform<<<dim3((N + 255) / 256, L), 256, 0, c->stream>>>(c->d_pk + (size_t)L * N, 0, 1, L, N,
-                                                                      c->seed, PUR_PK_A, 0, c->d_primes);
+    {
+      ProfScope ps_(c, "sample_uniform", 0.0, 0);
+      k_sample_uniform<<<dim3((N + 255) / 256, L), 256, 0, c->stream>>>(c->d_pk + (size_t)L * N, 0, 1, L, N,
+                                                                        c->seed, PUR_PK_A, 0, c->d_primes);
+    }
     check_launch(c);
     Scratch e(c, (size_t)N * 8), et(c, (size_t)L * N * 8);
-    k_sample_small<<<dim3((N + 255) / 256, 1), 256, 0, c->stream>>>(e.as<i64>(), N, 1, c->seed, PUR_PK_E, 0, 1,
-                                                                   c->d_cdt);
+    {
+      ProfScope ps_(c, "sample_small", 0.0, 0);
+      k_sample_small<<<dim3((N + 255) / 256, 1), 256, 0, c->stream>>>(e.as<i64>(), N, 1, c->seed, PUR_PK_E, 0, 1,
+                                                                     c->d_cdt);
+    }
     check_launch(c);
     signed_to_ntt(c, e.as<i64>(), et.as<u64>(), 1, L);
-    k_pk_combine<<<dim3((N + 255) / 256, L), 256, 0, c->stream>>>(c->d_pk, et.as<u64>(), c->d_sk, c->d_primes,
-                                                                  N, L);
+    {
+      ProfScope ps_(c, "keygen_combine", 0.0, 0);
+      k_pk_combine<<<dim3((N + 255) / 256, L), 256, 0, c->stream>>>(c->d_pk, et.as<u64>(), c->d_sk, c->d_primes,
+                                                                    N, L);
+    }
     check_launch(c);
   }
   c->has_pk = true;
@@ -914,9 +968,12 @@ he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, dou
   const int smem = in_smem ? M * 16 : 0;
   if (smem > 48 * 1024)
     HE_CK(cudaFuncSetAttribute(k_encode_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m.as<i64>(), flag.as<int>(), c->d_slot_index,
-                                                      c->d_fft_w, c->d_zeta, N, logM,
-                                                      in_smem ? nullptr : g.as<double2>());
+  {
+    ProfScope ps_(c, "encode_fft", 0.0, 0);
+    k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m.as<i64>(), flag.as<int>(), c->d_slot_index,
+                                                        c->d_fft_w, c->d_zeta, N, logM,
+                                                        in_smem ? nullptr : g.as<double2>());
+  }
   check_launch(c);
   int hflag = 0;
   HE_CK(cudaMemcpyAsync(&hflag, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -939,17 +996,23 @@ void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n) {
   Scratch coef(c, B * Lc * N * 8), X(c, B * N * 8);
   ntt_rows(c, pt->d, coef.as<u64>(), B, Lc, (size_t)Lc * N, (size_t)Lc * N, true);
   const size_t total = B * N;
-  k_crt_compose<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, c->stream>>>(
-      coef.as<u64>(), X.as<double>(), c->d_crt + c->hp.crt_off[pt->level], c->d_primes, N, Lc, total);
+  {
+    ProfScope ps_(c, "crt_compose", 0.0, 0);
+    k_crt_compose<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, c->stream>>>(
+        coef.as<u64>(), X.as<double>(), c->d_crt + c->hp.crt_off[pt->level], c->d_primes, N, Lc, total);
+  }
   check_launch(c);
   const bool in_smem = M <= 8192;
   Scratch g(c, in_smem ? 8 : B * M * 16);
   const int smem = in_smem ? M * 16 : 0;
   if (smem > 48 * 1024)
     HE_CK(cudaFuncSetAttribute(k_decode_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_decode_fft<<<(unsigned)B, 512, smem, c->stream>>>(X.as<double>(), n, pt->scale, out_dev, c->d_slot_index,
-                                                      c->d_fft_w, c->d_zeta, N, logM,
-                                                      in_smem ? nullptr : g.as<double2>());
+  {
+    ProfScope ps_(c, "decode_fft", 0.0, 0);
+    k_decode_fft<<<(unsigned)B, 512, smem, c->stream>>>(X.as<double>(), n, pt->scale, out_dev, c->d_slot_index,
+                                                        c->d_fft_w, c->d_zeta, N, logM,
+                                                        in_smem ? nullptr : g.as<double2>());
+  }
   check_launch(c);
 }
 
@@ -960,8 +1023,11 @@ he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
   const dim3 g((N + 255) / 256, std::min(B, 65535));
   const u64 pur[3] = {PUR_ENC_V, PUR_ENC_E0, PUR_ENC_E1};
   for (int w = 0; w < 3; ++w) {
-    k_sample_small<<<g, 256, 0, c->stream>>>(small.as<i64>() + (size_t)w * B * N, N, B, c->seed, pur[w], stream_id,
-                                            w == 0 ? 0 : 1, c->d_cdt);
+    {
+      ProfScope ps_(c, "sample_small", 0.0, 0);
+      k_sample_small<<<g, 256, 0, c->stream>>>(small.as<i64>() + (size_t)w * B * N, N, B, c->seed, pur[w], stream_id,
+                                              w == 0 ? 0 : 1, c->d_cdt);
+    }
     check_launch(c);
     // NTT into noise [b][w][Lc][N]
     JobSignedToNtt j{small.as<i64>() + (size_t)w * B * N, noise.as<u64>() + (size_t)w * Lc * N, N, Lc, (size_t)N,
@@ -970,9 +1036,12 @@ he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
   }
   he_ciphertext* ct = ct_new(c, B, 2, pt->level, pt->scale);
   const size_t rows = (size_t)B * Lc;
-  k_encrypt_combine<<<rows_grid2(c, rows), 256, 0, c->stream>>>(noise.as<u64>(), c->d_pk, pt->d,
-                                                               pt->B == 1 ? 0 : (size_t)Lc * N, ct->d, c->d_primes,
-                                                               N, Lc, c->L, rows);
+  {
+    ProfScope ps_(c, "encrypt_combine", 0.0, 0);
+    k_encrypt_combine<<<rows_grid2(c, rows), 256, 0, c->stream>>>(noise.as<u64>(), c->d_pk, pt->d,
+                                                                 pt->B == 1 ? 0 : (size_t)Lc * N, ct->d, c->d_primes,
+                                                                 N, Lc, c->L, rows);
+  }
   check_launch(c);
   return ct;
 }
@@ -981,8 +1050,11 @@ he_plaintext* decrypt(he_context* c, const he_ciphertext* ct) {
   const int Lc = ct->level + 1;
   he_plaintext* pt = pt_new(c, ct->B, ct->level, ct->scale);
   const size_t rows = (size_t)ct->B * Lc;
-  k_decrypt<<<rows_grid2(c, rows), 256, 0, c->stream>>>(ct->d, c->d_sk, pt->d, c->d_primes, c->N, Lc, ct->size,
-                                                       rows);
+  {
+    ProfScope ps_(c, "decrypt", 0.0, 0);
+    k_decrypt<<<rows_grid2(c, rows), 256, 0, c->stream>>>(ct->d, c->d_sk, pt->d, c->d_primes, c->N, Lc, ct->size,
+                                                         rows);
+  }
   check_launch(c);
   return pt;
 }
@@ -991,7 +1063,10 @@ int check_words(he_context* c, const u64* w, size_t items, int Lc) {
   Scratch flag(c, 4);
   HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
   const size_t rows = items * Lc;
-  k_check_words<<<rows_grid2(c, rows), 256, 0, c->stream>>>(w, c->d_primes, c->N, Lc, rows, flag.as<int>());
+  {
+    ProfScope ps_(c, "check_words", 0.0, 0);
+    k_check_words<<<rows_grid2(c, rows), 256, 0, c->stream>>>(w, c->d_primes, c->N, Lc, rows, flag.as<int>());
+  }
   check_launch(c);
   int h = 0;
   HE_CK(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));

@@ -1,0 +1,112 @@
+"""GPU parity of the paper's encrypted CNN (BASELINE config 4) through
+the C-ABI: im2col conv, square, FC1 (replicated-output diagonals), square, FC2.
+
+* bit-exact: the GPU chain, fed the oracle's input ciphertext and the oracle's
+  integer encodings of every weight plaintext (C7 injection), reproduces the
+  oracle's ciphertext words after every layer;
+* tolerance: the all-GPU path (its own encode / encrypt / decrypt / decode) gives
+  logits within 5e-3 of the float64 network with the same argmax (north_star).
+"""
+import numpy as np
+import pytest
+
+from oracle import circuits as OC
+from oracle.oracle import OracleContext
+from synthetic import CFG4, cnn_weights, mnist_like_images
+from test_layouts import float_net_numpy
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg4():
+    from paper_2104_03152_b200 import Context
+    from paper_2104_03152_b200.cnn import rotation_steps
+    steps = OC.cnn_rotation_steps()
+    assert steps == rotation_steps()
+    o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    o.keygen(steps)
+    g = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    g.he_keygen(steps)
+    return o, g
+
+
+def inj(g, o, vecs, scale, level):
+    ms = np.stack([o.encode_coeffs(v, scale)[1] for v in vecs])
+    return g.he_pt_from_int_coeffs(ms, scale, level)
+
+
+def test_cnn_layers_bit_exact(cfg4):
+    o, g = cfg4
+    w = cnn_weights(3)
+    imgs = mnist_like_images(2, 4)
+    ns, q, plan = o.slots, o.q, OC.CNN_PLAN
+    o_in = [OC.cnn_encrypt_input(o, img, b) for b, img in enumerate(imgs)]
+    lvl = o_in[0].level
+    x = g.he_ct_import_words(np.stack([c.words for c in o_in]), lvl, o_in[0].scale)
+    # conv (C18/C19)
+    K = [OC.conv_kernel_slots(w.conv_w[c].reshape(-1), 64, ns) for c in range(4)]
+    M = [OC.conv_mask_slots(c, 4, 64, ns) for c in range(4)]
+    gK = inj(g, o, K, float(q[lvl]) * 2.0 ** plan["conv_shift"], lvl)
+    gM = inj(g, o, M, float(q[lvl - 1]) * 2.0 ** plan["mask_shift"], lvl - 1)
+    s2 = (o_in[0].scale * gK.scale / q[lvl]) * gM.scale / q[lvl - 1]
+    gB = inj(g, o, [OC.conv_bias_slots(w.conv_b, 64, ns)], s2, lvl - 2)
+    x = g.he_im2col_conv_pt(x, gK, gM, gB, 64)
+    ref = [OC.im2col_conv(o, c, w.conv_w.reshape(4, -1), w.conv_b, 64, plan["conv_shift"], plan["mask_shift"])
+           for c in o_in]
+    W = x.words()
+    for b in range(2):
+        assert np.array_equal(W[b], ref[b].words), ("conv", b)
+    assert x.scale == ref[0].scale and x.level == ref[0].level
+    # square
+    x = g.he_square(x)
+    ref = [o.square(c) for c in ref]
+    W = x.words()
+    for b in range(2):
+        assert np.array_equal(W[b], ref[b].words), ("square1", b)
+    # FC1 (replicated output) and FC2
+    for name, Wm, bias, rep, shift in [("fc1", w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"]),
+                                       ("fc2", w.fc2_w.T, w.fc2_b, False, -plan["fc2_shift"])]:
+        lvl = ref[0].level
+        ps = float(q[lvl]) * 2.0 ** (-shift)
+        gD = inj(g, o, OC.vecmat_diagonals(Wm, ns, rep), ps, lvl)
+        bs = ref[0].scale * ps / q[lvl]
+        gb = inj(g, o, [OC.vecmat_bias_slots(bias, ns, rep)], bs, lvl - 1)
+        x = g.he_vec_mat_pt(x, gD, gb)
+        ref = [OC.vec_mat(o, c, Wm, bias, rep, shift) for c in ref]
+        W = x.words()
+        for b in range(2):
+            assert np.array_equal(W[b], ref[b].words), (name, b)
+        if name == "fc1":
+            x = g.he_square(x)
+            ref = [o.square(c) for c in ref]
+    assert x.level == 0
+    # decrypt + decode of the bit-exact result vs the oracle's
+    z = g.he_decode(g.he_decrypt(x), 10)
+    for b in range(2):
+        assert np.allclose(z[b], o.decode(o.decrypt(ref[b]), 10), rtol=1e-9, atol=1e-9)
+
+
+def test_cnn_all_gpu_tolerance(cfg4):
+    """Own encode/encrypt/decrypt/decode: logits within 5e-3 abs of float64, argmax equal."""
+    from paper_2104_03152_b200.cnn import EncryptedCNN
+    o, g = cfg4
+    w = cnn_weights(3)
+    net = EncryptedCNN(g, w)
+    imgs = mnist_like_images(16, 4)
+    logits = net.decrypt(net.forward(net.encrypt(imgs, 1000)))
+    for b, img in enumerate(imgs):
+        ref = float_net_numpy(img, w)
+        assert np.max(np.abs(logits[b] - ref)) < 5e-3, b
+        assert np.argmax(logits[b]) == np.argmax(ref)
+
+
+def test_cnn_batch_independence(cfg4):
+    """Items of a batch are independent: image b of a batch of 5 equals the same image alone."""
+    from paper_2104_03152_b200.cnn import EncryptedCNN
+    o, g = cfg4
+    net = EncryptedCNN(g, cnn_weights(3))
+    imgs = mnist_like_images(5, 4, start=100)
+    big = net.forward(net.encrypt(imgs, 7)).words()
+    one = net.forward(net.encrypt(imgs[3:4], 10)).words()
+    assert np.array_equal(big[3], one[0])
