@@ -93,6 +93,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     from paper_2104_03152_b200 import Context, he_im2col_encode
     from paper_2104_03152_b200.cnn import EncryptedCNN, rotation_steps
+    from paper_2104_03152_b200.dist import gather_to_rank0, max_over_ranks, shard_indices
     from synthetic import CFG4, cnn_weights, mnist_like_images
 
     torch.cuda.set_device(local_rank)
@@ -108,8 +109,7 @@ def run_ours(args, rank, world, local_rank):
 
     # this rank's shard of the image stream (image i depends only on (seed, i))
     def shard(step):
-        start = (step * world + rank) * B
-        return mnist_like_images(B, 4, start=start)
+        return mnist_like_images(B, 4, start=int(shard_indices(step, B, world, rank)[0]))
 
     n_batches = 2   # distinct input batches cycled through the steps
     imgs_host = [shard(s) for s in range(n_batches)]
@@ -140,11 +140,7 @@ def run_ours(args, rank, world, local_rank):
             fn(W + i)
         e1.record(stream)
         barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = max_over_ranks(e0.elapsed_time(e1), dev)
         return ms, ctx.he_launch_count() - l0
 
     # --- device-resident timed region (headline value) ---
@@ -199,10 +195,8 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and not args.no_extra:
         extra = micro_extra(ctx, stream, dev)
 
-    # result collection to rank 0 (outside the timed region): NCCL gather of logits
-    if world > 1:
-        gathered = [torch.empty_like(logits_dev) for _ in range(world)] if rank == 0 else None
-        dist.gather(logits_dev, gathered, dst=0)
+    # result collection to rank 0 (outside the timed region): NCCL gather of the logits
+    gather_to_rank0(logits_dev)
 
     return dict(value=value, ms=ms, launches=launches, clocks=clk.summary(), roofline=roofline,
                 breakdown=breakdown, e2e=e2e, extra=extra)
