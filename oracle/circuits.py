@@ -194,3 +194,16 @@ def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None) -> OCt:
     x = ctx.square(x)
     x = vec_mat(ctx, x, w.fc2_w.T, w.fc2_b, replicate_out=False, pt_scale_shift=-plan["fc2_shift"])
     return x
+
+
+# ------------------------------------------------------------ config 5b ---
+def deep_chain(ctx: OracleContext, ct: OCt, pts: np.ndarray, rot_steps=(1, 2, 4, 8)) -> OCt:
+    """A-cfg5b: for t < len(pts): ct <- rescale(ct * pt_t) with pt_t encoded at the
+    scale q_l of the prime the rescale drops (C3, so the ciphertext scale is unchanged); then
+    ct <- ct + rot(ct, s) for s in rot_steps."""
+    for z in pts:
+        lvl = ct.level
+        ct = ctx.rescale(ctx.mul_plain(ct, ctx.encode(z, float(ctx.q[lvl]), lvl)))
+    for s in rot_steps:
+        ct = ctx.add(ct, ctx.rotate(ct, s))
+    return ct

@@ -1,0 +1,92 @@
+"""GPU parity at BASELINE configs 3 and 5b (SURVEY §8(c) acceptance table):
+
+* config 3 — N=16384, 8 data + 2 special 50-bit primes (two-prime ModDown, C15 with k=2),
+  scale 2^50: every rotation by 2^r (r=0..13, 2^13 = n_s is the identity element kept as a
+  real key switch, C20) and ct x ct + relinearize + rescale, bit-exact; decrypted values
+  vs np.roll / products <= 1e-6.
+* config 5b — N=32768 (2-CTA cluster NTT), 18 + 2 50-bit primes, scale 2^40: the deep chain
+  of A-cfg5b (16 x mul_plain + rescale, then rotate-and-add by 1, 2, 4, 8), bit-exact with
+  injected oracle plaintexts, and decrypted vs float64 within the derived noise bound 1e-5
+  (DESIGN.md §3 R3: A-cfg5b's 1e-6 is below the circuit's own CKKS noise).
+"""
+import numpy as np
+import pytest
+
+from oracle import circuits as OC
+from oracle.oracle import OracleContext
+from synthetic import CFG3, CFG5B, deep_chain_plaintexts, messages
+
+pytestmark = pytest.mark.gpu
+
+
+def test_cfg3_rotations_and_mul_bit_exact():
+    from paper_2104_03152_b200 import Context
+    steps = [1 << r for r in range(14)]
+    o = OracleContext(CFG3.logN, CFG3.bits, CFG3.n_special, CFG3.seed)
+    o.keygen(steps)
+    g = Context(CFG3.logN, CFG3.bits, CFG3.n_special, CFG3.seed)
+    g.he_keygen(steps)
+    assert np.array_equal(g.he_key_export(3, 8192), o.galois_key(8192))
+    lvl, B = o.L - 1, 3
+    z = messages(B, o.slots, seed=CFG3.seed)
+    pts = [o.encode(z[b], 2.0 ** 50, lvl) for b in range(B)]
+    gct = g.he_encrypt(g.he_pt_import_words(np.stack([p.words for p in pts]), lvl, 2.0 ** 50), 0)
+    octs = [o.encrypt(pts[b], b) for b in range(B)]
+    W = gct.words()
+    for b in range(B):
+        assert np.array_equal(W[b], octs[b].words)
+    for s in steps:
+        r = g.he_rotate(gct, s)
+        assert np.array_equal(r.words()[0], o.rotate(octs[0], s).words), s
+        dec = g.he_decode(g.he_decrypt(r), o.slots)
+        for b in range(B):
+            assert np.max(np.abs(dec[b] - np.roll(z[b], -s))) < 1e-6, (s, b)
+    # ct_i x ct_{i+1} -> relinearize -> rescale (C20)
+    nxt = g.he_ct_import_words(np.stack([octs[(b + 1) % B].words for b in range(B)]), lvl, 2.0 ** 50)
+    m = g.he_rescale(g.he_relinearize(g.he_mul(gct, nxt)))
+    Wm = m.words()
+    for b in range(B):
+        ref = o.rescale(o.relinearize(o.tensor(octs[b], octs[(b + 1) % B])))
+        assert np.array_equal(Wm[b], ref.words), b
+        assert m.scale == ref.scale
+    dec = g.he_decode(g.he_decrypt(m), o.slots)
+    for b in range(B):
+        assert np.max(np.abs(dec[b] - z[b] * z[(b + 1) % B])) < 1e-6
+
+
+def test_cfg5b_deep_chain_bit_exact():
+    from paper_2104_03152_b200 import Context
+    steps = [1, 2, 4, 8]
+    o = OracleContext(CFG5B.logN, CFG5B.bits, CFG5B.n_special, CFG5B.seed)
+    o.keygen(steps)
+    g = Context(CFG5B.logN, CFG5B.bits, CFG5B.n_special, CFG5B.seed)
+    g.he_keygen(steps)
+    lvl = o.L - 1
+    z = messages(1, o.slots, seed=CFG5B.seed)[0]
+    P = deep_chain_plaintexts(16, o.slots, seed=CFG5B.seed)
+    opt = o.encode(z, 2.0 ** 40, lvl)
+    oct_ = o.encrypt(opt, 0)
+    ct = g.he_encrypt(g.he_pt_import_words(opt.words[None], lvl, 2.0 ** 40), 0)
+    assert np.array_equal(ct.words()[0], oct_.words)
+    ref = oct_
+    for t in range(16):
+        l = ref.level
+        _, m = o.encode_coeffs(P[t], float(o.q[l]))
+        ct = g.he_rescale(g.he_mul_plain(ct, g.he_pt_from_int_coeffs(m, float(o.q[l]), l)))
+        ref = o.rescale(o.mul_plain(ref, o.coeffs_to_pt(m, l, float(o.q[l]))))
+        assert np.array_equal(ct.words()[0], ref.words), t
+        assert ct.scale == 2.0 ** 40
+    for s in steps:
+        ct = g.he_add(ct, g.he_rotate(ct, s))
+        ref = o.add(ref, o.rotate(ref, s))
+        assert np.array_equal(ct.words()[0], ref.words), s
+    full = OC.deep_chain(o, oct_, P)
+    assert np.array_equal(full.words, ref.words)
+    y = z * np.prod(P, axis=0)
+    for s in steps:
+        y = y + np.roll(y, -s)
+    dec = g.he_decode(g.he_decrypt(ct), o.slots)[0]
+    # CKKS noise, not GPU error (the words are bit-exact above): per-slot noise after encryption
+    # and 16 rescales is ~1e-7 at 2^40 (fresh ~340 sqrt(N) / 2^40, rounding ~42 sqrt(N) / 2^40 per
+    # rescale), and the four rotate-and-adds sum 16 copies -> ~1-2e-6; DESIGN.md §3 R3
+    assert np.max(np.abs(dec - y)) < 1e-5
