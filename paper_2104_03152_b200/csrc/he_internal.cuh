@@ -41,7 +41,7 @@ struct he_context {
   uint64_t launches = 0;
   // device tables
   he::PrimeD* d_primes = nullptr;
-  he::u64 *d_tw = nullptr, *d_twsh = nullptr, *d_itw = nullptr, *d_itwsh = nullptr;
+  ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [NP][N] (w, floor(w 2^64 / q))
   he::u64* d_cdt = nullptr;
   he::u64 *d_P_mod = nullptr, *d_Pinv_mod = nullptr, *d_Ph_mod = nullptr;
   he::u64 *d_Phat_inv = nullptr, *d_Phat_mod = nullptr;
@@ -139,15 +139,15 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
   auto kern = k_ntt<LOGN, CL, INV, Job>;
   if (!configured) {
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (CL == 2) HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   if (nblk <= 0) return;
-  const u64* tw = INV ? c->d_itw : c->d_tw;
-  const u64* twsh = INV ? c->d_itwsh : c->d_twsh;
+  const ulonglong2* tw = INV ? c->d_itw2 : c->d_tw2;
   ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk);
   if (CL == 1) {
-    kern<<<nblk, G::T, G::SMEM, c->stream>>>(job, c->d_primes, tw, twsh);
+    kern<<<nblk, G::T, G::SMEM, c->stream>>>(job, c->d_primes, tw);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblk * CL);
@@ -161,7 +161,7 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    HE_CK(cudaLaunchKernelEx(&cfg, kern, job, (const PrimeD*)c->d_primes, tw, twsh));
+    HE_CK(cudaLaunchKernelEx(&cfg, kern, job, (const PrimeD*)c->d_primes, tw));
   }
   check_launch(c);
 }

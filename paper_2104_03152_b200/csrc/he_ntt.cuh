@@ -27,8 +27,10 @@ struct NttGeom {
   static constexpr int N = 1 << LOGN;
   static constexpr int LOGNL = LOGN - (CL == 2 ? 1 : 0);  // bits owned by one CTA
   static constexpr int NL = 1 << LOGNL;
-  static constexpr int R = LOGNL - 9 > 4 ? LOGNL - 9 : 4;  // log2 words per thread
-  static constexpr int T = NL >> R;                          // threads per CTA
+  static constexpr int R = LOGNL - 10 > 4 ? LOGNL - 10 : 4;  // log2 words per thread
+  static constexpr int T = NL >> R;                            // threads per CTA
+  // CTAs per SM the register budget is sized for (shared memory allows 3 at N=2^13)
+  static constexpr int MINB = NL <= 8192 ? 2 : 1;
   static constexpr int NPASS = (LOGNL + R - 1) / R;
   static constexpr int SMEM = (NL + NL / 16) * 8;
 };
@@ -54,8 +56,8 @@ __device__ __forceinline__ void gs_bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q, u
 // One pass over local bits [LO, LO+NB): each thread loads 2^NB words per
 // group (2^(R-NB) groups), runs NB stages in registers, writes them back.
 template <int LOGN, int CL, bool INV, int LO, int NB>
-__device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const u64* __restrict__ tw,
-                                         const u64* __restrict__ twsh, u64 q, u64 two_q) {
+__device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const ulonglong2* __restrict__ tw,
+                                         u64 q, u64 two_q) {
   typedef NttGeom<LOGN, CL> G;
   constexpr int NG = 1 << (G::R - NB);
   constexpr int E = 1 << NB;
@@ -77,7 +79,8 @@ __device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const u64*
           if (k & half) continue;
           const u32 j = gbase + base + (k << LO);
           const u32 ti = (1u << s) + (j >> (LOGN - s));
-          ct_bfly(x[k], x[k + half], __ldg(tw + ti), __ldg(twsh + ti), q, two_q);
+          const ulonglong2 w = __ldg(tw + ti);
+          ct_bfly(x[k], x[k + half], w.x, w.y, q, two_q);
         }
       }
     } else {
@@ -91,7 +94,8 @@ __device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const u64*
           if (k & half) continue;
           const u32 j = gbase + base + (k << LO);
           const u32 ti = (1u << s) + (j >> (LOGN - s));
-          gs_bfly(x[k], x[k + half], __ldg(tw + ti), __ldg(twsh + ti), q, two_q);
+          const ulonglong2 w = __ldg(tw + ti);
+          gs_bfly(x[k], x[k + half], w.x, w.y, q, two_q);
         }
       }
     }
@@ -102,28 +106,28 @@ __device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const u64*
 
 // Passes over the local problem: group p covers local bits [pR, min(pR+R, LOGNL)).
 template <int LOGN, int CL, bool INV, int P>
-__device__ __forceinline__ void ntt_passes(u64* sm, u32 tid, u32 gbase, const u64* tw,
-                                           const u64* twsh, u64 q, u64 two_q) {
+__device__ __forceinline__ void ntt_passes(u64* sm, u32 tid, u32 gbase, const ulonglong2* tw, u64 q,
+                                           u64 two_q) {
   typedef NttGeom<LOGN, CL> G;
   constexpr int GP = INV ? P : G::NPASS - 1 - P;  // forward runs top-down
   constexpr int LO = GP * G::R;
   constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-  ntt_pass<LOGN, CL, INV, LO, NB>(sm, tid, gbase, tw, twsh, q, two_q);
+  ntt_pass<LOGN, CL, INV, LO, NB>(sm, tid, gbase, tw, q, two_q);
   __syncthreads();
-  if constexpr (P + 1 < G::NPASS) ntt_passes<LOGN, CL, INV, P + 1>(sm, tid, gbase, tw, twsh, q, two_q);
+  if constexpr (P + 1 < G::NPASS) ntt_passes<LOGN, CL, INV, P + 1>(sm, tid, gbase, tw, q, two_q);
 }
 
 // Cross-CTA stage (bit LOGN-1) of the 2-CTA cluster transform, through DSMEM.
 template <int LOGN, bool INV>
-__device__ __forceinline__ void ntt_cross_stage(u64* sm, u32 tid, const u64* tw, const u64* twsh,
-                                                u64 q, u64 two_q) {
+__device__ __forceinline__ void ntt_cross_stage(u64* sm, u32 tid, const ulonglong2* tw, u64 q, u64 two_q) {
   namespace cg = cooperative_groups;
   typedef NttGeom<LOGN, 2> G;
   cg::cluster_group cl = cg::this_cluster();
   const u32 rank = cl.block_rank();
   u64* s0 = cl.map_shared_rank(sm, 0);
   u64* s1 = cl.map_shared_rank(sm, 1);
-  const u64 w = __ldg(tw + 1), wsh = __ldg(twsh + 1);
+  const ulonglong2 tw1 = __ldg(tw + 1);
+  const u64 w = tw1.x, wsh = tw1.y;
   for (u32 i = rank * (G::NL / 2) + tid; i < (rank + 1) * (G::NL / 2); i += G::T) {
     u64 x = s0[spad(i)], y = s1[spad(i)];
     if (!INV) ct_bfly(x, y, w, wsh, q, two_q);
@@ -144,9 +148,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 //   void store(int blk, u32 i, u64 v, const PrimeD&)  canonical output word i
 // blk = blockIdx.x / CL.
 template <int LOGN, int CL, bool INV, class Job>
-__global__ void __launch_bounds__(NttGeom<LOGN, CL>::T)
-k_ntt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict__ tw_all,
-      const u64* __restrict__ twsh_all) {
+__global__ void __launch_bounds__(NttGeom<LOGN, CL>::T, NttGeom<LOGN, CL>::MINB)
+k_ntt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __restrict__ tw_all) {
   typedef NttGeom<LOGN, CL> G;
   extern __shared__ u64 sm[];
   const u32 tid = threadIdx.x;
@@ -155,18 +158,17 @@ k_ntt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict__ tw_all
   const u32 gbase = rank * G::NL;
   const int pi = job.prime(blk);
   const PrimeD P = load_prime(primes, pi);
-  const u64* tw = tw_all + (size_t)pi * G::N;
-  const u64* twsh = twsh_all + (size_t)pi * G::N;
+  const ulonglong2* tw = tw_all + (size_t)pi * G::N;
   for (u32 i = tid; i < G::NL; i += G::T) sm[spad(i)] = job.load(blk, gbase + i, P);
   if (CL == 2) cluster_sync_all(); else __syncthreads();
   if (CL == 2 && !INV) {
-    ntt_cross_stage<LOGN, false>(sm, tid, tw, twsh, P.q, P.two_q);
+    ntt_cross_stage<LOGN, false>(sm, tid, tw, P.q, P.two_q);
     cluster_sync_all();
   }
-  ntt_passes<LOGN, CL, INV, 0>(sm, tid, gbase, tw, twsh, P.q, P.two_q);
+  ntt_passes<LOGN, CL, INV, 0>(sm, tid, gbase, tw, P.q, P.two_q);
   if (CL == 2 && INV) {
     cluster_sync_all();
-    ntt_cross_stage<LOGN, true>(sm, tid, tw, twsh, P.q, P.two_q);
+    ntt_cross_stage<LOGN, true>(sm, tid, tw, P.q, P.two_q);
     cluster_sync_all();
   }
   for (u32 i = tid; i < G::NL; i += G::T) {
@@ -185,10 +187,9 @@ k_ntt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict__ tw_all
 // Job provides prime(blk), load(blk,i,P) (coefficient-domain a),
 // factor(blk,i,P) (NTT-domain b at bit-reversed position i) and store.
 template <int LOGN, class Job>
-__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T)
-k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict__ tw_all,
-               const u64* __restrict__ twsh_all, const u64* __restrict__ itw_all,
-               const u64* __restrict__ itwsh_all) {
+__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T, NttGeom<LOGN, 1>::MINB)
+k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __restrict__ tw_all,
+               const ulonglong2* __restrict__ itw_all) {
   typedef NttGeom<LOGN, 1> G;
   extern __shared__ u64 sm[];
   const u32 tid = threadIdx.x;
@@ -197,8 +198,7 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict
   const PrimeD P = load_prime(primes, pi);
   for (u32 i = tid; i < G::NL; i += G::T) sm[spad(i)] = job.load(blk, i, P);
   __syncthreads();
-  ntt_passes<LOGN, 1, false, 0>(sm, tid, 0, tw_all + (size_t)pi * G::N, twsh_all + (size_t)pi * G::N,
-                                P.q, P.two_q);
+  ntt_passes<LOGN, 1, false, 0>(sm, tid, 0, tw_all + (size_t)pi * G::N, P.q, P.two_q);
   for (u32 i = tid; i < G::NL; i += G::T) {
     u64 v = sm[spad(i)];
     v = v >= P.two_q ? v - P.two_q : v;
@@ -206,8 +206,7 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const u64* __restrict
     sm[spad(i)] = mul_mod(v, job.factor(blk, i, P), P);
   }
   __syncthreads();
-  ntt_passes<LOGN, 1, true, 0>(sm, tid, 0, itw_all + (size_t)pi * G::N, itwsh_all + (size_t)pi * G::N,
-                               P.q, P.two_q);
+  ntt_passes<LOGN, 1, true, 0>(sm, tid, 0, itw_all + (size_t)pi * G::N, P.q, P.two_q);
   for (u32 i = tid; i < G::NL; i += G::T) job.store(blk, i, mul_shoup(sm[spad(i)], P.ninv, P.ninvsh, P.q), P);
 }
 

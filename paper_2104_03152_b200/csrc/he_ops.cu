@@ -69,10 +69,15 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
     p.r64 = (u64)((((u128)1) << 64) % hp.q[t]);
   }
   c->d_primes = upload(c, pd);
-  c->d_tw = upload(c, hp.tw);
-  c->d_twsh = upload(c, hp.twsh);
-  c->d_itw = upload(c, hp.itw);
-  c->d_itwsh = upload(c, hp.itwsh);
+  {
+    std::vector<ulonglong2> t2(hp.tw.size()), i2(hp.tw.size());
+    for (size_t k = 0; k < hp.tw.size(); ++k) {
+      t2[k] = make_ulonglong2(hp.tw[k], hp.twsh[k]);
+      i2[k] = make_ulonglong2(hp.itw[k], hp.itwsh[k]);
+    }
+    c->d_tw2 = upload(c, t2);
+    c->d_itw2 = upload(c, i2);
+  }
   c->d_cdt = upload(c, hp.cdt);
   c->d_P_mod = upload(c, hp.P_mod);
   c->d_Pinv_mod = upload(c, hp.Pinv_mod);
@@ -510,7 +515,7 @@ void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items,
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     {
       ProfScope ps_(c, "ntt_mul_intt", alg_bytes(j, nblk), nblk);
-      kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw, c->d_twsh, c->d_itw, c->d_itwsh);
+      kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw2, c->d_itw2);
     }
     check_launch(c);
   };
