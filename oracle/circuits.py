@@ -141,6 +141,23 @@ def vec_mat(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | None,
     return acc
 
 
+def vec_mat_lazy(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | None,
+                 replicate_out: bool, pt_scale_shift: int = 0) -> OCt:
+    """vec_mat with the diagonals' rotations sharing ONE ModDown (lazy ModDown,
+    DESIGN.md §3): same diagonals, scales and bias as vec_mat (C17); D_k is
+    encoded on the data limbs and the special limbs.  Rescale once, + bias."""
+    ns = ctx.slots
+    D = vecmat_diagonals(W, ns, replicate_out)
+    lvl = ct.level
+    pscale = _shifted(ctx.q[lvl], -pt_scale_shift)
+    Dqp = np.stack([ctx.coeffs_to_pt_qp(ctx.encode_coeffs(D[k], pscale)[1], lvl) for k in range(W.shape[0])])
+    acc = OCt(ctx.vec_mat_lazy_acc(ct, Dqp), lvl, ct.scale * pscale)
+    acc = ctx.rescale(acc)
+    if bias is not None:
+        acc = ctx.add_plain(acc, ctx.encode(vecmat_bias_slots(bias, ns, replicate_out), acc.scale, acc.level))
+    return acc
+
+
 def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarray | None,
                 chunk: int, kernel_shift: int = 0, mask_shift: int = 0) -> OCt:
     """Steps 12 (C18/C19): per channel t_c = rescale(ct * K_c), log2(#chunks)
@@ -185,14 +202,16 @@ def cnn_encrypt_input(ctx: OracleContext, img: np.ndarray, stream_id: int, plan=
     return ctx.encrypt(ctx.encode(slots, 2.0 ** plan["in_log2"], ctx.L - 1), stream_id)
 
 
-def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None) -> OCt:
+def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False) -> OCt:
+    """The paper's network; lazy=True uses vec_mat_lazy for FC1/FC2."""
     plan = plan or CNN_PLAN
+    vm = vec_mat_lazy if lazy else vec_mat
     x = im2col_conv(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64,
                     plan["conv_shift"], plan["mask_shift"])
     x = ctx.square(x)
-    x = vec_mat(ctx, x, w.fc1_w.T, w.fc1_b, replicate_out=True, pt_scale_shift=-plan["fc1_shift"])
+    x = vm(ctx, x, w.fc1_w.T, w.fc1_b, replicate_out=True, pt_scale_shift=-plan["fc1_shift"])
     x = ctx.square(x)
-    x = vec_mat(ctx, x, w.fc2_w.T, w.fc2_b, replicate_out=False, pt_scale_shift=-plan["fc2_shift"])
+    x = vm(ctx, x, w.fc2_w.T, w.fc2_b, replicate_out=False, pt_scale_shift=-plan["fc2_shift"])
     return x
 
 

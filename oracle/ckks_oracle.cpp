@@ -941,4 +941,101 @@ void orc_divround(void* h, const int* keep, int nkeep, const int* drop, int ndro
   divround(*c, std::vector<int>(keep, keep + nkeep), std::vector<int>(drop, drop + ndrop), xk, xd, o);
 }
 
+// vec_mat with ONE ModDown (DESIGN.md §3 "lazy ModDown"): the key-switch
+// inner products of all rotations are weighted by their diagonals and summed
+// in the extended basis Q_l P before a single DivRound by P:
+//   acc_p[t] = sum_{k>=1} D_k[t] . sum_j NTT_t([D_j(phi_k(c1))]_t) . ksk_k[j][p][t]
+//            + [t data limb] [P]_t (D_0[t] . c_p[t] + [p=0] sum_{k>=1} D_k[t] . phi_k(c0)[t])
+//   out_p = ModDown(acc_p)   (INTT, C15 DivRound by P, NTT; exact: ModDown(P X + Y) = X + ModDown(Y)).
+// diags: [n][l+1+K][N] NTT words, data limbs 0..l then the K special limbs.
+// Written unhoisted (phi_k applied to the ciphertext in the coefficient domain,
+// then the textbook key-switch digit lift), i.e. from the definitions.
+int orc_vec_mat_lazy(void* h, const uint64_t* ct, int level, const uint64_t* diags, int n, uint64_t* out) {
+  Ctx* c = (Ctx*)h;
+  const int N = c->N, Lc = level + 1, lk = LK(*c), nt = Lc + c->K;
+  const size_t P_ = (size_t)Lc * N;
+  std::vector<int> targets;
+  for (int i = 0; i < Lc; ++i) targets.push_back(i);
+  for (int k = 0; k < c->K; ++k) targets.push_back(c->L + k);
+  std::vector<u64> Pmod(nt);
+  for (int ti = 0; ti < nt; ++ti) {
+    u64 p = 1;
+    for (int k = 0; k < c->K; ++k) p = mulmod(p, c->q[c->L + k] % c->q[targets[ti]], c->q[targets[ti]]);
+    Pmod[ti] = p;
+  }
+  // acc[part][ti][n]
+  std::vector<u64> acc((size_t)2 * nt * N, 0);
+  auto A = [&](int p, int ti) { return &acc[((size_t)p * nt + ti) * N]; };
+  auto D = [&](int k, int ti) { return diags + ((size_t)k * nt + ti) * N; };
+  // k = 0: P D_0 c_p on the data limbs
+  for (int p = 0; p < 2; ++p)
+    for (int i = 0; i < Lc; ++i)
+      for (int m = 0; m < N; ++m)
+        A(p, i)[m] = addmod(A(p, i)[m], mulmod(Pmod[i], mulmod(D(0, i)[m], ct[p * P_ + (size_t)i * N + m], c->q[i]),
+                                               c->q[i]), c->q[i]);
+  std::vector<u64> phi(2 * P_), tmp(N), Dt(N);
+  std::vector<std::vector<i64>> Dj(Lc, std::vector<i64>(N));
+  for (int k = 1; k < n; ++k) {
+    const u64 g = galois_elt(*c, k);
+    auto it = c->gk.find(g);
+    if (it == c->gk.end()) return -1;
+    const std::vector<u64>& ksk = it->second;
+    for (int p = 0; p < 2; ++p)
+      for (int i = 0; i < Lc; ++i) {
+        std::memcpy(tmp.data(), ct + (size_t)p * P_ + (size_t)i * N, N * 8);
+        intt_limb(*c, i, tmp.data());
+        u64* o = &phi[(size_t)p * P_ + (size_t)i * N];
+        automorph_coeff(tmp.data(), o, N, g, c->q[i]);
+        ntt_limb(*c, i, o);
+      }
+    // P D_k phi_k(c0) on the data limbs
+    for (int i = 0; i < Lc; ++i)
+      for (int m = 0; m < N; ++m)
+        A(0, i)[m] = addmod(A(0, i)[m], mulmod(Pmod[i], mulmod(D(k, i)[m], phi[(size_t)i * N + m], c->q[i]), c->q[i]),
+                            c->q[i]);
+    // digits of phi_k(c1): INTT, centered lift (C16)
+    for (int j = 0; j < Lc; ++j) {
+      std::memcpy(tmp.data(), &phi[P_ + (size_t)j * N], N * 8);
+      intt_limb(*c, j, tmp.data());
+      for (int m = 0; m < N; ++m) Dj[j][m] = centered(tmp[m], c->q[j]);
+    }
+    for (int ti = 0; ti < nt; ++ti) {
+      const int t = targets[ti];
+      const u64 qt = c->q[t];
+      for (int j = 0; j < Lc; ++j) {
+        signed_to_ntt(*c, Dj[j].data(), t, Dt.data());
+        const u64* kb = &ksk[(((size_t)j * 2 + 0) * lk + t) * N];
+        const u64* ka = &ksk[(((size_t)j * 2 + 1) * lk + t) * N];
+        for (int m = 0; m < N; ++m) {
+          const u64 d = mulmod(D(k, ti)[m], Dt[m], qt);
+          A(0, ti)[m] = addmod(A(0, ti)[m], mulmod(d, kb[m], qt), qt);
+          A(1, ti)[m] = addmod(A(1, ti)[m], mulmod(d, ka[m], qt), qt);
+        }
+      }
+    }
+  }
+  // one ModDown per part
+  std::vector<int> keep(targets.begin(), targets.begin() + Lc), drop(targets.begin() + Lc, targets.end());
+  for (int p = 0; p < 2; ++p) {
+    for (int ti = 0; ti < nt; ++ti) intt_limb(*c, targets[ti], A(p, ti));
+    std::vector<const u64*> xk, xd;
+    std::vector<u64*> o;
+    for (int i = 0; i < Lc; ++i) {
+      xk.push_back(A(p, i));
+      o.push_back(out + (size_t)p * P_ + (size_t)i * N);
+    }
+    for (int k = 0; k < c->K; ++k) xd.push_back(A(p, Lc + k));
+    divround(*c, keep, drop, xk, xd, o);
+    for (int i = 0; i < Lc; ++i) ntt_limb(*c, i, o[i]);
+  }
+  return 0;
+}
+
+// Signed coefficients -> NTT words on data limbs 0..l and the K special limbs.
+void orc_coeffs_to_pt_qp(void* h, const int64_t* m, int level, uint64_t* pt) {
+  Ctx* c = (Ctx*)h;
+  for (int i = 0; i <= level; ++i) signed_to_ntt(*c, m, i, pt + (size_t)i * c->N);
+  for (int k = 0; k < c->K; ++k) signed_to_ntt(*c, m, c->L + k, pt + (size_t)(level + 1 + k) * c->N);
+}
+
 }  // extern "C"

@@ -94,6 +94,8 @@ def lib():
         L.orc_automorph_ntt.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_uint64,
                                         U64P]
         L.orc_rescale.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_int, U64P]
+        L.orc_vec_mat_lazy.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, U64P, ctypes.c_int, U64P]
+        L.orc_coeffs_to_pt_qp.argtypes = [ctypes.c_void_p, I64P, ctypes.c_int, U64P]
         L.orc_divround.argtypes = [ctypes.c_void_p, IP, ctypes.c_int, IP, ctypes.c_int, U64P,
                                    U64P, U64P]
         _lib = L
@@ -274,6 +276,23 @@ class OracleContext:
         out = np.zeros((level + 1, self.N), dtype=np.uint64)
         self.lib.orc_coeffs_to_pt(self.h, _p(m, I64P), level, _p(out, U64P))
         return OPt(out, level, float(scale))
+
+    def coeffs_to_pt_qp(self, m, level: int) -> np.ndarray:
+        """NTT words of signed coefficients on data limbs 0..level then the K special limbs."""
+        m = np.ascontiguousarray(m, dtype=np.int64)
+        out = np.zeros((level + 1 + self.K, self.N), dtype=np.uint64)
+        self.lib.orc_coeffs_to_pt_qp(self.h, _p(m, I64P), level, _p(out, U64P))
+        return out
+
+    def vec_mat_lazy_acc(self, ct: OCt, diags_qp: np.ndarray) -> np.ndarray:
+        """sum_k D_k (.) rot(ct, k) with one ModDown (see ckks_oracle.cpp orc_vec_mat_lazy);
+        diags_qp: [n][level+1+K][N]. Returns [2][level+1][N] (not rescaled)."""
+        d = _u64(diags_qp)
+        w = _u64(ct.words)
+        out = np.zeros((2, ct.level + 1, self.N), dtype=np.uint64)
+        if self.lib.orc_vec_mat_lazy(self.h, _p(w, U64P), ct.level, _p(d, U64P), d.shape[0], _p(out, U64P)) != 0:
+            raise KeyError("missing Galois key")
+        return out
 
     def encode(self, z, scale: float, level: int) -> OPt:
         _, m = self.encode_coeffs(z, scale)

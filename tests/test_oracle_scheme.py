@@ -237,3 +237,36 @@ def test_depth_accounting():
     assert np.max(np.abs(c.decode(c.decrypt(ct)) - x ** (2 ** (c.L - 1)))) < 1e-4
     with pytest.raises(ValueError):
         c.square(ct)
+
+
+# ---------------------------------------------- lazy-ModDown vec_mat pins ---
+def test_vec_mat_lazy_n1_equals_plain_exactly():
+    """With a single diagonal there is no rotation: ModDown(P D_0 c) must equal D_0 c exactly
+    (C15: ModDown(P X + Y) = X + ModDown(Y)), so vec_mat_lazy == vec_mat word for word."""
+    from oracle import circuits as OC
+    c = OracleContext(11, (50, 40, 40, 50, 50), 2, 5)
+    c.keygen([1])
+    rng = np.random.default_rng(1)
+    W = rng.normal(0, 0.1, (1, 1))
+    ct = c.encrypt(c.encode(rng.uniform(-1, 1, c.slots), 2.0 ** 30, 2), 0)
+    a = OC.vec_mat(c, ct, W, None, replicate_out=True)
+    b = OC.vec_mat_lazy(c, ct, W, None, replicate_out=True)
+    assert np.array_equal(a.words, b.words) and a.scale == b.scale
+
+
+@pytest.mark.parametrize("rep", [False, True])
+def test_vec_mat_lazy_matches_matmul(rep):
+    """Decrypted lazy vec_mat vs numpy x @ W (float definition) and vs the per-rotation-ModDown
+    vec_mat (both approximate the same product; they differ only by rounding noise)."""
+    from oracle import circuits as OC
+    c = OracleContext(12, (60, 40, 40, 60), 1, 0)
+    n, m = 16, (16 if rep else 5)
+    c.keygen(range(1, n))
+    rng = np.random.default_rng(2)
+    x, W, bias = rng.uniform(-1, 1, n), rng.normal(0, 0.1, (n, m)), rng.normal(0, 0.1, m)
+    ct = c.encrypt(c.encode(OC.replicate(x, c.slots), 2.0 ** 40, 2), 3)
+    y_lazy = c.decode(c.decrypt(OC.vec_mat_lazy(c, ct, W, bias, rep)), m)
+    y_plain = c.decode(c.decrypt(OC.vec_mat(c, ct, W, bias, rep)), m)
+    ref = x @ W + bias
+    assert np.max(np.abs(y_lazy - ref)) < 1e-6
+    assert np.max(np.abs(y_lazy - y_plain)) < 1e-6
