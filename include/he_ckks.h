@@ -221,6 +221,14 @@ he_status he_im2col_conv_pt(he_context* ctx, const he_ciphertext* ct, const he_p
 he_status he_vec_mat_encode(he_context* ctx, const double* W, int n, int m, const double* bias,
                             int replicate_out, int pt_scale_shift, int level, double in_scale,
                             he_plaintext** diags, he_plaintext** bias_pt);
+/* Lazy-ModDown form of he_vec_mat_encode: the n diagonals also carry the K
+ * special limbs (a "QP" plaintext), and he_vec_mat_pt given such diagonals
+ * sums every rotation's key-switch inner product, weighted by its diagonal, in
+ * the extended basis Q_l P and applies ONE ModDown (DESIGN.md §3/§5; the
+ * oracle's vec_mat_lazy).  Same scales, bias and level use as he_vec_mat_encode. */
+he_status he_vec_mat_encode_lazy(he_context* ctx, const double* W, int n, int m, const double* bias,
+                                 int replicate_out, int pt_scale_shift, int level, double in_scale,
+                                 he_plaintext** diags, he_plaintext** bias_pt);
 he_status he_im2col_conv_encode(he_context* ctx, const double* kernels, int n_channels, int kh, int kw,
                                 const double* bias, int chunk, int kernel_shift, int mask_shift,
                                 int level, double in_scale, he_plaintext** kernels_pt,
@@ -246,6 +254,12 @@ he_status he_pt_import_words(he_context* ctx, const uint64_t* src, int on_device
  * and NTT on device (C7 injection of an exactly-rounded encoding). */
 he_status he_pt_from_int_coeffs(he_context* ctx, const int64_t* m, size_t B, double scale, int level,
                                 he_plaintext** out);
+/* Same with the K special limbs appended (a QP plaintext, limbs 0..level then
+ * p_0..p_{K-1}), for he_vec_mat_pt's lazy-ModDown form. */
+he_status he_pt_from_int_coeffs_qp(he_context* ctx, const int64_t* m, size_t B, double scale, int level,
+                                   he_plaintext** out);
+/* Number of limbs per item of a plaintext (level+1, or level+1+K for QP). */
+he_status he_pt_limbs(const he_plaintext* pt, int* limbs);
 /* Export keys as NTT words: kind 0 = secret [L+K][N], 1 = public [2][L][N],
  * 2 = relin [L][2][L+K][N], 3 = Galois key of rotation `step` (same shape). */
 he_status he_key_export(he_context* ctx, int kind, int32_t step, uint64_t* dst);

@@ -93,6 +93,9 @@ _SIGS = {
     "he_pt_export_words": [VP, VP, VP, C.c_int],
     "he_pt_import_words": [VP, VP, C.c_int, SZ, C.c_int, C.c_double, VPP],
     "he_pt_from_int_coeffs": [VP, I64P, SZ, C.c_double, C.c_int, VPP],
+    "he_pt_from_int_coeffs_qp": [VP, I64P, SZ, C.c_double, C.c_int, VPP],
+    "he_pt_limbs": [VP, C.POINTER(C.c_int)],
+    "he_vec_mat_encode_lazy": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
     "he_key_export": [VP, C.c_int, C.c_int32, U64P],
     "he_key_words": [VP, C.c_int],
     "he_ntt_forward": [VP, VP, SZ, C.c_int],
@@ -169,9 +172,15 @@ class Plaintext:
     @property
     def scale(self): return self.info()[2]
 
+    @property
+    def limbs(self) -> int:
+        n = C.c_int()
+        _check(lib().he_pt_limbs(self.h, C.byref(n)))
+        return n.value
+
     def words(self) -> np.ndarray:
-        B, lvl, _ = self.info()
-        out = np.zeros((B, lvl + 1, self.ctx.N), dtype=np.uint64)
+        B = self.info()[0]
+        out = np.zeros((B, self.limbs, self.ctx.N), dtype=np.uint64)
         _check(lib().he_pt_export_words(self.ctx.h, self.h, _ptr(out), 0))
         return out
 
@@ -319,6 +328,13 @@ class Context:
                                            C.byref(h)))
         return Plaintext(self, h)
 
+    def he_pt_from_int_coeffs_qp(self, m, scale: float, level: int) -> Plaintext:
+        m2 = np.ascontiguousarray(np.atleast_2d(np.asarray(m, dtype=np.int64)))
+        h = C.c_void_p()
+        _check(lib().he_pt_from_int_coeffs_qp(self.h, m2.ctypes.data_as(I64P), m2.shape[0], float(scale), level,
+                                              C.byref(h)))
+        return Plaintext(self, h)
+
     def he_pt_import_words(self, w, level: int, scale: float) -> Plaintext:
         h = C.c_void_p()
         if _is_dev(w):
@@ -376,12 +392,13 @@ class Context:
                          None if b is None else b.ctypes.data_as(DP), int(bool(replicate_out)),
                          int(pt_scale_shift))
 
-    def he_vec_mat_encode(self, W, bias, replicate_out, pt_scale_shift, level, in_scale):
+    def he_vec_mat_encode(self, W, bias, replicate_out, pt_scale_shift, level, in_scale, lazy=False):
         W = np.ascontiguousarray(W, dtype=np.float64)
         n, m = W.shape
         b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
         d, bp = C.c_void_p(), C.c_void_p()
-        _check(lib().he_vec_mat_encode(self.h, W.ctypes.data_as(DP), n, m,
+        fn = lib().he_vec_mat_encode_lazy if lazy else lib().he_vec_mat_encode
+        _check(fn(self.h, W.ctypes.data_as(DP), n, m,
                                        None if b is None else b.ctypes.data_as(DP), int(bool(replicate_out)),
                                        int(pt_scale_shift), level, float(in_scale), C.byref(d), C.byref(bp)))
         return Plaintext(self, d), (Plaintext(self, bp) if bp.value else None)

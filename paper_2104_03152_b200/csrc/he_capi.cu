@@ -333,9 +333,14 @@ he_status he_negate(he_context* c, const he_ciphertext* a, he_ciphertext** out) 
   });
 }
 
+static void need_plain_q(const he_plaintext* p) {
+  need(!p->qp, HE_LAYOUT_MISMATCH, "QP plaintexts (with special limbs) are only accepted by he_vec_mat_pt");
+}
+
 he_status he_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext** out) {
   return guard([&] {
     need_ctx(c); need_ct(c, a); need_pt(c, p); need_out(out);
+    need_plain_q(p);
     need(a->level == p->level, HE_LEVEL_MISMATCH, "levels differ");
     need(a->scale == p->scale, HE_SCALE_MISMATCH, "scales differ");
     need_batch(a->B, p->B);
@@ -346,6 +351,7 @@ he_status he_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext
 he_status he_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext** out) {
   return guard([&] {
     need_ctx(c); need_ct(c, a); need_pt(c, p); need_out(out);
+    need_plain_q(p);
     need(a->level == p->level, HE_LEVEL_MISMATCH, "levels differ");
     need_batch(a->B, p->B);
     *out = ct_mul_plain(c, a, p);
@@ -457,6 +463,9 @@ he_status he_im2col_conv_pt(he_context* c, const he_ciphertext* ct, const he_pla
   return guard([&] {
     need_ctx(c); need_ct(c, ct); need_pt(c, kernels); need_pt(c, masks); need_out(out);
     conv_checks(c, ct, kernels->B, 1, chunk);
+    need_plain_q(kernels);
+    need_plain_q(masks);
+    if (bias) need_plain_q(bias);
     need(masks->B == kernels->B, HE_SHAPE_MISMATCH, "one mask per kernel");
     need(kernels->level == ct->level && masks->level == ct->level - 1, HE_LEVEL_MISMATCH,
          "kernels at the input level, masks one below");
@@ -551,8 +560,10 @@ he_status he_vec_mat_pt(he_context* c, const he_ciphertext* ct, const he_plainte
     need(ct->level >= 1, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
     need(diags->level == ct->level, HE_LEVEL_MISMATCH, "diagonals must be at the ciphertext level");
     need(diags->B >= 1 && diags->B <= c->N / 2, HE_SHAPE_MISMATCH, "1 <= n <= n_s diagonals");
+    need(!diags->qp || c->K > 0, HE_MISSING_KEY, "lazy ModDown needs special primes");
     if (bias_pt) {
       need_pt(c, bias_pt);
+      need_plain_q(bias_pt);
       need(bias_pt->B == 1, HE_SHAPE_MISMATCH, "bias is one plaintext");
       need(bias_pt->level == ct->level - 1, HE_LEVEL_MISMATCH, "bias at the rescaled level");
       need(bias_pt->scale == ct->scale * diags->scale / (double)c->hp.q[ct->level], HE_SCALE_MISMATCH,
@@ -563,7 +574,8 @@ he_status he_vec_mat_pt(he_context* c, const he_ciphertext* ct, const he_plainte
 }
 
 static void vecmat_encode(he_context* c, const double* W, int n, int m, const double* bias, int replicate_out,
-                          int pt_scale_shift, int l, double in_scale, he_plaintext** dp, he_plaintext** bp) {
+                          int pt_scale_shift, int l, double in_scale, he_plaintext** dp, he_plaintext** bp,
+                          int qp = 0) {
   need(W != nullptr, HE_INVALID_ARGUMENT, "null matrix");
   need(l >= 1 && l < c->L, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
   const int ns = c->N / 2;
@@ -571,7 +583,7 @@ static void vecmat_encode(he_context* c, const double* W, int n, int m, const do
   PtGuard pd, pb;
   {
     DevDoubles d(c, D.data(), D.size());
-    pd.p = encode(c, d.d, ns, n, shifted(c->hp.q[l], -pt_scale_shift), l);
+    pd.p = encode(c, d.d, ns, n, shifted(c->hp.q[l], -pt_scale_shift), l, qp);
   }
   if (bias) {
     std::vector<double> bs(ns, 0.0);
@@ -594,6 +606,17 @@ he_status he_vec_mat_encode(he_context* c, const double* W, int n, int m, const 
     need_ctx(c);
     need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
     vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, level, in_scale, diags, bias_pt);
+  });
+}
+
+he_status he_vec_mat_encode_lazy(he_context* c, const double* W, int n, int m, const double* bias,
+                                 int replicate_out, int pt_scale_shift, int level, double in_scale,
+                                 he_plaintext** diags, he_plaintext** bias_pt) {
+  return guard([&] {
+    need_ctx(c);
+    need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
+    need(c->K > 0, HE_INVALID_PARAMS, "lazy ModDown needs special primes");
+    vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, level, in_scale, diags, bias_pt, 1);
   });
 }
 
@@ -722,6 +745,26 @@ he_status he_pt_from_int_coeffs(he_context* c, const int64_t* m, size_t B, doubl
     Scratch d(c, B * c->N * 8);
     HE_CK(cudaMemcpyAsync(d.p, m, B * c->N * 8, cudaMemcpyHostToDevice, c->stream));
     *out = pt_from_int(c, d.as<i64>(), B, scale, level);
+  });
+}
+
+he_status he_pt_from_int_coeffs_qp(he_context* c, const int64_t* m, size_t B, double scale, int level,
+                                   he_plaintext** out) {
+  return guard([&] {
+    need_ctx(c); need_out(out);
+    need(m != nullptr && B >= 1, HE_INVALID_ARGUMENT, "bad source");
+    need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
+    need(c->K > 0, HE_INVALID_PARAMS, "no special primes");
+    Scratch d(c, B * c->N * 8);
+    HE_CK(cudaMemcpyAsync(d.p, m, B * c->N * 8, cudaMemcpyHostToDevice, c->stream));
+    *out = pt_from_int(c, d.as<i64>(), B, scale, level, 1);
+  });
+}
+
+he_status he_pt_limbs(const he_plaintext* pt, int* limbs) {
+  return guard([&] {
+    need(pt && limbs, HE_INVALID_ARGUMENT, "null argument");
+    *limbs = pt_limbs(pt);
   });
 }
 

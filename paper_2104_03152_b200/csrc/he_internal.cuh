@@ -74,7 +74,8 @@ struct he_plaintext {
   he_context* ctx;
   int B, level;
   double scale;
-  he::u64* d;  // [B][level+1][N]
+  he::u64* d;  // [B][level+1 (+K if qp)][N]
+  int qp = 0;  // 1: also carries the K special limbs (data limbs first), for lazy-ModDown products
 };
 
 namespace he {

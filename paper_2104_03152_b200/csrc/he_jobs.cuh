@@ -44,7 +44,11 @@ struct JobSignedToNtt {
   u64* dst;
   int N, nl;
   size_t src_bs, dst_bs;
-  __device__ int prime(int blk) const { return blk % nl; }
+  int lc, L;   // limbs >= lc are special limbs (prime L + limb - lc); lc = nl: data limbs only
+  __device__ int prime(int blk) const {
+    const int l = blk % nl;
+    return l < lc ? l : L + (l - lc);
+  }
   __device__ u64 load(int blk, u32 i, const PrimeD& P) const {
     return from_signed(poly[(size_t)(blk / nl) * src_bs + i], P);
   }
@@ -112,6 +116,9 @@ struct KsArgs {
   int add_gather;          // apply pi_g to the addsrc index
   const u64* D;            // nullable plaintext factor: D + kk*D_ks + i*N
   size_t D_ks;
+  // lazy ModDown: when set, the inner products are replaced by the extended-basis
+  // accumulator accx[b][part][Lc+K][N] (data limbs then specials), KB = 1
+  const u64* accx;
 };
 
 // Inner product over digits at target limb t for source position sn.
@@ -145,6 +152,7 @@ struct JobKsSpecial {
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
     int kk, b, part, k;
     dec(blk, kk, b, part, k);
+    if (a.accx) return a.accx[(((size_t)b * 2 + part) * (a.Lc + a.K) + a.Lc + k) * a.N + n];
     const u32 g = a.gal[kk];
     const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
     return ks_inner(a, kk, b, part, a.Lc + k, a.L + k, sn, n, P);
@@ -188,7 +196,8 @@ struct JobKsData {
     dec(blk, kk, b, part, i);
     const u32 g = a.gal[kk];
     const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
-    const u64 ip = ks_inner(a, kk, b, part, i, i, sn, n, P);
+    const u64 ip = a.accx ? a.accx[(((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N + n]
+                          : ks_inner(a, kk, b, part, i, i, sn, n, P);
     u64 u = mul_mod(sub_mod(ip, v, P.q), __ldg(a.Pinv_mod + i), P);
     const size_t LN = (size_t)a.Lc * a.N;
     if (part < a.add_parts)
@@ -246,14 +255,16 @@ inline double alg_bytes(const JobModUp& j, int nblk) {
   const int nt = j.Lc + j.K - 1;
   return 8.0 * j.N * (nblk + (double)nblk / nt);
 }
-inline double alg_bytes(const JobKsSpecial& j, int) {
+inline double alg_bytes(const JobKsSpecial& j, int nblk) {
   const KsArgs& a = j.a;
   const double N8 = 8.0 * a.N;
+  if (a.accx) return N8 * 2.0 * nblk;
   return N8 * ((double)a.B * a.Lc * a.K + (double)a.KB * 2 * a.Lc * a.K + (double)a.KB * a.B * 2 * a.K);
 }
-inline double alg_bytes(const JobKsData& j, int) {
+inline double alg_bytes(const JobKsData& j, int nblk) {
   const KsArgs& a = j.a;
   const double N8 = 8.0 * a.N;
+  if (a.accx) return N8 * ((double)nblk * 2 + (double)a.B * 2 * a.K);
   double w = (double)a.KB * a.B * 2 * a.K                  // tb
              + (double)a.B * a.Lc * a.Lc                   // ext data limbs (+ digit source diagonal)
              + (double)a.KB * 2 * a.Lc * a.Lc              // key rows of the data limbs

@@ -113,8 +113,8 @@ he_ciphertext* ct_new(he_context* c, int B, int size, int level, double scale) {
   }
   return ct;
 }
-he_plaintext* pt_new(he_context* c, int B, int level, double scale) {
-  he_plaintext* pt = new he_plaintext{c, B, level, scale, nullptr};
+he_plaintext* pt_new(he_context* c, int B, int level, double scale, int qp) {
+  he_plaintext* pt = new he_plaintext{c, B, level, scale, nullptr, qp};
   try {
     pt->d = dalloc_t<u64>(c, pt_words(pt));
   } catch (...) {
@@ -359,6 +359,76 @@ __global__ void k_check_words(const u64* __restrict__ w, const PrimeD* __restric
   }
 }
 
+// vec_mat with one lazy ModDown: extended-basis accumulator
+//   acc_p[t] = sum_{k>=1} D_k[t] sum_j x_j^{(k)}[t] ksk_k[j][p][t]
+//            + [t < Lc] [P]_t (D_0 c_p + [p = 0] sum_{k>=1} D_k phi_k(c0))
+// with x_j^{(k)}[t][n] = ext[j][t][pi_k(n)] (t != j) or c1[j][pi_k(n)] (t == j): the
+// hoisted digits of c1, permuted by the automorphism as they are gathered.
+struct LazyArgs {
+  int N, logN, Lc, K, L, NP, n;
+  const u64* ext;               // [B][Lc][Lc+K][N]
+  const u64* ct;                // [B][2][Lc][N]
+  const u64* diags;             // [n][Lc+K][N]
+  const u64* const* keys;       // [n] device pointers (entry 0 unused)
+  const u32* gal;               // [n]
+  const u64* P_mod;             // [NP]
+  u64* accx;                    // [B][2][Lc+K][N]
+};
+constexpr int LAZY_EPT = 2;
+__global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* __restrict__ primes) {
+  const int t = blockIdx.y, b = blockIdx.z, nt = a.Lc + a.K;
+  const int tp = t < a.Lc ? t : a.L + (t - a.Lc);
+  const PrimeD P = load_prime(primes, tp);
+  const size_t N = a.N, LN = (size_t)a.Lc * N;
+  const u64* c0 = a.ct + (size_t)b * 2 * LN;
+  const u64* c1 = c0 + LN;
+  const u64* ext = a.ext + (size_t)b * a.Lc * nt * N;
+  const bool data = t < a.Lc;
+  u32 nn[LAZY_EPT];
+  u64 acc0[LAZY_EPT], acc1[LAZY_EPT], cc0[LAZY_EPT], cc1[LAZY_EPT];
+#pragma unroll
+  for (int e = 0; e < LAZY_EPT; ++e) {
+    nn[e] = (blockIdx.x * LAZY_EPT + e) * blockDim.x + threadIdx.x;
+    acc0[e] = acc1[e] = cc0[e] = cc1[e] = 0;
+    if (data) {
+      const u64 d0 = a.diags[(size_t)t * N + nn[e]];
+      cc0[e] = mul_mod(d0, c0[(size_t)t * N + nn[e]], P);
+      cc1[e] = mul_mod(d0, c1[(size_t)t * N + nn[e]], P);
+    }
+  }
+  for (int k = 1; k < a.n; ++k) {
+    const u32 g = __ldg(a.gal + k);
+    const u64* key = a.keys[k];
+    const u64* Dk = a.diags + ((size_t)k * nt + t) * N;
+#pragma unroll
+    for (int e = 0; e < LAZY_EPT; ++e) {
+      const u32 n = nn[e], sn = galois_src(n, g, a.logN);
+      u64 ip0 = 0, ip1 = 0;
+      for (int j = 0; j < a.Lc; ++j) {
+        const u64 x = (t == j) ? c1[(size_t)j * N + sn] : ext[((size_t)j * nt + t) * N + sn];
+        const u64 kb = __ldg(key + (((size_t)j * 2 + 0) * a.NP + tp) * N + n);
+        const u64 ka = __ldg(key + (((size_t)j * 2 + 1) * a.NP + tp) * N + n);
+        ip0 = add_mod(ip0, mul_mod(x, kb, P), P.q);
+        ip1 = add_mod(ip1, mul_mod(x, ka, P), P.q);
+      }
+      const u64 d = __ldg(Dk + n);
+      acc0[e] = add_mod(acc0[e], mul_mod(d, ip0, P), P.q);
+      acc1[e] = add_mod(acc1[e], mul_mod(d, ip1, P), P.q);
+      if (data) cc0[e] = add_mod(cc0[e], mul_mod(d, c0[(size_t)t * N + sn], P), P.q);
+    }
+  }
+  const u64 Pt = __ldg(a.P_mod + tp);
+#pragma unroll
+  for (int e = 0; e < LAZY_EPT; ++e) {
+    if (data) {
+      acc0[e] = add_mod(acc0[e], mul_mod(Pt, cc0[e], P), P.q);
+      acc1[e] = add_mod(acc1[e], mul_mod(Pt, cc1[e], P), P.q);
+    }
+    a.accx[(((size_t)b * 2 + 0) * nt + t) * N + nn[e]] = acc0[e];
+    a.accx[(((size_t)b * 2 + 1) * nt + t) * N + nn[e]] = acc1[e];
+  }
+}
+
 // ======================================================== encode / decode ===
 // Canonical embedding (C6) with a length-M = N/2 complex FFT:
 //   encode  w_i = zeta^{-i} sum_r Z[r] omega^{-i r},  Z[r_j] = z_j,
@@ -547,8 +617,8 @@ void modmul_rows(he_context* c, const u64* a, const u64* b, u64* out, size_t ite
   check_launch(c);
 }
 
-void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int nl) {
-  JobSignedToNtt j{poly, dst, c->N, nl, (size_t)c->N, (size_t)nl * c->N};
+void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int nl, int lc) {
+  JobSignedToNtt j{poly, dst, c->N, nl, (size_t)c->N, (size_t)nl * c->N, lc < 0 ? nl : lc, c->L};
   launch_ntt<false>(c, j, (int)(items * nl));
 }
 
@@ -759,6 +829,40 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
 // vec_mat with pre-encoded diagonals (a14, C17): acc = sum_k rot(x, k) (.) D_k
 // with all rotations hoisted (one ModUp of c1 shared by every k), then one
 // rescale and the bias.
+static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
+                                      const std::vector<const u64*>& keys, const std::vector<u32>& gals) {
+  const int Lc = x->level + 1, n = diags->B, B = x->B, nt = Lc + c->K;
+  const size_t LN = (size_t)Lc * c->N, N = c->N;
+  Scratch kt(c, n * sizeof(u64*)), gt(c, n * sizeof(u32));
+  HE_CK(cudaMemcpyAsync(kt.p, keys.data(), n * sizeof(u64*), cudaMemcpyHostToDevice, c->stream));
+  HE_CK(cudaMemcpyAsync(gt.p, gals.data(), n * sizeof(u32), cudaMemcpyHostToDevice, c->stream));
+  u64* ext = n > 1 ? modup(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
+  he_ciphertext* acc = nullptr;
+  try {
+    Scratch accx(c, (size_t)B * 2 * nt * N * 8);
+    LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, n, ext, x->d, diags->d, kt.as<const u64*>(), gt.as<u32>(),
+                c->d_P_mod, accx.as<u64>()};
+    {
+      ProfScope ps_(c, "vecmat_lazy", 0.0, 0);
+      k_vecmat_lazy<<<dim3((unsigned)(N / (256 * LAZY_EPT)), nt, B), 256, 0, c->stream>>>(la, c->d_primes);
+    }
+    check_launch(c);
+    acc = ct_new(c, B, 2, x->level, x->scale * diags->scale);
+    KsArgs a = ks_base(c, B, Lc, nullptr, nullptr, 0);
+    a.gal[0] = 1;
+    a.accx = accx.as<u64>();
+    a.out = acc->d;
+    a.out_bs = 2 * LN;
+    ks_launch(c, a);
+  } catch (...) {
+    dfree(c, ext);
+    ct_free(acc);
+    throw;
+  }
+  dfree(c, ext);
+  return acc;
+}
+
 he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                           const he_plaintext* bias) {
   const int Lc = x->level + 1, n = diags->B, B = x->B;
@@ -768,6 +872,23 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
   for (int k = 1; k < n; ++k) {
     keys[k] = galois_key(c, k, &gals[k]);
     if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(k));
+  }
+  if (diags->qp) {
+    he_ciphertext* acc = ct_vec_mat_lazy(c, x, diags, keys, gals);
+    he_ciphertext* res = nullptr;
+    try {
+      res = ct_rescale(c, acc);
+    } catch (...) {
+      ct_free(acc);
+      throw;
+    }
+    ct_free(acc);
+    if (bias) {
+      he_ciphertext* r2 = ct_add_plain(c, res, bias);
+      ct_free(res);
+      res = r2;
+    }
+    return res;
   }
   // k = 0 term
   he_plaintext d0{c, 1, diags->level, diags->scale, diags->d};
@@ -964,7 +1085,7 @@ void keygen(he_context* c, const std::vector<int>& steps) {
 }
 
 // ---- encode / decode / encrypt / decrypt --------------------------------------
-he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level) {
+he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp) {
   const int N = c->N, M = N / 2, logM = c->logN - 1;
   Scratch m(c, B * N * 8), flag(c, 4);
   HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
@@ -984,14 +1105,14 @@ he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, dou
   HE_CK(cudaMemcpyAsync(&hflag, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
   HE_CK(cudaStreamSynchronize(c->stream));
   if (hflag) throw HeError(HE_SCALE_OVERFLOW, "encode: |scale * z| >= 2^62");
-  he_plaintext* pt = pt_new(c, (int)B, level, scale);
-  signed_to_ntt(c, m.as<i64>(), pt->d, B, level + 1);
+  he_plaintext* pt = pt_new(c, (int)B, level, scale, qp);
+  signed_to_ntt(c, m.as<i64>(), pt->d, B, pt_limbs(pt), level + 1);
   return pt;
 }
 
-he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level) {
-  he_plaintext* pt = pt_new(c, (int)B, level, scale);
-  signed_to_ntt(c, m_dev, pt->d, B, level + 1);
+he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level, int qp) {
+  he_plaintext* pt = pt_new(c, (int)B, level, scale, qp);
+  signed_to_ntt(c, m_dev, pt->d, B, pt_limbs(pt), level + 1);
   return pt;
 }
 
@@ -1036,7 +1157,7 @@ he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
     check_launch(c);
     // NTT into noise [b][w][Lc][N]
     JobSignedToNtt j{small.as<i64>() + (size_t)w * B * N, noise.as<u64>() + (size_t)w * Lc * N, N, Lc, (size_t)N,
-                     (size_t)3 * Lc * N};
+                     (size_t)3 * Lc * N, Lc, c->L};
     launch_ntt<false>(c, j, B * Lc);
   }
   he_ciphertext* ct = ct_new(c, B, 2, pt->level, pt->scale);

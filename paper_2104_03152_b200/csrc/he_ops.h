@@ -7,13 +7,14 @@
 namespace he {
 
 inline size_t ct_words(const he_ciphertext* c) { return (size_t)c->B * c->size * (c->level + 1) * c->ctx->N; }
-inline size_t pt_words(const he_plaintext* p) { return (size_t)p->B * (p->level + 1) * p->ctx->N; }
+inline int pt_limbs(const he_plaintext* p) { return p->level + 1 + (p->qp ? p->ctx->K : 0); }
+inline size_t pt_words(const he_plaintext* p) { return (size_t)p->B * pt_limbs(p) * p->ctx->N; }
 
 void context_init(he_context* c, const HostParams& hp, u64 seed);
 void context_destroy(he_context* c);
 
 he_ciphertext* ct_new(he_context* c, int B, int size, int level, double scale);
-he_plaintext* pt_new(he_context* c, int B, int level, double scale);
+he_plaintext* pt_new(he_context* c, int B, int level, double scale, int qp = 0);
 void ct_free(he_ciphertext* ct);
 void pt_free(he_plaintext* pt);
 
@@ -22,13 +23,13 @@ void ntt_rows(he_context* c, const u64* src, u64* dst, size_t items, int nl, siz
               bool inverse);
 void modmul_rows(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl);
 void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items, int nl);
-void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int nl);
+void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int nl, int lc = -1);
 int check_words(he_context* c, const u64* w, size_t items, int Lc);
 
 // scheme
 void keygen(he_context* c, const std::vector<int>& steps);
-he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level);
-he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level);
+he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp = 0);
+he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level, int qp = 0);
 void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n);
 he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id);
 he_plaintext* decrypt(he_context* c, const he_ciphertext* ct);

@@ -283,3 +283,23 @@ def test_vec_mat_batch_and_bias(tiny):
     for b in range(3):
         ref = OC.vec_mat(o2, octs[b], W, bias, replicate_out=True)
         assert np.array_equal(w[b], ref.words), b
+
+
+def test_vec_mat_lazy_bit_exact(cfg1):
+    """One-ModDown vec_mat (QP diagonals) vs the oracle's vec_mat_lazy, cfg1 shape, B=2."""
+    o, g = cfg1
+    x, W = vecmat_inputs(0)
+    lvl = o.L - 1
+    xs = OC.replicate(x, o.slots)
+    octs = [oracle_ct(o, xs, 2.0 ** 40, lvl, b) for b in range(2)]
+    D = OC.vecmat_diagonals(W, o.slots, False)
+    ps = float(o.q[lvl])
+    gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(d, ps)[1] for d in D]), ps, lvl)
+    assert gD.limbs == lvl + 1 + o.K
+    out = g.he_vec_mat_pt(g.he_ct_import_words(np.stack([c.words for c in octs]), lvl, 2.0 ** 40), gD)
+    W2 = out.words()
+    for b in range(2):
+        ref = OC.vec_mat_lazy(o, octs[b], W, None, replicate_out=False)
+        assert np.array_equal(W2[b], ref.words), b
+    y = g.he_decode(g.he_decrypt(out), 10)
+    assert np.max(np.abs(y - x @ W)) < 1e-6
