@@ -39,6 +39,7 @@ struct he_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
+  bool small_primes = false;  // every prime < 2^31: 64-bit lazy sums of 62-bit products
   // device tables
   he::PrimeD* d_primes = nullptr;
   ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [NP][N] (w, floor(w 2^64 / q))

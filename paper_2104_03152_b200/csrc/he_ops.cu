@@ -69,6 +69,8 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
     p.r64 = (u64)((((u128)1) << 64) % hp.q[t]);
   }
   c->d_primes = upload(c, pd);
+  c->small_primes = true;
+  for (u64 q : hp.q) c->small_primes = c->small_primes && q < (1ULL << 31);
   {
     std::vector<ulonglong2> t2(hp.tw.size()), i2(hp.tw.size());
     for (size_t k = 0; k < hp.tw.size(); ++k) {
@@ -375,6 +377,16 @@ struct LazyArgs {
   u64* accx;                    // [B][2][Lc+K][N]
 };
 constexpr int LAZY_EPT = 2;
+// SMALL: every prime < 2^31, so a product of two residues is < 2^62 and up to
+// four products (plus a reduced value) sum without overflow in 64 bits: one
+// IMAD.WIDE.U32 per term and one reduction per four terms.
+template <bool SMALL>
+__device__ __forceinline__ u64 mac_reduce(u64 acc, u64 a, u64 b, const PrimeD& P) {
+  if (SMALL) return reduce64(acc + (u64)(u32)a * (u32)b, P);
+  return add_mod(acc, mul_mod(a, b, P), P.q);
+}
+
+template <bool SMALL>
 __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* __restrict__ primes) {
   const int t = blockIdx.y, b = blockIdx.z, nt = a.Lc + a.K;
   const int tp = t < a.Lc ? t : a.L + (t - a.Lc);
@@ -392,8 +404,8 @@ __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* _
     acc0[e] = acc1[e] = cc0[e] = cc1[e] = 0;
     if (data) {
       const u64 d0 = a.diags[(size_t)t * N + nn[e]];
-      cc0[e] = mul_mod(d0, c0[(size_t)t * N + nn[e]], P);
-      cc1[e] = mul_mod(d0, c1[(size_t)t * N + nn[e]], P);
+      cc0[e] = mac_reduce<SMALL>(0, d0, c0[(size_t)t * N + nn[e]], P);
+      cc1[e] = mac_reduce<SMALL>(0, d0, c1[(size_t)t * N + nn[e]], P);
     }
   }
   for (int k = 1; k < a.n; ++k) {
@@ -408,21 +420,34 @@ __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* _
         const u64 x = (t == j) ? c1[(size_t)j * N + sn] : ext[((size_t)j * nt + t) * N + sn];
         const u64 kb = __ldg(key + (((size_t)j * 2 + 0) * a.NP + tp) * N + n);
         const u64 ka = __ldg(key + (((size_t)j * 2 + 1) * a.NP + tp) * N + n);
-        ip0 = add_mod(ip0, mul_mod(x, kb, P), P.q);
-        ip1 = add_mod(ip1, mul_mod(x, ka, P), P.q);
+        if (SMALL) {
+          ip0 += (u64)(u32)x * (u32)kb;
+          ip1 += (u64)(u32)x * (u32)ka;
+          if ((j & 3) == 3) {
+            ip0 = reduce64(ip0, P);
+            ip1 = reduce64(ip1, P);
+          }
+        } else {
+          ip0 = add_mod(ip0, mul_mod(x, kb, P), P.q);
+          ip1 = add_mod(ip1, mul_mod(x, ka, P), P.q);
+        }
+      }
+      if (SMALL) {
+        ip0 = reduce64(ip0, P);
+        ip1 = reduce64(ip1, P);
       }
       const u64 d = __ldg(Dk + n);
-      acc0[e] = add_mod(acc0[e], mul_mod(d, ip0, P), P.q);
-      acc1[e] = add_mod(acc1[e], mul_mod(d, ip1, P), P.q);
-      if (data) cc0[e] = add_mod(cc0[e], mul_mod(d, c0[(size_t)t * N + sn], P), P.q);
+      acc0[e] = mac_reduce<SMALL>(acc0[e], d, ip0, P);
+      acc1[e] = mac_reduce<SMALL>(acc1[e], d, ip1, P);
+      if (data) cc0[e] = mac_reduce<SMALL>(cc0[e], d, c0[(size_t)t * N + sn], P);
     }
   }
   const u64 Pt = __ldg(a.P_mod + tp);
 #pragma unroll
   for (int e = 0; e < LAZY_EPT; ++e) {
     if (data) {
-      acc0[e] = add_mod(acc0[e], mul_mod(Pt, cc0[e], P), P.q);
-      acc1[e] = add_mod(acc1[e], mul_mod(Pt, cc1[e], P), P.q);
+      acc0[e] = mac_reduce<SMALL>(acc0[e], Pt, cc0[e], P);
+      acc1[e] = mac_reduce<SMALL>(acc1[e], Pt, cc1[e], P);
     }
     a.accx[(((size_t)b * 2 + 0) * nt + t) * N + nn[e]] = acc0[e];
     a.accx[(((size_t)b * 2 + 1) * nt + t) * N + nn[e]] = acc1[e];
@@ -843,8 +868,13 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
     LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, n, ext, x->d, diags->d, kt.as<const u64*>(), gt.as<u32>(),
                 c->d_P_mod, accx.as<u64>()};
     {
-      ProfScope ps_(c, "vecmat_lazy", 0.0, 0);
-      k_vecmat_lazy<<<dim3((unsigned)(N / (256 * LAZY_EPT)), nt, B), 256, 0, c->stream>>>(la, c->d_primes);
+      // algorithmic bytes: ext + ct + accumulators once per item, keys and diagonals once per launch
+      const double bytes = 8.0 * N * ((double)B * Lc * nt + (double)B * 2 * Lc + (double)B * 2 * nt +
+                                      (double)(n - 1) * 2 * Lc * nt + (double)n * nt);
+      ProfScope ps_(c, "vecmat_lazy", bytes, B * nt);
+      const dim3 grid((unsigned)(N / (256 * LAZY_EPT)), nt, B);
+      if (c->small_primes) k_vecmat_lazy<true><<<grid, 256, 0, c->stream>>>(la, c->d_primes);
+      else k_vecmat_lazy<false><<<grid, 256, 0, c->stream>>>(la, c->d_primes);
     }
     check_launch(c);
     acc = ct_new(c, B, 2, x->level, x->scale * diags->scale);
