@@ -51,8 +51,18 @@ __device__ __forceinline__ u64 barrett128(u64 lo, u64 hi, u64 q, u64 mu, u32 k) 
   r = r >= q ? r - q : r;
   return r >= q ? r - q : r;
 }
+// Barrett for q < 2^31 (k <= 31) and x = a b < 2^{2k}: the same HAC 14.42
+// steps with every intermediate in one 32x32->64 multiply.
+__device__ __forceinline__ u64 barrett_small(u64 x, u64 q, u64 mu, u32 k) {
+  const u32 q1 = (u32)(x >> (k - 1));
+  const u32 q3 = (u32)(((u64)q1 * (u32)mu) >> (k + 1));
+  u64 r = x - (u64)q3 * (u32)q;
+  r = r >= q ? r - q : r;
+  return r >= q ? r - q : r;
+}
 // a * b mod q for a, b < q.
 __device__ __forceinline__ u64 mul_mod(u64 a, u64 b, const PrimeD& P) {
+  if (P.k <= 31) return barrett_small((u64)(u32)a * (u32)b, P.q, P.mu, P.k);
   return barrett128(a * b, __umul64hi(a, b), P.q, P.mu, P.k);
 }
 // Reduce any 64-bit word mod q: qh = floor(x mu64 / 2^64) >= floor(x/q) - 2,

@@ -43,6 +43,7 @@ struct he_context {
   // device tables
   he::PrimeD* d_primes = nullptr;
   ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [NP][N] (w, floor(w 2^64 / q))
+  uint2 *d_tw32 = nullptr, *d_itw32 = nullptr;      // [NP][N] (w, floor(w 2^32 / q)); small primes only
   he::u64* d_cdt = nullptr;
   he::u64 *d_P_mod = nullptr, *d_Pinv_mod = nullptr, *d_Ph_mod = nullptr;
   he::u64 *d_Phat_inv = nullptr, *d_Phat_mod = nullptr;
@@ -168,8 +169,33 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
   check_launch(c);
 }
 
+template <int LOGN, bool INV, class Job>
+void launch_ntt32_t(he_context* c, const Job& job, int nblk) {
+  typedef NttGeom<LOGN, 1> G;
+  static bool configured = false;
+  auto kern = k_ntt32<LOGN, INV, Job>;
+  if (!configured) {
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NttGeom32<LOGN>::SMEM));
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    configured = true;
+  }
+  if (nblk <= 0) return;
+  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk);
+  kern<<<nblk, G::T, NttGeom32<LOGN>::SMEM, c->stream>>>(job, c->d_primes, INV ? c->d_itw32 : c->d_tw32);
+  check_launch(c);
+}
+
 template <bool INV, class Job>
 void launch_ntt(he_context* c, const Job& job, int nblk) {
+  if (c->small_primes && c->d_tw32 && c->logN <= 14) {
+    switch (c->logN) {
+      case 10: launch_ntt32_t<10, INV>(c, job, nblk); return;
+      case 11: launch_ntt32_t<11, INV>(c, job, nblk); return;
+      case 12: launch_ntt32_t<12, INV>(c, job, nblk); return;
+      case 13: launch_ntt32_t<13, INV>(c, job, nblk); return;
+      case 14: launch_ntt32_t<14, INV>(c, job, nblk); return;
+    }
+  }
   switch (c->logN) {
     case 10: launch_ntt_t<10, 1, INV>(c, job, nblk); break;
     case 11: launch_ntt_t<11, 1, INV>(c, job, nblk); break;

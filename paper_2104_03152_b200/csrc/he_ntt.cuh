@@ -210,4 +210,103 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __r
   for (u32 i = tid; i < G::NL; i += G::T) job.store(blk, i, mul_shoup(sm[spad(i)], P.ninv, P.ninvsh, P.q), P);
 }
 
+// ===================================================== 32-bit arithmetic ===
+// Contexts whose primes are all < 2^31 (BASELINE config 4) run the same
+// network on u32 registers and shared memory (half the smem, 32x32-bit Shoup
+// products); HBM words stay u64.  Strict butterflies: values stay in [0, q)
+// (2q < 2^32, but 4q may not be).  Twiddle table entries are (w, floor(w 2^32 / q));
+// entry 0 of the inverse table holds (N^{-1}, its companion).
+__device__ __forceinline__ u32 spad32(u32 i) { return i + (i >> 5); }
+
+__device__ __forceinline__ u32 shoup32(u32 x, u32 w, u32 wsh, u32 q) {
+  u32 r = x * w - __umulhi(x, wsh) * q;   // [0, 2q)
+  return r >= q ? r - q : r;
+}
+__device__ __forceinline__ void ct_bfly32(u32& x, u32& y, u32 w, u32 wsh, u32 q) {
+  const u32 T = shoup32(y, w, wsh, q);
+  u32 u = x + T;
+  u = u >= q ? u - q : u;
+  u32 v = x - T + q;
+  v = v >= q ? v - q : v;
+  x = u;
+  y = v;
+}
+__device__ __forceinline__ void gs_bfly32(u32& x, u32& y, u32 w, u32 wsh, u32 q) {
+  u32 u = x + y;
+  u = u >= q ? u - q : u;
+  const u32 v = x - y + q;   // (0, 2q)
+  x = u;
+  y = shoup32(v, w, wsh, q);
+}
+
+template <int LOGN, bool INV, int LO, int NB>
+__device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __restrict__ tw, u32 q) {
+  typedef NttGeom<LOGN, 1> G;
+  constexpr int NG = 1 << (G::R - NB);
+  constexpr int E = 1 << NB;
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    const u32 g = tid + gi * G::T;
+    const u32 base = ((g >> LO) << (LO + NB)) | (g & ((1u << LO) - 1u));
+    u32 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = sm[spad32(base + (k << LO))];
+#pragma unroll
+    for (int ss = 0; ss < NB; ++ss) {
+      const int b = INV ? LO + ss : LO + NB - 1 - ss;
+      const int s = LOGN - 1 - b;
+      const int half = INV ? 1 << ss : 1 << (NB - 1 - ss);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & half) continue;
+        const u32 j = base + (k << LO);
+        const uint2 w = __ldg(tw + (1u << s) + (j >> (LOGN - s)));
+        if (!INV) ct_bfly32(x[k], x[k + half], w.x, w.y, q);
+        else gs_bfly32(x[k], x[k + half], w.x, w.y, q);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) sm[spad32(base + (k << LO))] = x[k];
+  }
+}
+
+template <int LOGN, bool INV, int P>
+__device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, u32 q) {
+  typedef NttGeom<LOGN, 1> G;
+  constexpr int GP = INV ? P : G::NPASS - 1 - P;
+  constexpr int LO = GP * G::R;
+  constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+  ntt_pass32<LOGN, INV, LO, NB>(sm, tid, tw, q);
+  __syncthreads();
+  if constexpr (P + 1 < G::NPASS) ntt_passes32<LOGN, INV, P + 1>(sm, tid, tw, q);
+}
+
+template <int LOGN>
+struct NttGeom32 {
+  static constexpr int SMEM = ((1 << LOGN) + (1 << LOGN) / 32) * 4;
+  static constexpr int MINB = (1 << LOGN) <= 8192 ? 3 : 2;
+};
+
+template <int LOGN, bool INV, class Job>
+__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T, NttGeom32<LOGN>::MINB)
+k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all) {
+  typedef NttGeom<LOGN, 1> G;
+  extern __shared__ u32 sm32[];
+  const u32 tid = threadIdx.x;
+  const int blk = blockIdx.x;
+  const int pi = job.prime(blk);
+  const PrimeD P = load_prime(primes, pi);
+  const uint2* tw = tw_all + (size_t)pi * G::N;
+  const u32 q = (u32)P.q;
+  for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)job.load(blk, i, P);
+  __syncthreads();
+  ntt_passes32<LOGN, INV, 0>(sm32, tid, tw, q);
+  const uint2 ni = __ldg(tw);
+  for (u32 i = tid; i < G::NL; i += G::T) {
+    u32 v = sm32[spad32(i)];
+    if (INV) v = shoup32(v, ni.x, ni.y, q);
+    job.store(blk, i, (u64)v, P);
+  }
+}
+
 }  // namespace he

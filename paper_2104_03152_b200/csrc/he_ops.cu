@@ -71,6 +71,20 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
   c->d_primes = upload(c, pd);
   c->small_primes = true;
   for (u64 q : hp.q) c->small_primes = c->small_primes && q < (1ULL << 31);
+  if (c->small_primes) {
+    std::vector<uint2> t32(hp.tw.size()), i32(hp.tw.size());
+    for (size_t k = 0; k < hp.tw.size(); ++k) {
+      const u64 q = hp.q[k / hp.N];
+      t32[k] = make_uint2((u32)hp.tw[k], (u32)(((u64)hp.tw[k] << 32) / q));
+      i32[k] = make_uint2((u32)hp.itw[k], (u32)(((u64)hp.itw[k] << 32) / q));
+    }
+    for (int t = 0; t < c->NP; ++t) {   // entry 0 of the inverse table: N^{-1} and its companion
+      const u64 q = hp.q[t], ni = hp.ninv[t];
+      i32[(size_t)t * hp.N] = make_uint2((u32)ni, (u32)((ni << 32) / q));
+    }
+    c->d_tw32 = upload(c, t32);
+    c->d_itw32 = upload(c, i32);
+  }
   {
     std::vector<ulonglong2> t2(hp.tw.size()), i2(hp.tw.size());
     for (size_t k = 0; k < hp.tw.size(); ++k) {

@@ -39,10 +39,13 @@ def _from_dev(t):
     return t.cpu().numpy().view(np.uint64)
 
 
-@pytest.mark.parametrize("logN,L,B", [(10, 3, 5), (13, 4, 3), (14, 8, 2), (15, 4, 2)])
-def test_ntt_forward_inverse_bit_exact(torch_cuda, logN, L, B):
+@pytest.mark.parametrize("logN,L,B,small", [(10, 3, 5, False), (13, 4, 3, False), (14, 8, 2, False),
+                                            (15, 4, 2, False), (10, 3, 3, True), (13, 4, 3, True),
+                                            (14, 3, 2, True)])
+def test_ntt_forward_inverse_bit_exact(torch_cuda, logN, L, B, small):
+    """small: every prime < 2^31 -> the 32-bit arithmetic engine (k_ntt32) runs."""
     torch = torch_cuda
-    bits = CFG2_PRIME_BITS(L)
+    bits = (31, 26, 30, 20, 28, 31)[:L] if small else CFG2_PRIME_BITS(L)
     o = OracleContext(logN, bits, 0, 1)
     g = gpu_ctx(logN, bits, 0, 1)
     N = 1 << logN
