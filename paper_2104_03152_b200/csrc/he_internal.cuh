@@ -57,6 +57,7 @@ struct he_context {
   he::u64* d_pk = nullptr;   // [2][L][N]
   he::u64* d_rlk = nullptr;  // [L][2][NP][N]
   std::map<he::u64, he::u64*> gk;  // Galois element -> [L][2][NP][N]
+  std::map<he::u64, uint32_t*> gk32;  // small primes: the same keys as u32 in Montgomery form (k 2^32 mod q)
   std::vector<void*> owned;        // device allocations freed with the context
   // opt-in profiler: CUDA events around every NTT-family launch
   struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; };
@@ -78,6 +79,7 @@ struct he_plaintext {
   double scale;
   he::u64* d;  // [B][level+1 (+K if qp)][N]
   int qp = 0;  // 1: also carries the K special limbs (data limbs first), for lazy-ModDown products
+  uint32_t* dm = nullptr;  // small primes: cached Montgomery-form u32 copy (lazy vec_mat)
 };
 
 namespace he {

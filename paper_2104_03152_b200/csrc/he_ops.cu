@@ -113,6 +113,7 @@ void context_destroy(he_context* c) {
   cudaStreamSynchronize(c->stream);
   for (void* p : c->owned) cudaFree(p);
   for (auto& kv : c->gk) cudaFree(kv.second);
+  for (auto& kv : c->gk32) cudaFree(kv.second);
   if (c->d_sk) cudaFree(c->d_sk);
   if (c->d_pk) cudaFree(c->d_pk);
   if (c->d_rlk) cudaFree(c->d_rlk);
@@ -146,6 +147,7 @@ void ct_free(he_ciphertext* ct) {
 }
 void pt_free(he_plaintext* pt) {
   if (!pt) return;
+  dfree(pt->ctx, pt->dm);
   dfree(pt->ctx, pt->d);
   delete pt;
 }
@@ -314,6 +316,11 @@ __global__ void k_ksk_combine(u64* __restrict__ key, const u64* __restrict__ e_n
   }
 }
 
+__global__ void k_narrow(const u64* __restrict__ src, u32* __restrict__ dst, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = (u32)src[i];
+}
+
 // Sum over kk of tmp[kk][item] into acc (vec_mat rotation chunks).
 __global__ void k_accumulate(u64* __restrict__ acc, const u64* __restrict__ tmp, int KB, size_t chunk_words,
                              const PrimeD* __restrict__ primes, int N, int Lc, size_t rows) {
@@ -465,6 +472,118 @@ __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* _
     }
     a.accx[(((size_t)b * 2 + 0) * nt + t) * N + nn[e]] = acc0[e];
     a.accx[(((size_t)b * 2 + 1) * nt + t) * N + nn[e]] = acc1[e];
+  }
+}
+
+// Small-prime lazy accumulator (all primes < 2^31): the item's digits for
+// target t are staged in shared memory as u32 (the automorphism gathers hit
+// smem), keys and diagonals are read as u32 copies in Montgomery form
+// (k' = k 2^32 mod q), and every product is reduced with one 32-bit
+// Montgomery REDC per PAIR of products (x0 k0' + x1 k1' < q 2^32).  Results
+// are the exact residues, bit-identical to the generic path.  One CTA per
+// (target limb t, item b).
+constexpr int LAZY_SM_T = 1024, LAZY_SM_EPT = 2;
+
+__device__ __forceinline__ u32 redc32(u64 T, u32 q, u32 qneg_inv) {
+  const u32 m = (u32)T * qneg_inv;
+  const u32 t = (u32)((T + (u64)m * q) >> 32);
+  return t >= q ? t - q : t;
+}
+__device__ __forceinline__ u32 mont_neg_inv(u32 q) {  // -q^{-1} mod 2^32 (q odd)
+  u32 inv = q;
+  for (int i = 0; i < 5; ++i) inv *= 2u - q * inv;
+  return 0u - inv;
+}
+__device__ __forceinline__ u32 addq(u32 a, u32 b, u32 q) {
+  const u32 s = a + b;
+  return s >= q ? s - q : s;
+}
+
+template <int LC>
+__global__ void __launch_bounds__(LAZY_SM_T, 1)
+k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
+                   const PrimeD* __restrict__ primes) {
+  extern __shared__ u32 xs[];
+  const int t = blockIdx.x, b = blockIdx.y, nt = LC + a.K;
+  const int tp = t < LC ? t : a.L + (t - LC);
+  const PrimeD P = load_prime(primes, tp);
+  const u32 q = (u32)P.q, qi = mont_neg_inv(q);
+  const u32 N = a.N, NP = a.NP;
+  const u64* c0 = a.ct + (size_t)b * 2 * LC * N;
+  const u64* c1 = c0 + (size_t)LC * N;
+  const bool data = t < LC;
+#pragma unroll
+  for (int j = 0; j < LC; ++j) {
+    const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
+    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
+  }
+  u32* c0s = xs + LC * N;
+  if (data)
+    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) c0s[i] = (u32)c0[(size_t)t * N + i];
+  __syncthreads();
+  // P' = [P]_q 2^32 mod q (Montgomery form)
+  const u32 Pm = (u32)((((u64)__ldg(a.P_mod + tp)) << 32) % q);
+  const u32 keyrow = tp * N, kpart = NP * N, kdig = 2 * NP * N;
+  for (u32 tile = 0; tile < N; tile += LAZY_SM_T * LAZY_SM_EPT) {
+    u32 nn[LAZY_SM_EPT], acc0[LAZY_SM_EPT], acc1[LAZY_SM_EPT], cc0[LAZY_SM_EPT], cc1[LAZY_SM_EPT];
+#pragma unroll
+    for (int e = 0; e < LAZY_SM_EPT; ++e) {
+      nn[e] = tile + e * LAZY_SM_T + threadIdx.x;
+      acc0[e] = acc1[e] = cc0[e] = cc1[e] = 0;
+      if (data) {
+        const u32 d0 = __ldg(dm + t * N + nn[e]);
+        cc0[e] = redc32((u64)d0 * c0s[nn[e]], q, qi);
+        cc1[e] = redc32((u64)d0 * xs[t * N + nn[e]], q, qi);   // the t == j digit is c1[t]
+      }
+    }
+    for (int k = 1; k < a.n; ++k) {
+      const u32 g = __ldg(a.gal + k);
+      const u32* key = keys32[k] + keyrow;
+      const u32* Dk = dm + ((u32)k * nt + t) * N;
+#pragma unroll
+      for (int e = 0; e < LAZY_SM_EPT; ++e) {
+        const u32 n = nn[e], sn = galois_src(n, g, a.logN);
+        u32 ip0 = 0, ip1 = 0;
+#pragma unroll
+        for (int j = 0; j < LC; j += 2) {
+          const u32 x0 = xs[j * N + sn];
+          u64 s0 = (u64)x0 * __ldg(key + j * kdig + n);
+          u64 s1 = (u64)x0 * __ldg(key + j * kdig + kpart + n);
+          if (j + 1 < LC) {
+            const u32 x1 = xs[(j + 1) * N + sn];
+            s0 += (u64)x1 * __ldg(key + (j + 1) * kdig + n);
+            s1 += (u64)x1 * __ldg(key + (j + 1) * kdig + kpart + n);
+          }
+          ip0 = addq(ip0, redc32(s0, q, qi), q);
+          ip1 = addq(ip1, redc32(s1, q, qi), q);
+        }
+        const u32 d = __ldg(Dk + n);
+        acc0[e] = addq(acc0[e], redc32((u64)d * ip0, q, qi), q);
+        acc1[e] = addq(acc1[e], redc32((u64)d * ip1, q, qi), q);
+        if (data) cc0[e] = addq(cc0[e], redc32((u64)d * c0s[sn], q, qi), q);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < LAZY_SM_EPT; ++e) {
+      if (data) {
+        acc0[e] = addq(acc0[e], redc32((u64)Pm * cc0[e], q, qi), q);
+        acc1[e] = addq(acc1[e], redc32((u64)Pm * cc1[e], q, qi), q);
+      }
+      a.accx[(((size_t)b * 2 + 0) * nt + t) * N + nn[e]] = acc0[e];
+      a.accx[(((size_t)b * 2 + 1) * nt + t) * N + nn[e]] = acc1[e];
+    }
+  }
+}
+
+// Montgomery-form u32 copy of residues: out[i] = in[i] 2^32 mod q_{prime(i)}.
+// rows of N words; row r is limb r % nl with limbs >= lc special (prime L + l - lc).
+__global__ void k_to_mont32(const u64* __restrict__ in, u32* __restrict__ out, const PrimeD* __restrict__ primes,
+                            int N, int nl, int lc, int L, size_t rows) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int l = (int)(r % nl);
+    const u64 q = load_prime(primes, l < lc ? l : L + (l - lc)).q;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+      out[r * N + n] = (u32)((in[r * N + n] << 32) % q);
   }
 }
 
@@ -872,8 +991,19 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
                                       const std::vector<const u64*>& keys, const std::vector<u32>& gals) {
   const int Lc = x->level + 1, n = diags->B, B = x->B, nt = Lc + c->K;
   const size_t LN = (size_t)Lc * c->N, N = c->N;
-  Scratch kt(c, n * sizeof(u64*)), gt(c, n * sizeof(u32));
+  Scratch kt(c, n * sizeof(u64*)), gt(c, n * sizeof(u32)), k32t(c, n * sizeof(u32*));
   HE_CK(cudaMemcpyAsync(kt.p, keys.data(), n * sizeof(u64*), cudaMemcpyHostToDevice, c->stream));
+  std::vector<const u32*> keys32;
+  if (c->small_primes) {
+    keys32.push_back(nullptr);
+    for (int k = 1; k < n; ++k) {
+      auto it = c->gk32.find(gals[k]);
+      if (it == c->gk32.end()) break;
+      keys32.push_back(it->second);
+    }
+    if (keys32.size() == (size_t)n)
+      HE_CK(cudaMemcpyAsync(k32t.p, keys32.data(), n * sizeof(u32*), cudaMemcpyHostToDevice, c->stream));
+  }
   HE_CK(cudaMemcpyAsync(gt.p, gals.data(), n * sizeof(u32), cudaMemcpyHostToDevice, c->stream));
   u64* ext = n > 1 ? modup(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
   he_ciphertext* acc = nullptr;
@@ -886,9 +1016,36 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
       const double bytes = 8.0 * N * ((double)B * Lc * nt + (double)B * 2 * Lc + (double)B * 2 * nt +
                                       (double)(n - 1) * 2 * Lc * nt + (double)n * nt);
       ProfScope ps_(c, "vecmat_lazy", bytes, B * nt);
-      const dim3 grid((unsigned)(N / (256 * LAZY_EPT)), nt, B);
-      if (c->small_primes) k_vecmat_lazy<true><<<grid, 256, 0, c->stream>>>(la, c->d_primes);
-      else k_vecmat_lazy<false><<<grid, 256, 0, c->stream>>>(la, c->d_primes);
+      const size_t smem = ((size_t)Lc + 1) * N * 4;
+      if (c->small_primes && smem <= 200 * 1024 && Lc <= 8 && keys32.size() == (size_t)n &&
+          N % (LAZY_SM_T * LAZY_SM_EPT) == 0) {
+        if (!diags->dm) {   // Montgomery u32 copy of the diagonals, cached on the plaintext
+          const size_t rows = (size_t)n * nt;
+          u32* dmp = dalloc_t<u32>(c, rows * N);
+          k_to_mont32<<<dim3((unsigned)((N + 255) / 256), (unsigned)std::min<size_t>(rows, 65535)), 256, 0,
+                        c->stream>>>(diags->d, dmp, c->d_primes, (int)N, nt, Lc, c->L, rows);
+          check_launch(c);
+          const_cast<he_plaintext*>(diags)->dm = dmp;
+        }
+        auto launch = [&](auto kern) {
+          HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, k32t.as<const u32*>(), diags->dm, c->d_primes);
+        };
+        switch (Lc) {
+          case 1: launch(k_vecmat_lazy_mont<1>); break;
+          case 2: launch(k_vecmat_lazy_mont<2>); break;
+          case 3: launch(k_vecmat_lazy_mont<3>); break;
+          case 4: launch(k_vecmat_lazy_mont<4>); break;
+          case 5: launch(k_vecmat_lazy_mont<5>); break;
+          case 6: launch(k_vecmat_lazy_mont<6>); break;
+          case 7: launch(k_vecmat_lazy_mont<7>); break;
+          default: launch(k_vecmat_lazy_mont<8>); break;
+        }
+      } else {
+        const dim3 grid((unsigned)(N / (256 * LAZY_EPT)), nt, B);
+        if (c->small_primes) k_vecmat_lazy<true><<<grid, 256, 0, c->stream>>>(la, c->d_primes);
+        else k_vecmat_lazy<false><<<grid, 256, 0, c->stream>>>(la, c->d_primes);
+      }
     }
     check_launch(c);
     acc = ct_new(c, B, 2, x->level, x->scale * diags->scale);
@@ -1123,6 +1280,15 @@ void keygen(he_context* c, const std::vector<int>& steps) {
       HE_CK(cudaMalloc(&key, kw * 8));
       c->gk[g] = key;
       make_ksk(c, key, PUR_GK_A, PUR_GK_E, g << 8, (u32)g);
+      if (c->small_primes) {
+        u32* k32 = nullptr;
+        HE_CK(cudaMalloc(&k32, kw * 4));
+        c->gk32[g] = k32;
+        const size_t rows = (size_t)L * 2 * NP;
+        k_to_mont32<<<dim3((N + 255) / 256, (unsigned)std::min<size_t>(rows, 65535)), 256, 0, c->stream>>>(
+            key, k32, c->d_primes, N, NP, NP, L, rows);
+        check_launch(c);
+      }
     }
   }
   HE_CK(cudaStreamSynchronize(c->stream));
