@@ -56,6 +56,7 @@ struct he_context {
   he::u64* d_sk = nullptr;   // [NP][N]
   he::u64* d_pk = nullptr;   // [2][L][N]
   he::u64* d_rlk = nullptr;  // [L][2][NP][N]
+  uint32_t* d_rlk32 = nullptr;  // small primes: Montgomery-form u32 copy
   std::map<he::u64, he::u64*> gk;  // Galois element -> [L][2][NP][N]
   std::map<he::u64, uint32_t*> gk32;  // small primes: the same keys as u32 in Montgomery form (k 2^32 mod q)
   std::vector<void*> owned;        // device allocations freed with the context

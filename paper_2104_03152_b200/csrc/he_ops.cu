@@ -117,6 +117,7 @@ void context_destroy(he_context* c) {
   if (c->d_sk) cudaFree(c->d_sk);
   if (c->d_pk) cudaFree(c->d_pk);
   if (c->d_rlk) cudaFree(c->d_rlk);
+  if (c->d_rlk32) cudaFree(c->d_rlk32);
 }
 
 // ============================================================== handles ===
@@ -575,6 +576,64 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
   }
 }
 
+// Fused ModUp + key inner product for small primes (a9 without materialising
+// the extended digits): CTA (target limb t, item b) loops over the digits j:
+// lift [d]_{q_j} (coefficients) into q_t (C16), 32-bit NTT in smem, then
+// accx_p[t][n] += X_j[pi_g(n)] ksk[j][p][t][n] with the Montgomery-form key.
+// For j == t the digit is the NTT word itself (dsrc).  Output feeds the
+// accx-mode ModDown jobs.
+struct FusedArgs {
+  int N, logN, Lc, K, L, NP;
+  u32 gal;
+  const u64* coef;     // [B][Lc][N] INTT'd digits
+  const u64* dsrc;     // digit source NTT words, item stride dsrc_bs
+  size_t dsrc_bs;
+  const u32* key32;    // [L][2][NP][N] Montgomery form
+  const u64* qtab;
+  u64* accx;           // [B][2][Lc+K][N]
+};
+template <int LOGN>
+__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T, (1 << LOGN) <= 8192 ? 2 : 1)
+k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all) {
+  typedef NttGeom<LOGN, 1> G;
+  extern __shared__ u32 sm32[];
+  u32* buf = sm32;                                  // NTT workspace (padded)
+  u32* acc = sm32 + G::N + G::N / 32;               // [2][N]
+  const int t = blockIdx.x, b = blockIdx.y, nt = a.Lc + a.K;
+  const int tp = t < a.Lc ? t : a.L + (t - a.Lc);
+  const PrimeD P = load_prime(primes, tp);
+  const u32 q = (u32)P.q, qi = mont_neg_inv(q);
+  const uint2* tw = tw_all + (size_t)tp * G::N;
+  const u32 tid = threadIdx.x;
+  for (u32 i = tid; i < 2 * G::N; i += G::T) acc[i] = 0;
+  const u32* key = a.key32 + (size_t)tp * G::N;
+  const u32 kpart = (u32)a.NP * G::N, kdig = 2 * kpart;
+  for (int j = 0; j < a.Lc; ++j) {
+    if (j == t) {
+      const u64* src = a.dsrc + (size_t)b * a.dsrc_bs + (size_t)j * G::N;
+      for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)src[i];
+    } else {
+      const u64* src = a.coef + ((size_t)b * a.Lc + j) * G::N;
+      const u64 qj = __ldg(a.qtab + j);
+      for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)lift_centered(src[i], qj, P);
+      __syncthreads();
+      ntt_passes32<LOGN, false, 0>(buf, tid, tw, q);
+    }
+    __syncthreads();
+    for (u32 n = tid; n < G::N; n += G::T) {
+      const u32 sn = a.gal == 1 ? n : galois_src(n, a.gal, LOGN);
+      const u32 x = buf[spad32(sn)];
+      acc[n] = addq(acc[n], redc32((u64)x * __ldg(key + j * kdig + n), q, qi), q);
+      acc[G::N + n] = addq(acc[G::N + n], redc32((u64)x * __ldg(key + j * kdig + kpart + n), q, qi), q);
+    }
+    __syncthreads();
+  }
+  for (u32 n = tid; n < G::N; n += G::T) {
+    a.accx[(((size_t)b * 2 + 0) * nt + t) * G::N + n] = acc[n];
+    a.accx[(((size_t)b * 2 + 1) * nt + t) * G::N + n] = acc[G::N + n];
+  }
+}
+
 // Montgomery-form u32 copy of residues: out[i] = in[i] 2^32 mod q_{prime(i)}.
 // rows of N words; row r is limb r % nl with limbs >= lc special (prime L + l - lc).
 __global__ void k_to_mont32(const u64* __restrict__ in, u32* __restrict__ out, const PrimeD* __restrict__ primes,
@@ -924,6 +983,39 @@ static void ks_launch(he_context* c, KsArgs& a) {
   launch_ntt<false>(c, jd, a.KB * a.B * 2 * a.Lc);
 }
 
+// Fused small-prime key switch: INTT of the digit source, k_modup_ip32 (ModUp
+// and inner product without the extended digits in HBM), then the accx-mode
+// ModDown with the caller's epilogue (epi.out, addsrc, acc_in ...).
+static bool fused_ks_ok(he_context* c) { return c->small_primes && c->d_tw32 && c->logN <= 14; }
+
+static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, const u32* key32, u32 g,
+                     KsArgs& epi) {
+  const size_t N = c->N;
+  const int nt = Lc + c->K;
+  Scratch coef(c, (size_t)B * Lc * N * 8), accx(c, (size_t)B * 2 * nt * N * 8);
+  ntt_rows(c, dsrc, coef.as<u64>(), B, Lc, bs, (size_t)Lc * N, true);
+  FusedArgs fa{c->N, c->logN, Lc, c->K, c->L, c->NP, g, coef.as<u64>(), dsrc, bs, key32, c->d_q, accx.as<u64>()};
+  auto launch = [&](auto kern, int T) {
+    const int smem = (int)((N + N / 32 + 2 * N) * 4);
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // algorithmic bytes: digits read once per item, key rows once per launch, accumulators written once
+    const double bytes = 8.0 * N * ((double)B * Lc + (double)B * 2 * nt) + 4.0 * N * 2 * Lc * nt;
+    ProfScope ps_(c, "ks_modup_ip", bytes, B * nt);
+    kern<<<dim3(nt, B), T, smem, c->stream>>>(fa, c->d_primes, c->d_tw32);
+  };
+  switch (c->logN) {
+    case 10: launch(k_modup_ip32<10>, NttGeom<10, 1>::T); break;
+    case 11: launch(k_modup_ip32<11>, NttGeom<11, 1>::T); break;
+    case 12: launch(k_modup_ip32<12>, NttGeom<12, 1>::T); break;
+    case 13: launch(k_modup_ip32<13>, NttGeom<13, 1>::T); break;
+    default: launch(k_modup_ip32<14>, NttGeom<14, 1>::T); break;
+  }
+  check_launch(c);
+  epi.accx = accx.as<u64>();
+  epi.gal[0] = g;
+  ks_launch(c, epi);
+}
+
 const u64* galois_key(he_context* c, int step, u32* gal_out) {
   const u64 g = galois_element(c->N, step);
   auto it = c->gk.find(g);
@@ -936,6 +1028,21 @@ he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a) {
   const int Lc = a->level + 1;
   const size_t LN = (size_t)Lc * c->N;
   he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
+  if (fused_ks_ok(c) && c->d_rlk32) {
+    KsArgs k = ks_base(c, a->B, Lc, nullptr, nullptr, 0);
+    k.out = o->d;
+    k.out_bs = 2 * LN;
+    k.addsrc = a->d;
+    k.add_bs = 3 * LN;
+    k.add_parts = 2;
+    try {
+      ks_fused(c, a->d + 2 * LN, 3 * LN, a->B, Lc, c->d_rlk32, 1, k);
+    } catch (...) {
+      ct_free(o);
+      throw;
+    }
+    return o;
+  }
   u64* ext = modup(c, a->d + 2 * LN, 3 * LN, a->B, Lc);
   KsArgs k = ks_base(c, a->B, Lc, ext, a->d + 2 * LN, 3 * LN);
   k.keys[0] = c->d_rlk;
@@ -963,6 +1070,24 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
   const u64* key = galois_key(c, step, &g);
   if (!key) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
   he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
+  auto it32 = c->gk32.find(g);
+  if (fused_ks_ok(c) && it32 != c->gk32.end()) {
+    KsArgs k = ks_base(c, a->B, Lc, nullptr, nullptr, 0);
+    k.out = o->d;
+    k.out_bs = 2 * LN;
+    k.addsrc = a->d;
+    k.add_bs = 2 * LN;
+    k.add_parts = 1;
+    k.add_gather = 1;
+    if (add_input) k.acc_in = a->d;
+    try {
+      ks_fused(c, a->d + LN, 2 * LN, a->B, Lc, it32->second, g, k);
+    } catch (...) {
+      ct_free(o);
+      throw;
+    }
+    return o;
+  }
   u64* ext = modup(c, a->d + LN, 2 * LN, a->B, Lc);
   KsArgs k = ks_base(c, a->B, Lc, ext, a->d + LN, 2 * LN);
   k.keys[0] = key;
@@ -1273,6 +1398,13 @@ void keygen(he_context* c, const std::vector<int>& steps) {
     HE_CK(cudaMalloc(&c->d_rlk, kw * 8));
     make_ksk(c, c->d_rlk, PUR_RLK_A, PUR_RLK_E, 0, 0);
     c->has_rlk = true;
+    if (c->small_primes) {
+      HE_CK(cudaMalloc(&c->d_rlk32, kw * 4));
+      const size_t rows = (size_t)L * 2 * NP;
+      k_to_mont32<<<dim3((N + 255) / 256, (unsigned)std::min<size_t>(rows, 65535)), 256, 0, c->stream>>>(
+          c->d_rlk, c->d_rlk32, c->d_primes, N, NP, NP, L, rows);
+      check_launch(c);
+    }
     for (int st : steps) {
       const u64 g = galois_element(N, st);
       if (c->gk.count(g)) continue;
