@@ -303,3 +303,69 @@ def test_vec_mat_lazy_bit_exact(cfg1):
         assert np.array_equal(W2[b], ref.words), b
     y = g.he_decode(g.he_decrypt(out), 10)
     assert np.max(np.abs(y - x @ W)) < 1e-6
+
+
+# ------------------------------------------- small-prime (32-bit) engine ---
+SMALL = dict(logN=11, bits=(31, 26, 26, 26, 31), K=1, seed=13)
+
+
+@pytest.fixture(scope="module")
+def small():
+    from paper_2104_03152_b200 import Context
+    steps = [1, 5, -3, 1024]
+    o = OracleContext(SMALL["logN"], SMALL["bits"], SMALL["K"], SMALL["seed"])
+    o.keygen(steps)
+    g = Context(SMALL["logN"], SMALL["bits"], SMALL["K"], SMALL["seed"])
+    g.he_keygen(steps)
+    return o, g, steps
+
+
+def test_small_prime_keyswitch_paths_bit_exact(small):
+    """All primes < 2^31: rotate / rotate-and-add (fused ModUp + Montgomery inner product),
+    relinearize, square and rescale through the 32-bit engine, at every level, word for word."""
+    o, g, steps = small
+    assert np.array_equal(g.he_key_export(2), o.relin_key())
+    for lvl in range(o.L):
+        x = rand_ct(o, lvl, 3, 40 + lvl)
+        gx = g.he_ct_import_words(x, lvl, 1.0)
+        for st in steps:
+            w = g.he_rotate(gx, st).words()
+            for b in range(3):
+                assert np.array_equal(w[b], o.rotate(OCt(x[b], lvl, 1.0), st).words), (lvl, st, b)
+        x3 = rand_ct(o, lvl, 2, 60 + lvl, size=3)
+        w = g.he_relinearize(g.he_ct_import_words(x3, lvl, 1.0, size=3)).words()
+        for b in range(2):
+            assert np.array_equal(w[b], o.relinearize(OCt(x3[b], lvl, 1.0)).words), (lvl, b)
+        if lvl >= 1:
+            w = g.he_rescale(gx).words()
+            for b in range(3):
+                assert np.array_equal(w[b], o.rescale(OCt(x[b], lvl, 1.0)).words), (lvl, b)
+    z = messages(2, o.slots, seed=3)
+    lvl = o.L - 1
+    cts = [oracle_ct(o, z[b], 2.0 ** 26, lvl, b) for b in range(2)]
+    gsq = g.he_square(g.he_ct_import_words(np.stack([c.words for c in cts]), lvl, 2.0 ** 26))
+    for b in range(2):
+        assert np.array_equal(gsq.words()[b], o.square(cts[b]).words)
+
+
+def test_small_prime_vec_mat_both_forms_bit_exact(small):
+    o, g, _ = small
+    from paper_2104_03152_b200 import Context
+    n = 8
+    o2 = OracleContext(SMALL["logN"], SMALL["bits"], SMALL["K"], 21)
+    o2.keygen(range(1, n))
+    g2 = Context(SMALL["logN"], SMALL["bits"], SMALL["K"], 21)
+    g2.he_keygen(range(1, n))
+    rng = np.random.default_rng(9)
+    W = rng.normal(0, 0.1, (n, n))
+    lvl = o2.L - 1
+    octs = [oracle_ct(o2, OC.replicate(rng.uniform(-1, 1, n), o2.slots), 2.0 ** 26, lvl, b) for b in range(3)]
+    gct = g2.he_ct_import_words(np.stack([c.words for c in octs]), lvl, 2.0 ** 26)
+    D = OC.vecmat_diagonals(W, o2.slots, True)
+    ps = float(o2.q[lvl])
+    ms = np.stack([o2.encode_coeffs(d, ps)[1] for d in D])
+    plain = g2.he_vec_mat_pt(gct, g2.he_pt_from_int_coeffs(ms, ps, lvl)).words()
+    lazy = g2.he_vec_mat_pt(gct, g2.he_pt_from_int_coeffs_qp(ms, ps, lvl)).words()
+    for b in range(3):
+        assert np.array_equal(plain[b], OC.vec_mat(o2, octs[b], W, None, True).words), b
+        assert np.array_equal(lazy[b], OC.vec_mat_lazy(o2, octs[b], W, None, True).words), b
