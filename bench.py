@@ -35,7 +35,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "encrypted 28x28 CNN inferences/s/box"
+# ALU roofline of the integer kernels: a 32-bit Shoup/Montgomery modular
+# butterfly needs >= 3 FMA-pipe (IMAD.HI, IMAD, IMAD) and >= 5 ALU-pipe (2 IADD3, 3 min-based
+# conditional subtractions) instructions; the ALU pipe (64 lanes/clk/SM) binds first:
+# 64 / 5 = 12.8 modular ops/clk/SM x 148 SMs x 1.965 GHz (max SM clock, held under this load).
+ALU_PEAK_GOPS = 12.8 * 148 * 1.965
 UNIT = "images/s"
+
+
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from one `ncu --set full` capture of the
+# bench command (profiles/r01_ncu_summary.md), batch 256
+TRAFFIC = {}
+try:
+    TRAFFIC = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+except Exception:
+    pass
 
 
 def load_peaks():
@@ -160,16 +174,21 @@ def run_ours(args, rank, world, local_rank):
     prof = ctx.he_profile_read()
     ctx.he_profile_enable(False)
     tot = sum(v[1] for v in prof.values())
+    prof = {k: (v + [0.0] * 5)[:5] for k, v in prof.items()}
     top = max(prof, key=lambda k: prof[k][1])
-    n_l, t_ms, alg_b, _ = prof[top]
+    n_l, t_ms, alg_b, _, alg_ops = prof[top]
     peaks = load_peaks()
-    achieved = (alg_b / n_l) / (t_ms / n_l / 1e3) / 1e9 if t_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
-                "share_of_step": round(t_ms / 2 / prof_step_ms, 3),
-                "alg_bytes_per_launch": alg_b / n_l, "us_per_launch": round(t_ms / n_l * 1e3, 2),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
-                if not peaks.get("_fallback") else "fallback 6650 GB/s"}
+    sec = t_ms / n_l / 1e3
+    gbs = (alg_b / n_l) / sec / 1e9 if t_ms > 0 else 0.0
+    gops = (alg_ops / n_l) / sec / 1e9 if t_ms > 0 else 0.0
+    roofline = {"bound": "alu", "kernel": top, "achieved": round(gops, 1), "peak": round(ALU_PEAK_GOPS, 1),
+                "unit": "Gmodop/s", "frac": round(gops / ALU_PEAK_GOPS, 4), "traffic": TRAFFIC.get(top),
+                "alg_ops_per_launch": alg_ops / n_l, "alg_bytes_per_launch": alg_b / n_l,
+                "hbm_achieved_GBps": round(gbs, 1), "hbm_peak_GBps": peaks["hbm_gbs"],
+                "hbm_frac": round(gbs / peaks["hbm_gbs"], 4),
+                "share_of_step": round(t_ms / 2 / prof_step_ms, 3), "us_per_launch": round(sec * 1e6, 2),
+                "peak_source": "ALU: derived (DESIGN.md §5: 12.8 modular ops/clk/SM x 148 x 1.965 GHz); HBM: "
+                               + ("MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback")}
     breakdown = {k: {"launches_per_step": v[0] / 2, "ms_per_step": round(v[1] / 2, 3),
                      "share": round(v[1] / tot, 3)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
 

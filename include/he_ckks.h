@@ -283,8 +283,9 @@ he_status he_ntt_mul_intt(he_context* ctx, const uint64_t* a, const uint64_t* b,
  * by CUDA events recorded on the context stream.  he_profile_read
  * synchronises the stream and writes a JSON object into buf (NUL-terminated,
  * truncated to len):  {"<kernel tag>": [launches, total_ms, alg_bytes,
- * blocks], ...}  where alg_bytes are the algorithmic bytes of those launches
- * (0 where not modelled).  Reading resets the records. */
+ * blocks, alg_ops], ...}  where alg_bytes / alg_ops are the algorithmic bytes
+ * and modular operations (butterflies + multiply-accumulates) of those
+ * launches (0 where not modelled).  Reading resets the records. */
 he_status he_profile_enable(he_context* ctx, int on);
 he_status he_profile_read(he_context* ctx, char* buf, size_t len);
 

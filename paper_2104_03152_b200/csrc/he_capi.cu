@@ -176,7 +176,7 @@ he_status he_profile_read(he_context* c, char* buf, size_t len) {
     need_ctx(c);
     need(buf != nullptr && len > 0, HE_INVALID_ARGUMENT, "null buffer");
     HE_CK(cudaStreamSynchronize(c->stream));
-    struct Acc { long n = 0; double ms = 0, bytes = 0, blocks = 0; };
+    struct Acc { long n = 0; double ms = 0, bytes = 0, blocks = 0, ops = 0; };
     std::map<std::string, Acc> acc;
     for (auto& r : c->prof) {
       float ms = 0;
@@ -186,6 +186,7 @@ he_status he_profile_read(he_context* c, char* buf, size_t len) {
       a.ms += ms;
       a.bytes += r.bytes;
       a.blocks += r.blocks;
+      a.ops += r.ops;
       c->ev_pool.push_back(r.a);
       c->ev_pool.push_back(r.b);
     }
@@ -193,8 +194,8 @@ he_status he_profile_read(he_context* c, char* buf, size_t len) {
     std::string js = "{";
     for (auto& kv : acc) {
       char tmp[256];
-      snprintf(tmp, sizeof(tmp), "%s\"%s\": [%ld, %.6f, %.1f, %.0f]", js.size() > 1 ? ", " : "", kv.first.c_str(),
-               kv.second.n, kv.second.ms, kv.second.bytes, kv.second.blocks);
+      snprintf(tmp, sizeof(tmp), "%s\"%s\": [%ld, %.6f, %.1f, %.0f, %.1f]", js.size() > 1 ? ", " : "",
+               kv.first.c_str(), kv.second.n, kv.second.ms, kv.second.bytes, kv.second.blocks, kv.second.ops);
       js += tmp;
     }
     js += "}";

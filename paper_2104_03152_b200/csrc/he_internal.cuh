@@ -61,7 +61,7 @@ struct he_context {
   std::map<he::u64, uint32_t*> gk32;  // small primes: the same keys as u32 in Montgomery form (k 2^32 mod q)
   std::vector<void*> owned;        // device allocations freed with the context
   // opt-in profiler: CUDA events around every NTT-family launch
-  struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; };
+  struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; double ops; };
   bool prof_on = false;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
@@ -121,8 +121,8 @@ inline cudaEvent_t prof_event(he_context* c) {
 struct ProfScope {
   he_context* c;
   he_context::ProfRec rec;
-  ProfScope(he_context* c_, const char* tag, double bytes, int blocks) : c(c_) {
-    rec = he_context::ProfRec{tag, nullptr, nullptr, bytes, blocks};
+  ProfScope(he_context* c_, const char* tag, double bytes, int blocks, double ops = 0.0) : c(c_) {
+    rec = he_context::ProfRec{tag, nullptr, nullptr, bytes, blocks, ops};
     if (c->prof_on) {
       rec.a = prof_event(c);
       rec.b = prof_event(c);
@@ -151,7 +151,8 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
   }
   if (nblk <= 0) return;
   const ulonglong2* tw = INV ? c->d_itw2 : c->d_tw2;
-  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk);
+  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk,
+               c->prof_on ? alg_ops(job, nblk, LOGN) : 0.0);
   if (CL == 1) {
     kern<<<nblk, G::T, G::SMEM, c->stream>>>(job, c->d_primes, tw);
   } else {
@@ -183,7 +184,8 @@ void launch_ntt32_t(he_context* c, const Job& job, int nblk) {
     configured = true;
   }
   if (nblk <= 0) return;
-  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk);
+  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk,
+               c->prof_on ? alg_ops(job, nblk, LOGN) : 0.0);
   kern<<<nblk, G::T, NttGeom32<LOGN>::SMEM, c->stream>>>(job, c->d_primes, INV ? c->d_itw32 : c->d_tw32);
   check_launch(c);
 }

@@ -279,4 +279,19 @@ inline double alg_bytes(const JobRescaleData& j, int nblk) {
   return 8.0 * j.N * (2.0 * nblk + (double)nblk / (j.Lc - 1));
 }
 
+// Algorithmic modular operations of one launch (DESIGN.md §5 ALU roofline):
+// (N/2) log2 N butterflies per limb transform, plus one per modular
+// multiply-accumulate of the fused inner products / epilogues.
+inline double ntt_ops(int N, int logN) { return 0.5 * N * logN; }
+template <class Job>
+inline double alg_ops(const Job& j, int nblk, int logN) { return nblk * ntt_ops(j.N, logN); }
+inline double alg_ops(const JobKsSpecial& j, int nblk, int logN) {
+  const KsArgs& a = j.a;
+  return nblk * (ntt_ops(a.N, logN) + (a.accx ? 0.0 : (double)a.Lc * a.N) + a.N);
+}
+inline double alg_ops(const JobKsData& j, int nblk, int logN) {
+  const KsArgs& a = j.a;
+  return nblk * (ntt_ops(a.N, logN) + (a.accx ? 0.0 : (double)a.Lc * a.N) + (double)a.K * a.N + 2.0 * a.N);
+}
+
 }  // namespace he

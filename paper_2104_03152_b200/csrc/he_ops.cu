@@ -801,7 +801,7 @@ void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items,
     static_cast<void>(T);
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     {
-      ProfScope ps_(c, "ntt_mul_intt", alg_bytes(j, nblk), nblk);
+      ProfScope ps_(c, "ntt_mul_intt", alg_bytes(j, nblk), nblk, nblk * (2 * ntt_ops(c->N, c->logN) + c->N));
       kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw2, c->d_itw2);
     }
     check_launch(c);
@@ -1000,7 +1000,8 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     // algorithmic bytes: digits read once per item, key rows once per launch, accumulators written once
     const double bytes = 8.0 * N * ((double)B * Lc + (double)B * 2 * nt) + 4.0 * N * 2 * Lc * nt;
-    ProfScope ps_(c, "ks_modup_ip", bytes, B * nt);
+    const double ops = (double)B * (Lc * (nt - 1)) * ntt_ops((int)N, c->logN) + (double)B * nt * Lc * 2 * N;
+    ProfScope ps_(c, "ks_modup_ip", bytes, B * nt, ops);
     kern<<<dim3(nt, B), T, smem, c->stream>>>(fa, c->d_primes, c->d_tw32);
   };
   switch (c->logN) {
@@ -1140,7 +1141,9 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
       // algorithmic bytes: ext + ct + accumulators once per item, keys and diagonals once per launch
       const double bytes = 8.0 * N * ((double)B * Lc * nt + (double)B * 2 * Lc + (double)B * 2 * nt +
                                       (double)(n - 1) * 2 * Lc * nt + (double)n * nt);
-      ProfScope ps_(c, "vecmat_lazy", bytes, B * nt);
+      // one multiply-accumulate per key row, per diagonal product and per phi_k(c0) product
+      const double ops = (double)B * (n - 1) * N * (nt * (2.0 * Lc + 2.0) + Lc);
+      ProfScope ps_(c, "vecmat_lazy", bytes, B * nt, ops);
       const size_t smem = ((size_t)Lc + 1) * N * 4;
       if (c->small_primes && smem <= 200 * 1024 && Lc <= 8 && keys32.size() == (size_t)n &&
           N % (LAZY_SM_T * LAZY_SM_EPT) == 0) {
