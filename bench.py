@@ -105,7 +105,7 @@ class ClockSampler:
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2104_03152_b200 import Context, he_im2col_encode
+    from paper_2104_03152_b200 import Context, he_im2col_encode_batch
     from paper_2104_03152_b200.cnn import EncryptedCNN, rotation_steps
     from paper_2104_03152_b200.dist import gather_to_rank0, max_over_ranks, shard_indices
     from synthetic import CFG4, cnn_weights, mnist_like_images
@@ -127,7 +127,7 @@ def run_ours(args, rank, world, local_rank):
 
     n_batches = 2   # distinct input batches cycled through the steps
     imgs_host = [shard(s) for s in range(n_batches)]
-    slots_host = [np.stack([he_im2col_encode(im, 7, 7, 3, ns)[0] for im in imgs]) for imgs in imgs_host]
+    slots_host = [he_im2col_encode_batch(imgs, 7, 7, 3, ns) for imgs in imgs_host]
     slots_dev = [torch.from_numpy(s).to(dev) for s in slots_host]
     logits_dev = torch.empty((B, net.n_out), dtype=torch.float64, device=dev)
 
@@ -200,8 +200,7 @@ def run_ours(args, rank, world, local_rank):
     def step_e2e(i):
         imgs = pinned[i % n_batches].numpy()
         sb = slot_buf.numpy()
-        for b in range(B):
-            sb[b] = he_im2col_encode(imgs[b], 7, 7, 3, ns)[0]
+        he_im2col_encode_batch(imgs, 7, 7, 3, ns, out=sb)   # client im2col into pinned memory
         pt = ctx.he_encode(sb, 2.0 ** net.plan["in_log2"], net.top)   # H2D inside the C call
         ct = ctx.he_encrypt(pt, 2_000_000 + i * B)
         logits_host[:] = ctx.he_decode(ctx.he_decrypt(net.forward(ct)), net.n_out)   # D2H inside
@@ -271,21 +270,29 @@ def micro_extra(ctx_cnn, stream, dev):
 
 
 # ------------------------------------------------------- oracle (CPU) ---
-def oracle_sample(images: int = 1):
-    """Oracle CNN (encrypt + forward + decrypt) on `images` images; returns (images/s, threads, note)."""
+_ORACLE = {}
+
+
+def oracle_sample(images: int = 1, start: int = 10_000):
+    """Oracle CNN (encrypt + forward + decrypt, lazy-ModDown FC layers like the GPU default) on
+    `images` independent images, in parallel over host threads (the oracle's C calls release the
+    GIL); returns (images/s, threads, seconds)."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import circuits as OC
     from oracle.oracle import OracleContext
     from synthetic import CFG4, cnn_weights, mnist_like_images
-    o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-    o.keygen(OC.cnn_rotation_steps())
+    if "o" not in _ORACLE:   # keys are made once (excluded from timing, like the GPU arm)
+        o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+        o.keygen(OC.cnn_rotation_steps())
+        _ORACLE["o"] = o
+    o = _ORACLE["o"]
     w = cnn_weights(CFG4.seed)
-    imgs = mnist_like_images(images, 4, start=10_000)
+    imgs = mnist_like_images(images, 4, start=start)
     cores = os.cpu_count() or 1
 
     def one(i):
-        ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + i)
-        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w)), 10)
+        ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + start + i)
+        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True)), 10)
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=min(images, cores)) as ex:
@@ -297,18 +304,17 @@ def oracle_sample(images: int = 1):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    # each step: one full image through the oracle (encrypt + forward + decrypt), images
-    # processed in parallel over the host cores as the oracle allows (independent items)
-    per_step = 1
-    from oracle import circuits as OC  # noqa: F401  (import cost outside timing)
+    # each step: one image per host core through the oracle (encrypt + forward + decrypt),
+    # in parallel over the cores (independent images, the oracle's only parallelism)
+    per_step = os.cpu_count() or 1
     times = []
     for i in range(args.warmup + args.steps):
-        v, cores, dt = oracle_sample(per_step)
+        v, cores, dt = oracle_sample(per_step, start=10_000 + i * per_step)
         if i >= args.warmup:
             times.append(dt)
     ms = 1e3 * sum(times) / len(times)
     value = per_step / (ms / 1e3)
-    return dict(value=value, ms=ms, cores=1)
+    return dict(value=value, ms=ms, cores=per_step, per_step=per_step)
 
 
 def main():
@@ -345,10 +351,13 @@ def main():
             line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
                     "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms"],
                     "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-                    "data": "synthetic", "config": dict(config, batch_per_gpu=1, global_batch=1,
-                                                        reference="CPU oracle (oracle/), 1 image per step"),
+                    "data": "synthetic", "config": dict(config, batch_per_gpu=r["per_step"],
+                                                        global_batch=r["per_step"],
+                                                        reference=f"CPU oracle (oracle/), {r['per_step']} images "
+                                                                  "per step, one per host core"),
                     "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
-                                     "sample": "1 image (encrypt + forward + decrypt) per step"},
+                                     "sample": f"{r['per_step']} images (encrypt + forward + decrypt) per step, "
+                                               "in parallel over the host cores"},
                     "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
             print(json.dumps(line), flush=True)
         if world > 1:

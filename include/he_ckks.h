@@ -184,6 +184,9 @@ he_status he_rotate(he_context* ctx, const he_ciphertext* a, int32_t k, he_ciphe
  * power of two >= #windows.  Writes *windows / *chunk if non-NULL. */
 he_status he_im2col_encode(const double* img, int H, int W, int kh, int kw, int stride,
                            size_t n_slots, double* slots_out, int* windows, int* chunk);
+/* Batched form: imgs[B][H][W] -> slots_out[B][n_slots] (host, float64). */
+he_status he_im2col_encode_batch(const double* imgs, size_t B, int H, int W, int kh, int kw, int stride,
+                                 size_t n_slots, double* slots_out);
 /* im2col convolution on the encrypted side (C18/C19): for every output
  * channel c: t_c = rescale(ct * K_c); log2(n_s/chunk) rounds t_c += rot(t_c,
  * chunk 2^r); then sum_c t_c * Mask_c, rescale, + bias.  kernels[C][kh*kw],

@@ -5,5 +5,5 @@ built from ``csrc/`` for sm_100a; ``ckks`` is its thin Python binding and
 ``cnn`` drives the paper's encrypted CNN through it.  This package never
 imports ``oracle/`` (test infrastructure).
 """
-from .ckks import (Ciphertext, Context, HEError, Plaintext, he_im2col_encode, lib,  # noqa: F401
-                   LIB_PATH)
+from .ckks import (Ciphertext, Context, HEError, Plaintext, he_im2col_encode, he_im2col_encode_batch,  # noqa: F401
+                   lib, LIB_PATH)

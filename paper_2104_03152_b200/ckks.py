@@ -75,6 +75,7 @@ _SIGS = {
     "he_rotate": [VP, VP, C.c_int32, VPP],
     "he_im2col_encode": [DP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, SZ, DP, C.POINTER(C.c_int),
                          C.POINTER(C.c_int)],
+    "he_im2col_encode_batch": [DP, SZ, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, SZ, DP],
     "he_im2col_conv": [VP, VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, VPP],
     "he_vec_mat": [VP, VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, VPP],
     "he_vec_mat_pt": [VP, VP, VP, VP, VPP],
@@ -443,6 +444,17 @@ class Context:
 
     def he_ntt_mul_intt(self, a, b, out, B: int, nl: int) -> None:
         _check(lib().he_ntt_mul_intt(self.h, _ptr(a), _ptr(b), _ptr(out), B, nl))
+
+
+def he_im2col_encode_batch(imgs, kh: int, kw: int, stride: int, n_slots: int, out=None):
+    """imgs [B][H][W] float64 -> slots [B][n_slots] (C18), one C call for the batch."""
+    imgs = np.ascontiguousarray(imgs, dtype=np.float64)
+    B, H, W = imgs.shape
+    if out is None:
+        out = np.zeros((B, n_slots), dtype=np.float64)
+    _check(lib().he_im2col_encode_batch(imgs.ctypes.data_as(DP), B, H, W, kh, kw, stride, n_slots,
+                                        out.ctypes.data_as(DP)))
+    return out
 
 
 def he_im2col_encode(img, kh: int, kw: int, stride: int, n_slots: int):

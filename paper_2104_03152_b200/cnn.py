@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .ckks import Context, he_im2col_encode
+from .ckks import Context, he_im2col_encode_batch
 
 PLAN = dict(in_log2=30, kernel_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=4)
 CHUNK = 64          # next power of two >= 64 windows (C18)
@@ -61,7 +61,7 @@ class EncryptedCNN:
         self.n_out = int(np.asarray(w.fc2_w).shape[0])
 
     def im2col(self, imgs: np.ndarray) -> np.ndarray:
-        return np.stack([he_im2col_encode(img, KH, KW, STRIDE, self.ctx.slots)[0] for img in imgs])
+        return he_im2col_encode_batch(imgs, KH, KW, STRIDE, self.ctx.slots)
 
     def encrypt(self, imgs: np.ndarray, stream_id: int = 0):
         """Client side: im2col (host) -> encode -> encrypt, images [B][28][28]."""

@@ -448,6 +448,16 @@ he_status he_im2col_encode(const double* img, int H, int W, int kh, int kw, int 
   });
 }
 
+he_status he_im2col_encode_batch(const double* imgs, size_t B, int H, int W, int kh, int kw, int stride,
+                                 size_t n_slots, double* slots_out) {
+  for (size_t b = 0; b < B; ++b) {
+    he_status st = he_im2col_encode(imgs + b * (size_t)H * W, H, W, kh, kw, stride, n_slots, slots_out + b * n_slots,
+                                    nullptr, nullptr);
+    if (st != HE_OK) return st;
+  }
+  return HE_OK;
+}
+
 static void conv_checks(he_context* c, const he_ciphertext* ct, int C, int taps, int chunk) {
   const int ns = c->N / 2;
   need(ct->size == 2, HE_SHAPE_MISMATCH, "conv needs a size-2 ciphertext");
