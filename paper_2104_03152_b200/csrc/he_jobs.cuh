@@ -22,6 +22,23 @@ struct JobLimbs {
   }
 };
 
+// Plain transform writing u32 words (small-prime contexts: every residue < 2^31).
+struct JobLimbsTo32 {
+  static constexpr const char* kName = "ntt_limbs";
+  const u64* src;
+  u32* dst;
+  int N, nl;
+  size_t src_bs, dst_bs;
+  __device__ int prime(int blk) const { return blk % nl; }
+  __device__ u64 load(int blk, u32 i, const PrimeD&) const {
+    return src[(size_t)(blk / nl) * src_bs + (size_t)(blk % nl) * N + i];
+  }
+  __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
+    dst[(size_t)(blk / nl) * dst_bs + (size_t)(blk % nl) * N + i] = (u32)v;
+  }
+};
+inline double alg_bytes(const JobLimbsTo32& j, int nblk) { return 12.0 * j.N * nblk; }
+
 // Fused ring product out = INTT(NTT(a) (.) b) (config 2 "fwd -> modmul -> inv").
 struct JobRingMul {
   static constexpr const char* kName = "ntt_mul_intt";

@@ -582,10 +582,20 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
 // accx_p[t][n] += X_j[pi_g(n)] ksk[j][p][t][n] with the Montgomery-form key.
 // For j == t the digit is the NTT word itself (dsrc).  Output feeds the
 // accx-mode ModDown jobs.
+// C16 centered lift of r < q_j into q_t with 32-bit arithmetic (q_j, q_t < 2^31):
+// [r]_t or q_t - [q_j - r]_t, each reduced by one umulhi Barrett (mut = floor(2^32 / q_t)).
+__device__ __forceinline__ u32 lift32(u32 r, u32 qj, u32 qt, u32 mut) {
+  const bool neg = r > (qj - 1) / 2;
+  const u32 m = neg ? qj - r : r;
+  u32 v = m - __umulhi(m, mut) * qt;
+  v = v >= qt ? v - qt : v;
+  return neg ? (v ? qt - v : 0u) : v;
+}
+
 struct FusedArgs {
   int N, logN, Lc, K, L, NP;
   u32 gal;
-  const u64* coef;     // [B][Lc][N] INTT'd digits
+  const u32* coef;     // [B][Lc][N] INTT'd digits (u32)
   const u64* dsrc;     // digit source NTT words, item stride dsrc_bs
   size_t dsrc_bs;
   const u32* key32;    // [L][2][NP][N] Montgomery form
@@ -608,14 +618,15 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
   for (u32 i = tid; i < 2 * G::N; i += G::T) acc[i] = 0;
   const u32* key = a.key32 + (size_t)tp * G::N;
   const u32 kpart = (u32)a.NP * G::N, kdig = 2 * kpart;
+  const u32 mut = (u32)((1ULL << 32) / q);
   for (int j = 0; j < a.Lc; ++j) {
     if (j == t) {
       const u64* src = a.dsrc + (size_t)b * a.dsrc_bs + (size_t)j * G::N;
       for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)src[i];
     } else {
-      const u64* src = a.coef + ((size_t)b * a.Lc + j) * G::N;
-      const u64 qj = __ldg(a.qtab + j);
-      for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)lift_centered(src[i], qj, P);
+      const u32* src = a.coef + ((size_t)b * a.Lc + j) * G::N;
+      const u32 qj = (u32)__ldg(a.qtab + j);
+      for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = lift32(src[i], qj, q, mut);
       __syncthreads();
       ntt_passes32<LOGN, false, 0>(buf, tid, tw, q);
     }
@@ -992,14 +1003,17 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
                      KsArgs& epi) {
   const size_t N = c->N;
   const int nt = Lc + c->K;
-  Scratch coef(c, (size_t)B * Lc * N * 8), accx(c, (size_t)B * 2 * nt * N * 8);
-  ntt_rows(c, dsrc, coef.as<u64>(), B, Lc, bs, (size_t)Lc * N, true);
-  FusedArgs fa{c->N, c->logN, Lc, c->K, c->L, c->NP, g, coef.as<u64>(), dsrc, bs, key32, c->d_q, accx.as<u64>()};
+  Scratch coef(c, (size_t)B * Lc * N * 4), accx(c, (size_t)B * 2 * nt * N * 8);
+  {
+    JobLimbsTo32 j{dsrc, coef.as<u32>(), c->N, Lc, bs, (size_t)Lc * N};
+    launch_ntt<true>(c, j, B * Lc);
+  }
+  FusedArgs fa{c->N, c->logN, Lc, c->K, c->L, c->NP, g, coef.as<u32>(), dsrc, bs, key32, c->d_q, accx.as<u64>()};
   auto launch = [&](auto kern, int T) {
     const int smem = (int)((N + N / 32 + 2 * N) * 4);
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     // algorithmic bytes: digits read once per item, key rows once per launch, accumulators written once
-    const double bytes = 8.0 * N * ((double)B * Lc + (double)B * 2 * nt) + 4.0 * N * 2 * Lc * nt;
+    const double bytes = 4.0 * N * B * Lc + 8.0 * N * B * 2 * nt + 4.0 * N * 2 * Lc * nt;
     const double ops = (double)B * (Lc * (nt - 1)) * ntt_ops((int)N, c->logN) + (double)B * nt * Lc * 2 * N;
     ProfScope ps_(c, "ks_modup_ip", bytes, B * nt, ops);
     kern<<<dim3(nt, B), T, smem, c->stream>>>(fa, c->d_primes, c->d_tw32);
