@@ -266,6 +266,12 @@ def micro_extra(ctx_cnn, stream, dev):
     out["keyswitch_cfg3"] = {"shape": "N=16384, 8+2 x 50-bit primes, 256 ciphertexts, top level",
                              "rotations_per_s": round(Bc * len(steps) / s_rot, 1),
                              "mul_relin_rescale_per_s": round(Bc / s_mul, 1)}
+    del c3, ct
+    # config 1: one encrypted vec-mat (x 64 values replicated, W 64x10), batch 1: latency
+    from bench_configs import cfg1_latency, cfg5b_throughput
+    out["vecmat_cfg1"] = cfg1_latency(stream, t)
+    # config 5b: deep chain, N=32768, 18+2 x 50-bit primes, 16 x (mul_plain + rescale) + 4 rotate-and-add
+    out["deep_chain_cfg5b"] = cfg5b_throughput(stream, t, dev)
     return out
 
 
