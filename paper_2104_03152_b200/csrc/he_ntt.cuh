@@ -218,22 +218,21 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __r
 // entry 0 of the inverse table holds (N^{-1}, its companion).
 __device__ __forceinline__ u32 spad32(u32 i) { return i + (i >> 5); }
 
+// Conditional subtraction as an unsigned min: x - q wraps above 2^31 when
+// x < q (all values < 2q < 2^32), so min(x, x - q) is the reduced value; one
+// VIADDMNMX instead of ISETP + SEL.
+__device__ __forceinline__ u32 csub32(u32 x, u32 q) { return min(x, x - q); }
 __device__ __forceinline__ u32 shoup32(u32 x, u32 w, u32 wsh, u32 q) {
-  u32 r = x * w - __umulhi(x, wsh) * q;   // [0, 2q)
-  return r >= q ? r - q : r;
+  return csub32(x * w - __umulhi(x, wsh) * q, q);   // [0, 2q) -> [0, q)
 }
 __device__ __forceinline__ void ct_bfly32(u32& x, u32& y, u32 w, u32 wsh, u32 q) {
   const u32 T = shoup32(y, w, wsh, q);
-  u32 u = x + T;
-  u = u >= q ? u - q : u;
-  u32 v = x - T + q;
-  v = v >= q ? v - q : v;
+  const u32 u = csub32(x + T, q);
+  y = csub32(x - T + q, q);
   x = u;
-  y = v;
 }
 __device__ __forceinline__ void gs_bfly32(u32& x, u32& y, u32 w, u32 wsh, u32 q) {
-  u32 u = x + y;
-  u = u >= q ? u - q : u;
+  const u32 u = csub32(x + y, q);
   const u32 v = x - y + q;   // (0, 2q)
   x = u;
   y = shoup32(v, w, wsh, q);

@@ -487,18 +487,15 @@ constexpr int LAZY_SM_T = 1024, LAZY_SM_EPT = 2;
 
 __device__ __forceinline__ u32 redc32(u64 T, u32 q, u32 qneg_inv) {
   const u32 m = (u32)T * qneg_inv;
-  const u32 t = (u32)((T + (u64)m * q) >> 32);
-  return t >= q ? t - q : t;
+  const u32 t = (u32)((T + (u64)m * q) >> 32);   // < 2q
+  return csub32(t, q);
 }
 __device__ __forceinline__ u32 mont_neg_inv(u32 q) {  // -q^{-1} mod 2^32 (q odd)
   u32 inv = q;
   for (int i = 0; i < 5; ++i) inv *= 2u - q * inv;
   return 0u - inv;
 }
-__device__ __forceinline__ u32 addq(u32 a, u32 b, u32 q) {
-  const u32 s = a + b;
-  return s >= q ? s - q : s;
-}
+__device__ __forceinline__ u32 addq(u32 a, u32 b, u32 q) { return csub32(a + b, q); }
 
 template <int LC>
 __global__ void __launch_bounds__(LAZY_SM_T, 1)
@@ -587,8 +584,7 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
 __device__ __forceinline__ u32 lift32(u32 r, u32 qj, u32 qt, u32 mut) {
   const bool neg = r > (qj - 1) / 2;
   const u32 m = neg ? qj - r : r;
-  u32 v = m - __umulhi(m, mut) * qt;
-  v = v >= qt ? v - qt : v;
+  const u32 v = csub32(m - __umulhi(m, mut) * qt, qt);
   return neg ? (v ? qt - v : 0u) : v;
 }
 
