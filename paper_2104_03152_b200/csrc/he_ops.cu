@@ -501,6 +501,9 @@ template <int LC>
 __global__ void __launch_bounds__(LAZY_SM_T, 1)
 k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
                    const PrimeD* __restrict__ primes) {
+  // each thread owns 4 consecutive coefficients: key rows, diagonals and the
+  // outputs move as 16-byte vectors; the automorphism gathers come from smem
+  constexpr int V = 4;
   extern __shared__ u32 xs[];
   const int t = blockIdx.x, b = blockIdx.y, nt = LC + a.K;
   const int tp = t < LC ? t : a.L + (t - LC);
@@ -519,57 +522,79 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
   if (data)
     for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) c0s[i] = (u32)c0[(size_t)t * N + i];
   __syncthreads();
-  // P' = [P]_q 2^32 mod q (Montgomery form)
   const u32 Pm = (u32)((((u64)__ldg(a.P_mod + tp)) << 32) % q);
   const u32 keyrow = tp * N, kpart = NP * N, kdig = 2 * NP * N;
-  for (u32 tile = 0; tile < N; tile += LAZY_SM_T * LAZY_SM_EPT) {
-    u32 nn[LAZY_SM_EPT], acc0[LAZY_SM_EPT], acc1[LAZY_SM_EPT], cc0[LAZY_SM_EPT], cc1[LAZY_SM_EPT];
+  for (u32 tile = 0; tile < N; tile += LAZY_SM_T * V) {
+    const u32 n0 = tile + threadIdx.x * V;
+    u32 acc0[V], acc1[V], cc0[V], cc1[V];
+    {
+      uint4 d0 = make_uint4(0, 0, 0, 0);
+      if (data) d0 = __ldg(reinterpret_cast<const uint4*>(dm + t * N + n0));
+      const u32 dd[V] = {d0.x, d0.y, d0.z, d0.w};
 #pragma unroll
-    for (int e = 0; e < LAZY_SM_EPT; ++e) {
-      nn[e] = tile + e * LAZY_SM_T + threadIdx.x;
-      acc0[e] = acc1[e] = cc0[e] = cc1[e] = 0;
-      if (data) {
-        const u32 d0 = __ldg(dm + t * N + nn[e]);
-        cc0[e] = redc32((u64)d0 * c0s[nn[e]], q, qi);
-        cc1[e] = redc32((u64)d0 * xs[t * N + nn[e]], q, qi);   // the t == j digit is c1[t]
+      for (int e = 0; e < V; ++e) {
+        acc0[e] = acc1[e] = cc0[e] = cc1[e] = 0;
+        if (data) {
+          cc0[e] = redc32((u64)dd[e] * c0s[n0 + e], q, qi);
+          cc1[e] = redc32((u64)dd[e] * xs[t * N + n0 + e], q, qi);   // the t == j digit is c1[t]
+        }
       }
     }
     for (int k = 1; k < a.n; ++k) {
       const u32 g = __ldg(a.gal + k);
-      const u32* key = keys32[k] + keyrow;
-      const u32* Dk = dm + ((u32)k * nt + t) * N;
+      const u32* key = keys32[k] + keyrow + n0;
+      const uint4 dv = __ldg(reinterpret_cast<const uint4*>(dm + ((u32)k * nt + t) * N + n0));
+      const u32 dd[V] = {dv.x, dv.y, dv.z, dv.w};
+      u32 sn[V];
 #pragma unroll
-      for (int e = 0; e < LAZY_SM_EPT; ++e) {
-        const u32 n = nn[e], sn = galois_src(n, g, a.logN);
-        u32 ip0 = 0, ip1 = 0;
+      for (int e = 0; e < V; ++e) sn[e] = galois_src(n0 + e, g, a.logN);
+      u32 ip0[V], ip1[V];
 #pragma unroll
-        for (int j = 0; j < LC; j += 2) {
-          const u32 x0 = xs[j * N + sn];
-          u64 s0 = (u64)x0 * __ldg(key + j * kdig + n);
-          u64 s1 = (u64)x0 * __ldg(key + j * kdig + kpart + n);
-          if (j + 1 < LC) {
-            const u32 x1 = xs[(j + 1) * N + sn];
-            s0 += (u64)x1 * __ldg(key + (j + 1) * kdig + n);
-            s1 += (u64)x1 * __ldg(key + (j + 1) * kdig + kpart + n);
-          }
-          ip0 = addq(ip0, redc32(s0, q, qi), q);
-          ip1 = addq(ip1, redc32(s1, q, qi), q);
+      for (int e = 0; e < V; ++e) ip0[e] = ip1[e] = 0;
+#pragma unroll
+      for (int j = 0; j < LC; j += 2) {
+        const uint4 kb0 = __ldg(reinterpret_cast<const uint4*>(key + j * kdig));
+        const uint4 ka0 = __ldg(reinterpret_cast<const uint4*>(key + j * kdig + kpart));
+        uint4 kb1 = make_uint4(0, 0, 0, 0), ka1 = make_uint4(0, 0, 0, 0);
+        if (j + 1 < LC) {
+          kb1 = __ldg(reinterpret_cast<const uint4*>(key + (j + 1) * kdig));
+          ka1 = __ldg(reinterpret_cast<const uint4*>(key + (j + 1) * kdig + kpart));
         }
-        const u32 d = __ldg(Dk + n);
-        acc0[e] = addq(acc0[e], redc32((u64)d * ip0, q, qi), q);
-        acc1[e] = addq(acc1[e], redc32((u64)d * ip1, q, qi), q);
-        if (data) cc0[e] = addq(cc0[e], redc32((u64)d * c0s[sn], q, qi), q);
+        const u32 b0[V] = {kb0.x, kb0.y, kb0.z, kb0.w}, a0[V] = {ka0.x, ka0.y, ka0.z, ka0.w};
+        const u32 b1[V] = {kb1.x, kb1.y, kb1.z, kb1.w}, a1[V] = {ka1.x, ka1.y, ka1.z, ka1.w};
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const u32 x0 = xs[j * N + sn[e]];
+          u64 s0 = (u64)x0 * b0[e], s1 = (u64)x0 * a0[e];
+          if (j + 1 < LC) {
+            const u32 x1 = xs[(j + 1) * N + sn[e]];
+            s0 += (u64)x1 * b1[e];
+            s1 += (u64)x1 * a1[e];
+          }
+          ip0[e] = addq(ip0[e], redc32(s0, q, qi), q);
+          ip1[e] = addq(ip1[e], redc32(s1, q, qi), q);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        acc0[e] = addq(acc0[e], redc32((u64)dd[e] * ip0[e], q, qi), q);
+        acc1[e] = addq(acc1[e], redc32((u64)dd[e] * ip1[e], q, qi), q);
+        if (data) cc0[e] = addq(cc0[e], redc32((u64)dd[e] * c0s[sn[e]], q, qi), q);
       }
     }
+    u64* o0 = a.accx + (((size_t)b * 2 + 0) * nt + t) * N + n0;
+    u64* o1 = a.accx + (((size_t)b * 2 + 1) * nt + t) * N + n0;
 #pragma unroll
-    for (int e = 0; e < LAZY_SM_EPT; ++e) {
+    for (int e = 0; e < V; ++e) {
       if (data) {
         acc0[e] = addq(acc0[e], redc32((u64)Pm * cc0[e], q, qi), q);
         acc1[e] = addq(acc1[e], redc32((u64)Pm * cc1[e], q, qi), q);
       }
-      a.accx[(((size_t)b * 2 + 0) * nt + t) * N + nn[e]] = acc0[e];
-      a.accx[(((size_t)b * 2 + 1) * nt + t) * N + nn[e]] = acc1[e];
     }
+    reinterpret_cast<ulonglong2*>(o0)[0] = make_ulonglong2(acc0[0], acc0[1]);
+    reinterpret_cast<ulonglong2*>(o0)[1] = make_ulonglong2(acc0[2], acc0[3]);
+    reinterpret_cast<ulonglong2*>(o1)[0] = make_ulonglong2(acc1[0], acc1[1]);
+    reinterpret_cast<ulonglong2*>(o1)[1] = make_ulonglong2(acc1[2], acc1[3]);
   }
 }
 
@@ -1156,7 +1181,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
       ProfScope ps_(c, "vecmat_lazy", bytes, B * nt, ops);
       const size_t smem = ((size_t)Lc + 1) * N * 4;
       if (c->small_primes && smem <= 200 * 1024 && Lc <= 8 && keys32.size() == (size_t)n &&
-          N % (LAZY_SM_T * LAZY_SM_EPT) == 0) {
+          N % (LAZY_SM_T * 4) == 0) {
         if (!diags->dm) {   // Montgomery u32 copy of the diagonals, cached on the plaintext
           const size_t rows = (size_t)n * nt;
           u32* dmp = dalloc_t<u32>(c, rows * N);
