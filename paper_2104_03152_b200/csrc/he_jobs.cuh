@@ -134,9 +134,15 @@ struct KsArgs {
   const u64* D;            // nullable plaintext factor: D + kk*D_ks + i*N
   size_t D_ks;
   // lazy ModDown: when set, the inner products are replaced by the extended-basis
-  // accumulator accx[b][part][Lc+K][N] (data limbs then specials), KB = 1
+  // accumulator accx[b][part][Lc+K][N] (data limbs then specials), KB = 1;
+  // accx32: the accumulator words are u32 (small-prime fused key switch)
   const u64* accx;
+  int accx32;
 };
+
+__device__ __forceinline__ u64 accx_word(const KsArgs& a, size_t i) {
+  return a.accx32 ? (u64)reinterpret_cast<const u32*>(a.accx)[i] : a.accx[i];
+}
 
 // Inner product over digits at target limb t for source position sn.
 __device__ __forceinline__ u64 ks_inner(const KsArgs& a, int kk, int b, int part, int t, int tprime,
@@ -169,7 +175,7 @@ struct JobKsSpecial {
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
     int kk, b, part, k;
     dec(blk, kk, b, part, k);
-    if (a.accx) return a.accx[(((size_t)b * 2 + part) * (a.Lc + a.K) + a.Lc + k) * a.N + n];
+    if (a.accx) return accx_word(a, (((size_t)b * 2 + part) * (a.Lc + a.K) + a.Lc + k) * a.N + n);
     const u32 g = a.gal[kk];
     const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
     return ks_inner(a, kk, b, part, a.Lc + k, a.L + k, sn, n, P);
@@ -213,7 +219,7 @@ struct JobKsData {
     dec(blk, kk, b, part, i);
     const u32 g = a.gal[kk];
     const u32 sn = g == 1 ? n : galois_src(n, g, a.logN);
-    const u64 ip = a.accx ? a.accx[(((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N + n]
+    const u64 ip = a.accx ? accx_word(a, (((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N + n)
                           : ks_inner(a, kk, b, part, i, i, sn, n, P);
     u64 u = mul_mod(sub_mod(ip, v, P.q), __ldg(a.Pinv_mod + i), P);
     const size_t LN = (size_t)a.Lc * a.N;

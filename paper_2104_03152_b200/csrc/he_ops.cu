@@ -652,17 +652,33 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
       ntt_passes32<LOGN, false, 0>(buf, tid, tw, q);
     }
     __syncthreads();
-    for (u32 n = tid; n < G::N; n += G::T) {
-      const u32 sn = a.gal == 1 ? n : galois_src(n, a.gal, LOGN);
-      const u32 x = buf[spad32(sn)];
-      acc[n] = addq(acc[n], redc32((u64)x * __ldg(key + j * kdig + n), q, qi), q);
-      acc[G::N + n] = addq(acc[G::N + n], redc32((u64)x * __ldg(key + j * kdig + kpart + n), q, qi), q);
+    // 4 consecutive coefficients per step: 16-byte key loads and accumulator updates
+    for (u32 n0 = tid * 4; n0 < G::N; n0 += G::T * 4) {
+      const uint4 kb = __ldg(reinterpret_cast<const uint4*>(key + j * kdig + n0));
+      const uint4 ka = __ldg(reinterpret_cast<const uint4*>(key + j * kdig + kpart + n0));
+      uint4 a0 = *reinterpret_cast<uint4*>(acc + n0), a1 = *reinterpret_cast<uint4*>(acc + G::N + n0);
+      const u32 kbv[4] = {kb.x, kb.y, kb.z, kb.w}, kav[4] = {ka.x, ka.y, ka.z, ka.w};
+      u32 r0[4] = {a0.x, a0.y, a0.z, a0.w}, r1[4] = {a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const u32 n = n0 + e;
+        const u32 sn = a.gal == 1 ? n : galois_src(n, a.gal, LOGN);
+        const u32 x = buf[spad32(sn)];
+        r0[e] = addq(r0[e], redc32((u64)x * kbv[e], q, qi), q);
+        r1[e] = addq(r1[e], redc32((u64)x * kav[e], q, qi), q);
+      }
+      *reinterpret_cast<uint4*>(acc + n0) = make_uint4(r0[0], r0[1], r0[2], r0[3]);
+      *reinterpret_cast<uint4*>(acc + G::N + n0) = make_uint4(r1[0], r1[1], r1[2], r1[3]);
     }
     __syncthreads();
   }
-  for (u32 n = tid; n < G::N; n += G::T) {
-    a.accx[(((size_t)b * 2 + 0) * nt + t) * G::N + n] = acc[n];
-    a.accx[(((size_t)b * 2 + 1) * nt + t) * G::N + n] = acc[G::N + n];
+  // accumulators leave as u32 (every residue < 2^31); the accx-mode ModDown reads u32
+  u32* out = reinterpret_cast<u32*>(a.accx);
+  for (u32 n0 = tid * 4; n0 < G::N; n0 += G::T * 4) {
+    *reinterpret_cast<uint4*>(out + (((size_t)b * 2 + 0) * nt + t) * G::N + n0) =
+        *reinterpret_cast<const uint4*>(acc + n0);
+    *reinterpret_cast<uint4*>(out + (((size_t)b * 2 + 1) * nt + t) * G::N + n0) =
+        *reinterpret_cast<const uint4*>(acc + G::N + n0);
   }
 }
 
@@ -1024,7 +1040,7 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
                      KsArgs& epi) {
   const size_t N = c->N;
   const int nt = Lc + c->K;
-  Scratch coef(c, (size_t)B * Lc * N * 4), accx(c, (size_t)B * 2 * nt * N * 8);
+  Scratch coef(c, (size_t)B * Lc * N * 4), accx(c, (size_t)B * 2 * nt * N * 4);
   {
     JobLimbsTo32 j{dsrc, coef.as<u32>(), c->N, Lc, bs, (size_t)Lc * N};
     launch_ntt<true>(c, j, B * Lc);
@@ -1034,7 +1050,7 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
     const int smem = (int)((N + N / 32 + 2 * N) * 4);
     HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     // algorithmic bytes: digits read once per item, key rows once per launch, accumulators written once
-    const double bytes = 4.0 * N * B * Lc + 8.0 * N * B * 2 * nt + 4.0 * N * 2 * Lc * nt;
+    const double bytes = 4.0 * N * B * Lc + 4.0 * N * B * 2 * nt + 4.0 * N * 2 * Lc * nt;
     const double ops = (double)B * (Lc * (nt - 1)) * ntt_ops((int)N, c->logN) + (double)B * nt * Lc * 2 * N;
     ProfScope ps_(c, "ks_modup_ip", bytes, B * nt, ops);
     kern<<<dim3(nt, B), T, smem, c->stream>>>(fa, c->d_primes, c->d_tw32);
@@ -1048,6 +1064,7 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
   }
   check_launch(c);
   epi.accx = accx.as<u64>();
+  epi.accx32 = 1;
   epi.gal[0] = g;
   ks_launch(c, epi);
 }
