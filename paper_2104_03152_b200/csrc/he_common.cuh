@@ -72,6 +72,13 @@ __device__ __forceinline__ u64 reduce64(u64 x, const PrimeD& P) {
   r = r >= P.q ? r - P.q : r;
   return r >= P.q ? r - P.q : r;
 }
+// x mod q for x < 2^32 and q < 2^31: q_hat = umulhi(x, floor(2^32 / q)) >= floor(x/q) - 1,
+// so one conditional subtraction (as an unsigned min) finishes.
+__device__ __forceinline__ u64 reduce32(u32 x, const PrimeD& P) {
+  const u32 q = (u32)P.q, mu32 = (u32)(P.mu64 >> 32);
+  const u32 r = x - __umulhi(x, mu32) * q;
+  return min(r, r - q);
+}
 // Shoup: x * w mod q in [0, 2q) for any 64-bit x, w < q, wsh = floor(w 2^64 / q).
 __device__ __forceinline__ u64 mul_shoup_lazy(u64 x, u64 w, u64 wsh, u64 q) {
   return x * w - __umul64hi(x, wsh) * q;

@@ -184,7 +184,9 @@ struct JobKsSpecial {
     int kk, b, part, k;
     dec(blk, kk, b, part, k);
     const u64 y = add_mod(v, __ldg(a.Ph_mod + a.L + k), P.q);
-    a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n] = mul_mod(y, __ldg(a.Phat_inv + k), P);
+    // one special prime: (P/p_0)^{-1} = 1
+    a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n] =
+        a.K == 1 ? y : mul_mod(y, __ldg(a.Phat_inv + k), P);
   }
 };
 
@@ -206,9 +208,13 @@ struct JobKsData {
     int kk, b, part, i;
     dec(blk, kk, b, part, i);
     u64 conv = 0;
-    for (int k = 0; k < a.K; ++k) {
-      const u64 t = a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n];
-      conv = add_mod(conv, mul_mod(reduce64(t, P), __ldg(a.Phat_mod + (size_t)k * a.NP + i), P), P.q);
+    if (a.K == 1 && P.k <= 31) {   // one special prime: weight P/p_0 = 1, residues < 2^31
+      conv = reduce32((u32)a.tb[(((size_t)kk * a.B + b) * 2 + part) * a.N + n], P);
+    } else {
+      for (int k = 0; k < a.K; ++k) {
+        const u64 t = a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n];
+        conv = add_mod(conv, mul_mod(reduce64(t, P), __ldg(a.Phat_mod + (size_t)k * a.NP + i), P), P.q);
+      }
     }
     // the +[P/2]_{q_i} of C15 is added to every COEFFICIENT, so it is folded
     // here (coefficient domain) rather than after the transform
@@ -259,7 +265,9 @@ struct JobRescaleData {
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
     // [y]_{q_i} - [h]_{q_i}: h is added to every coefficient (C15), so it is
     // folded in before the forward transform
-    return sub_mod(reduce64(y[(size_t)(blk / (Lc - 1)) * N + n], P), __ldg(h + blk % (Lc - 1)), P.q);
+    const u64 yv = y[(size_t)(blk / (Lc - 1)) * N + n];
+    return sub_mod(P.k <= 31 && yv < (1ULL << 32) ? reduce32((u32)yv, P) : reduce64(yv, P), __ldg(h + blk % (Lc - 1)),
+                   P.q);
   }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
