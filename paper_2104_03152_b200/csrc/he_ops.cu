@@ -1195,7 +1195,10 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
                                       (double)(n - 1) * 2 * Lc * nt + (double)n * nt);
       // one multiply-accumulate per key row, per diagonal product and per phi_k(c0) product
       const double ops = (double)B * (n - 1) * N * (nt * (2.0 * Lc + 2.0) + Lc);
-      ProfScope ps_(c, "vecmat_lazy", bytes, B * nt, ops);
+      static const char* const tags[9] = {"vecmat_lazy", "vecmat_lazy_L1", "vecmat_lazy_L2", "vecmat_lazy_L3",
+                                          "vecmat_lazy_L4", "vecmat_lazy_L5", "vecmat_lazy_L6", "vecmat_lazy_L7",
+                                          "vecmat_lazy_L8"};
+      ProfScope ps_(c, tags[Lc <= 8 ? Lc : 0], bytes, B * nt, ops);
       const size_t smem = ((size_t)Lc + 1) * N * 4;
       if (c->small_primes && smem <= 200 * 1024 && Lc <= 8 && keys32.size() == (size_t)n &&
           N % (LAZY_SM_T * 4) == 0) {
