@@ -238,7 +238,22 @@ __device__ __forceinline__ void gs_bfly32(u32& x, u32& y, u32 w, u32 wsh, u32 q)
   y = shoup32(v, w, wsh, q);
 }
 
-template <int LOGN, bool INV, int LO, int NB>
+// Harvey-lazy 32-bit butterflies for q < 2^30 (4q < 2^32): CT keeps values in
+// [0, 4q), GS in [0, 2q); one conditional subtraction per butterfly.
+__device__ __forceinline__ void ct_bfly32_lazy(u32& x, u32& y, u32 w, u32 wsh, u32 q) {
+  const u32 X = min(x, x - 2 * q);
+  const u32 T = y * w - __umulhi(y, wsh) * q;   // [0, 2q)
+  x = X + T;
+  y = X - T + 2 * q;
+}
+__device__ __forceinline__ void gs_bfly32_lazy(u32& x, u32& y, u32 w, u32 wsh, u32 q) {
+  const u32 u = min(x + y, x + y - 2 * q);
+  const u32 v = x - y + 2 * q;                   // (0, 4q)
+  x = u;
+  y = v * w - __umulhi(v, wsh) * q;              // [0, 2q)
+}
+
+template <int LOGN, bool INV, int LO, int NB, bool LAZY = false>
 __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __restrict__ tw, u32 q) {
   typedef NttGeom<LOGN, 1> G;
   constexpr int NG = 1 << (G::R - NB);
@@ -260,8 +275,13 @@ __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __rest
         if (k & half) continue;
         const u32 j = base + (k << LO);
         const uint2 w = __ldg(tw + (1u << s) + (j >> (LOGN - s)));
-        if (!INV) ct_bfly32(x[k], x[k + half], w.x, w.y, q);
-        else gs_bfly32(x[k], x[k + half], w.x, w.y, q);
+        if (LAZY) {
+          if (!INV) ct_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
+          else gs_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
+        } else {
+          if (!INV) ct_bfly32(x[k], x[k + half], w.x, w.y, q);
+          else gs_bfly32(x[k], x[k + half], w.x, w.y, q);
+        }
       }
     }
 #pragma unroll
@@ -269,15 +289,26 @@ __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __rest
   }
 }
 
-template <int LOGN, bool INV, int P>
+template <int LOGN, bool INV, int P, bool LAZY = false>
 __device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, u32 q) {
   typedef NttGeom<LOGN, 1> G;
   constexpr int GP = INV ? P : G::NPASS - 1 - P;
   constexpr int LO = GP * G::R;
   constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-  ntt_pass32<LOGN, INV, LO, NB>(sm, tid, tw, q);
+  ntt_pass32<LOGN, INV, LO, NB, LAZY>(sm, tid, tw, q);
   __syncthreads();
-  if constexpr (P + 1 < G::NPASS) ntt_passes32<LOGN, INV, P + 1>(sm, tid, tw, q);
+  if constexpr (P + 1 < G::NPASS) ntt_passes32<LOGN, INV, P + 1, LAZY>(sm, tid, tw, q);
+}
+// Runs the lazy network when q < 2^30; outputs are then in [0, 4q) (forward) or
+// [0, 2q) (inverse) and must be reduced by the caller (ntt_reduce32).
+template <int LOGN, bool INV>
+__device__ __forceinline__ void ntt_run32(u32* sm, u32 tid, const uint2* tw, u32 q) {
+  if (q < (1u << 30)) ntt_passes32<LOGN, INV, 0, true>(sm, tid, tw, q);
+  else ntt_passes32<LOGN, INV, 0, false>(sm, tid, tw, q);
+}
+__device__ __forceinline__ u32 ntt_reduce32(u32 v, u32 q) {
+  v = min(v, v - 2 * q);   // no-op unless q < 2^30 (then v < 4q)
+  return min(v, v - q);
 }
 
 template <int LOGN>
@@ -299,11 +330,11 @@ k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw
   const u32 q = (u32)P.q;
   for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)job.load(blk, i, P);
   __syncthreads();
-  ntt_passes32<LOGN, INV, 0>(sm32, tid, tw, q);
+  ntt_run32<LOGN, INV>(sm32, tid, tw, q);
   const uint2 ni = __ldg(tw);
   for (u32 i = tid; i < G::NL; i += G::T) {
     u32 v = sm32[spad32(i)];
-    if (INV) v = shoup32(v, ni.x, ni.y, q);
+    v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
     job.store(blk, i, (u64)v, P);
   }
 }

@@ -649,7 +649,7 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
       const u32 qj = (u32)__ldg(a.qtab + j);
       for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = lift32(src[i], qj, q, mut);
       __syncthreads();
-      ntt_passes32<LOGN, false, 0>(buf, tid, tw, q);
+      ntt_run32<LOGN, false>(buf, tid, tw, q);   // values in [0, 4q) when q < 2^30: x k' < 4q^2 < q 2^32 still REDCs
     }
     __syncthreads();
     // 4 consecutive coefficients per step: 16-byte key loads and accumulator updates
