@@ -206,6 +206,12 @@ def run_ours(args, rank, world, local_rank):
         logits_host[:] = ctx.he_decode(ctx.he_decrypt(net.forward(ct)), net.n_out)   # D2H inside
 
     e2e_ms, _ = timed(step_e2e, args.steps, 1)
+    # communication per inference: serialized encrypted input + encrypted logits of one image
+    one = ctx.he_encrypt(ctx.he_encode(slots_dev[0][:1], 2.0 ** net.plan["in_log2"], net.top), 7)
+    up = len(ctx.he_ct_serialize(one))
+    down = len(ctx.he_ct_serialize(net.forward(one)))
+    comm = {"input_bytes": up, "output_bytes": down, "total_bytes": up + down, "paper_total": "427 KB (PAPER.md:120)",
+            "format": "bit-packed NTT words, w_i = bit_length(q_i) (DESIGN.md §3 wire format)"}
     e2e = {"value": world * B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": B * ns * 8, "d2h_bytes_per_step": B * net.n_out * 8}
 
@@ -216,6 +222,7 @@ def run_ours(args, rank, world, local_rank):
     # result collection to rank 0 (outside the timed region): NCCL gather of the logits
     gather_to_rank0(logits_dev)
 
+    extra["communication_cfg4"] = comm
     return dict(value=value, ms=ms, launches=launches, clocks=clk.summary(), roofline=roofline,
                 breakdown=breakdown, e2e=e2e, extra=extra)
 

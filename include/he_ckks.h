@@ -269,6 +269,22 @@ he_status he_key_export(he_context* ctx, int kind, int32_t step, uint64_t* dst);
 /* Number of words he_key_export writes for `kind`. */
 size_t he_key_words(const he_context* ctx, int kind);
 
+/* ---- wire format ("427KB of communication") ----
+ * A 64-byte header (magic "HECKKS01", u32 log2N, u32 B, u32 size, u32 level,
+ * f64 scale, u64 payload_bytes, u32 n_limbs, 20 zero bytes) followed by, for
+ * every item b, poly p and limb i, the N stored NTT-domain words of limb i
+ * written with w_i = bit_length(q_i) bits each, least significant bit first,
+ * as little-endian 64-bit words (N w_i is a multiple of 64, so each limb
+ * segment is 64-bit aligned).  Packing and unpacking run on the device. */
+/* Total serialized bytes (header + payload) of ct. */
+he_status he_ct_serialized_size(he_context* ctx, const he_ciphertext* ct, size_t* bytes);
+/* Write header + payload to dst (host, or device when on_device != 0). */
+he_status he_ct_serialize(he_context* ctx, const he_ciphertext* ct, void* dst, int on_device);
+/* Read a serialized ciphertext of len bytes; rejects a bad header, a wrong
+ * length or a residue >= its prime (HE_INVALID_ARGUMENT), other parameters
+ * (HE_PARAM_MISMATCH). */
+he_status he_ct_deserialize(he_context* ctx, const void* src, int on_device, size_t len, he_ciphertext** out);
+
 /* ---- ring primitives (BASELINE config 2 microbench) ------ */
 /* In-place batched forward / inverse negacyclic NTT (C5) of device words
  * d[B][n_limbs][N], limb i modulo prime i (n_limbs <= L+K). */

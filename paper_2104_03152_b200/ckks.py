@@ -99,6 +99,9 @@ _SIGS = {
     "he_vec_mat_encode_lazy": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
     "he_key_export": [VP, C.c_int, C.c_int32, U64P],
     "he_key_words": [VP, C.c_int],
+    "he_ct_serialized_size": [VP, VP, C.POINTER(SZ)],
+    "he_ct_serialize": [VP, VP, VP, C.c_int],
+    "he_ct_deserialize": [VP, VP, C.c_int, SZ, VPP],
     "he_ntt_forward": [VP, VP, SZ, C.c_int],
     "he_ntt_inverse": [VP, VP, SZ, C.c_int],
     "he_modmul": [VP, VP, VP, VP, SZ, C.c_int],
@@ -431,6 +434,19 @@ class Context:
                           chunk: int) -> Ciphertext:
         return self._ct2(lib().he_im2col_conv_pt, ct.h, kernels.h, masks.h, None if bias is None else bias.h,
                          int(chunk))
+
+    # -- wire format -------------------------------------------------------------
+    def he_ct_serialize(self, ct: Ciphertext) -> bytes:
+        n = SZ()
+        _check(lib().he_ct_serialized_size(self.h, ct.h, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().he_ct_serialize(self.h, ct.h, buf, 0))
+        return buf.raw
+
+    def he_ct_deserialize(self, data: bytes) -> Ciphertext:
+        h = C.c_void_p()
+        _check(lib().he_ct_deserialize(self.h, data, 0, len(data), C.byref(h)))
+        return Ciphertext(self, h)
 
     # -- ring primitives (device tensors [B][nl][N] uint64 / int64) --------------
     def he_ntt_forward(self, d, B: int, nl: int) -> None:

@@ -812,6 +812,85 @@ he_status he_key_export(he_context* c, int kind, int32_t step, uint64_t* dst) {
   });
 }
 
+// ------------------------------------------------------------ wire format ---
+namespace {
+struct WireHeader {
+  char magic[8];
+  uint32_t log2N, B, size, level;
+  double scale;
+  uint64_t payload_bytes;
+  uint32_t n_limbs;
+  char pad[20];
+};
+static_assert(sizeof(WireHeader) == 64, "wire header is 64 bytes");
+const char kMagic[8] = {'H', 'E', 'C', 'K', 'K', 'S', '0', '1'};
+}  // namespace
+
+he_status he_ct_serialized_size(he_context* c, const he_ciphertext* ct, size_t* bytes) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(bytes);
+    *bytes = sizeof(WireHeader) + wire_payload_bytes(c, ct);
+  });
+}
+
+he_status he_ct_serialize(he_context* c, const he_ciphertext* ct, void* dst, int on_device) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(dst);
+    WireHeader h;
+    memset(&h, 0, sizeof(h));
+    memcpy(h.magic, kMagic, 8);
+    h.log2N = c->logN;
+    h.B = ct->B;
+    h.size = ct->size;
+    h.level = ct->level;
+    h.scale = ct->scale;
+    h.payload_bytes = wire_payload_bytes(c, ct);
+    h.n_limbs = ct->level + 1;
+    char* d = (char*)dst;
+    if (on_device) {
+      HE_CK(cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+      wire_pack(c, ct, (u64*)(d + sizeof(h)));
+    } else {
+      memcpy(d, &h, sizeof(h));
+      Scratch buf(c, h.payload_bytes);
+      wire_pack(c, ct, buf.as<u64>());
+      HE_CK(cudaMemcpyAsync(d + sizeof(h), buf.p, h.payload_bytes, cudaMemcpyDeviceToHost, c->stream));
+      HE_CK(cudaStreamSynchronize(c->stream));
+    }
+  });
+}
+
+he_status he_ct_deserialize(he_context* c, const void* src, int on_device, size_t len, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_out(out);
+    need(src != nullptr && len >= sizeof(WireHeader), HE_INVALID_ARGUMENT, "truncated wire data");
+    WireHeader h;
+    if (on_device) {
+      HE_CK(cudaMemcpyAsync(&h, src, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      HE_CK(cudaStreamSynchronize(c->stream));
+    } else {
+      memcpy(&h, src, sizeof(h));
+    }
+    need(memcmp(h.magic, kMagic, 8) == 0, HE_INVALID_ARGUMENT, "bad wire magic");
+    need((int)h.log2N == c->logN, HE_PARAM_MISMATCH, "ring degree differs from the context's");
+    need(h.size == 2 || h.size == 3, HE_SHAPE_MISMATCH, "size must be 2 or 3");
+    need((int)h.level < c->L && h.n_limbs == h.level + 1 && h.B >= 1, HE_INVALID_ARGUMENT, "bad header");
+    // payload length implied by the context's primes must match the header and the buffer
+    size_t expect = 0;
+    for (uint32_t i = 0; i <= h.level; ++i) expect += (size_t)c->N * c->hp.kbits[i] / 8;
+    expect *= (size_t)h.B * h.size;
+    need(expect == h.payload_bytes && len == sizeof(h) + expect, HE_INVALID_ARGUMENT, "wire length mismatch");
+    const char* s = (const char*)src + sizeof(h);
+    if (on_device) {
+      *out = wire_unpack(c, (const u64*)s, h.B, (int)h.size, (int)h.level, h.scale);
+    } else {
+      Scratch buf(c, expect);
+      HE_CK(cudaMemcpyAsync(buf.p, s, expect, cudaMemcpyHostToDevice, c->stream));
+      *out = wire_unpack(c, buf.as<u64>(), h.B, (int)h.size, (int)h.level, h.scale);
+    }
+  });
+}
+
 // ------------------------------------------------------------ ring prims ---
 static void ring_checks(he_context* c, const void* p, size_t B, int nl) {
   need_ctx(c);

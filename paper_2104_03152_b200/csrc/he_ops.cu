@@ -694,6 +694,116 @@ __global__ void k_to_mont32(const u64* __restrict__ in, u32* __restrict__ out, c
   }
 }
 
+// ============================================================ wire format ===
+// (DESIGN.md §3): limb segment (b, p, i) holds N words of w_i = bitlen(q_i) bits,
+// LSB first, in 64-bit words; N w_i is a multiple of 64, so segments are aligned.
+// Pack: one thread per output word, gathering the <= 64/w + 2 residues it covers.
+__global__ void k_wire_pack(const u64* __restrict__ src, u64* __restrict__ out, const u32* __restrict__ width,
+                            const u64* __restrict__ seg_word, int N, int Lc, size_t nseg) {
+  for (size_t sg = blockIdx.y; sg < nseg; sg += gridDim.y) {
+    const int i = (int)(sg % Lc);
+    const u32 w = width[i];
+    const u64* x = src + sg * N;
+    u64* o = out + seg_word[sg];
+    const u32 nw = (u32)((u64)N * w / 64);
+    for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < nw; k += gridDim.x * blockDim.x) {
+      const u64 bit0 = (u64)k * 64;
+      u32 c = (u32)(bit0 / w);
+      long pos = (long)((u64)c * w) - (long)bit0;   // <= 0
+      u64 acc = 0;
+      for (; pos < 64 && c < (u32)N; ++c, pos += w) acc |= pos < 0 ? x[c] >> (-pos) : x[c] << pos;
+      o[k] = acc;
+    }
+  }
+}
+// Unpack: one thread per residue; flags any residue >= q (corrupt input).
+__global__ void k_wire_unpack(const u64* __restrict__ in, u64* __restrict__ dst, const u32* __restrict__ width,
+                              const u64* __restrict__ seg_word, const PrimeD* __restrict__ primes, int N, int Lc,
+                              size_t nseg, int* bad) {
+  for (size_t sg = blockIdx.y; sg < nseg; sg += gridDim.y) {
+    const int i = (int)(sg % Lc);
+    const u32 w = width[i];
+    const u64 q = load_prime(primes, i).q;
+    const u64* s = in + seg_word[sg];
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+      const u64 bit = (u64)c * w;
+      const u32 k = (u32)(bit >> 6), off = (u32)(bit & 63);
+      u64 v = s[k] >> off;
+      if (off + w > 64) v |= s[k + 1] << (64 - off);
+      v &= (w == 64) ? ~0ULL : ((1ULL << w) - 1);
+      if (v >= q) atomicOr(bad, 1);
+      dst[sg * N + c] = v;
+    }
+  }
+}
+
+static void wire_tables(he_context* c, int level, size_t B, int size, std::vector<u32>& width,
+                        std::vector<u64>& seg_word, u64& total_words) {
+  const int Lc = level + 1;
+  width.resize(Lc);
+  for (int i = 0; i < Lc; ++i) width[i] = (u32)c->hp.kbits[i];
+  seg_word.resize(B * size * Lc);
+  u64 off = 0;
+  for (size_t sg = 0; sg < seg_word.size(); ++sg) {
+    seg_word[sg] = off;
+    off += (u64)c->N * width[sg % Lc] / 64;
+  }
+  total_words = off;
+}
+
+size_t wire_payload_bytes(he_context* c, const he_ciphertext* ct) {
+  std::vector<u32> w;
+  std::vector<u64> sw;
+  u64 tot;
+  wire_tables(c, ct->level, ct->B, ct->size, w, sw, tot);
+  return tot * 8;
+}
+
+void wire_pack(he_context* c, const he_ciphertext* ct, u64* out_dev) {
+  std::vector<u32> w;
+  std::vector<u64> sw;
+  u64 tot;
+  wire_tables(c, ct->level, ct->B, ct->size, w, sw, tot);
+  Scratch dw(c, w.size() * 4), ds(c, sw.size() * 8);
+  HE_CK(cudaMemcpyAsync(dw.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  HE_CK(cudaMemcpyAsync(ds.p, sw.data(), sw.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  const size_t nseg = sw.size();
+  {
+    ProfScope ps_(c, "wire_pack", 8.0 * c->N * nseg + 8.0 * tot, 0);
+    k_wire_pack<<<dim3((c->N * 62 / 64 + 255) / 256, (unsigned)std::min<size_t>(nseg, 65535)), 256, 0, c->stream>>>(
+        ct->d, out_dev, dw.as<u32>(), ds.as<u64>(), c->N, ct->level + 1, nseg);
+  }
+  check_launch(c);
+  HE_CK(cudaStreamSynchronize(c->stream));   // the scratch tables are freed on return
+}
+
+he_ciphertext* wire_unpack(he_context* c, const u64* in_dev, size_t B, int size, int level, double scale) {
+  std::vector<u32> w;
+  std::vector<u64> sw;
+  u64 tot;
+  wire_tables(c, level, B, size, w, sw, tot);
+  Scratch dw(c, w.size() * 4), ds(c, sw.size() * 8), flag(c, 4);
+  HE_CK(cudaMemcpyAsync(dw.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  HE_CK(cudaMemcpyAsync(ds.p, sw.data(), sw.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
+  he_ciphertext* ct = ct_new(c, (int)B, size, level, scale);
+  const size_t nseg = sw.size();
+  {
+    ProfScope ps_(c, "wire_unpack", 8.0 * c->N * nseg + 8.0 * tot, 0);
+    k_wire_unpack<<<dim3((c->N + 255) / 256, (unsigned)std::min<size_t>(nseg, 65535)), 256, 0, c->stream>>>(
+        in_dev, ct->d, dw.as<u32>(), ds.as<u64>(), c->d_primes, c->N, level + 1, nseg, flag.as<int>());
+  }
+  check_launch(c);
+  int h = 0;
+  HE_CK(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  HE_CK(cudaStreamSynchronize(c->stream));
+  if (h) {
+    ct_free(ct);
+    throw HeError(HE_INVALID_ARGUMENT, "wire: residue not reduced mod its prime (corrupt payload)");
+  }
+  return ct;
+}
+
 // ======================================================== encode / decode ===
 // Canonical embedding (C6) with a length-M = N/2 complex FFT:
 //   encode  w_i = zeta^{-i} sum_r Z[r] omega^{-i r},  Z[r_j] = z_j,

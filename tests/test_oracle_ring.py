@@ -239,3 +239,24 @@ def test_sampler_statistics_and_determinism():
     assert int(u.max()) < ctx.q[0] and abs(u.astype(np.float64).mean() / ctx.q[0] - 0.5) < 0.01
     assert np.array_equal(ctx.sample_cdt(sid(9, 7, 0)), ctx.sample_cdt(sid(9, 7, 0)))
     assert not np.array_equal(ctx.sample_ternary(sid(P_ENC_V, 1, 0)), ctx.sample_ternary(sid(P_ENC_V, 2, 0)))
+
+
+# ------------------------------------------------------- wire format pin ---
+def test_wire_reference_packer_vs_bitstring():
+    """oracle/wire.py against an independent construction: each residue written as a w-bit
+    little-endian bit string, concatenated, packed with numpy.packbits(bitorder='little')."""
+    from oracle import wire
+    rng = np.random.default_rng(0)
+    primes = [(1 << 31) - 1, (1 << 26) - 5, (1 << 20) + 7]
+    N, level = 64, 2
+    w = np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in primes]) for _ in range(2)])[None]
+    blob = wire.pack(w, primes, level, 1.0)
+    bits = []
+    for p in range(2):
+        for i, q in enumerate(primes):
+            wd = int(q).bit_length()
+            for x in w[0, p, i]:
+                bits.extend((int(x) >> k) & 1 for k in range(wd))
+    ref = np.packbits(np.array(bits, dtype=np.uint8), bitorder="little").tobytes()
+    assert blob[wire.HEADER_BYTES:] == ref
+    assert blob[:8] == b"HECKKS01" and len(blob) == 64 + len(ref)
