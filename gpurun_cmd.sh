@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_wire.py -q -m gpu 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_circuits.py -q -m gpu 2>&1 | tail -25

@@ -178,7 +178,29 @@ he_status he_rescale(he_context* ctx, const he_ciphertext* a, he_ciphertext** ou
 /* rotate left by k (Galois automorphism 5^k + key switch). */
 he_status he_rotate(he_context* ctx, const he_ciphertext* a, int32_t k, he_ciphertext** out);
 
+/* Drop limbs above `level` (level <= ct level): the ciphertext mod Q_level
+ * decrypts to the same message; scale unchanged.  Used to align levels. */
+he_status he_mod_switch_to(he_context* ctx, const he_ciphertext* a, int level, he_ciphertext** out);
+
 /* ---- composite ops ----------------------------------- */
+/* Encrypted dot product (Table 5 "dot"): mul (at the lower
+ * level) -> relinearize -> rescale, then rotate-and-add by 1, 2, 4, ... < n:
+ * slot 0 holds sum_{i<n} a_i b_i (slots >= n must be zero).  Needs Galois keys
+ * for the powers of two below n. */
+he_status he_dot(he_context* ctx, const he_ciphertext* a, const he_ciphertext* b, int n, he_ciphertext** out);
+/* Encrypted x plain dot product (Table 5 "dot_plain"): z[n_s] encoded at q_l,
+ * mul_plain, rescale, the same rotate-and-add. */
+he_status he_dot_plain(he_context* ctx, const he_ciphertext* a, const double* z, size_t nz, int n,
+                       he_ciphertext** out);
+/* x^p with depth ceil(log2 p) (PAPER.md:58 "depth-optimal", :166): squares for
+ * x^(2^k), x^i = x^(2^k) x^(i-2^k) otherwise. */
+he_status he_power(he_context* ctx, const he_ciphertext* x, int p, he_ciphertext** out);
+/* sum_{i<=d} coeffs[i] x^i (Table 4 "polyval"); every term is
+ * formed at the level of x^d and rescaled once; the terms' tracked scales agree
+ * up to double rounding and are summed at the first term's scale. */
+he_status he_polyval(he_context* ctx, const he_ciphertext* x, const double* coeffs, int n_coeffs,
+                     he_ciphertext** out);
+
 /* Client-side im2col + vertical scan (C18), host only, float64: image
  * img[H][W] -> slots[n_s] with slot = tap * chunk + window, chunk = next
  * power of two >= #windows.  Writes *windows / *chunk if non-NULL. */

@@ -226,3 +226,86 @@ def deep_chain(ctx: OracleContext, ct: OCt, pts: np.ndarray, rot_steps=(1, 2, 4,
     for s in rot_steps:
         ct = ctx.add(ct, ctx.rotate(ct, s))
     return ct
+
+
+# ------------------------------------------- SURVEY 8(f) #2 / #4 circuits ---
+def mod_switch(ctx: OracleContext, ct: OCt, level: int) -> OCt:
+    """Drop limbs level+1..: the ciphertext mod Q_level decrypts to the same message (|m| < Q_level/2);
+    the scale is unchanged."""
+    assert level <= ct.level
+    return OCt(ct.words[:, : level + 1].copy(), level, ct.scale)
+
+
+def mul_relin_rescale(ctx: OracleContext, a: OCt, b: OCt) -> OCt:
+    """ct x ct at the lower of the two levels: tensor, relinearize, rescale (C14)."""
+    lvl = min(a.level, b.level)
+    return ctx.rescale(ctx.relinearize(ctx.tensor(mod_switch(ctx, a, lvl), mod_switch(ctx, b, lvl))))
+
+
+def fold_sum(ctx: OracleContext, ct: OCt, n: int) -> OCt:
+    """Rotate-and-add by 1, 2, 4, ... < n (n rounded up to a power of two): slot 0 = sum of slots 0..n-1
+    (zeros beyond n)."""
+    s = 1
+    while s < n:
+        ct = ctx.add(ct, ctx.rotate(ct, s))
+        s <<= 1
+    return ct
+
+
+def dot(ctx: OracleContext, a: OCt, b: OCt, n: int) -> OCt:
+    """Encrypted dot product (Table 5 'dot'): sum_i a_i b_i into slot 0."""
+    return fold_sum(ctx, mul_relin_rescale(ctx, a, b), n)
+
+
+def dot_plain(ctx: OracleContext, a: OCt, z: np.ndarray, n: int) -> OCt:
+    """Encrypted x plain dot product (Table 5 'dot_plain'): z encoded at q_l so the rescale restores
+    the ciphertext scale."""
+    lvl = a.level
+    t = ctx.rescale(ctx.mul_plain(a, ctx.encode(z, float(ctx.q[lvl]), lvl)))
+    return fold_sum(ctx, t, n)
+
+
+def powers(ctx: OracleContext, x: OCt, d: int) -> dict:
+    """x^1..x^d at minimal depth: x^(2^k) by squaring; x^i = x^(2^k) * x^(i - 2^k), 2^k < i < 2^(k+1)
+    (depth ceil(log2 i), PAPER.md:58 'depth-optimal')."""
+    P = {1: x}
+    k = 1
+    while 2 * k <= d:
+        P[2 * k] = ctx.square(P[k])
+        k *= 2
+    for i in range(2, d + 1):
+        if i not in P:
+            hi = 1 << (i.bit_length() - 1)
+            P[i] = mul_relin_rescale(ctx, P[hi], P[i - hi])
+    return P
+
+
+def power(ctx: OracleContext, x: OCt, p: int) -> OCt:
+    return powers(ctx, x, p)[p]
+
+
+def polyval(ctx: OracleContext, x: OCt, coeffs) -> OCt:
+    """sum_i c_i x^i (Table 4 'polyval').  Every term c_i x^i (i >= 1) is formed at the
+    level l_d of x^d: mod-switch x^i to l_d, multiply by c_i encoded at scale S q_{l_d} / scale(x^i)
+    (S = scale of x^d), rescale -> level l_d - 1, scale ~= S.  The tracked scales of the terms agree
+    only up to double rounding, so the terms are summed at the first term's scale (DESIGN.md §3);
+    c_0 is added at that scale."""
+    coeffs = [float(c) for c in coeffs]
+    d = len(coeffs) - 1
+    assert d >= 1
+    P = powers(ctx, x, d)
+    ld, S = P[d].level, P[d].scale
+    acc = None
+    for i in range(1, d + 1):
+        if coeffs[i] == 0.0:
+            continue
+        xi = mod_switch(ctx, P[i], ld)
+        sc = S * float(ctx.q[ld]) / xi.scale
+        t = ctx.rescale(ctx.mul_plain(xi, ctx.encode(np.full(ctx.slots, coeffs[i]), sc, ld)))
+        if acc is None:
+            acc = t
+        else:
+            acc = OCt(ctx._pw(0, acc.words, t.words, acc.level), acc.level, acc.scale)
+    if coeffs[0] != 0.0:
+        acc = ctx.add_plain(acc, ctx.encode(np.full(ctx.slots, coeffs[0]), acc.scale, acc.level))
+    return acc

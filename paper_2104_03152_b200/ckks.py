@@ -75,6 +75,11 @@ _SIGS = {
     "he_rotate": [VP, VP, C.c_int32, VPP],
     "he_im2col_encode": [DP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, SZ, DP, C.POINTER(C.c_int),
                          C.POINTER(C.c_int)],
+    "he_mod_switch_to": [VP, VP, C.c_int, VPP],
+    "he_dot": [VP, VP, VP, C.c_int, VPP],
+    "he_dot_plain": [VP, VP, DP, SZ, C.c_int, VPP],
+    "he_power": [VP, VP, C.c_int, VPP],
+    "he_polyval": [VP, VP, DP, C.c_int, VPP],
     "he_im2col_encode_batch": [DP, SZ, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, SZ, DP],
     "he_im2col_conv": [VP, VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, VPP],
     "he_vec_mat": [VP, VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, VPP],
@@ -387,6 +392,18 @@ class Context:
     def he_relinearize(self, a): return self._ct2(lib().he_relinearize, a.h)
     def he_rescale(self, a): return self._ct2(lib().he_rescale, a.h)
     def he_rotate(self, a, k: int): return self._ct2(lib().he_rotate, a.h, int(k))
+
+    def he_mod_switch_to(self, a, level: int): return self._ct2(lib().he_mod_switch_to, a.h, int(level))
+    def he_dot(self, a, b, n: int): return self._ct2(lib().he_dot, a.h, b.h, int(n))
+    def he_power(self, a, p: int): return self._ct2(lib().he_power, a.h, int(p))
+
+    def he_dot_plain(self, a, z, n: int):
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        return self._ct2(lib().he_dot_plain, a.h, z.ctypes.data_as(DP), z.size, int(n))
+
+    def he_polyval(self, a, coeffs):
+        cf = np.ascontiguousarray(coeffs, dtype=np.float64)
+        return self._ct2(lib().he_polyval, a.h, cf.ctypes.data_as(DP), cf.size)
 
     def he_vec_mat(self, ct, W, bias=None, replicate_out=False, pt_scale_shift=0) -> Ciphertext:
         W = np.ascontiguousarray(W, dtype=np.float64)

@@ -427,6 +427,212 @@ he_status he_rotate(he_context* c, const he_ciphertext* a, int32_t k, he_ciphert
   });
 }
 
+// ------------------------------------------- level alignment + circuits ---
+namespace {
+struct CtGuard {
+  he_ciphertext* p = nullptr;
+  ~CtGuard() { ct_free(p); }
+  he_ciphertext* release() {
+    he_ciphertext* r = p;
+    p = nullptr;
+    return r;
+  }
+};
+
+he_ciphertext* mod_switch(he_context* c, const he_ciphertext* a, int level) {
+  he_ciphertext* o = ct_new(c, a->B, a->size, level, a->scale);
+  const size_t N8 = (size_t)c->N * 8;
+  HE_CK(cudaMemcpy2DAsync(o->d, (level + 1) * N8, a->d, (a->level + 1) * N8, (level + 1) * N8,
+                          (size_t)a->B * a->size, cudaMemcpyDeviceToDevice, c->stream));
+  return o;
+}
+
+// tensor -> relinearize -> rescale at the lower of the two levels (C14)
+he_ciphertext* mul_relin_rescale(he_context* c, const he_ciphertext* a, const he_ciphertext* b) {
+  const int lvl = std::min(a->level, b->level);
+  need(lvl >= 1, HE_LEVEL_EXHAUSTED, "multiplication needs a level to rescale");
+  CtGuard am, bm, t, r;
+  if (a->level != lvl) am.p = mod_switch(c, a, lvl);
+  if (b->level != lvl) bm.p = mod_switch(c, b, lvl);
+  t.p = ct_tensor(c, am.p ? am.p : a, bm.p ? bm.p : b);
+  r.p = ct_relinearize(c, t.p);
+  return ct_rescale(c, r.p);
+}
+
+// rotate-and-add by 1, 2, 4, ... < n
+he_ciphertext* fold_sum(he_context* c, he_ciphertext* t, int n) {
+  for (int s = 1; s < n; s <<= 1) {
+    he_ciphertext* u = ct_rotate(c, t, s, true);
+    ct_free(t);
+    t = u;
+  }
+  return t;
+}
+
+void need_fold_keys(he_context* c, int n) {
+  for (int s = 1; s < n; s <<= 1) {
+    u32 g;
+    need(galois_key(c, s, &g) != nullptr, HE_MISSING_GALOIS_KEY, "dot needs Galois keys for powers of two below n");
+  }
+}
+
+// x^1..x^d, depth-optimal (oracle circuits.powers)
+std::map<int, he_ciphertext*> powers(he_context* c, const he_ciphertext* x, int d) {
+  std::map<int, he_ciphertext*> P;
+  P[1] = nullptr;   // x itself (not owned)
+  auto get = [&](int i) -> const he_ciphertext* { return i == 1 ? x : P[i]; };
+  try {
+    for (int k = 1; 2 * k <= d; k *= 2) {
+      const he_ciphertext* base = get(k);
+      need(base->level >= 1, HE_LEVEL_EXHAUSTED, "power: levels exhausted");
+      CtGuard t, r;
+      t.p = ct_tensor(c, base, base);
+      r.p = ct_relinearize(c, t.p);
+      P[2 * k] = ct_rescale(c, r.p);
+    }
+    for (int i = 2; i <= d; ++i) {
+      if (P.count(i)) continue;
+      int hi = 1;
+      while (2 * hi <= i) hi *= 2;
+      P[i] = mul_relin_rescale(c, get(hi), get(i - hi));
+    }
+  } catch (...) {
+    for (auto& kv : P) ct_free(kv.second);
+    throw;
+  }
+  return P;
+}
+void free_powers(std::map<int, he_ciphertext*>& P) {
+  for (auto& kv : P) ct_free(kv.second);
+  P.clear();
+}
+}  // namespace
+
+he_status he_mod_switch_to(he_context* c, const he_ciphertext* a, int level, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    need(level >= 0 && level <= a->level, HE_LEVEL_MISMATCH, "target level must be in [0, ct level]");
+    *out = mod_switch(c, a, level);
+  });
+}
+
+he_status he_dot(he_context* c, const he_ciphertext* a, const he_ciphertext* b, int n, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_ct(c, b); need_out(out);
+    need(a->size == 2 && b->size == 2, HE_SHAPE_MISMATCH, "dot needs size-2 ciphertexts");
+    need(n >= 1 && n <= c->N / 2, HE_SHAPE_MISMATCH, "1 <= n <= n_s");
+    need_batch(a->B, b->B);
+    need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
+    need_fold_keys(c, n);
+    *out = fold_sum(c, mul_relin_rescale(c, a, b), n);
+  });
+}
+
+he_status he_dot_plain(he_context* c, const he_ciphertext* a, const double* z, size_t nz, int n,
+                       he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_out(out);
+    need(z != nullptr && nz <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "z must hold <= n_s values");
+    need(n >= 1 && n <= c->N / 2, HE_SHAPE_MISMATCH, "1 <= n <= n_s");
+    need(a->level >= 1, HE_LEVEL_EXHAUSTED, "dot_plain consumes one level");
+    need_fold_keys(c, n);
+    PtGuard pz;
+    {
+      DevDoubles d(c, z, nz);
+      pz.p = encode(c, d.d, nz, 1, (double)c->hp.q[a->level], a->level);
+    }
+    CtGuard m;
+    m.p = ct_mul_plain(c, a, pz.p);
+    he_ciphertext* t = ct_rescale(c, m.p);
+    *out = fold_sum(c, t, n);
+  });
+}
+
+he_status he_power(he_context* c, const he_ciphertext* x, int p, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, x); need_out(out);
+    need(x->size == 2, HE_SHAPE_MISMATCH, "power needs a size-2 ciphertext");
+    need(p >= 1, HE_INVALID_ARGUMENT, "p >= 1");
+    if (p == 1) {
+      *out = mod_switch(c, x, x->level);
+      return;
+    }
+    need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
+    int depth = 0;
+    while ((1 << depth) < p) ++depth;
+    need(x->level >= depth, HE_LEVEL_EXHAUSTED, "power: not enough levels");
+    auto P = powers(c, x, p);
+    he_ciphertext* r = P[p];
+    P[p] = nullptr;
+    free_powers(P);
+    *out = r;
+  });
+}
+
+he_status he_polyval(he_context* c, const he_ciphertext* x, const double* coeffs, int n_coeffs,
+                     he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, x); need_out(out);
+    need(coeffs != nullptr && n_coeffs >= 2, HE_INVALID_ARGUMENT, "need degree >= 1");
+    need(x->size == 2, HE_SHAPE_MISMATCH, "polyval needs a size-2 ciphertext");
+    const int d = n_coeffs - 1;
+    int depth = 0;
+    while ((1 << depth) < d) ++depth;
+    need(x->level >= depth + 1, HE_LEVEL_EXHAUSTED, "polyval: not enough levels");
+    need(d == 1 || c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
+    auto P = powers(c, x, d);
+    CtGuard acc;
+    try {
+      const he_ciphertext* xd = d == 1 ? x : P[d];
+      const int ld = xd->level;
+      const double S = xd->scale;
+      const int ns = c->N / 2;
+      for (int i = 1; i <= d; ++i) {
+        if (coeffs[i] == 0.0) continue;
+        const he_ciphertext* xi = i == 1 ? x : P[i];
+        CtGuard xm;
+        if (xi->level != ld) xm.p = mod_switch(c, xi, ld);
+        const he_ciphertext* xs = xm.p ? xm.p : xi;
+        const double sc = S * (double)c->hp.q[ld] / xs->scale;
+        std::vector<double> cv(ns, coeffs[i]);
+        PtGuard pc;
+        {
+          DevDoubles dd(c, cv.data(), cv.size());
+          pc.p = encode(c, dd.d, ns, 1, sc, ld);
+        }
+        CtGuard m;
+        m.p = ct_mul_plain(c, xs, pc.p);
+        he_ciphertext* t = ct_rescale(c, m.p);
+        if (!acc.p) {
+          acc.p = t;
+        } else {   // equal scales up to double rounding: summed at acc's scale
+          he_ciphertext* s2 = ct_binop(c, 0, acc.p, t);
+          ct_free(t);
+          ct_free(acc.p);
+          acc.p = s2;
+        }
+      }
+      need(acc.p != nullptr, HE_INVALID_ARGUMENT, "all non-constant coefficients are zero");
+      if (coeffs[0] != 0.0) {
+        std::vector<double> cv(ns, coeffs[0]);
+        PtGuard pc;
+        {
+          DevDoubles dd(c, cv.data(), cv.size());
+          pc.p = encode(c, dd.d, ns, 1, acc.p->scale, acc.p->level);
+        }
+        he_ciphertext* s2 = ct_add_plain(c, acc.p, pc.p);
+        ct_free(acc.p);
+        acc.p = s2;
+      }
+    } catch (...) {
+      free_powers(P);
+      throw;
+    }
+    free_powers(P);
+    *out = acc.release();
+  });
+}
+
 // ------------------------------------------------------------- composite ---
 he_status he_im2col_encode(const double* img, int H, int W, int kh, int kw, int stride, size_t n_slots,
                            double* slots_out, int* windows, int* chunk) {

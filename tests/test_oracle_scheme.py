@@ -270,3 +270,27 @@ def test_vec_mat_lazy_matches_matmul(rep):
     ref = x @ W + bias
     assert np.max(np.abs(y_lazy - ref)) < 1e-6
     assert np.max(np.abs(y_lazy - y_plain)) < 1e-6
+
+
+# ------------------------------------ SURVEY 8(f) #2/#4 circuit pins (float) ---
+def test_dot_power_polyval_circuits_vs_float():
+    """dot / dot_plain / power / polyval compositions decrypt to numpy's values (the definitions)."""
+    from oracle import circuits as OC
+    c = OracleContext(12, (60, 40, 40, 40, 60), 1, 7)
+    c.keygen([1, 2, 4, 8, 16, 32])
+    rng = np.random.default_rng(3)
+    n = 37
+    x, y = np.zeros(c.slots), np.zeros(c.slots)
+    x[:n], y[:n] = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    lvl = c.L - 1
+    cx, cy = c.encrypt(c.encode(x, 2.0 ** 40, lvl), 1), c.encrypt(c.encode(y, 2.0 ** 40, lvl), 2)
+    assert abs(c.decode(c.decrypt(OC.dot(c, cx, cy, n)), 1)[0] - x @ y) < 1e-6
+    assert abs(c.decode(c.decrypt(OC.dot_plain(c, cx, y, n)), 1)[0] - x @ y) < 1e-6
+    for p in (2, 3, 4):
+        r = OC.power(c, cx, p)
+        assert r.level == lvl - (p - 1).bit_length()          # depth ceil(log2 p)
+        assert np.max(np.abs(c.decode(c.decrypt(r), n) - x[:n] ** p)) < 1e-6
+    r = OC.polyval(c, cx, [0.0, 1.0, 2.0])                      # Table 4: 2x^2 + x
+    assert np.max(np.abs(c.decode(c.decrypt(r), n) - (2 * x[:n] ** 2 + x[:n]))) < 1e-6
+    r = OC.polyval(c, cx, [0.5, -1.0, 0.25, 0.125])
+    assert np.max(np.abs(c.decode(c.decrypt(r), n) - (0.5 - x[:n] + 0.25 * x[:n] ** 2 + 0.125 * x[:n] ** 3))) < 1e-6
