@@ -275,10 +275,12 @@ def micro_extra(ctx_cnn, stream, dev):
                              "mul_relin_rescale_per_s": round(Bc / s_mul, 1)}
     del c3, ct
     # config 1: one encrypted vec-mat (x 64 values replicated, W 64x10), batch 1: latency
-    from bench_configs import cfg1_latency, cfg5b_throughput
+    from bench_configs import cfg1_latency, cfg5b_throughput, table45_ops
     out["vecmat_cfg1"] = cfg1_latency(stream, t)
     # config 5b: deep chain, N=32768, 18+2 x 50-bit primes, 16 x (mul_plain + rescale) + 4 rotate-and-add
     out["deep_chain_cfg5b"] = cfg5b_throughput(stream, t, dev)
+    # PAPER.md Tables 4-5 op set at the paper's parameters (latency, one ciphertext)
+    out["ops_table45"] = table45_ops(stream, t)
     return out
 
 

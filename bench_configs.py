@@ -59,3 +59,44 @@ def cfg5b_throughput(stream, timer, dev, B: int = 512):
     return {"shape": "N=32768, 18+2 x 50-bit primes, scale 2^40, batch 512, 16 x (mul_plain+rescale) + 4 rotate-and-add",
             "ciphertexts_per_s": round(B / s, 1), "ms_per_batch": round(s * 1e3, 2),
             "rotations_per_s": round(B * 4 / s, 1)}
+
+
+# PAPER.md Tables 4-5 at shape 256 (c4.2xlarge, 8 vCPU; ms): context for the op latencies below
+PAPER_T45_MS = {"negate": 0.07, "square": 4.29, "polyval_2x2_x": 10.55, "add": 0.08, "multiply": 4.45,
+                "sub": 0.08, "dot": 20.15, "add_plain": 0.8, "multiply_plain": 1.75, "sub_plain": 0.8,
+                "dot_plain": 17.37}
+
+
+def table45_ops(stream, timer, batch: int = 1):
+    """The paper's unary/binary op benchmarks at its parameters: N=8192, a 200-bit
+    modulus ([60,40,40,60]: the same 200 bits), vector shape 256, one ciphertext; device-timed."""
+    from paper_2104_03152_b200 import Context
+    c = Context(13, (60, 40, 40, 60), 1, 11)
+    c.he_set_stream(stream)
+    c.he_keygen([1 << k for k in range(8)])
+    rng = np.random.default_rng(11)
+    n = 256
+    x, y = np.zeros((batch, c.slots)), np.zeros((batch, c.slots))
+    x[:, :n], y[:, :n] = rng.uniform(-1, 1, (batch, n)), rng.uniform(-1, 1, (batch, n))
+    lvl = c.L - 1
+    a, b = c.he_encrypt(c.he_encode(x, 2.0 ** 40, lvl), 0), c.he_encrypt(c.he_encode(y, 2.0 ** 40, lvl), batch)
+    pa = c.he_encode(y, 2.0 ** 40, lvl)
+    pm = c.he_encode(y, float(c.q[lvl]), lvl)
+    ops = {
+        "negate": lambda: c.he_negate(a),
+        "square": lambda: c.he_square(a),
+        "polyval_2x2_x": lambda: c.he_polyval(a, [0.0, 1.0, 2.0]),
+        "add": lambda: c.he_add(a, b),
+        "multiply": lambda: c.he_rescale(c.he_relinearize(c.he_mul(a, b))),
+        "sub": lambda: c.he_sub(a, b),
+        "dot": lambda: c.he_dot(a, b, n),
+        "add_plain": lambda: c.he_add_plain(a, pa),
+        "multiply_plain": lambda: c.he_rescale(c.he_mul_plain(a, pm)),
+        "sub_plain": lambda: c.he_add_plain(a, c.he_encode(-y, 2.0 ** 40, lvl)),
+        "dot_plain": lambda: c.he_dot_plain(a, y[0], n),
+    }
+    out = {"shape": f"N=8192, [60,40,40,60] (200-bit), vector 256, batch {batch}; paper = c4.2xlarge CPU ms"}
+    for k, f in ops.items():
+        s = timer(f, reps=20)
+        out[k] = {"ms": round(s * 1e3, 4), "paper_ms": PAPER_T45_MS[k]}
+    return out
