@@ -1,6 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench19.json 2> gpurun_out/bench19.err; echo bench rc=$?
-tail -3 gpurun_out/bench19.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench19.json'))
-print(d['value'], d['e2e']['value']); print(json.dumps(d['extra']['ops_table45'])); print(d['extra']['communication_cfg4'])"
+timeout 900 python -m pytest tests/test_gpu_edges.py -q -m gpu 2>&1 | tail -25
