@@ -309,3 +309,41 @@ def polyval(ctx: OracleContext, x: OCt, coeffs) -> OCt:
     if coeffs[0] != 0.0:
         acc = ctx.add_plain(acc, ctx.encode(np.full(ctx.slots, coeffs[0]), acc.scale, acc.level))
     return acc
+
+
+# ------------------------------------------ BSGS vec_mat ---
+def bsgs_diagonals(D: np.ndarray, g: int) -> np.ndarray:
+    """Baby-step/giant-step diagonals: E[k2][k1] = rot(D_{k1 + g k2}, -g k2) (zero past n), so that
+    rot(sum_k1 E[k2][k1] (.) rot(x, k1), g k2) = sum_k1 D_{k1 + g k2} (.) rot(x, k1 + g k2)."""
+    n, ns = D.shape
+    n2 = -(-n // g)
+    E = np.zeros((n2, g, ns))
+    for k2 in range(n2):
+        for k1 in range(g):
+            k = k1 + g * k2
+            if k < n:
+                E[k2, k1] = np.roll(D[k], g * k2)      # rot(v, -s) = np.roll(v, s)
+    return E
+
+
+def vec_mat_bsgs(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | None,
+                 replicate_out: bool, pt_scale_shift: int = 0, g: int = 64) -> OCt:
+    """vec_mat by baby steps k1 < g (one lazy-ModDown accumulation per giant step k2, all sharing the
+    rotations of x by k1) and giant steps (a full rotation of each inner sum by g k2), then one
+    rescale and the bias: sum_k2 rot(inner_k2, g k2) = sum_k D_k (.) rot(x, k) (C17)."""
+    ns = ctx.slots
+    D = vecmat_diagonals(W, ns, replicate_out)
+    E = bsgs_diagonals(D, g)
+    lvl = ct.level
+    pscale = _shifted(ctx.q[lvl], -pt_scale_shift)
+    acc = None
+    for k2 in range(E.shape[0]):
+        Eqp = np.stack([ctx.coeffs_to_pt_qp(ctx.encode_coeffs(E[k2, k1], pscale)[1], lvl) for k1 in range(g)])
+        inner = OCt(ctx.vec_mat_lazy_acc(ct, Eqp), lvl, ct.scale * pscale)
+        if k2:
+            inner = ctx.rotate(inner, g * k2)
+        acc = inner if acc is None else ctx.add(acc, inner)
+    acc = ctx.rescale(acc)
+    if bias is not None:
+        acc = ctx.add_plain(acc, ctx.encode(vecmat_bias_slots(bias, ns, replicate_out), acc.scale, acc.level))
+    return acc

@@ -294,3 +294,24 @@ def test_dot_power_polyval_circuits_vs_float():
     assert np.max(np.abs(c.decode(c.decrypt(r), n) - (2 * x[:n] ** 2 + x[:n]))) < 1e-6
     r = OC.polyval(c, cx, [0.5, -1.0, 0.25, 0.125])
     assert np.max(np.abs(c.decode(c.decrypt(r), n) - (0.5 - x[:n] + 0.25 * x[:n] ** 2 + 0.125 * x[:n] ** 3))) < 1e-6
+
+
+def test_vec_mat_bsgs_pins():
+    """BSGS vec_mat: with one giant step (g >= n) it IS vec_mat_lazy (word for word); otherwise it
+    decrypts to x @ W (float definition) like the other two forms."""
+    from oracle import circuits as OC
+    c = OracleContext(12, (60, 40, 40, 60), 1, 0)
+    n, m = 16, 16
+    c.keygen(range(1, n))
+    rng = np.random.default_rng(4)
+    x, W, bias = rng.uniform(-1, 1, n), rng.normal(0, 0.1, (n, m)), rng.normal(0, 0.1, m)
+    ct = c.encrypt(c.encode(OC.replicate(x, c.slots), 2.0 ** 40, 2), 3)
+    one = OC.vec_mat_bsgs(c, ct, W, bias, True, g=16)
+    assert np.array_equal(one.words, OC.vec_mat_lazy(c, ct, W, bias, True).words)
+    for g in (4, 8):
+        y = c.decode(c.decrypt(OC.vec_mat_bsgs(c, ct, W, bias, True, g=g)), m)
+        assert np.max(np.abs(y - (x @ W + bias))) < 1e-6
+    # E construction: rot(E[k2][k1], g k2) = D_{k1 + g k2}
+    D = OC.vecmat_diagonals(W, c.slots, True)
+    E = OC.bsgs_diagonals(D, 4)
+    assert np.array_equal(np.roll(E[2, 1], -8), D[9])
