@@ -254,6 +254,17 @@ he_status he_vec_mat_encode(he_context* ctx, const double* W, int n, int m, cons
 he_status he_vec_mat_encode_lazy(he_context* ctx, const double* W, int n, int m, const double* bias,
                                  int replicate_out, int pt_scale_shift, int level, double in_scale,
                                  he_plaintext** diags, he_plaintext** bias_pt);
+/* Baby-step/giant-step form: the QP diagonals are emitted in
+ * the order E[k2][k1] = rot(D_{k1 + g k2}, -g k2) (zero past n), G = ceil(n/g)
+ * <= 4 groups of g; he_vec_mat_pt (or he_vec_mat_bsgs_pt) then computes the
+ * inner product of each baby step rot(x, k1), k1 < g, once for all groups
+ * (one lazy ModDown per group) and adds rot(inner_k2, g k2) (oracle
+ * vec_mat_bsgs).  Needs Galois keys for 1..g-1 and g, 2g, ... */
+he_status he_vec_mat_encode_bsgs(he_context* ctx, const double* W, int n, int m, const double* bias,
+                                 int replicate_out, int pt_scale_shift, int level, double in_scale, int g,
+                                 he_plaintext** diags, he_plaintext** bias_pt);
+he_status he_vec_mat_bsgs_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* diags, int g,
+                             const he_plaintext* bias_pt, he_ciphertext** out);
 he_status he_im2col_conv_encode(he_context* ctx, const double* kernels, int n_channels, int kh, int kw,
                                 const double* bias, int chunk, int kernel_shift, int mask_shift,
                                 int level, double in_scale, he_plaintext** kernels_pt,

@@ -34,10 +34,12 @@ def rotation_steps(ns: int = 4096, chunk: int = CHUNK) -> list:
 class EncryptedCNN:
     """conv_w [4,1,7,7], conv_b [4], fc1_w [64,256], fc1_b [64], fc2_w [10,64], fc2_b [10] (PyTorch layouts)."""
 
-    def __init__(self, ctx: Context, w, plan=None, lazy: bool = True):
-        """lazy: FC1/FC2 with one ModDown per vec_mat (he_vec_mat_encode_lazy; oracle vec_mat_lazy),
-        else one ModDown per rotation (oracle vec_mat)."""
+    def __init__(self, ctx: Context, w, plan=None, lazy: bool = True, bsgs: bool = True):
+        """FC layers: bsgs (default) = baby-step/giant-step with lazy ModDown (oracle vec_mat_bsgs,
+        baby step n/4); lazy = one ModDown per vec_mat (oracle vec_mat_lazy); neither = one ModDown
+        per rotation (oracle vec_mat)."""
         self.ctx, self.plan, self.lazy = ctx, dict(plan or PLAN), lazy
+        self.bsgs = bsgs and lazy
         L = ctx.L
         self.top = L - 1
         in_scale = 2.0 ** self.plan["in_log2"]
@@ -50,14 +52,16 @@ class EncryptedCNN:
         lvl = self.top - 2
         s = s * s / ctx.q[lvl]          # square: tensor, relin, rescale
         lvl -= 1
+        g1 = np.asarray(w.fc1_w).shape[1] // 4 if self.bsgs else 0
         self.fc1_d, self.fc1_b = ctx.he_vec_mat_encode(np.asarray(w.fc1_w).T, w.fc1_b, True,
-                                                       -self.plan["fc1_shift"], lvl, s, lazy=lazy)
+                                                       -self.plan["fc1_shift"], lvl, s, lazy=lazy, bsgs_g=g1)
         s = s * self.fc1_d.scale / ctx.q[lvl]
         lvl -= 1
         s = s * s / ctx.q[lvl]
         lvl -= 1
+        g2 = np.asarray(w.fc2_w).shape[1] // 4 if self.bsgs else 0
         self.fc2_d, self.fc2_b = ctx.he_vec_mat_encode(np.asarray(w.fc2_w).T, w.fc2_b, False,
-                                                       self.plan["fc2_shift"], lvl, s, lazy=lazy)
+                                                       self.plan["fc2_shift"], lvl, s, lazy=lazy, bsgs_g=g2)
         self.n_out = int(np.asarray(w.fc2_w).shape[0])
 
     def im2col(self, imgs: np.ndarray) -> np.ndarray:

@@ -792,15 +792,29 @@ he_status he_vec_mat_pt(he_context* c, const he_ciphertext* ct, const he_plainte
 
 static void vecmat_encode(he_context* c, const double* W, int n, int m, const double* bias, int replicate_out,
                           int pt_scale_shift, int l, double in_scale, he_plaintext** dp, he_plaintext** bp,
-                          int qp = 0) {
+                          int qp = 0, int g = 0) {
   need(W != nullptr, HE_INVALID_ARGUMENT, "null matrix");
   need(l >= 1 && l < c->L, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
   const int ns = c->N / 2;
   std::vector<double> D = vecmat_diagonals(W, n, m, ns, replicate_out != 0);
+  int items = n;
+  if (g > 0) {   // BSGS order: E[k2][k1] = rot(D_{k1 + g k2}, -g k2), zero past n
+    const int n2 = (n + g - 1) / g;
+    std::vector<double> E((size_t)n2 * g * ns, 0.0);
+    for (int k2 = 0; k2 < n2; ++k2)
+      for (int k1 = 0; k1 < g; ++k1) {
+        const int k = k1 + g * k2;
+        if (k >= n) continue;
+        for (int j = 0; j < ns; ++j) E[((size_t)k2 * g + k1) * ns + (j + g * k2) % ns] = D[(size_t)k * ns + j];
+      }
+    D.swap(E);
+    items = n2 * g;
+  }
   PtGuard pd, pb;
   {
     DevDoubles d(c, D.data(), D.size());
-    pd.p = encode(c, d.d, ns, n, shifted(c->hp.q[l], -pt_scale_shift), l, qp);
+    pd.p = encode(c, d.d, ns, items, shifted(c->hp.q[l], -pt_scale_shift), l, qp);
+    pd.p->bsgs_g = g;
   }
   if (bias) {
     std::vector<double> bs(ns, 0.0);
@@ -834,6 +848,37 @@ he_status he_vec_mat_encode_lazy(he_context* c, const double* W, int n, int m, c
     need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
     need(c->K > 0, HE_INVALID_PARAMS, "lazy ModDown needs special primes");
     vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, level, in_scale, diags, bias_pt, 1);
+  });
+}
+
+he_status he_vec_mat_encode_bsgs(he_context* c, const double* W, int n, int m, const double* bias,
+                                 int replicate_out, int pt_scale_shift, int level, double in_scale, int g,
+                                 he_plaintext** diags, he_plaintext** bias_pt) {
+  return guard([&] {
+    need_ctx(c);
+    need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
+    need(c->K > 0, HE_INVALID_PARAMS, "lazy ModDown needs special primes");
+    need(g >= 1 && g <= n && (n + g - 1) / g <= 4, HE_SHAPE_MISMATCH, "baby step g: 1 <= g <= n, at most 4 giant steps");
+    vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, level, in_scale, diags, bias_pt, 1, g);
+  });
+}
+
+he_status he_vec_mat_bsgs_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags, int g,
+                             const he_plaintext* bias_pt, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_pt(c, diags); need_out(out);
+    need(diags->qp && c->K > 0, HE_LAYOUT_MISMATCH, "BSGS needs QP diagonals");
+    need(ct->size == 2 && ct->level >= 1, HE_LEVEL_EXHAUSTED, "vec_mat needs a size-2 ciphertext with a level");
+    need(diags->level == ct->level, HE_LEVEL_MISMATCH, "diagonals must be at the ciphertext level");
+    need(g >= 1 && diags->B % g == 0 && diags->B / g <= 4, HE_SHAPE_MISMATCH, "diags must be G <= 4 groups of g");
+    if (bias_pt) {
+      need_pt(c, bias_pt);
+      need_plain_q(bias_pt);
+      need(bias_pt->B == 1 && bias_pt->level == ct->level - 1, HE_LEVEL_MISMATCH, "bias at the rescaled level");
+      need(bias_pt->scale == ct->scale * diags->scale / (double)c->hp.q[ct->level], HE_SCALE_MISMATCH,
+           "bias scale must equal the output scale");
+    }
+    *out = ct_vec_mat_bsgs(c, ct, diags, g, bias_pt);
   });
 }
 

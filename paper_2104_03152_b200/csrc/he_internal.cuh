@@ -81,6 +81,7 @@ struct he_plaintext {
   he::u64* d;  // [B][level+1 (+K if qp)][N]
   int qp = 0;  // 1: also carries the K special limbs (data limbs first), for lazy-ModDown products
   uint32_t* dm = nullptr;  // small primes: cached Montgomery-form u32 copy (lazy vec_mat)
+  int bsgs_g = 0;          // > 0: vec_mat diagonals in baby-step/giant-step order E[k2][k1], baby step g
 };
 
 namespace he {

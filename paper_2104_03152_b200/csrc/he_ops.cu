@@ -598,6 +598,109 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
   }
 }
 
+// Baby-step/giant-step lazy accumulator (small primes): for baby steps k1 < g
+// the inner product of rot(x, k1) is computed ONCE and accumulated into all G
+// giant-step groups with their own (pre-rotated, Montgomery u32) diagonals
+// E[k2][k1]; P (.) c0 is staged so the c0 term joins before the diagonal:
+//   acc_p[k2] += E[k2][k1] (ip_p + [p = 0] P c0[pi_k1(n)]).
+// accx: [G][B][2][Lc+K][N] u32.  Two coefficients per thread (8-byte vectors).
+template <int LC, int G>
+__global__ void __launch_bounds__(LAZY_SM_T, 1)
+k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
+                   const PrimeD* __restrict__ primes) {
+  constexpr int V = 2;
+  extern __shared__ u32 xs[];
+  const int t = blockIdx.x, b = blockIdx.y, nt = LC + a.K;
+  const int tp = t < LC ? t : a.L + (t - LC);
+  const PrimeD P = load_prime(primes, tp);
+  const u32 q = (u32)P.q, qi = mont_neg_inv(q);
+  const u32 N = a.N, NP = a.NP;
+  const u64* c0 = a.ct + (size_t)b * 2 * LC * N;
+  const u64* c1 = c0 + (size_t)LC * N;
+  const bool data = t < LC;
+  const u32 Pm = (u32)((((u64)__ldg(a.P_mod + tp)) << 32) % q);
+#pragma unroll
+  for (int j = 0; j < LC; ++j) {
+    const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
+    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
+  }
+  u32* c0p = xs + LC * N;   // P c0[t] (plain residues)
+  if (data)
+    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) c0p[i] = redc32((u64)(u32)c0[(size_t)t * N + i] * Pm, q, qi);
+  __syncthreads();
+  const u32 keyrow = tp * N, kpart = NP * N, kdig = 2 * NP * N;
+  const size_t gstride = (size_t)g * nt * N;   // between giant-step groups in dm
+  for (u32 tile = 0; tile < N; tile += LAZY_SM_T * V) {
+    const u32 n0 = tile + threadIdx.x * V;
+    u32 acc0[G][V], acc1[G][V];
+#pragma unroll
+    for (int k2 = 0; k2 < G; ++k2) {
+      const uint2 d0 = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + (size_t)t * N + n0));
+      const u32 dd[V] = {d0.x, d0.y};
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        if (data) {   // k1 = 0: P E[k2][0] (.) c
+          acc0[k2][e] = redc32((u64)dd[e] * c0p[n0 + e], q, qi);
+          acc1[k2][e] = redc32((u64)dd[e] * redc32((u64)xs[t * N + n0 + e] * Pm, q, qi), q, qi);
+        } else {
+          acc0[k2][e] = acc1[k2][e] = 0;
+        }
+      }
+    }
+    for (int k = 1; k < g; ++k) {
+      const u32 gal = __ldg(a.gal + k);
+      const u32* key = keys32[k] + keyrow + n0;
+      u32 sn[V], y0[V], y1[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        sn[e] = galois_src(n0 + e, gal, a.logN);
+        y0[e] = data ? c0p[sn[e]] : 0u;
+        y1[e] = 0;
+      }
+#pragma unroll
+      for (int j = 0; j < LC; j += 2) {
+        const uint2 kb0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig));
+        const uint2 ka0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig + kpart));
+        uint2 kb1 = make_uint2(0, 0), ka1 = make_uint2(0, 0);
+        if (j + 1 < LC) {
+          kb1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig));
+          ka1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig + kpart));
+        }
+        const u32 b0[V] = {kb0.x, kb0.y}, a0[V] = {ka0.x, ka0.y}, b1[V] = {kb1.x, kb1.y}, a1[V] = {ka1.x, ka1.y};
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const u32 x0 = xs[j * N + sn[e]];
+          u64 s0 = (u64)x0 * b0[e], s1 = (u64)x0 * a0[e];
+          if (j + 1 < LC) {
+            const u32 x1 = xs[(j + 1) * N + sn[e]];
+            s0 += (u64)x1 * b1[e];
+            s1 += (u64)x1 * a1[e];
+          }
+          y0[e] = addq(y0[e], redc32(s0, q, qi), q);
+          y1[e] = addq(y1[e], redc32(s1, q, qi), q);
+        }
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < G; ++k2) {
+        const uint2 dv = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + ((size_t)k * nt + t) * N + n0));
+        const u32 dd[V] = {dv.x, dv.y};
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          acc0[k2][e] = addq(acc0[k2][e], redc32((u64)dd[e] * y0[e], q, qi), q);
+          acc1[k2][e] = addq(acc1[k2][e], redc32((u64)dd[e] * y1[e], q, qi), q);
+        }
+      }
+    }
+    u32* out = reinterpret_cast<u32*>(a.accx);
+#pragma unroll
+    for (int k2 = 0; k2 < G; ++k2) {
+      const size_t base = ((((size_t)k2 * gridDim.y + b) * 2) * nt + t) * N + n0;
+      *reinterpret_cast<uint2*>(out + base) = make_uint2(acc0[k2][0], acc0[k2][1]);
+      *reinterpret_cast<uint2*>(out + base + (size_t)nt * N) = make_uint2(acc1[k2][0], acc1[k2][1]);
+    }
+  }
+}
+
 // Fused ModUp + key inner product for small primes (a9 without materialising
 // the extended digits): CTA (target limb t, item b) loops over the digits j:
 // lift [d]_{q_j} (coefficients) into q_t (C16), 32-bit NTT in smem, then
@@ -1359,6 +1462,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
 
 he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                           const he_plaintext* bias) {
+  if (diags->bsgs_g > 0) return ct_vec_mat_bsgs(c, x, diags, diags->bsgs_g, bias);
   const int Lc = x->level + 1, n = diags->B, B = x->B;
   const size_t LN = (size_t)Lc * c->N;
   std::vector<const u64*> keys(n);
@@ -1444,6 +1548,131 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
     res = r2;
   }
   return res;
+}
+
+// BSGS vec_mat: diags = G groups of g QP diagonals E[k2][k1].
+he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags, int g,
+                               const he_plaintext* bias) {
+  const int Lc = x->level + 1, B = x->B, nt = Lc + c->K, G = diags->B / g;
+  const size_t N = c->N, LN = (size_t)Lc * N;
+  std::vector<const u64*> keys(g);
+  std::vector<u32> gals(g, 1);
+  for (int k = 1; k < g; ++k) {
+    keys[k] = galois_key(c, k, &gals[k]);
+    if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for baby step " + std::to_string(k));
+  }
+  for (int k2 = 1; k2 < G; ++k2) {
+    u32 gg;
+    if (!galois_key(c, g * k2, &gg))
+      throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for giant step " + std::to_string(g * k2));
+  }
+  std::vector<const u32*> keys32;
+  if (c->small_primes) {
+    keys32.push_back(nullptr);
+    for (int k = 1; k < g; ++k) {
+      auto it = c->gk32.find(gals[k]);
+      if (it == c->gk32.end()) break;
+      keys32.push_back(it->second);
+    }
+  }
+  const size_t smem = ((size_t)Lc + 1) * N * 4;
+  const bool fused = c->small_primes && keys32.size() == (size_t)g && smem <= 200 * 1024 && Lc <= 8 && G <= 4 &&
+                     N % (LAZY_SM_T * 2) == 0 && B <= 65535;
+  std::vector<he_ciphertext*> inner(G, nullptr);
+  auto cleanup = [&] {
+    for (auto* p : inner) ct_free(p);
+  };
+  try {
+    if (fused) {
+      if (!diags->dm) {
+        const size_t rows = (size_t)diags->B * nt;
+        u32* dmp = dalloc_t<u32>(c, rows * N);
+        k_to_mont32<<<dim3((unsigned)((N + 255) / 256), (unsigned)std::min<size_t>(rows, 65535)), 256, 0,
+                      c->stream>>>(diags->d, dmp, c->d_primes, (int)N, nt, Lc, c->L, rows);
+        check_launch(c);
+        const_cast<he_plaintext*>(diags)->dm = dmp;
+      }
+      Scratch kt(c, g * sizeof(u32*)), gt(c, g * sizeof(u32));
+      HE_CK(cudaMemcpyAsync(kt.p, keys32.data(), g * sizeof(u32*), cudaMemcpyHostToDevice, c->stream));
+      HE_CK(cudaMemcpyAsync(gt.p, gals.data(), g * sizeof(u32), cudaMemcpyHostToDevice, c->stream));
+      u64* ext = modup(c, x->d + LN, 2 * LN, B, Lc);
+      Scratch accx(c, (size_t)G * B * 2 * nt * N * 4);
+      try {
+        LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, ext, x->d, nullptr, nullptr, gt.as<u32>(), c->d_P_mod,
+                    accx.as<u64>()};
+        {
+          const double bytes = 8.0 * N * ((double)B * Lc * nt + 2.0 * B * Lc) + 4.0 * N * G * B * 2 * nt +
+                               4.0 * N * ((double)(g - 1) * 2 * Lc * nt + (double)G * g * nt);
+          const double ops = (double)B * (g - 1) * N * (nt * (2.0 * Lc + 2.0 * G) + Lc);
+          static const char* const tags[9] = {"vecmat_bsgs", "vecmat_bsgs_L1", "vecmat_bsgs_L2", "vecmat_bsgs_L3",
+                                              "vecmat_bsgs_L4", "vecmat_bsgs_L5", "vecmat_bsgs_L6", "vecmat_bsgs_L7",
+                                              "vecmat_bsgs_L8"};
+          ProfScope ps_(c, tags[Lc], bytes, B * nt, ops);
+          auto launch = [&](auto kern) {
+            HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, g, kt.as<const u32*>(), diags->dm, c->d_primes);
+          };
+#define HE_BSGS_CASE(LCV)                                                        \
+  case LCV:                                                                      \
+    if (G == 1) launch(k_vecmat_bsgs_mont<LCV, 1>);                              \
+    else if (G == 2) launch(k_vecmat_bsgs_mont<LCV, 2>);                         \
+    else if (G == 3) launch(k_vecmat_bsgs_mont<LCV, 3>);                         \
+    else launch(k_vecmat_bsgs_mont<LCV, 4>);                                     \
+    break;
+          switch (Lc) {
+            HE_BSGS_CASE(1) HE_BSGS_CASE(2) HE_BSGS_CASE(3) HE_BSGS_CASE(4)
+            HE_BSGS_CASE(5) HE_BSGS_CASE(6) HE_BSGS_CASE(7) default: HE_BSGS_CASE(8)
+          }
+#undef HE_BSGS_CASE
+        }
+        check_launch(c);
+        for (int k2 = 0; k2 < G; ++k2) {
+          inner[k2] = ct_new(c, B, 2, x->level, x->scale * diags->scale);
+          KsArgs a = ks_base(c, B, Lc, nullptr, nullptr, 0);
+          a.gal[0] = 1;
+          a.accx = reinterpret_cast<const u64*>(accx.as<u32>() + (size_t)k2 * B * 2 * nt * N);
+          a.accx32 = 1;
+          a.out = inner[k2]->d;
+          a.out_bs = 2 * LN;
+          ks_launch(c, a);
+        }
+      } catch (...) {
+        dfree(c, ext);
+        throw;
+      }
+      dfree(c, ext);
+    } else {   // generic: one lazy accumulation per giant step (no sharing of the baby-step products)
+      for (int k2 = 0; k2 < G; ++k2) {
+        he_plaintext view{c, g, diags->level, diags->scale, diags->d + (size_t)k2 * g * nt * N, 1};
+        std::vector<const u64*> kk(keys.begin(), keys.end());
+        inner[k2] = ct_vec_mat_lazy(c, x, &view, kk, gals);
+        dfree(c, view.dm);
+      }
+    }
+    // giant steps: acc = sum_k2 rot(inner_k2, g k2)
+    he_ciphertext* acc = inner[0];
+    inner[0] = nullptr;
+    for (int k2 = 1; k2 < G; ++k2) {
+      he_ciphertext* r = ct_rotate(c, inner[k2], g * k2, false);
+      ct_free(inner[k2]);
+      inner[k2] = nullptr;
+      he_ciphertext* s2 = ct_binop(c, 0, acc, r);
+      ct_free(r);
+      ct_free(acc);
+      acc = s2;
+    }
+    he_ciphertext* res = ct_rescale(c, acc);
+    ct_free(acc);
+    if (bias) {
+      he_ciphertext* r2 = ct_add_plain(c, res, bias);
+      ct_free(res);
+      res = r2;
+    }
+    return res;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
 }
 
 // im2col conv on the encrypted side (a15, C18/C19).

@@ -44,6 +44,8 @@ he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a);
 he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool add_input);
 he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                           const he_plaintext* bias);
+he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags, int g,
+                               const he_plaintext* bias);
 he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
                        const he_plaintext* masks, const he_plaintext* bias, int chunk);
 const u64* galois_key(he_context* c, int step, u32* gal_out);

@@ -36,10 +36,11 @@ def inj(g, o, vecs, scale, level):
     return g.he_pt_from_int_coeffs(ms, scale, level)
 
 
-@pytest.mark.parametrize("lazy", [False, True])
+@pytest.mark.parametrize("lazy", [False, True, "bsgs"])
 def test_cnn_layers_bit_exact(cfg4, lazy):
     """lazy=False: FC layers with one ModDown per rotation (oracle vec_mat); lazy=True: one
-    ModDown per vec_mat (oracle vec_mat_lazy, QP diagonals)."""
+    ModDown per vec_mat (oracle vec_mat_lazy, QP diagonals); "bsgs": baby step n/4 with one lazy
+    ModDown per giant step (oracle vec_mat_bsgs)."""
     o, g = cfg4
     w = cnn_weights(3)
     imgs = mnist_like_images(2, 4)
@@ -73,15 +74,22 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         lvl = ref[0].level
         ps = float(q[lvl]) * 2.0 ** (-shift)
         Dv = OC.vecmat_diagonals(Wm, ns, rep)
-        if lazy:
-            gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in Dv]), ps, lvl)
-        else:
-            gD = inj(g, o, Dv, ps, lvl)
         bs = ref[0].scale * ps / q[lvl]
         gb = inj(g, o, [OC.vecmat_bias_slots(bias, ns, rep)], bs, lvl - 1)
-        x = g.he_vec_mat_pt(x, gD, gb)
-        vm = OC.vec_mat_lazy if lazy else OC.vec_mat
-        ref = [vm(o, c, Wm, bias, rep, shift) for c in ref]
+        if lazy == "bsgs":
+            gg = Wm.shape[0] // 4
+            E = OC.bsgs_diagonals(Dv, gg).reshape(-1, ns)
+            gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in E]), ps, lvl)
+            x = g.he_vec_mat_bsgs_pt(x, gD, gg, gb)
+            ref = [OC.vec_mat_bsgs(o, c, Wm, bias, rep, shift, g=gg) for c in ref]
+        else:
+            if lazy:
+                gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in Dv]), ps, lvl)
+            else:
+                gD = inj(g, o, Dv, ps, lvl)
+            x = g.he_vec_mat_pt(x, gD, gb)
+            vm = OC.vec_mat_lazy if lazy else OC.vec_mat
+            ref = [vm(o, c, Wm, bias, rep, shift) for c in ref]
         W = x.words()
         for b in range(2):
             assert np.array_equal(W[b], ref[b].words), (name, b)
@@ -95,13 +103,13 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         assert np.allclose(z[b], o.decode(o.decrypt(ref[b]), 10), rtol=1e-9, atol=1e-9)
 
 
-@pytest.mark.parametrize("lazy", [False, True])
+@pytest.mark.parametrize("lazy", [False, True, "bsgs"])
 def test_cnn_all_gpu_tolerance(cfg4, lazy):
     """Own encode/encrypt/decrypt/decode: logits within 5e-3 abs of float64, argmax equal."""
     from paper_2104_03152_b200.cnn import EncryptedCNN
     o, g = cfg4
     w = cnn_weights(3)
-    net = EncryptedCNN(g, w, lazy=lazy)
+    net = EncryptedCNN(g, w, lazy=bool(lazy), bsgs=(lazy == "bsgs"))
     imgs = mnist_like_images(16, 4)
     logits = net.decrypt(net.forward(net.encrypt(imgs, 1000)))
     for b, img in enumerate(imgs):

@@ -369,3 +369,34 @@ def test_small_prime_vec_mat_both_forms_bit_exact(small):
     for b in range(3):
         assert np.array_equal(plain[b], OC.vec_mat(o2, octs[b], W, None, True).words), b
         assert np.array_equal(lazy[b], OC.vec_mat_lazy(o2, octs[b], W, None, True).words), b
+
+
+@pytest.mark.parametrize("which", ["cfg1", "small"])
+def test_vec_mat_bsgs_bit_exact(which, cfg1, small):
+    """BSGS vec_mat vs the oracle's vec_mat_bsgs: 64-bit generic path (cfg1, n=64, g=16) and the
+    fused small-prime kernel (n=8, g=4), batch 2."""
+    if which == "cfg1":
+        o, g = cfg1
+        x, W = vecmat_inputs(0)
+        gg, rep, scale = 16, False, 2.0 ** 40
+    else:
+        from paper_2104_03152_b200 import Context
+        o = OracleContext(SMALL["logN"], SMALL["bits"], SMALL["K"], 31)
+        o.keygen(range(1, 8))
+        g = Context(SMALL["logN"], SMALL["bits"], SMALL["K"], 31)
+        g.he_keygen(range(1, 8))
+        rng = np.random.default_rng(8)
+        x, W = rng.uniform(-1, 1, 8), rng.normal(0, 0.1, (8, 8))
+        gg, rep, scale = 4, True, 2.0 ** 26
+    lvl = o.L - 1
+    xs = OC.replicate(x, o.slots)
+    octs = [oracle_ct(o, xs, scale, lvl, b) for b in range(2)]
+    ps = float(o.q[lvl])
+    E = OC.bsgs_diagonals(OC.vecmat_diagonals(W, o.slots, rep), gg).reshape(-1, o.slots)
+    gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in E]), ps, lvl)
+    out = g.he_vec_mat_bsgs_pt(g.he_ct_import_words(np.stack([c.words for c in octs]), lvl, scale), gD, gg)
+    Wo = out.words()
+    for b in range(2):
+        assert np.array_equal(Wo[b], OC.vec_mat_bsgs(o, octs[b], W, None, rep, g=gg).words), b
+    y = g.he_decode(g.he_decrypt(out), W.shape[1])
+    assert np.max(np.abs(y - x @ W)) < (1e-6 if which == "cfg1" else 5e-3)
