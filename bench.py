@@ -205,7 +205,7 @@ def run_ours(args, rank, world, local_rank):
         ct = ctx.he_encrypt(pt, 2_000_000 + i * B)
         logits_host[:] = ctx.he_decode(ctx.he_decrypt(net.forward(ct)), net.n_out)   # D2H inside
 
-    e2e_ms, _ = timed(step_e2e, args.steps, 1)
+    e2e_ms, _ = timed(step_e2e, args.steps, args.warmup)
     # communication per inference: serialized encrypted input + encrypted logits of one image
     one = ctx.he_encrypt(ctx.he_encode(slots_dev[0][:1], 2.0 ** net.plan["in_log2"], net.top), 7)
     up = len(ctx.he_ct_serialize(one))

@@ -253,8 +253,12 @@ __device__ __forceinline__ void gs_bfly32_lazy(u32& x, u32& y, u32 w, u32 wsh, u
   y = v * w - __umulhi(v, wsh) * q;              // [0, 2q)
 }
 
-template <int LOGN, bool INV, int LO, int NB, bool LAZY = false>
-__device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __restrict__ tw, u32 q) {
+// One pass over bits [LO, LO+NB) reading its inputs through ld(i) and writing its
+// outputs through st(i, v): shared memory for the inner passes; the job's
+// load (first forward pass) or the final scaling + store (last inverse pass)
+// when fused, which saves a shared-memory round trip and a barrier.
+template <int LOGN, bool INV, int LO, int NB, bool LAZY, class LD, class ST>
+__device__ __forceinline__ void ntt_pass32_io(u32 tid, const uint2* __restrict__ tw, u32 q, LD ld, ST st) {
   typedef NttGeom<LOGN, 1> G;
   constexpr int NG = 1 << (G::R - NB);
   constexpr int E = 1 << NB;
@@ -264,7 +268,7 @@ __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __rest
     const u32 base = ((g >> LO) << (LO + NB)) | (g & ((1u << LO) - 1u));
     u32 x[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = sm[spad32(base + (k << LO))];
+    for (int k = 0; k < E; ++k) x[k] = ld(base + (k << LO));
 #pragma unroll
     for (int ss = 0; ss < NB; ++ss) {
       const int b = INV ? LO + ss : LO + NB - 1 - ss;
@@ -285,20 +289,66 @@ __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __rest
       }
     }
 #pragma unroll
-    for (int k = 0; k < E; ++k) sm[spad32(base + (k << LO))] = x[k];
+    for (int k = 0; k < E; ++k) st(base + (k << LO), x[k]);
   }
 }
 
-template <int LOGN, bool INV, int P, bool LAZY = false>
+template <int LOGN, bool INV, int LO, int NB, bool LAZY = false>
+__device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __restrict__ tw, u32 q) {
+  ntt_pass32_io<LOGN, INV, LO, NB, LAZY>(
+      tid, tw, q, [&](u32 i) { return sm[spad32(i)]; }, [&](u32 i, u32 v) { sm[spad32(i)] = v; });
+}
+
+// Passes P0 .. PEND-1 (pass P covers bit group GP = INV ? P : NPASS-1-P).
+template <int LOGN, bool INV, int P, bool LAZY = false, int PEND = NttGeom<LOGN, 1>::NPASS>
 __device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, u32 q) {
   typedef NttGeom<LOGN, 1> G;
-  constexpr int GP = INV ? P : G::NPASS - 1 - P;
-  constexpr int LO = GP * G::R;
-  constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-  ntt_pass32<LOGN, INV, LO, NB, LAZY>(sm, tid, tw, q);
-  __syncthreads();
-  if constexpr (P + 1 < G::NPASS) ntt_passes32<LOGN, INV, P + 1, LAZY>(sm, tid, tw, q);
+  if constexpr (P < PEND) {
+    constexpr int GP = INV ? P : G::NPASS - 1 - P;
+    constexpr int LO = GP * G::R;
+    constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+    ntt_pass32<LOGN, INV, LO, NB, LAZY>(sm, tid, tw, q);
+    __syncthreads();
+    ntt_passes32<LOGN, INV, P + 1, LAZY, PEND>(sm, tid, tw, q);
+  }
 }
+
+// Forward transform whose first pass reads the input through ld(i) (no staging
+// of the input in shared memory); result left in sm (lazy range when q < 2^30).
+template <int LOGN, class LD>
+__device__ __forceinline__ void ntt_fwd32_from(u32* sm, u32 tid, const uint2* tw, u32 q, LD ld) {
+  typedef NttGeom<LOGN, 1> G;
+  constexpr int LO = (G::NPASS - 1) * G::R, NB = G::LOGNL - LO;
+  auto st = [&](u32 i, u32 v) { sm[spad32(i)] = v; };
+  if (q < (1u << 30)) {
+    ntt_pass32_io<LOGN, false, LO, NB, true>(tid, tw, q, ld, st);
+    __syncthreads();
+    ntt_passes32<LOGN, false, 1, true>(sm, tid, tw, q);
+  } else {
+    ntt_pass32_io<LOGN, false, LO, NB, false>(tid, tw, q, ld, st);
+    __syncthreads();
+    ntt_passes32<LOGN, false, 1, false>(sm, tid, tw, q);
+  }
+}
+
+// Inverse transform of the values in sm whose last pass hands each output,
+// scaled by N^{-1} (canonical), to st(i, v) instead of shared memory.
+template <int LOGN, class ST>
+__device__ __forceinline__ void ntt_inv32_to(u32* sm, u32 tid, const uint2* tw, u32 q, ST st) {
+  typedef NttGeom<LOGN, 1> G;
+  constexpr int LO = (G::NPASS - 1) * G::R, NB = G::LOGNL - LO;
+  const uint2 ni = __ldg(tw);
+  auto ld = [&](u32 i) { return sm[spad32(i)]; };
+  auto fin = [&](u32 i, u32 v) { st(i, shoup32(v, ni.x, ni.y, q)); };
+  if (q < (1u << 30)) {
+    ntt_passes32<LOGN, true, 0, true, G::NPASS - 1>(sm, tid, tw, q);
+    ntt_pass32_io<LOGN, true, LO, NB, true>(tid, tw, q, ld, fin);
+  } else {
+    ntt_passes32<LOGN, true, 0, false, G::NPASS - 1>(sm, tid, tw, q);
+    ntt_pass32_io<LOGN, true, LO, NB, false>(tid, tw, q, ld, fin);
+  }
+}
+
 // Runs the lazy network when q < 2^30; outputs are then in [0, 4q) (forward) or
 // [0, 2q) (inverse) and must be reduced by the caller (ntt_reduce32).
 template <int LOGN, bool INV>

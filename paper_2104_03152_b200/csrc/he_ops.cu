@@ -750,9 +750,9 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
     } else {
       const u32* src = a.coef + ((size_t)b * a.Lc + j) * G::N;
       const u32 qj = (u32)__ldg(a.qtab + j);
-      for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = lift32(src[i], qj, q, mut);
-      __syncthreads();
-      ntt_run32<LOGN, false>(buf, tid, tw, q);   // values in [0, 4q) when q < 2^30: x k' < 4q^2 < q 2^32 still REDCs
+      // the lift feeds the first butterfly pass directly; values end in [0, 4q)
+      // when q < 2^30: x k' < 4q^2 < q 2^32 still REDCs
+      ntt_fwd32_from<LOGN>(buf, tid, tw, q, [&](u32 i) { return lift32(src[i], qj, q, mut); });
     }
     __syncthreads();
     // 4 consecutive coefficients per step: 16-byte key loads and accumulator updates
