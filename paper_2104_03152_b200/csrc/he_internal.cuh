@@ -58,7 +58,13 @@ struct he_context {
   he::u64* d_rlk = nullptr;  // [L][2][NP][N]
   uint32_t* d_rlk32 = nullptr;  // small primes: Montgomery-form u32 copy
   std::map<he::u64, he::u64*> gk;  // Galois element -> [L][2][NP][N]
-  std::map<he::u64, uint32_t*> gk32;  // small primes: the same keys as u32 in Montgomery form (k 2^32 mod q)
+  std::map<he::u64, uint32_t*> gk32;
+  // device tables indexed by rotation step k in [0, n_s]: Galois element and key
+  // pointers (null where no key), built at keygen so the vec_mat paths issue no
+  // host-to-device copies (a pageable copy may synchronise the stream)
+  uint32_t* d_step_gal = nullptr;
+  const he::u64** d_step_key = nullptr;
+  const uint32_t** d_step_key32 = nullptr;  // small primes: the same keys as u32 in Montgomery form (k 2^32 mod q)
   std::vector<void*> owned;        // device allocations freed with the context
   // opt-in profiler: CUDA events around every NTT-family launch
   struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; double ops; };

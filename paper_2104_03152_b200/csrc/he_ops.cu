@@ -1382,8 +1382,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
                                       const std::vector<const u64*>& keys, const std::vector<u32>& gals) {
   const int Lc = x->level + 1, n = diags->B, B = x->B, nt = Lc + c->K;
   const size_t LN = (size_t)Lc * c->N, N = c->N;
-  Scratch kt(c, n * sizeof(u64*)), gt(c, n * sizeof(u32)), k32t(c, n * sizeof(u32*));
-  HE_CK(cudaMemcpyAsync(kt.p, keys.data(), n * sizeof(u64*), cudaMemcpyHostToDevice, c->stream));
+  // steps 1..n-1: the per-step device tables built at keygen (no host copies here)
   std::vector<const u32*> keys32;
   if (c->small_primes) {
     keys32.push_back(nullptr);
@@ -1392,15 +1391,15 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
       if (it == c->gk32.end()) break;
       keys32.push_back(it->second);
     }
-    if (keys32.size() == (size_t)n)
-      HE_CK(cudaMemcpyAsync(k32t.p, keys32.data(), n * sizeof(u32*), cudaMemcpyHostToDevice, c->stream));
   }
-  HE_CK(cudaMemcpyAsync(gt.p, gals.data(), n * sizeof(u32), cudaMemcpyHostToDevice, c->stream));
+  const u64* const* kt = c->d_step_key;
+  const u32* const* k32t = c->d_step_key32;
+  const u32* gt = c->d_step_gal;
   u64* ext = n > 1 ? modup(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
   he_ciphertext* acc = nullptr;
   try {
     Scratch accx(c, (size_t)B * 2 * nt * N * 8);
-    LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, n, ext, x->d, diags->d, kt.as<const u64*>(), gt.as<u32>(),
+    LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, n, ext, x->d, diags->d, kt, gt,
                 c->d_P_mod, accx.as<u64>()};
     {
       // algorithmic bytes: ext + ct + accumulators once per item, keys and diagonals once per launch
@@ -1425,7 +1424,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
         }
         auto launch = [&](auto kern) {
           HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, k32t.as<const u32*>(), diags->dm, c->d_primes);
+          kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, k32t, diags->dm, c->d_primes);
         };
         switch (Lc) {
           case 1: launch(k_vecmat_lazy_mont<1>); break;
@@ -1592,13 +1591,12 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
         check_launch(c);
         const_cast<he_plaintext*>(diags)->dm = dmp;
       }
-      Scratch kt(c, g * sizeof(u32*)), gt(c, g * sizeof(u32));
-      HE_CK(cudaMemcpyAsync(kt.p, keys32.data(), g * sizeof(u32*), cudaMemcpyHostToDevice, c->stream));
-      HE_CK(cudaMemcpyAsync(gt.p, gals.data(), g * sizeof(u32), cudaMemcpyHostToDevice, c->stream));
+      const u32* const* kt = c->d_step_key32;   // baby steps 1..g-1 (keygen tables)
+      const u32* gt = c->d_step_gal;
       u64* ext = modup(c, x->d + LN, 2 * LN, B, Lc);
       Scratch accx(c, (size_t)G * B * 2 * nt * N * 4);
       try {
-        LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, ext, x->d, nullptr, nullptr, gt.as<u32>(), c->d_P_mod,
+        LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, ext, x->d, nullptr, nullptr, gt, c->d_P_mod,
                     accx.as<u64>()};
         {
           const double bytes = 8.0 * N * ((double)B * Lc * nt + 2.0 * B * Lc) + 4.0 * N * G * B * 2 * nt +
@@ -1610,7 +1608,7 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
           ProfScope ps_(c, tags[Lc], bytes, B * nt, ops);
           auto launch = [&](auto kern) {
             HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, g, kt.as<const u32*>(), diags->dm, c->d_primes);
+            kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, g, kt, diags->dm, c->d_primes);
           };
 #define HE_BSGS_CASE(LCV)                                                        \
   case LCV:                                                                      \
@@ -1819,6 +1817,30 @@ void keygen(he_context* c, const std::vector<int>& steps) {
         check_launch(c);
       }
     }
+  }
+  {   // per-step device tables
+    const int ns = N / 2;
+    std::vector<u32> sg(ns + 1);
+    std::vector<const u64*> sk(ns + 1, nullptr);
+    std::vector<const u32*> sk32(ns + 1, nullptr);
+    for (int k = 0; k <= ns; ++k) {
+      const u64 g = galois_element(N, k == 0 ? ns : k);
+      sg[k] = (u32)g;
+      auto it = c->gk.find(g);
+      if (it != c->gk.end()) sk[k] = it->second;
+      auto it32 = c->gk32.find(g);
+      if (it32 != c->gk32.end()) sk32[k] = it32->second;
+    }
+    sg[0] = 1;
+    HE_CK(cudaMalloc(&c->d_step_gal, sg.size() * 4));
+    HE_CK(cudaMalloc(&c->d_step_key, sk.size() * sizeof(u64*)));
+    HE_CK(cudaMalloc(&c->d_step_key32, sk32.size() * sizeof(u32*)));
+    HE_CK(cudaMemcpy(c->d_step_gal, sg.data(), sg.size() * 4, cudaMemcpyHostToDevice));
+    HE_CK(cudaMemcpy(c->d_step_key, sk.data(), sk.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+    HE_CK(cudaMemcpy(c->d_step_key32, sk32.data(), sk32.size() * sizeof(u32*), cudaMemcpyHostToDevice));
+    c->owned.push_back(c->d_step_gal);
+    c->owned.push_back((void*)c->d_step_key);
+    c->owned.push_back((void*)c->d_step_key32);
   }
   HE_CK(cudaStreamSynchronize(c->stream));
 }
