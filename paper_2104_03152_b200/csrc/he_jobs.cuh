@@ -74,6 +74,46 @@ struct JobSignedToNtt {
   }
 };
 
+// Fused encryption (C13, kernel K8): the small polynomial of one draw (v
+// ternary C10, e0 / e1 CDT C11) is sampled inside the transform's load from
+// Philox stream (purpose, stream_id + b), and the transform's store
+// accumulates it into the ciphertext:
+//   which 0 (v):  c0 = v b + m,  c1 = v a;   which 1 (e0): c0 += e0;   which 2 (e1): c1 += e1.
+struct JobEncrypt {
+  static constexpr const char* kName = "encrypt_ntt";
+  u64* ct;                 // [B][2][Lc][N]
+  const u64* pk;           // [2][L][N]
+  const u64* pt;           // [Bp][Lc][N]
+  size_t pt_bs;
+  const u64* cdt;          // 20-entry table
+  u64 seed, stream0;
+  int N, Lc, L, which;
+  __device__ int prime(int blk) const { return blk % Lc; }
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
+    const u64 obj = stream0 + (u64)(blk / Lc);
+    if (which == 0) return from_signed(sample_ternary(seed, stream_sid(PUR_ENC_V, obj, 0), n), P);
+    return from_signed(sample_cdt(seed, stream_sid(which == 1 ? PUR_ENC_E0 : PUR_ENC_E1, obj, 0), n, cdt), P);
+  }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
+    const int b = blk / Lc, i = blk % Lc;
+    const size_t LN = (size_t)Lc * N;
+    u64* c0 = ct + (size_t)b * 2 * LN + (size_t)i * N + n;
+    u64* c1 = c0 + LN;
+    if (which == 0) {
+      const u64 m = pt[(size_t)b * pt_bs + (size_t)i * N + n];
+      *c0 = add_mod(mul_mod(v, pk[(size_t)i * N + n], P), m, P.q);
+      *c1 = mul_mod(v, pk[((size_t)L + i) * N + n], P);
+    } else if (which == 1) {
+      *c0 = add_mod(*c0, v, P.q);
+    } else {
+      *c1 = add_mod(*c1, v, P.q);
+    }
+  }
+};
+inline double alg_bytes(const JobEncrypt& j, int nblk) {
+  return j.which == 0 ? 8.0 * j.N * nblk * 4 : 8.0 * j.N * nblk * 2;
+}
+
 // ModUp (a9, first half): digit j's coefficient residues [d]_{q_j} (already
 // INTT'd), centered lift (C16) into target t != j, NTT_t.
 //   coef: [B][Lc][N]; ext: [B][Lc][Lc+K][N] (t < Lc data, t >= Lc special).

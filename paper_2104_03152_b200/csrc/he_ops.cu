@@ -1904,32 +1904,20 @@ void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n) {
 }
 
 he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
-  const int N = c->N, Lc = pt->level + 1, B = pt->B;
-  // small polys [which][B][N]: v (C10 ternary), e0, e1 (C11 CDT); item b uses stream stream_id + b
-  Scratch small(c, (size_t)3 * B * N * 8), noise(c, (size_t)B * 3 * Lc * N * 8);
-  const dim3 g((N + 255) / 256, std::min(B, 65535));
-  const u64 pur[3] = {PUR_ENC_V, PUR_ENC_E0, PUR_ENC_E1};
-  for (int w = 0; w < 3; ++w) {
-    {
-      ProfScope ps_(c, "sample_small", 0.0, 0);
-      k_sample_small<<<g, 256, 0, c->stream>>>(small.as<i64>() + (size_t)w * B * N, N, B, c->seed, pur[w], stream_id,
-                                              w == 0 ? 0 : 1, c->d_cdt);
-    }
-    check_launch(c);
-    // NTT into noise [b][w][Lc][N]
-    JobSignedToNtt j{small.as<i64>() + (size_t)w * B * N, noise.as<u64>() + (size_t)w * Lc * N, N, Lc, (size_t)N,
-                     (size_t)3 * Lc * N, Lc, c->L};
-    launch_ntt<false>(c, j, B * Lc);
-  }
+  // three transforms with the Philox draws in their loads and the ciphertext
+  // accumulation in their stores (JobEncrypt): v -> (v b + m, v a), + e0, + e1
+  const int Lc = pt->level + 1, B = pt->B;
   he_ciphertext* ct = ct_new(c, B, 2, pt->level, pt->scale);
-  const size_t rows = (size_t)B * Lc;
-  {
-    ProfScope ps_(c, "encrypt_combine", 0.0, 0);
-    k_encrypt_combine<<<rows_grid2(c, rows), 256, 0, c->stream>>>(noise.as<u64>(), c->d_pk, pt->d,
-                                                                 pt->B == 1 ? 0 : (size_t)Lc * N, ct->d, c->d_primes,
-                                                                 N, Lc, c->L, rows);
+  try {
+    for (int w = 0; w < 3; ++w) {
+      JobEncrypt j{ct->d, c->d_pk, pt->d, pt->B == 1 ? 0 : (size_t)Lc * c->N, c->d_cdt, c->seed, stream_id,
+                   c->N, Lc, c->L, w};
+      launch_ntt<false>(c, j, B * Lc);
+    }
+  } catch (...) {
+    ct_free(ct);
+    throw;
   }
-  check_launch(c);
   return ct;
 }
 
