@@ -158,8 +158,26 @@ def vec_mat_lazy(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | 
     return acc
 
 
+def hoisted_fold(ctx: OracleContext, t: OCt, chunk: int, n1: int) -> OCt:
+    """sum_{m < ns/chunk} rot(t, chunk m) as two hoisted lazy-ModDown sums (DESIGN.md §3 'hoisted
+    conv fold'): u = sum_{b < n1} rot(t, chunk b), then sum_{a < n2} rot(u, chunk n1 a), n1 n2 =
+    ns/chunk.  The diagonals are the plaintext polynomial 1 (the constant-1 slots encoded at scale 1,
+    i.e. m = 1 exactly), so the ciphertext scale is unchanged."""
+    n_chunks = ctx.slots // chunk
+    assert n_chunks % n1 == 0
+    n2 = n_chunks // n1
+    one = np.zeros((ctx.N,), dtype=np.int64)
+    one[0] = 1
+    for n, step in ((n1, chunk), (n2, chunk * n1)):
+        if n == 1:
+            continue
+        D = np.stack([ctx.coeffs_to_pt_qp(one, t.level)] * n)
+        t = OCt(ctx.vec_mat_lazy_acc(t, D, step), t.level, t.scale)
+    return t
+
+
 def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarray | None,
-                chunk: int, kernel_shift: int = 0, mask_shift: int = 0) -> OCt:
+                chunk: int, kernel_shift: int = 0, mask_shift: int = 0, fold_n1: int = 0) -> OCt:
     """Steps 12 (C18/C19): per channel t_c = rescale(ct * K_c), log2(#chunks)
     rounds t_c += rot(t_c, chunk 2^r); sum_c t_c * Mask_c; rescale; + bias."""
     ns = ctx.slots
@@ -169,8 +187,11 @@ def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarr
     for c in range(n_ch):
         K = conv_kernel_slots(kernels[c], chunk, ns)
         t = ctx.rescale(ctx.mul_plain(ct, ctx.encode(K, _shifted(ctx.q[lvl], kernel_shift), lvl)))
-        for step in conv_fold_steps(chunk, ns):
-            t = ctx.add(t, ctx.rotate(t, step))
+        if fold_n1:     # hoisted two-level fold (same sum, different rounding)
+            t = hoisted_fold(ctx, t, chunk, fold_n1)
+        else:           # log2(#chunks) rotate-and-add rounds
+            for step in conv_fold_steps(chunk, ns):
+                t = ctx.add(t, ctx.rotate(t, step))
         ts.append(t)
     lvl2 = ts[0].level
     acc = None
@@ -191,9 +212,14 @@ def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarr
 CNN_PLAN = dict(in_log2=30, conv_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=-4)
 
 
-def cnn_rotation_steps(ns: int = 4096, chunk: int = 64) -> list:
-    """A-rot: exactly the circuit's steps: FC1 1..255, FC2 1..63 and the conv fold."""
-    return sorted(set(range(1, 256)) | set(conv_fold_steps(chunk, ns)))
+def cnn_rotation_steps(ns: int = 4096, chunk: int = 64, fold_n1: int = 0) -> list:
+    """A-rot: exactly the circuit's steps: FC1 1..255, FC2 1..63 and the conv fold (log2 steps, or
+    chunk b and chunk n1 a for the hoisted fold)."""
+    steps = set(range(1, 256)) | set(conv_fold_steps(chunk, ns))
+    if fold_n1:
+        n2 = ns // chunk // fold_n1
+        steps |= {chunk * b for b in range(1, fold_n1)} | {chunk * fold_n1 * a for a in range(1, n2)}
+    return sorted(steps)
 
 
 def cnn_encrypt_input(ctx: OracleContext, img: np.ndarray, stream_id: int, plan=None) -> OCt:

@@ -950,7 +950,14 @@ void orc_divround(void* h, const int* keep, int nkeep, const int* drop, int ndro
 // diags: [n][l+1+K][N] NTT words, data limbs 0..l then the K special limbs.
 // Written unhoisted (phi_k applied to the ciphertext in the coefficient domain,
 // then the textbook key-switch digit lift), i.e. from the definitions.
+int orc_vec_mat_lazy_step(void* h, const uint64_t* ct, int level, const uint64_t* diags, int n, int step,
+                          uint64_t* out);
 int orc_vec_mat_lazy(void* h, const uint64_t* ct, int level, const uint64_t* diags, int n, uint64_t* out) {
+  return orc_vec_mat_lazy_step(h, ct, level, diags, n, 1, out);
+}
+// Same with diagonal k applied to rot(ct, k * step) (strided rotation sums).
+int orc_vec_mat_lazy_step(void* h, const uint64_t* ct, int level, const uint64_t* diags, int n, int step,
+                          uint64_t* out) {
   Ctx* c = (Ctx*)h;
   const int N = c->N, Lc = level + 1, lk = LK(*c), nt = Lc + c->K;
   const size_t P_ = (size_t)Lc * N;
@@ -976,7 +983,7 @@ int orc_vec_mat_lazy(void* h, const uint64_t* ct, int level, const uint64_t* dia
   std::vector<u64> phi(2 * P_), tmp(N), Dt(N);
   std::vector<std::vector<i64>> Dj(Lc, std::vector<i64>(N));
   for (int k = 1; k < n; ++k) {
-    const u64 g = galois_elt(*c, k);
+    const u64 g = galois_elt(*c, k * step);
     auto it = c->gk.find(g);
     if (it == c->gk.end()) return -1;
     const std::vector<u64>& ksk = it->second;

@@ -95,6 +95,8 @@ def lib():
                                         U64P]
         L.orc_rescale.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_int, U64P]
         L.orc_vec_mat_lazy.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, U64P, ctypes.c_int, U64P]
+        L.orc_vec_mat_lazy_step.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, U64P, ctypes.c_int, ctypes.c_int,
+                                            U64P]
         L.orc_coeffs_to_pt_qp.argtypes = [ctypes.c_void_p, I64P, ctypes.c_int, U64P]
         L.orc_divround.argtypes = [ctypes.c_void_p, IP, ctypes.c_int, IP, ctypes.c_int, U64P,
                                    U64P, U64P]
@@ -284,13 +286,14 @@ class OracleContext:
         self.lib.orc_coeffs_to_pt_qp(self.h, _p(m, I64P), level, _p(out, U64P))
         return out
 
-    def vec_mat_lazy_acc(self, ct: OCt, diags_qp: np.ndarray) -> np.ndarray:
-        """sum_k D_k (.) rot(ct, k) with one ModDown (see ckks_oracle.cpp orc_vec_mat_lazy);
+    def vec_mat_lazy_acc(self, ct: OCt, diags_qp: np.ndarray, step: int = 1) -> np.ndarray:
+        """sum_k D_k (.) rot(ct, k step) with one ModDown (see ckks_oracle.cpp orc_vec_mat_lazy);
         diags_qp: [n][level+1+K][N]. Returns [2][level+1][N] (not rescaled)."""
         d = _u64(diags_qp)
         w = _u64(ct.words)
         out = np.zeros((2, ct.level + 1, self.N), dtype=np.uint64)
-        if self.lib.orc_vec_mat_lazy(self.h, _p(w, U64P), ct.level, _p(d, U64P), d.shape[0], _p(out, U64P)) != 0:
+        if self.lib.orc_vec_mat_lazy_step(self.h, _p(w, U64P), ct.level, _p(d, U64P), d.shape[0], step,
+                                          _p(out, U64P)) != 0:
             raise KeyError("missing Galois key")
         return out
 

@@ -134,3 +134,16 @@ def test_oracle_cnn_end_to_end():
     ref = float_net_numpy(img, w)
     assert np.max(np.abs(z - ref)) < 5e-3
     assert np.argmax(z) == np.argmax(ref)
+
+
+def test_hoisted_fold_is_the_same_sum():
+    """The hoisted two-level fold sums rot(t, chunk m) over all m exactly like the log2 rotate-and-add
+    fold (slot simulator): 8 x 8 = 64 chunks."""
+    rng = np.random.default_rng(0)
+    t = rng.normal(size=NS)
+    ref = t.copy()
+    for step in C.conv_fold_steps(64, NS):
+        ref = ref + np.roll(ref, -step)
+    u = sum(np.roll(t, -64 * b) for b in range(8))
+    s = sum(np.roll(u, -512 * a) for a in range(8))
+    assert np.allclose(s, ref, atol=1e-9)

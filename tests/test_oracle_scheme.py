@@ -315,3 +315,24 @@ def test_vec_mat_bsgs_pins():
     D = OC.vecmat_diagonals(W, c.slots, True)
     E = OC.bsgs_diagonals(D, 4)
     assert np.array_equal(np.roll(E[2, 1], -8), D[9])
+
+
+def test_hoisted_fold_oracle_pins():
+    """Oracle hoisted fold: decrypts to the log2 fold's values (same sum), and with n1 = #chunks
+    (one level) on two chunks it equals a single lazy vec_mat with all-one diagonals."""
+    from oracle import circuits as OC
+    c = OracleContext(11, (50, 40, 40, 50), 1, 3)
+    chunk, ns = 64, 1024
+    c.keygen(sorted(set(OC.conv_fold_steps(chunk, ns)) | {64 * b for b in range(1, 4)} | {256 * a for a in range(1, 4)}))
+    z = np.random.default_rng(1).uniform(-1, 1, ns)
+    ct = c.encrypt(c.encode(z, 2.0 ** 30, 2), 0)
+    folded = ct
+    for step in OC.conv_fold_steps(chunk, ns):
+        folded = c.add(folded, c.rotate(folded, step))
+    h = OC.hoisted_fold(c, ct, chunk, 4)
+    assert h.level == ct.level and h.scale == ct.scale
+    # both forms compute the same sum of 16 rotated copies; their errors are CKKS noise only:
+    # fresh noise ~340 sqrt(N) / 2^30 ~ 1.4e-5 per slot, summed over 16 copies -> <= ~2e-4
+    ref = sum(np.roll(z, -64 * m) for m in range(16))
+    assert np.max(np.abs(c.decode(c.decrypt(h)) - ref)) < 2e-4
+    assert np.max(np.abs(c.decode(c.decrypt(folded)) - ref)) < 2e-4
