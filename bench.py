@@ -106,7 +106,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2104_03152_b200 import Context, he_im2col_encode_batch
-    from paper_2104_03152_b200.cnn import EncryptedCNN, rotation_steps
+    from paper_2104_03152_b200.cnn import FOLD_N1, EncryptedCNN, rotation_steps
     from paper_2104_03152_b200.dist import gather_to_rank0, max_over_ranks, shard_indices
     from synthetic import CFG4, cnn_weights, mnist_like_images
 
@@ -117,8 +117,8 @@ def run_ours(args, rank, world, local_rank):
 
     ctx = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
     ctx.he_set_stream(stream)
-    ctx.he_keygen(rotation_steps())
-    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed))
+    ctx.he_keygen(rotation_steps(fold_n1=FOLD_N1))
+    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed), fold_n1=FOLD_N1)
     ns = ctx.slots
 
     # this rank's shard of the image stream (image i depends only on (seed, i))
@@ -368,7 +368,8 @@ def main():
 
     config = {"workload": "BASELINE config 5 (config-4 CNN on seeded synthetic 28x28 images, sharded)",
               "network": "conv7x7s3x4 -> x^2 -> fc256x64 -> x^2 -> fc64x10 (PAPER.md:98)",
-              "ckks": "N=8192, primes [31,26x6,31], scale 2^26 (input 2^30), 259 Galois keys",
+              "ckks": "N=8192, primes [31,26x6,31], scale 2^26 (input 2^30), 267 Galois keys",
+              "evaluation": "conv: hoisted 8x8 lazy fold; FC: BSGS (baby step n/4) with lazy ModDown (DESIGN.md §3)",
               "batch_per_gpu": args.batch, "global_batch": args.batch * world,
               "step": "encode+encrypt+conv+square+fc1+square+fc2+decrypt+decode",
               "parallelism": f"dp{world} (independent images, no data-path collective)",

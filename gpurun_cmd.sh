@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_scheme.py tests/test_gpu_edges.py tests/test_gpu_configs.py -q -m gpu -k "encrypt or empty or ragged or cfg3" 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+for i in 1 2; do timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extra > gpurun_out/bench24_$i.json 2>gpurun_out/bench24.err; python -c "
+import json; d=json.load(open('gpurun_out/bench24_$i.json'))
+print(round(d['value']), round(d['e2e']['value']), d['ms_per_step'], d['roofline']['kernel'], d['roofline']['frac'])
+print({k:v['ms_per_step'] for k,v in list(d['breakdown'].items())[:12]})"; done
+tail -2 gpurun_out/bench24.err

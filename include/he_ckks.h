@@ -236,6 +236,13 @@ he_status he_im2col_conv_pt(he_context* ctx, const he_ciphertext* ct, const he_p
                             const he_plaintext* masks, const he_plaintext* bias_pt, int chunk,
                             he_ciphertext** out);
 
+/* Same with the fold computed as two hoisted lazy-ModDown rotation sums:
+ * u = sum_{b<n1} rot(t, chunk b), then sum_{a<n2} rot(u, chunk n1 a), n1 n2 =
+ * n_s / chunk (the same sum as the log2 fold, rounded once per level; oracle
+ * circuits.hoisted_fold).  Needs keys for chunk b and chunk n1 a. */
+he_status he_im2col_conv_hoisted_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* kernels,
+                                    const he_plaintext* masks, const he_plaintext* bias_pt, int chunk, int n1,
+                                    he_ciphertext** out);
 /* Encode-once forms of the two composite ops' plaintexts (weights stay
  * resident on the device across batches; PAPER.md:98 excludes weight
  * preparation from the timed forward).  `level` / `in_scale` describe the

@@ -85,6 +85,7 @@ _SIGS = {
     "he_vec_mat": [VP, VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, VPP],
     "he_vec_mat_pt": [VP, VP, VP, VP, VPP],
     "he_im2col_conv_pt": [VP, VP, VP, VP, VP, C.c_int, VPP],
+    "he_im2col_conv_hoisted_pt": [VP, VP, VP, VP, VP, C.c_int, C.c_int, VPP],
     "he_vec_mat_encode": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
     "he_im2col_conv_encode": [VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_int,
                               C.c_double, VPP, VPP, VPP],
@@ -458,6 +459,11 @@ class Context:
         return self._ct2(lib().he_im2col_conv, ct.h, k.ctypes.data_as(DP), Cn, kh, kw,
                          None if b is None else b.ctypes.data_as(DP), int(chunk), int(kernel_shift),
                          int(mask_shift))
+
+    def he_im2col_conv_hoisted_pt(self, ct, kernels: Plaintext, masks: Plaintext, bias: Plaintext | None,
+                                  chunk: int, n1: int) -> Ciphertext:
+        return self._ct2(lib().he_im2col_conv_hoisted_pt, ct.h, kernels.h, masks.h,
+                         None if bias is None else bias.h, int(chunk), int(n1))
 
     def he_im2col_conv_pt(self, ct, kernels: Plaintext, masks: Plaintext, bias: Plaintext | None,
                           chunk: int) -> Ciphertext:

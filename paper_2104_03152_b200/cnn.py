@@ -21,24 +21,32 @@ KH = KW = 7
 STRIDE = 3
 
 
-def rotation_steps(ns: int = 4096, chunk: int = CHUNK) -> list:
-    """A-rot: FC1 diagonals 1..255 (FC2's 1..63 are a subset) and the conv fold chunk * 2^r."""
+FOLD_N1 = 8        # hoisted conv fold: 8 x 8 chunks
+
+
+def rotation_steps(ns: int = 4096, chunk: int = CHUNK, fold_n1: int = 0) -> list:
+    """A-rot: FC1 diagonals 1..255 (FC2's 1..63 are a subset) and the conv fold chunk * 2^r (plus
+    chunk b and chunk n1 a for the hoisted fold)."""
     fold = []
     s = chunk
     while s < ns:
         fold.append(s)
         s <<= 1
-    return sorted(set(range(1, 256)) | set(fold))
+    steps = set(range(1, 256)) | set(fold)
+    if fold_n1:
+        n2 = ns // chunk // fold_n1
+        steps |= {chunk * b for b in range(1, fold_n1)} | {chunk * fold_n1 * a for a in range(1, n2)}
+    return sorted(steps)
 
 
 class EncryptedCNN:
     """conv_w [4,1,7,7], conv_b [4], fc1_w [64,256], fc1_b [64], fc2_w [10,64], fc2_b [10] (PyTorch layouts)."""
 
-    def __init__(self, ctx: Context, w, plan=None, lazy: bool = True, bsgs: bool = True):
+    def __init__(self, ctx: Context, w, plan=None, lazy: bool = True, bsgs: bool = True, fold_n1: int = 0):
         """FC layers: bsgs (default) = baby-step/giant-step with lazy ModDown (oracle vec_mat_bsgs,
         baby step n/4); lazy = one ModDown per vec_mat (oracle vec_mat_lazy); neither = one ModDown
         per rotation (oracle vec_mat)."""
-        self.ctx, self.plan, self.lazy = ctx, dict(plan or PLAN), lazy
+        self.ctx, self.plan, self.lazy, self.fold_n1 = ctx, dict(plan or PLAN), lazy, fold_n1
         self.bsgs = bsgs and lazy
         L = ctx.L
         self.top = L - 1
@@ -76,7 +84,10 @@ class EncryptedCNN:
     def forward(self, ct):
         """Server side: conv -> square -> FC1 -> square -> FC2."""
         c = self.ctx
-        x = c.he_im2col_conv_pt(ct, self.conv_k, self.conv_m, self.conv_b, CHUNK)
+        if self.fold_n1:
+            x = c.he_im2col_conv_hoisted_pt(ct, self.conv_k, self.conv_m, self.conv_b, CHUNK, self.fold_n1)
+        else:
+            x = c.he_im2col_conv_pt(ct, self.conv_k, self.conv_m, self.conv_b, CHUNK)
         x = c.he_square(x)
         x = c.he_vec_mat_pt(x, self.fc1_d, self.fc1_b)
         x = c.he_square(x)

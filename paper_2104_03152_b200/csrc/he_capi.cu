@@ -675,8 +675,39 @@ static void conv_checks(he_context* c, const he_ciphertext* ct, int C, int taps,
   need(c->has_rlk || true, HE_MISSING_KEY, "");
 }
 
+static he_status conv_pt_impl(he_context* c, const he_ciphertext* ct, const he_plaintext* kernels,
+                              const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1,
+                              he_ciphertext** out);
+
 he_status he_im2col_conv_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* kernels,
                             const he_plaintext* masks, const he_plaintext* bias, int chunk, he_ciphertext** out) {
+  return conv_pt_impl(c, ct, kernels, masks, bias, chunk, 0, out);
+}
+
+he_status he_im2col_conv_hoisted_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* kernels,
+                                    const he_plaintext* masks, const he_plaintext* bias, int chunk, int n1,
+                                    he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c);
+    need(n1 >= 1 && chunk >= 1 && (c->N / 2 / chunk) % n1 == 0, HE_LAYOUT_MISMATCH, "n1 must divide n_s / chunk");
+    need(c->K > 0, HE_INVALID_PARAMS, "lazy ModDown needs special primes");
+    const int nc = c->N / 2 / chunk, n2 = nc / n1;
+    for (int b = 1; b < n1; ++b) {
+      u32 g;
+      need(galois_key(c, chunk * b, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * b");
+    }
+    for (int a = 1; a < n2; ++a) {
+      u32 g;
+      need(galois_key(c, chunk * n1 * a, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * n1 * a");
+    }
+    he_status st = conv_pt_impl(c, ct, kernels, masks, bias, chunk, n1, out);
+    if (st != HE_OK) throw HeError(st, he_last_error());
+  });
+}
+
+static he_status conv_pt_impl(he_context* c, const he_ciphertext* ct, const he_plaintext* kernels,
+                              const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1,
+                              he_ciphertext** out) {
   return guard([&] {
     need_ctx(c); need_ct(c, ct); need_pt(c, kernels); need_pt(c, masks); need_out(out);
     conv_checks(c, ct, kernels->B, 1, chunk);
@@ -694,11 +725,12 @@ he_status he_im2col_conv_pt(he_context* c, const he_ciphertext* ct, const he_pla
       const double s2 = s1 * masks->scale / (double)c->hp.q[ct->level - 1];
       need(bias->scale == s2, HE_SCALE_MISMATCH, "bias scale must equal the output scale");
     }
-    for (int step = chunk; step < c->N / 2; step <<= 1) {
-      u32 g;
-      need(galois_key(c, step, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
-    }
-    *out = ct_conv(c, ct, kernels, masks, bias, chunk);
+    if (fold_n1 == 0)
+      for (int step = chunk; step < c->N / 2; step <<= 1) {
+        u32 g;
+        need(galois_key(c, step, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
+      }
+    *out = ct_conv(c, ct, kernels, masks, bias, chunk, fold_n1);
   });
 }
 

@@ -397,8 +397,10 @@ struct LazyArgs {
   const u32* gal;               // [n]
   const u64* P_mod;             // [NP]
   u64* accx;                    // [B][2][Lc+K][N]
+  int step = 1;                 // diagonal k multiplies rot(x, k * step) (tables indexed by step)
 };
 constexpr int LAZY_EPT = 2;
+constexpr size_t kMaxSmem = 232448;   // opt-in dynamic shared memory per block on sm_100 (227 KB)
 // SMALL: every prime < 2^31, so a product of two residues is < 2^62 and up to
 // four products (plus a reduced value) sum without overflow in 64 bits: one
 // IMAD.WIDE.U32 per term and one reduction per four terms.
@@ -431,8 +433,8 @@ __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* _
     }
   }
   for (int k = 1; k < a.n; ++k) {
-    const u32 g = __ldg(a.gal + k);
-    const u64* key = a.keys[k];
+    const u32 g = __ldg(a.gal + k * a.step);
+    const u64* key = a.keys[k * a.step];
     const u64* Dk = a.diags + ((size_t)k * nt + t) * N;
 #pragma unroll
     for (int e = 0; e < LAZY_EPT; ++e) {
@@ -541,8 +543,8 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
       }
     }
     for (int k = 1; k < a.n; ++k) {
-      const u32 g = __ldg(a.gal + k);
-      const u32* key = keys32[k] + keyrow + n0;
+      const u32 g = __ldg(a.gal + k * a.step);
+      const u32* key = keys32[k * a.step] + keyrow + n0;
       const uint4 dv = __ldg(reinterpret_cast<const uint4*>(dm + ((u32)k * nt + t) * N + n0));
       const u32 dd[V] = {dv.x, dv.y, dv.z, dv.w};
       u32 sn[V];
@@ -648,8 +650,8 @@ k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, con
       }
     }
     for (int k = 1; k < g; ++k) {
-      const u32 gal = __ldg(a.gal + k);
-      const u32* key = keys32[k] + keyrow + n0;
+      const u32 gal = __ldg(a.gal + k * a.step);
+      const u32* key = keys32[k * a.step] + keyrow + n0;
       u32 sn[V], y0[V], y1[V];
 #pragma unroll
       for (int e = 0; e < V; ++e) {
@@ -1379,7 +1381,8 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
 // with all rotations hoisted (one ModUp of c1 shared by every k), then one
 // rescale and the bias.
 static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
-                                      const std::vector<const u64*>& keys, const std::vector<u32>& gals) {
+                                      const std::vector<const u64*>& keys, const std::vector<u32>& gals,
+                                      int step = 1) {
   const int Lc = x->level + 1, n = diags->B, B = x->B, nt = Lc + c->K;
   const size_t LN = (size_t)Lc * c->N, N = c->N;
   // steps 1..n-1: the per-step device tables built at keygen (no host copies here)
@@ -1400,7 +1403,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
   try {
     Scratch accx(c, (size_t)B * 2 * nt * N * 8);
     LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, n, ext, x->d, diags->d, kt, gt,
-                c->d_P_mod, accx.as<u64>()};
+                c->d_P_mod, accx.as<u64>(), step};
     {
       // algorithmic bytes: ext + ct + accumulators once per item, keys and diagonals once per launch
       const double bytes = 8.0 * N * ((double)B * Lc * nt + (double)B * 2 * Lc + (double)B * 2 * nt +
@@ -1412,8 +1415,8 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
                                           "vecmat_lazy_L8"};
       ProfScope ps_(c, tags[Lc <= 8 ? Lc : 0], bytes, B * nt, ops);
       const size_t smem = ((size_t)Lc + 1) * N * 4;
-      if (c->small_primes && smem <= 200 * 1024 && Lc <= 8 && keys32.size() == (size_t)n &&
-          N % (LAZY_SM_T * 4) == 0) {
+      if (c->small_primes && smem <= kMaxSmem && Lc <= 8 && keys32.size() == (size_t)n &&
+          N % (LAZY_SM_T * 4) == 0 && step == 1) {
         if (!diags->dm) {   // Montgomery u32 copy of the diagonals, cached on the plaintext
           const size_t rows = (size_t)n * nt;
           u32* dmp = dalloc_t<u32>(c, rows * N);
@@ -1423,7 +1426,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
           const_cast<he_plaintext*>(diags)->dm = dmp;
         }
         auto launch = [&](auto kern) {
-          HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
           kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, k32t, diags->dm, c->d_primes);
         };
         switch (Lc) {
@@ -1550,20 +1553,17 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
 }
 
 // BSGS vec_mat: diags = G groups of g QP diagonals E[k2][k1].
-he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags, int g,
-                               const he_plaintext* bias) {
+// Baby-step part: inner[k2] = ModDown(sum_{k1 < g} E[k2][k1] (.) rot(x, k1 step)) for the G
+// groups of diags (unrescaled, scale x.scale * diags.scale).
+static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
+                                              int g, int step) {
   const int Lc = x->level + 1, B = x->B, nt = Lc + c->K, G = diags->B / g;
   const size_t N = c->N, LN = (size_t)Lc * N;
   std::vector<const u64*> keys(g);
   std::vector<u32> gals(g, 1);
   for (int k = 1; k < g; ++k) {
-    keys[k] = galois_key(c, k, &gals[k]);
-    if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for baby step " + std::to_string(k));
-  }
-  for (int k2 = 1; k2 < G; ++k2) {
-    u32 gg;
-    if (!galois_key(c, g * k2, &gg))
-      throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for giant step " + std::to_string(g * k2));
+    keys[k] = galois_key(c, k * step, &gals[k]);
+    if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for baby step " + std::to_string(k * step));
   }
   std::vector<const u32*> keys32;
   if (c->small_primes) {
@@ -1575,7 +1575,7 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
     }
   }
   const size_t smem = ((size_t)Lc + 1) * N * 4;
-  const bool fused = c->small_primes && keys32.size() == (size_t)g && smem <= 200 * 1024 && Lc <= 8 && G <= 4 &&
+  const bool fused = c->small_primes && keys32.size() == (size_t)g && smem <= kMaxSmem && Lc <= 8 && G <= 4 &&
                      N % (LAZY_SM_T * 2) == 0 && B <= 65535;
   std::vector<he_ciphertext*> inner(G, nullptr);
   auto cleanup = [&] {
@@ -1597,7 +1597,7 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
       Scratch accx(c, (size_t)G * B * 2 * nt * N * 4);
       try {
         LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, ext, x->d, nullptr, nullptr, gt, c->d_P_mod,
-                    accx.as<u64>()};
+                    accx.as<u64>(), step};
         {
           const double bytes = 8.0 * N * ((double)B * Lc * nt + 2.0 * B * Lc) + 4.0 * N * G * B * 2 * nt +
                                4.0 * N * ((double)(g - 1) * 2 * Lc * nt + (double)G * g * nt);
@@ -1607,7 +1607,7 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
                                               "vecmat_bsgs_L8"};
           ProfScope ps_(c, tags[Lc], bytes, B * nt, ops);
           auto launch = [&](auto kern) {
-            HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
             kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, g, kt, diags->dm, c->d_primes);
           };
 #define HE_BSGS_CASE(LCV)                                                        \
@@ -1643,10 +1643,30 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
       for (int k2 = 0; k2 < G; ++k2) {
         he_plaintext view{c, g, diags->level, diags->scale, diags->d + (size_t)k2 * g * nt * N, 1};
         std::vector<const u64*> kk(keys.begin(), keys.end());
-        inner[k2] = ct_vec_mat_lazy(c, x, &view, kk, gals);
+        inner[k2] = ct_vec_mat_lazy(c, x, &view, kk, gals, step);
         dfree(c, view.dm);
       }
     }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  return inner;
+}
+
+he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags, int g,
+                               const he_plaintext* bias) {
+  const int G = diags->B / g;
+  for (int k2 = 1; k2 < G; ++k2) {
+    u32 gg;
+    if (!galois_key(c, g * k2, &gg))
+      throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for giant step " + std::to_string(g * k2));
+  }
+  std::vector<he_ciphertext*> inner = bsgs_inner(c, x, diags, g, 1);
+  auto cleanup = [&] {
+    for (auto* p : inner) ct_free(p);
+  };
+  try {
     // giant steps: acc = sum_k2 rot(inner_k2, g k2)
     he_ciphertext* acc = inner[0];
     inner[0] = nullptr;
@@ -1673,9 +1693,36 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
   }
 }
 
-// im2col conv on the encrypted side (a15, C18/C19).
+__global__ void k_fill_u64(u64* __restrict__ p, size_t n, u64 v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// sum_{k < n} rot(x, k step) with ONE lazy ModDown: the baby-step machinery with unit
+// diagonals (the plaintext polynomial 1, whose NTT words are all 1); scale unchanged.
+static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step) {
+  if (n == 1) {
+    he_ciphertext* o = ct_new(c, x->B, x->size, x->level, x->scale);
+    HE_CK(cudaMemcpyAsync(o->d, x->d, ct_words(x) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return o;
+  }
+  he_plaintext* ones = pt_new(c, n, x->level, 1.0, 1);
+  std::vector<he_ciphertext*> inner;
+  try {
+    k_fill_u64<<<148 * 4, 256, 0, c->stream>>>(ones->d, pt_words(ones), 1);
+    check_launch(c);
+    inner = bsgs_inner(c, x, ones, n, step);
+  } catch (...) {
+    pt_free(ones);
+    throw;
+  }
+  pt_free(ones);
+  return inner[0];
+}
+
+// im2col conv on the encrypted side (a15, C18/C19).  fold_n1 = 0: the paper's log2 rotate-and-add
+// fold; fold_n1 > 0: the same sum as two hoisted lazy rotation sums (n1 x n2 chunks).
 he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
-                       const he_plaintext* masks, const he_plaintext* bias, int chunk) {
+                       const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1) {
   const int Lc = x->level + 1, C = kernels->B, B = x->B;
   const size_t LN = (size_t)Lc * c->N;
   he_ciphertext* T = ct_new(c, B * C, 2, x->level, x->scale * kernels->scale);
@@ -1692,10 +1739,20 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
     ct_free(T);
     T = nullptr;
     const int ns = c->N / 2;
-    for (int step = chunk; step < ns; step <<= 1) {
-      he_ciphertext* t2 = ct_rotate(c, t, step, true);
+    if (fold_n1 > 0) {
+      const int n_chunks = ns / chunk, n2 = n_chunks / fold_n1;
+      he_ciphertext* t2 = ct_rot_sum(c, t, fold_n1, chunk);
       ct_free(t);
       t = t2;
+      t2 = ct_rot_sum(c, t, n2, chunk * fold_n1);
+      ct_free(t);
+      t = t2;
+    } else {
+      for (int step = chunk; step < ns; step <<= 1) {
+        he_ciphertext* t2 = ct_rotate(c, t, step, true);
+        ct_free(t);
+        t = t2;
+      }
     }
     const int Lc2 = t->level + 1;
     he_ciphertext* acc = ct_new(c, B, 2, t->level, t->scale * masks->scale);
