@@ -303,7 +303,7 @@ _ORACLE = {}
 
 
 def oracle_sample(images: int = 1, start: int = 10_000):
-    """Oracle CNN (encrypt + forward + decrypt, lazy-ModDown FC layers like the GPU default) on
+    """Oracle CNN (encrypt + forward + decrypt, the GPU arm's evaluation schedule) on
     `images` independent images, in parallel over host threads (the oracle's C calls release the
     GIL); returns (images/s, threads, seconds)."""
     from concurrent.futures import ThreadPoolExecutor
@@ -312,7 +312,7 @@ def oracle_sample(images: int = 1, start: int = 10_000):
     from synthetic import CFG4, cnn_weights, mnist_like_images
     if "o" not in _ORACLE:   # keys are made once (excluded from timing, like the GPU arm)
         o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-        o.keygen(OC.cnn_rotation_steps())
+        o.keygen(OC.cnn_rotation_steps(fold_n1=8))
         _ORACLE["o"] = o
     o = _ORACLE["o"]
     w = cnn_weights(CFG4.seed)
@@ -321,7 +321,8 @@ def oracle_sample(images: int = 1, start: int = 10_000):
 
     def one(i):
         ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + start + i)
-        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True)), 10)
+        # the same evaluation schedule as the GPU arm: hoisted 8 x 8 conv fold, BSGS FC layers
+        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True, bsgs=True, fold_n1=8)), 10)
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=min(images, cores)) as ex:

@@ -228,16 +228,22 @@ def cnn_encrypt_input(ctx: OracleContext, img: np.ndarray, stream_id: int, plan=
     return ctx.encrypt(ctx.encode(slots, 2.0 ** plan["in_log2"], ctx.L - 1), stream_id)
 
 
-def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False) -> OCt:
-    """The paper's network; lazy=True uses vec_mat_lazy for FC1/FC2."""
+def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False, bsgs: bool = False,
+                fold_n1: int = 0) -> OCt:
+    """The paper's network; lazy=True uses vec_mat_lazy for FC1/FC2, bsgs=True
+    vec_mat_bsgs (baby step n/4); fold_n1 > 0 the hoisted conv fold."""
     plan = plan or CNN_PLAN
-    vm = vec_mat_lazy if lazy else vec_mat
+
+    def vm(x, W, b, rep, shift):
+        if bsgs:
+            return vec_mat_bsgs(ctx, x, W, b, rep, shift, g=W.shape[0] // 4)
+        return (vec_mat_lazy if lazy else vec_mat)(ctx, x, W, b, rep, shift)
     x = im2col_conv(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64,
-                    plan["conv_shift"], plan["mask_shift"])
+                    plan["conv_shift"], plan["mask_shift"], fold_n1=fold_n1)
     x = ctx.square(x)
-    x = vm(ctx, x, w.fc1_w.T, w.fc1_b, replicate_out=True, pt_scale_shift=-plan["fc1_shift"])
+    x = vm(x, w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"])
     x = ctx.square(x)
-    x = vm(ctx, x, w.fc2_w.T, w.fc2_b, replicate_out=False, pt_scale_shift=-plan["fc2_shift"])
+    x = vm(x, w.fc2_w.T, w.fc2_b, False, -plan["fc2_shift"])
     return x
 
 

@@ -147,3 +147,18 @@ def test_hoisted_fold_is_the_same_sum():
     u = sum(np.roll(t, -64 * b) for b in range(8))
     s = sum(np.roll(u, -512 * a) for a in range(8))
     assert np.allclose(s, ref, atol=1e-9)
+
+
+@pytest.mark.slow
+def test_oracle_cnn_fast_schedule_end_to_end():
+    """The oracle with the bench's evaluation schedule (hoisted conv fold, BSGS FC layers) meets the
+    same 5e-3 / argmax bar against the float network."""
+    from oracle.oracle import OracleContext
+    w = cnn_weights(3)
+    img = mnist_like_images(1, 4, start=9)[0]
+    ctx = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    ctx.keygen(C.cnn_rotation_steps(fold_n1=8))
+    out = C.cnn_forward(ctx, C.cnn_encrypt_input(ctx, img, 0), w, lazy=True, bsgs=True, fold_n1=8)
+    z = ctx.decode(ctx.decrypt(out), 10)
+    ref = float_net_numpy(img, w)
+    assert np.max(np.abs(z - ref)) < 5e-3 and np.argmax(z) == np.argmax(ref)
