@@ -101,6 +101,15 @@ __device__ __forceinline__ u64 lift_centered(u64 r, u64 qj, const PrimeD& T) {
   return red ? T.q - red : 0;
 }
 
+// C16 centered lift of r < q_j into q_t with 32-bit arithmetic (q_j, q_t < 2^31):
+// [r]_t or q_t - [q_j - r]_t, each reduced by one umulhi Barrett (mut = floor(2^32 / q_t)).
+__device__ __forceinline__ u32 lift32(u32 r, u32 qj, u32 qt, u32 mut) {
+  const bool neg = r > (qj - 1) / 2;
+  const u32 m = neg ? qj - r : r;
+  const u32 v = min(m - __umulhi(m, mut) * qt, m - __umulhi(m, mut) * qt - qt);
+  return neg ? (v ? qt - v : 0u) : v;
+}
+
 // C8/a8: NTT-domain automorphism index.  out[j] = in[pi_g(j)] with
 // 2 brv(pi_g(j)) + 1 = g (2 brv(j) + 1) mod 2N.
 __device__ __forceinline__ u32 brv_bits(u32 x, int logN) { return __brev(x) >> (32 - logN); }

@@ -398,6 +398,7 @@ struct LazyArgs {
   const u64* P_mod;             // [NP]
   u64* accx;                    // [B][2][Lc+K][N]
   int step = 1;                 // diagonal k multiplies rot(x, k * step) (tables indexed by step)
+  const u32* ext32 = nullptr;   // small primes: the extended digits as u32 (replaces ext)
 };
 constexpr int LAZY_EPT = 2;
 constexpr size_t kMaxSmem = 232448;   // opt-in dynamic shared memory per block on sm_100 (227 KB)
@@ -517,8 +518,14 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
   const bool data = t < LC;
 #pragma unroll
   for (int j = 0; j < LC; ++j) {
-    const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
-    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
+    if (t == j || !a.ext32) {
+      const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
+      for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
+    } else {
+      const u32* src = a.ext32 + (((size_t)b * LC + j) * nt + t) * N;
+      for (u32 i = threadIdx.x * 4; i < N; i += LAZY_SM_T * 4)
+        *reinterpret_cast<uint4*>(xs + j * N + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+    }
   }
   u32* c0s = xs + LC * N;
   if (data)
@@ -623,8 +630,14 @@ k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, con
   const u32 Pm = (u32)((((u64)__ldg(a.P_mod + tp)) << 32) % q);
 #pragma unroll
   for (int j = 0; j < LC; ++j) {
-    const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
-    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
+    if (t == j || !a.ext32) {
+      const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
+      for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
+    } else {
+      const u32* src = a.ext32 + (((size_t)b * LC + j) * nt + t) * N;
+      for (u32 i = threadIdx.x * 4; i < N; i += LAZY_SM_T * 4)
+        *reinterpret_cast<uint4*>(xs + j * N + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+    }
   }
   u32* c0p = xs + LC * N;   // P c0[t] (plain residues)
   if (data)
@@ -709,15 +722,6 @@ k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, con
 // accx_p[t][n] += X_j[pi_g(n)] ksk[j][p][t][n] with the Montgomery-form key.
 // For j == t the digit is the NTT word itself (dsrc).  Output feeds the
 // accx-mode ModDown jobs.
-// C16 centered lift of r < q_j into q_t with 32-bit arithmetic (q_j, q_t < 2^31):
-// [r]_t or q_t - [q_j - r]_t, each reduced by one umulhi Barrett (mut = floor(2^32 / q_t)).
-__device__ __forceinline__ u32 lift32(u32 r, u32 qj, u32 qt, u32 mut) {
-  const bool neg = r > (qj - 1) / 2;
-  const u32 m = neg ? qj - r : r;
-  const u32 v = csub32(m - __umulhi(m, mut) * qt, qt);
-  return neg ? (v ? qt - v : 0u) : v;
-}
-
 struct FusedArgs {
   int N, logN, Lc, K, L, NP;
   u32 gal;
@@ -1216,6 +1220,20 @@ static u64* modup(he_context* c, const u64* dsrc, size_t bs, int B, int Lc) {
   return ext;
 }
 
+// Small-prime ModUp: u32 digits and u32 extended digits ([B][Lc][Lc+K][N] u32).
+static u32* modup32(he_context* c, const u64* dsrc, size_t bs, int B, int Lc) {
+  const size_t N = c->N;
+  Scratch coef(c, (size_t)B * Lc * N * 4);
+  {
+    JobLimbsTo32 j{dsrc, coef.as<u32>(), c->N, Lc, bs, (size_t)Lc * N};
+    launch_ntt<true>(c, j, B * Lc);
+  }
+  u32* ext = dalloc_t<u32>(c, (size_t)B * Lc * (Lc + c->K) * N);
+  JobModUp32 j{coef.as<u32>(), ext, c->d_q, c->N, Lc, c->K, c->L};
+  launch_ntt<false>(c, j, B * Lc * (Lc + c->K - 1));
+  return ext;
+}
+
 static KsArgs ks_base(he_context* c, int B, int Lc, const u64* ext, const u64* dsrc, size_t dsrc_bs) {
   KsArgs a;
   memset(&a, 0, sizeof(a));
@@ -1398,12 +1416,15 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
   const u64* const* kt = c->d_step_key;
   const u32* const* k32t = c->d_step_key32;
   const u32* gt = c->d_step_gal;
-  u64* ext = n > 1 ? modup(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
+  const bool smem_path = c->small_primes && ((size_t)Lc + 1) * N * 4 <= kMaxSmem && Lc <= 8 &&
+                         keys32.size() == (size_t)n && N % (LAZY_SM_T * 4) == 0 && step == 1;
+  u64* ext = (n > 1 && !smem_path) ? modup(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
+  u32* ext32 = (n > 1 && smem_path) ? modup32(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
   he_ciphertext* acc = nullptr;
   try {
     Scratch accx(c, (size_t)B * 2 * nt * N * 8);
     LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, n, ext, x->d, diags->d, kt, gt,
-                c->d_P_mod, accx.as<u64>(), step};
+                c->d_P_mod, accx.as<u64>(), step, ext32};
     {
       // algorithmic bytes: ext + ct + accumulators once per item, keys and diagonals once per launch
       const double bytes = 8.0 * N * ((double)B * Lc * nt + (double)B * 2 * Lc + (double)B * 2 * nt +
@@ -1415,8 +1436,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
                                           "vecmat_lazy_L8"};
       ProfScope ps_(c, tags[Lc <= 8 ? Lc : 0], bytes, B * nt, ops);
       const size_t smem = ((size_t)Lc + 1) * N * 4;
-      if (c->small_primes && smem <= kMaxSmem && Lc <= 8 && keys32.size() == (size_t)n &&
-          N % (LAZY_SM_T * 4) == 0 && step == 1) {
+      if (smem_path) {
         if (!diags->dm) {   // Montgomery u32 copy of the diagonals, cached on the plaintext
           const size_t rows = (size_t)n * nt;
           u32* dmp = dalloc_t<u32>(c, rows * N);
@@ -1455,10 +1475,12 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
     ks_launch(c, a);
   } catch (...) {
     dfree(c, ext);
+    dfree(c, ext32);
     ct_free(acc);
     throw;
   }
   dfree(c, ext);
+  dfree(c, ext32);
   return acc;
 }
 
@@ -1593,11 +1615,11 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
       }
       const u32* const* kt = c->d_step_key32;   // baby steps 1..g-1 (keygen tables)
       const u32* gt = c->d_step_gal;
-      u64* ext = modup(c, x->d + LN, 2 * LN, B, Lc);
+      u32* ext = modup32(c, x->d + LN, 2 * LN, B, Lc);
       Scratch accx(c, (size_t)G * B * 2 * nt * N * 4);
       try {
-        LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, ext, x->d, nullptr, nullptr, gt, c->d_P_mod,
-                    accx.as<u64>(), step};
+        LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, nullptr, x->d, nullptr, nullptr, gt, c->d_P_mod,
+                    accx.as<u64>(), step, ext};
         {
           const double bytes = 8.0 * N * ((double)B * Lc * nt + 2.0 * B * Lc) + 4.0 * N * G * B * 2 * nt +
                                4.0 * N * ((double)(g - 1) * 2 * Lc * nt + (double)G * g * nt);
