@@ -315,16 +315,27 @@ struct JobKsData {
   }
 };
 
+// Rescale source: row r of x, or (conv, C18) the product ct_b (.) K_c formed on
+// the fly for row r = (b C + c) 2 + p, so the products never reach HBM.
+struct RescaleSrc {
+  const u64* x;     // [R][Lc][N], or the ciphertexts [B][2][Lc][N] when K is set
+  const u64* K;     // nullable: [C][Lc][N] plaintexts
+  int C, N, Lc;
+  __device__ __forceinline__ u64 at(int r, int i, u32 n, const PrimeD& P) const {
+    if (!K) return x[((size_t)r * Lc + i) * N + n];
+    const int b = r / (2 * C), rem = r % (2 * C), c = rem >> 1, p = rem & 1;
+    return mul_mod(x[(((size_t)b * 2 + p) * Lc + i) * N + n], K[((size_t)c * Lc + i) * N + n], P);
+  }
+};
+
 // a11 rescale, step 1: INTT of the last limb l, y = [x_l + (q_l-1)/2]_{q_l}.
 struct JobRescaleLast {
   static constexpr const char* kName = "rescale_last";
-  const u64* x;     // [R][Lc][N] (R = B*size rows of polynomials)
+  RescaleSrc src;
   u64* y;           // [R][N]
   int N, Lc;
   __device__ int prime(int) const { return Lc - 1; }
-  __device__ u64 load(int blk, u32 n, const PrimeD&) const {
-    return x[((size_t)blk * Lc + Lc - 1) * N + n];
-  }
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const { return src.at(blk, Lc - 1, n, P); }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     y[(size_t)blk * N + n] = add_mod(v, (P.q - 1) >> 1, P.q);
   }
@@ -332,7 +343,7 @@ struct JobRescaleLast {
 // a11 rescale, step 2: out_i = (x_i - NTT_i([y]_{q_i} - [h]_{q_i})) [q_l^{-1}]_{q_i}.
 struct JobRescaleData {
   static constexpr const char* kName = "rescale_data";
-  const u64* x;
+  RescaleSrc src;
   const u64* y;
   u64* out;         // [R][Lc-1][N]
   const u64* h;     // [Lc-1] (q_l-1)/2 mod q_i   (row l of rs_h)
@@ -348,8 +359,7 @@ struct JobRescaleData {
   }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
-    const u64 xi = x[((size_t)r * Lc + i) * N + n];
-    const u64 t = sub_mod(xi, v, P.q);
+    const u64 t = sub_mod(src.at(r, i, n, P), v, P.q);
     out[((size_t)r * (Lc - 1) + i) * N + n] = mul_mod(t, __ldg(qinv + i), P);
   }
 };

@@ -1195,16 +1195,21 @@ he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphert
 }
 
 // ---- rescale (a11, C15) ----------------------------------------------------
-he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a) {
-  const int Lc = a->level + 1, l = a->level;
-  he_ciphertext* o = ct_new(c, a->B, a->size, l - 1, a->scale / (double)c->hp.q[l]);
-  const size_t R = (size_t)a->B * a->size;
+// rows R of polynomials at level l (src: rows of x, or ct (.) K products) -> out [R][l][N]
+static void rescale_rows(he_context* c, const RescaleSrc& src, size_t R, int l, u64* out) {
+  const int Lc = l + 1;
   Scratch y(c, R * c->N * 8);
-  JobRescaleLast j1{a->d, y.as<u64>(), c->N, Lc};
+  JobRescaleLast j1{src, y.as<u64>(), c->N, Lc};
   launch_ntt<true>(c, j1, (int)R);
-  JobRescaleData j2{a->d, y.as<u64>(), o->d, c->d_rs_h + (size_t)l * c->L, c->d_rs_qinv + (size_t)l * c->L,
-                    c->N, Lc};
+  JobRescaleData j2{src, y.as<u64>(), out, c->d_rs_h + (size_t)l * c->L, c->d_rs_qinv + (size_t)l * c->L, c->N, Lc};
   launch_ntt<false>(c, j2, (int)(R * (Lc - 1)));
+}
+
+he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a) {
+  const int l = a->level;
+  he_ciphertext* o = ct_new(c, a->B, a->size, l - 1, a->scale / (double)c->hp.q[l]);
+  RescaleSrc src{a->d, nullptr, 0, c->N, l + 1};
+  rescale_rows(c, src, (size_t)a->B * a->size, l, o->d);
   return o;
 }
 
@@ -1746,20 +1751,12 @@ static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, i
 he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
                        const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1) {
   const int Lc = x->level + 1, C = kernels->B, B = x->B;
-  const size_t LN = (size_t)Lc * c->N;
-  he_ciphertext* T = ct_new(c, B * C, 2, x->level, x->scale * kernels->scale);
-  const size_t rows = (size_t)B * C * 2 * Lc;
-  {
-    ProfScope ps_(c, "conv_mul_plain", 0.0, 0);
-    k_mul_plain_outer<<<rows_grid2(c, rows), 256, 0, c->stream>>>(x->d, kernels->d, T->d, c->d_primes, c->N, Lc, C,
-                                                                  rows);
-  }
-  check_launch(c);
-  he_ciphertext* t = nullptr;
+  // t_c = rescale(ct (.) K_c) for all (b, c): the products are formed inside the rescale (C18)
+  he_ciphertext* T = nullptr;
+  he_ciphertext* t = ct_new(c, B * C, 2, x->level - 1, (x->scale * kernels->scale) / (double)c->hp.q[x->level]);
   try {
-    t = ct_rescale(c, T);
-    ct_free(T);
-    T = nullptr;
+    RescaleSrc src{x->d, kernels->d, C, c->N, Lc};
+    rescale_rows(c, src, (size_t)B * C * 2, x->level, t->d);
     const int ns = c->N / 2;
     if (fold_n1 > 0) {
       const int n_chunks = ns / chunk, n2 = n_chunks / fold_n1;
