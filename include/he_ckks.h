@@ -44,6 +44,9 @@
  * Errors: every function returns he_status (0 = HE_OK).  On failure nothing
  * is written to the output pointers and he_last_error() returns a
  * thread-local message.  No C++ exception crosses this boundary.
+ *
+ * Threads: a context (and the handles made from it) is used by one host thread
+ * at a time; distinct contexts are independent.
  */
 #ifndef HE_CKKS_H_
 #define HE_CKKS_H_
@@ -120,6 +123,8 @@ he_status he_context_cdt(const he_context* ctx, uint64_t* table_out);
 /* Make all subsequent calls on ctx run on `stream` (a cudaStream_t, e.g. a
  * torch.cuda.Stream's cuda_stream).  NULL selects the legacy default stream. */
 he_status he_set_stream(he_context* ctx, void* stream);
+/* (Switching streams first synchronizes the old one: the context caches freed device
+ * scratch blocks by size and hands them to later work in stream order.) */
 /* Block until all work queued on the context's stream is done. */
 he_status he_sync(he_context* ctx);
 

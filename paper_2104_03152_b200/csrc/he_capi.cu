@@ -151,6 +151,8 @@ he_status he_context_cdt(const he_context* c, uint64_t* table_out) {
 he_status he_set_stream(he_context* c, void* stream) {
   return guard([&] {
     need_ctx(c);
+    // cached scratch blocks were last used on the old stream
+    if ((cudaStream_t)stream != c->stream) HE_CK(cudaStreamSynchronize(c->stream));
     c->stream = (cudaStream_t)stream;
   });
 }

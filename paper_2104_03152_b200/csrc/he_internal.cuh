@@ -66,6 +66,12 @@ struct he_context {
   const he::u64** d_step_key = nullptr;
   const uint32_t** d_step_key32 = nullptr;  // small primes: the same keys as u32 in Montgomery form (k 2^32 mod q)
   std::vector<void*> owned;        // device allocations freed with the context
+  // Stream-ordered caching allocator (he_ops.cu dalloc/dfree): freed blocks are kept in
+  // exact-size bins and reused by later work on c->stream (the steady-state pipeline asks for
+  // the same sizes every step; cudaMallocAsync growing its pool stalled the host 30-530 ms).
+  std::map<size_t, std::vector<void*>> free_bins;
+  std::map<void*, size_t> live_bytes;
+  size_t cached_bytes = 0;
   // opt-in profiler: CUDA events around every NTT-family launch
   struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; double ops; };
   bool prof_on = false;

@@ -318,11 +318,20 @@ struct JobKsData {
 // Rescale source: row r of x, or (conv, C18) the product ct_b (.) K_c formed on
 // the fly for row r = (b C + c) 2 + p, so the products never reach HBM.
 struct RescaleSrc {
-  const u64* x;     // [R][Lc][N], or the ciphertexts [B][2][Lc][N] when K is set
+  const u64* x;     // [R][Lc][N], or ciphertexts (see mask_sum / K)
   const u64* K;     // nullable: [C][Lc][N] plaintexts
   int C, N, Lc;
+  int mask_sum = 0; // 1: row r = b 2 + p is sum_c x[b C + c][p] (.) K_c (conv masks, C19)
   __device__ __forceinline__ u64 at(int r, int i, u32 n, const PrimeD& P) const {
     if (!K) return x[((size_t)r * Lc + i) * N + n];
+    if (mask_sum) {
+      const int b = r >> 1, p = r & 1;
+      u64 acc = 0;
+      for (int c = 0; c < C; ++c)
+        acc = add_mod(acc, mul_mod(x[((((size_t)b * C + c) * 2 + p) * Lc + i) * N + n], K[((size_t)c * Lc + i) * N + n], P),
+                      P.q);
+      return acc;
+    }
     const int b = r / (2 * C), rem = r % (2 * C), c = rem >> 1, p = rem & 1;
     return mul_mod(x[(((size_t)b * 2 + p) * Lc + i) * N + n], K[((size_t)c * Lc + i) * N + n], P);
   }

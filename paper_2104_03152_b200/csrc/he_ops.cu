@@ -11,19 +11,52 @@
 namespace he {
 
 // ======================================================== memory / setup ===
+// Blocks are binned by exact size (rounded to 512 B).  All kernels of a context run on
+// c->stream, so a block freed after enqueuing its last use can be handed to work enqueued
+// later on the same stream; he_set_stream synchronizes the old stream before switching.
+static size_t bin_size(size_t bytes) { return (std::max<size_t>(bytes, 8) + 511) & ~(size_t)511; }
+
+void trim_cache(he_context* c) {
+  if (c->free_bins.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->free_bins)
+    for (void* p : kv.second) cudaFree(p);
+  c->free_bins.clear();
+  c->cached_bytes = 0;
+}
+
 void* dalloc(he_context* c, size_t bytes) {
-  if (bytes == 0) bytes = 8;
+  const size_t sz = bin_size(bytes);
+  auto it = c->free_bins.find(sz);
+  if (it != c->free_bins.end() && !it->second.empty()) {
+    void* p = it->second.back();
+    it->second.pop_back();
+    c->cached_bytes -= sz;
+    c->live_bytes[p] = sz;
+    return p;
+  }
   void* p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes, c->stream);
+  cudaError_t e = cudaMalloc(&p, sz);
+  if (e == cudaErrorMemoryAllocation && c->cached_bytes) {
+    cudaGetLastError();
+    trim_cache(c);
+    e = cudaMalloc(&p, sz);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw HeError(e == cudaErrorMemoryAllocation ? HE_OUT_OF_MEMORY : HE_CUDA_ERROR,
-                  std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+                  std::string("cudaMalloc: ") + cudaGetErrorString(e));
   }
+  c->live_bytes[p] = sz;
   return p;
 }
 void dfree(he_context* c, void* p) {
-  if (p) cudaFreeAsync(p, c->stream);
+  if (!p) return;
+  auto it = c->live_bytes.find(p);
+  if (it == c->live_bytes.end()) return;
+  c->free_bins[it->second].push_back(p);
+  c->cached_bytes += it->second;
+  c->live_bytes.erase(it);
 }
 
 template <class T>
@@ -49,12 +82,6 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
     throw HeError(HE_CUDA_ERROR, "no CUDA device available (the library has no CPU fallback)");
   }
   HE_CK(cudaGetDevice(&c->device));
-  // keep freed blocks cached in the stream-ordered pool
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
-    u64 thr = ~0ULL;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
   std::vector<PrimeD> pd(c->NP);
   for (int t = 0; t < c->NP; ++t) {
     PrimeD& p = pd[t];
@@ -118,6 +145,9 @@ void context_destroy(he_context* c) {
   if (c->d_pk) cudaFree(c->d_pk);
   if (c->d_rlk) cudaFree(c->d_rlk);
   if (c->d_rlk32) cudaFree(c->d_rlk32);
+  trim_cache(c);
+  for (auto& kv : c->live_bytes) cudaFree(kv.first);
+  c->live_bytes.clear();
 }
 
 // ============================================================== handles ===
@@ -335,44 +365,7 @@ __global__ void k_accumulate(u64* __restrict__ acc, const u64* __restrict__ tmp,
   }
 }
 
-// conv (C18): T[b*C + c] = ct_b (.) K_c
-__global__ void k_mul_plain_outer(const u64* __restrict__ ct, const u64* __restrict__ K, u64* __restrict__ out,
-                                  const PrimeD* __restrict__ primes, int N, int Lc, int C, size_t rows) {
-  // rows = B * C * 2 * Lc
-  const size_t LN = (size_t)Lc * N;
-  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
-    const int i = (int)(r % Lc);
-    const int part = (int)((r / Lc) & 1);
-    const size_t bc = r / (2 * Lc);
-    const int c = (int)(bc % C);
-    const size_t b = bc / C;
-    const PrimeD P = load_prime(primes, i);
-    const u64* x = ct + b * 2 * LN + part * LN + (size_t)i * N;
-    const u64* k = K + c * LN + (size_t)i * N;
-    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
-      out[r * N + n] = mul_mod(x[n], k[n], P);
-  }
-}
 
-// conv (C19): out[b] = sum_c T[b*C + c] (.) M_c
-__global__ void k_mask_sum(const u64* __restrict__ T, const u64* __restrict__ M, u64* __restrict__ out,
-                           const PrimeD* __restrict__ primes, int N, int Lc, int C, size_t rows) {
-  // rows = B * 2 * Lc
-  const size_t LN = (size_t)Lc * N;
-  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
-    const int i = (int)(r % Lc);
-    const int part = (int)((r / Lc) & 1);
-    const size_t b = r / (2 * Lc);
-    const PrimeD P = load_prime(primes, i);
-    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-      u64 s = 0;
-      for (int c = 0; c < C; ++c)
-        s = add_mod(s, mul_mod(T[((b * C + c) * 2 + part) * LN + (size_t)i * N + n], M[c * LN + (size_t)i * N + n], P),
-                    P.q);
-      out[r * N + n] = s;
-    }
-  }
-}
 
 __global__ void k_check_words(const u64* __restrict__ w, const PrimeD* __restrict__ primes, int N, int Lc,
                               size_t rows, int* bad) {
@@ -1773,19 +1766,17 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
         t = t2;
       }
     }
-    const int Lc2 = t->level + 1;
-    he_ciphertext* acc = ct_new(c, B, 2, t->level, t->scale * masks->scale);
-    const size_t rows2 = (size_t)B * 2 * Lc2;
-    {
-      ProfScope ps_(c, "conv_mask_sum", 0.0, 0);
-      k_mask_sum<<<rows_grid2(c, rows2), 256, 0, c->stream>>>(t->d, masks->d, acc->d, c->d_primes, c->N, Lc2, C,
-                                                              rows2);
+    // sum_c t_c (.) Mask_c formed inside the second rescale (C19)
+    he_ciphertext* r = ct_new(c, B, 2, t->level - 1, (t->scale * masks->scale) / (double)c->hp.q[t->level]);
+    try {
+      RescaleSrc src{t->d, masks->d, C, c->N, t->level + 1, 1};
+      rescale_rows(c, src, (size_t)B * 2, t->level, r->d);
+    } catch (...) {
+      ct_free(r);
+      throw;
     }
-    check_launch(c);
     ct_free(t);
     t = nullptr;
-    he_ciphertext* r = ct_rescale(c, acc);
-    ct_free(acc);
     if (bias) {
       he_ciphertext* r2 = ct_add_plain(c, r, bias);
       ct_free(r);
