@@ -109,7 +109,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2104_03152_b200 import Context, he_im2col_encode_batch
-    from paper_2104_03152_b200.cnn import FOLD_N1, EncryptedCNN, rotation_steps
+    from paper_2104_03152_b200.cnn import CONV_G, EncryptedCNN, rotation_steps
     from paper_2104_03152_b200.dist import gather_to_rank0, max_over_ranks, shard_indices
     from synthetic import CFG4, cnn_weights, mnist_like_images
 
@@ -120,8 +120,8 @@ def run_ours(args, rank, world, local_rank):
 
     ctx = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
     ctx.he_set_stream(stream)
-    ctx.he_keygen(rotation_steps(fold_n1=FOLD_N1))
-    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed), fold_n1=FOLD_N1)
+    ctx.he_keygen(rotation_steps(conv_g=CONV_G, fc_bsgs=True))
+    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed), conv_g=CONV_G)
     ns = ctx.slots
 
     # this rank's shard of the image stream (image i depends only on (seed, i))
@@ -189,7 +189,7 @@ def run_ours(args, rank, world, local_rank):
                 "alg_ops_per_launch": alg_ops / n_l, "alg_bytes_per_launch": alg_b / n_l,
                 "hbm_achieved_GBps": round(gbs, 1), "hbm_peak_GBps": peaks["hbm_gbs"],
                 "hbm_frac": round(gbs / peaks["hbm_gbs"], 4),
-                "share_of_step": round(t_ms / 2 / prof_step_ms, 3), "us_per_launch": round(sec * 1e6, 2),
+                "share_of_step": round(t_ms / tot, 3), "us_per_launch": round(sec * 1e6, 2),
                 "peak_source": "ALU: derived (DESIGN.md §5: 12.8 modular ops/clk/SM x 148 x 1.965 GHz); HBM: "
                                + ("MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback")}
     breakdown = {k: {"launches_per_step": v[0] / 2, "ms_per_step": round(v[1] / 2, 3),
@@ -312,10 +312,11 @@ def oracle_sample(images: int = 1, start: int = 10_000):
     from concurrent.futures import ThreadPoolExecutor
     from oracle import circuits as OC
     from oracle.oracle import OracleContext
+    from paper_2104_03152_b200.cnn import CONV_G
     from synthetic import CFG4, cnn_weights, mnist_like_images
     if "o" not in _ORACLE:   # keys are made once (excluded from timing, like the GPU arm)
         o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-        o.keygen(OC.cnn_rotation_steps(fold_n1=8))
+        o.keygen(OC.cnn_rotation_steps(conv_g=CONV_G, fc_bsgs=True))
         _ORACLE["o"] = o
     o = _ORACLE["o"]
     w = cnn_weights(CFG4.seed)
@@ -323,9 +324,9 @@ def oracle_sample(images: int = 1, start: int = 10_000):
     cores = os.cpu_count() or 1
 
     def one(i):
-        ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + start + i)
-        # the same evaluation schedule as the GPU arm: hoisted 8 x 8 conv fold, BSGS FC layers
-        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True, bsgs=True, fold_n1=8)), 10)
+        ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + start + i, OC.CNN_PLAN_BSGS)
+        # the same evaluation schedule as the GPU arm: one-level conv, BSGS FC layers
+        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True, bsgs=True, conv_g=CONV_G)), 10)
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=min(images, cores)) as ex:
@@ -372,8 +373,9 @@ def main():
 
     config = {"workload": "BASELINE config 5 (config-4 CNN on seeded synthetic 28x28 images, sharded)",
               "network": "conv7x7s3x4 -> x^2 -> fc256x64 -> x^2 -> fc64x10 (PAPER.md:98)",
-              "ckks": "N=8192, primes [31,26x6,31], scale 2^26 (input 2^30), 267 Galois keys",
-              "evaluation": "conv: hoisted 8x8 lazy fold; FC: BSGS (baby step n/4) with lazy ModDown (DESIGN.md §3)",
+              "ckks": "N=8192, primes [31,26x6,31] (input at level 5, scale 2^30), 77 Galois keys",
+              "evaluation": "conv: one level, 8 baby x 8 giant chunk steps; FC: BSGS (baby step n/4); "
+                            "every rotation sum with one lazy ModDown (DESIGN.md §3)",
               "batch_per_gpu": args.batch, "global_batch": args.batch * world,
               "step": "encode+encrypt+conv+square+fc1+square+fc2+decrypt+decode",
               "parallelism": f"dp{world} (independent images, no data-path collective)",

@@ -248,6 +248,26 @@ he_status he_im2col_conv_pt(he_context* ctx, const he_ciphertext* ct, const he_p
 he_status he_im2col_conv_hoisted_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* kernels,
                                     const he_plaintext* masks, const he_plaintext* bias_pt, int chunk, int n1,
                                     he_ciphertext** out);
+/* One-level im2col conv (DESIGN.md §3 "conv as a baby-step/giant-step product";
+ * oracle circuits.im2col_conv_bsgs).  The paper's conv (C18/C19)
+ * is out = sum_c Mask_c (.) sum_{m < n_chunks} rot(ct (.) K_c, chunk m) + bias.
+ * Slot products commute with rotations of both factors and Mask_c has period
+ * C chunks, so with m = b + g a (C | g, g | n_chunks):
+ *   out = sum_{a < n2} rot(v, chunk g a) + bias,  v = sum_{b < g} D_b (.) rot(ct, chunk b),
+ *   D_b = sum_c Mask_c (.) rot(K_c, chunk b).
+ * he_im2col_conv_bsgs_encode: kernels [C][kh][kw] row-major float64, bias [C]
+ * (may be NULL); *diags = g QP plaintexts D_b at scale q_level 2^pt_shift,
+ * *bias_pt at level-1 and the output scale in_scale * diags.scale / q_level.
+ * he_im2col_conv_bsgs_pt: v by one lazy ModDown over the g baby steps, one
+ * rescale, the n2 giant steps as one hoisted unit-diagonal rotation sum, +
+ * bias.  Consumes ONE level (the paper's form consumes two).  Needs Galois
+ * keys for chunk b (b < g) and chunk g a (a < n2); errors as he_vec_mat_pt,
+ * HE_LAYOUT_MISMATCH if C does not divide g or g does not divide n_s / chunk. */
+he_status he_im2col_conv_bsgs_encode(he_context* ctx, const double* kernels, int C, int kh, int kw,
+                                     const double* bias, int chunk, int g, int pt_shift, int level,
+                                     double in_scale, he_plaintext** diags, he_plaintext** bias_pt);
+he_status he_im2col_conv_bsgs_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* diags,
+                                 const he_plaintext* bias_pt, int chunk, int g, he_ciphertext** out);
 /* Encode-once forms of the two composite ops' plaintexts (weights stay
  * resident on the device across batches; PAPER.md:98 excludes weight
  * preparation from the timed forward).  `level` / `in_scale` describe the

@@ -176,6 +176,56 @@ def hoisted_fold(ctx: OracleContext, t: OCt, chunk: int, n1: int) -> OCt:
     return t
 
 
+def rot_sum(ctx: OracleContext, t: OCt, n: int, step: int) -> OCt:
+    """sum_{k < n} rot(t, step k) with ONE lazy ModDown: the lazy vec_mat with unit diagonals (the
+    plaintext polynomial 1, i.e. the constant-1 slots encoded at scale 1, m = 1 exactly), so the
+    ciphertext scale is unchanged."""
+    if n == 1:
+        return t
+    one = np.zeros((ctx.N,), dtype=np.int64)
+    one[0] = 1
+    D = np.stack([ctx.coeffs_to_pt_qp(one, t.level)] * n)
+    return OCt(ctx.vec_mat_lazy_acc(t, D, step), t.level, t.scale)
+
+
+def conv_bsgs_diagonals(kernels: np.ndarray, chunk: int, ns: int, g: int) -> np.ndarray:
+    """D_b = sum_c Mask_c * rot(K_c, chunk b), b < g (slot vectors; rot = left rotation,
+    rot(v, k)[s] = v[s + k]).  Written from C18/C19: K_c and Mask_c as conv_kernel_slots /
+    conv_mask_slots."""
+    n_ch = kernels.shape[0]
+    D = np.zeros((g, ns))
+    for b in range(g):
+        for c in range(n_ch):
+            D[b] += conv_mask_slots(c, n_ch, chunk, ns) * np.roll(conv_kernel_slots(kernels[c], chunk, ns),
+                                                                  -chunk * b)
+    return D
+
+
+def im2col_conv_bsgs(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarray | None,
+                     chunk: int, g: int, pt_shift: int = 0) -> OCt:
+    """The im2col conv (C18/C19) as ONE level (DESIGN.md §3 'conv as a baby-step/giant-step
+    product').  The paper's result is out = sum_c Mask_c * sum_{m < n_chunks} rot(ct * K_c, chunk m)
+    (+ bias).  Slot products commute with rotations applied to both factors, and Mask_c has
+    period C chunks, so for C | g and m = b + g a:
+        out = sum_{a < n2} rot(v, chunk g a),  v = sum_{b < g} D_b * rot(ct, chunk b)
+    with D_b = conv_bsgs_diagonals.  v is the lazy vec_mat (one ModDown) with the g QP diagonals
+    D_b at scale q_l 2^pt_shift and rotation step chunk; rescale once; the giant steps are a
+    unit-diagonal rotation sum (rot_sum); + bias."""
+    ns = ctx.slots
+    n_ch = kernels.shape[0]
+    n_chunks = ns // chunk
+    assert g % n_ch == 0 and n_chunks % g == 0
+    lvl = ct.level
+    pscale = _shifted(ctx.q[lvl], pt_shift)
+    D = conv_bsgs_diagonals(kernels, chunk, ns, g)
+    Dqp = np.stack([ctx.coeffs_to_pt_qp(ctx.encode_coeffs(D[b], pscale)[1], lvl) for b in range(g)])
+    v = ctx.rescale(OCt(ctx.vec_mat_lazy_acc(ct, Dqp, chunk), lvl, ct.scale * pscale))
+    out = rot_sum(ctx, v, n_chunks // g, chunk * g)
+    if bias is not None:
+        out = ctx.add_plain(out, ctx.encode(conv_bias_slots(bias, chunk, ns), out.scale, out.level))
+    return out
+
+
 def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarray | None,
                 chunk: int, kernel_shift: int = 0, mask_shift: int = 0, fold_n1: int = 0) -> OCt:
     """Steps 12 (C18/C19): per channel t_c = rescale(ct * K_c), log2(#chunks)
@@ -210,36 +260,59 @@ def im2col_conv(ctx: OracleContext, ct: OCt, kernels: np.ndarray, bias: np.ndarr
 # Scale schedule of the CNN (R1/R2): log2 of the input scale and
 # the plaintext-scale shifts relative to the prime each following rescale drops.
 CNN_PLAN = dict(in_log2=30, conv_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=-4)
+# With the one-level conv (im2col_conv_bsgs) the input is encrypted one level lower (level L-2,
+# the circuit then ends at level 0) and the conv plaintext carries the whole conv shift; the final
+# scale is the same 2^22 (2 (2 (30 - 2) - 26 - 4) - 26 - 4 = 22).
+CNN_PLAN_BSGS = dict(in_log2=30, conv_shift=-2, fc1_shift=-4, fc2_shift=-4, in_level_drop=1)
+CONV_G = 8          # baby steps of the one-level conv: 8 chunks x 8 giant steps
 
 
-def cnn_rotation_steps(ns: int = 4096, chunk: int = 64, fold_n1: int = 0) -> list:
-    """A-rot: exactly the circuit's steps: FC1 1..255, FC2 1..63 and the conv fold (log2 steps, or
-    chunk b and chunk n1 a for the hoisted fold)."""
-    steps = set(range(1, 256)) | set(conv_fold_steps(chunk, ns))
-    if fold_n1:
-        n2 = ns // chunk // fold_n1
-        steps |= {chunk * b for b in range(1, fold_n1)} | {chunk * fold_n1 * a for a in range(1, n2)}
+def cnn_rotation_steps(ns: int = 4096, chunk: int = 64, fold_n1: int = 0, conv_g: int = 0,
+                       fc_bsgs: bool = False) -> list:
+    """A-rot: exactly the circuit's steps.  FC: 1..255 (FC2's 1..63 are a subset), or with
+    fc_bsgs the baby steps 1..g-1 and giant steps g k2 of FC1 (n 256, g 64) and FC2 (n 64, g 16).
+    Conv: the log2 fold steps chunk 2^r, or chunk b and chunk n1 a (hoisted fold, fold_n1), or
+    chunk b and chunk g a (one-level conv, conv_g)."""
+    if fc_bsgs:
+        steps = set()
+        for n in (256, 64):
+            g = n // 4
+            steps |= set(range(1, g)) | {g * k2 for k2 in range(1, (n + g - 1) // g)}
+    else:
+        steps = set(range(1, 256))
+    n1 = conv_g or fold_n1
+    if n1:
+        n2 = ns // chunk // n1
+        steps |= {chunk * b for b in range(1, n1)} | {chunk * n1 * a for a in range(1, n2)}
+    else:
+        steps |= set(conv_fold_steps(chunk, ns))
     return sorted(steps)
 
 
 def cnn_encrypt_input(ctx: OracleContext, img: np.ndarray, stream_id: int, plan=None) -> OCt:
     plan = plan or CNN_PLAN
     slots = im2col_slots(img, 7, 7, 3, ctx.slots)
-    return ctx.encrypt(ctx.encode(slots, 2.0 ** plan["in_log2"], ctx.L - 1), stream_id)
+    level = ctx.L - 1 - plan.get("in_level_drop", 0)
+    return ctx.encrypt(ctx.encode(slots, 2.0 ** plan["in_log2"], level), stream_id)
 
 
 def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False, bsgs: bool = False,
-                fold_n1: int = 0) -> OCt:
+                fold_n1: int = 0, conv_g: int = 0) -> OCt:
     """The paper's network; lazy=True uses vec_mat_lazy for FC1/FC2, bsgs=True
-    vec_mat_bsgs (baby step n/4); fold_n1 > 0 the hoisted conv fold."""
-    plan = plan or CNN_PLAN
+    vec_mat_bsgs (baby step n/4); fold_n1 > 0 the hoisted conv fold; conv_g > 0 the one-level
+    conv (im2col_conv_bsgs, plan CNN_PLAN_BSGS, input from cnn_encrypt_input with that plan)."""
+    plan = plan or (CNN_PLAN_BSGS if conv_g else CNN_PLAN)
 
     def vm(x, W, b, rep, shift):
         if bsgs:
             return vec_mat_bsgs(ctx, x, W, b, rep, shift, g=W.shape[0] // 4)
         return (vec_mat_lazy if lazy else vec_mat)(ctx, x, W, b, rep, shift)
-    x = im2col_conv(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64,
-                    plan["conv_shift"], plan["mask_shift"], fold_n1=fold_n1)
+    if conv_g:
+        x = im2col_conv_bsgs(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64, conv_g,
+                             plan["conv_shift"])
+    else:
+        x = im2col_conv(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64,
+                        plan["conv_shift"], plan["mask_shift"], fold_n1=fold_n1)
     x = ctx.square(x)
     x = vm(x, w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"])
     x = ctx.square(x)

@@ -86,6 +86,9 @@ _SIGS = {
     "he_vec_mat_pt": [VP, VP, VP, VP, VPP],
     "he_im2col_conv_pt": [VP, VP, VP, VP, VP, C.c_int, VPP],
     "he_im2col_conv_hoisted_pt": [VP, VP, VP, VP, VP, C.c_int, C.c_int, VPP],
+    "he_im2col_conv_bsgs_pt": [VP, VP, VP, VP, C.c_int, C.c_int, VPP],
+    "he_im2col_conv_bsgs_encode": [VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_double, VPP, VPP],
     "he_vec_mat_encode": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
     "he_im2col_conv_encode": [VP, DP, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_int,
                               C.c_double, VPP, VPP, VPP],
@@ -464,6 +467,21 @@ class Context:
                                   chunk: int, n1: int) -> Ciphertext:
         return self._ct2(lib().he_im2col_conv_hoisted_pt, ct.h, kernels.h, masks.h,
                          None if bias is None else bias.h, int(chunk), int(n1))
+
+    def he_im2col_conv_bsgs_encode(self, kernels, bias, chunk, g, pt_shift, level, in_scale):
+        """kernels [C][kh][kw] float64 -> (g QP diagonals D_b, bias plaintext or None)."""
+        k = np.ascontiguousarray(kernels, dtype=np.float64)
+        Cn, kh, kw = k.shape[0], k.shape[-2], k.shape[-1]
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+        dp, bp = C.c_void_p(), C.c_void_p()
+        _check(lib().he_im2col_conv_bsgs_encode(self.h, k.ctypes.data_as(DP), Cn, kh, kw,
+                                                None if b is None else b.ctypes.data_as(DP), int(chunk), int(g),
+                                                int(pt_shift), level, float(in_scale), C.byref(dp), C.byref(bp)))
+        return Plaintext(self, dp), (Plaintext(self, bp) if bp.value else None)
+
+    def he_im2col_conv_bsgs_pt(self, ct, diags: Plaintext, bias: Plaintext | None, chunk: int, g: int) -> Ciphertext:
+        return self._ct2(lib().he_im2col_conv_bsgs_pt, ct.h, diags.h, None if bias is None else bias.h,
+                         int(chunk), int(g))
 
     def he_im2col_conv_pt(self, ct, kernels: Plaintext, masks: Plaintext, bias: Plaintext | None,
                           chunk: int) -> Ciphertext:

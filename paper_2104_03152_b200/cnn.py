@@ -7,7 +7,8 @@ the calls and holds the resident weight plaintexts (encoded once).
 
 Scale schedule: input encoded at 2^30; conv
 kernels at q_l (shift 0), masks at q_{l-1} 2^-4, FC1 diagonals at q_l, FC2
-diagonals at q_l 2^-4.  Rotation keys: exactly the circuit's steps (A-rot).
+diagonals at q_l 2^-4.  With the one-level conv (PLAN_BSGS): input at level
+L-2, conv diagonals at q_l 2^-2, FC1 at q_l 2^-4, FC2 at q_l 2^-4.  Rotation keys: exactly the circuit's steps (A-rot).
 """
 from __future__ import annotations
 
@@ -16,6 +17,10 @@ import numpy as np
 from .ckks import Context, he_im2col_encode_batch
 
 PLAN = dict(in_log2=30, kernel_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=4)
+# One-level conv (he_im2col_conv_bsgs_pt; oracle CNN_PLAN_BSGS): the input is encrypted one level
+# lower, the conv plaintext is at q_l 2^conv_shift, FC1 at q_l 2^fc1_shift, FC2 at q_l 2^-fc2_shift.
+PLAN_BSGS = dict(in_log2=30, conv_shift=-2, fc1_shift=-4, fc2_shift=4, in_level_drop=1)
+CONV_G = 8          # one-level conv: 8 baby steps (chunks) x 8 giant steps
 CHUNK = 64          # next power of two >= 64 windows (C18)
 KH = KW = 7
 STRIDE = 3
@@ -24,40 +29,58 @@ STRIDE = 3
 FOLD_N1 = 8        # hoisted conv fold: 8 x 8 chunks
 
 
-def rotation_steps(ns: int = 4096, chunk: int = CHUNK, fold_n1: int = 0) -> list:
-    """A-rot: FC1 diagonals 1..255 (FC2's 1..63 are a subset) and the conv fold chunk * 2^r (plus
-    chunk b and chunk n1 a for the hoisted fold)."""
-    fold = []
-    s = chunk
-    while s < ns:
-        fold.append(s)
-        s <<= 1
-    steps = set(range(1, 256)) | set(fold)
-    if fold_n1:
-        n2 = ns // chunk // fold_n1
-        steps |= {chunk * b for b in range(1, fold_n1)} | {chunk * fold_n1 * a for a in range(1, n2)}
+def rotation_steps(ns: int = 4096, chunk: int = CHUNK, fold_n1: int = 0, conv_g: int = 0,
+                   fc_bsgs: bool = False) -> list:
+    """A-rot, exactly the circuit's steps.  FC: 1..255, or with fc_bsgs the baby steps 1..g-1 and
+    giant steps g k2 of FC1 (n 256, g 64) and FC2 (n 64, g 16).  Conv: chunk 2^r (log2 fold), or
+    chunk b and chunk n1 a (hoisted fold) / chunk b and chunk g a (one-level conv)."""
+    if fc_bsgs:
+        steps = set()
+        for n in (256, 64):
+            g = n // 4
+            steps |= set(range(1, g)) | {g * k2 for k2 in range(1, (n + g - 1) // g)}
+    else:
+        steps = set(range(1, 256))
+    n1 = conv_g or fold_n1
+    if n1:
+        n2 = ns // chunk // n1
+        steps |= {chunk * b for b in range(1, n1)} | {chunk * n1 * a for a in range(1, n2)}
+    else:
+        s = chunk
+        while s < ns:
+            steps.add(s)
+            s <<= 1
     return sorted(steps)
 
 
 class EncryptedCNN:
     """conv_w [4,1,7,7], conv_b [4], fc1_w [64,256], fc1_b [64], fc2_w [10,64], fc2_b [10] (PyTorch layouts)."""
 
-    def __init__(self, ctx: Context, w, plan=None, lazy: bool = True, bsgs: bool = True, fold_n1: int = 0):
+    def __init__(self, ctx: Context, w, plan=None, lazy: bool = True, bsgs: bool = True, fold_n1: int = 0,
+                 conv_g: int = 0):
         """FC layers: bsgs (default) = baby-step/giant-step with lazy ModDown (oracle vec_mat_bsgs,
         baby step n/4); lazy = one ModDown per vec_mat (oracle vec_mat_lazy); neither = one ModDown
-        per rotation (oracle vec_mat)."""
-        self.ctx, self.plan, self.lazy, self.fold_n1 = ctx, dict(plan or PLAN), lazy, fold_n1
+        per rotation (oracle vec_mat).  Conv: conv_g > 0 = the one-level conv (plan PLAN_BSGS),
+        else fold_n1 > 0 = the hoisted two-level fold, else the paper's log2 fold."""
+        self.ctx, self.lazy, self.fold_n1, self.conv_g = ctx, lazy, fold_n1, conv_g
+        self.plan = dict(plan or (PLAN_BSGS if conv_g else PLAN))
         self.bsgs = bsgs and lazy
         L = ctx.L
-        self.top = L - 1
+        self.top = L - 1 - self.plan.get("in_level_drop", 0)
         in_scale = 2.0 ** self.plan["in_log2"]
         k = np.asarray(w.conv_w, dtype=np.float64).reshape(w.conv_w.shape[0], KH, KW)
-        self.conv_k, self.conv_m, self.conv_b = ctx.he_im2col_conv_encode(
-            k, w.conv_b, CHUNK, self.plan["kernel_shift"], self.plan["mask_shift"], self.top, in_scale)
-        # scale after conv and square (tracked exactly like the library does)
-        s = in_scale * self.conv_k.scale / ctx.q[self.top]
-        s = s * self.conv_m.scale / ctx.q[self.top - 1]
-        lvl = self.top - 2
+        if conv_g:
+            self.conv_d, self.conv_b = ctx.he_im2col_conv_bsgs_encode(
+                k, w.conv_b, CHUNK, conv_g, self.plan["conv_shift"], self.top, in_scale)
+            s = in_scale * self.conv_d.scale / ctx.q[self.top]
+            lvl = self.top - 1
+        else:
+            self.conv_k, self.conv_m, self.conv_b = ctx.he_im2col_conv_encode(
+                k, w.conv_b, CHUNK, self.plan["kernel_shift"], self.plan["mask_shift"], self.top, in_scale)
+            # scale after conv and square (tracked exactly like the library does)
+            s = in_scale * self.conv_k.scale / ctx.q[self.top]
+            s = s * self.conv_m.scale / ctx.q[self.top - 1]
+            lvl = self.top - 2
         s = s * s / ctx.q[lvl]          # square: tensor, relin, rescale
         lvl -= 1
         g1 = np.asarray(w.fc1_w).shape[1] // 4 if self.bsgs else 0
@@ -84,7 +107,9 @@ class EncryptedCNN:
     def forward(self, ct):
         """Server side: conv -> square -> FC1 -> square -> FC2."""
         c = self.ctx
-        if self.fold_n1:
+        if self.conv_g:
+            x = c.he_im2col_conv_bsgs_pt(ct, self.conv_d, self.conv_b, CHUNK, self.conv_g)
+        elif self.fold_n1:
             x = c.he_im2col_conv_hoisted_pt(ct, self.conv_k, self.conv_m, self.conv_b, CHUNK, self.fold_n1)
         else:
             x = c.he_im2col_conv_pt(ct, self.conv_k, self.conv_m, self.conv_b, CHUNK)

@@ -787,6 +787,89 @@ he_status he_im2col_conv_encode(he_context* c, const double* kernels, int C, int
   });
 }
 
+// One-level conv plaintexts (oracle circuits.conv_bsgs_diagonals): D_b = sum_c Mask_c (.) rot(K_c, chunk b),
+// b < g, as QP plaintexts at q_l 2^pt_shift (level l); bias at the output scale (level l-1).
+static void conv_bsgs_encode(he_context* c, const double* kernels, int C, int kh, int kw, const double* bias,
+                             int chunk, int g, int pt_shift, int l, double in_scale, he_plaintext** dp,
+                             he_plaintext** bp) {
+  const int ns = c->N / 2, taps = kh * kw;
+  need(kernels != nullptr, HE_INVALID_ARGUMENT, "null kernels");
+  need(c->K > 0, HE_INVALID_PARAMS, "the one-level conv needs special primes (lazy ModDown)");
+  need(l >= 1 && l < c->L, HE_LEVEL_EXHAUSTED, "the one-level conv consumes one level");
+  need(C >= 1 && taps >= 1, HE_SHAPE_MISMATCH, "need at least one channel and tap");
+  need(chunk >= 1 && (chunk & (chunk - 1)) == 0 && ns % chunk == 0, HE_LAYOUT_MISMATCH,
+       "chunk must be a power of two dividing n_s");
+  need((size_t)taps * chunk <= (size_t)ns, HE_LAYOUT_MISMATCH, "taps x chunk exceeds the slots");
+  const int nch = ns / chunk;
+  need(g >= 1 && g % C == 0 && nch % g == 0, HE_LAYOUT_MISMATCH,
+       "g must be a multiple of C dividing n_s / chunk (Mask_c has period C chunks)");
+  // slot s of D_b: only channel c = (s / chunk) mod C has Mask_c[s] = 1; rot(K_c, chunk b)[s] =
+  // K_c[s + chunk b] = kernel_c[tap] with tap = (s / chunk + b) mod n_chunks when tap < taps
+  std::vector<double> D((size_t)g * ns, 0.0);
+  for (int b = 0; b < g; ++b)
+    for (int s = 0; s < ns; ++s) {
+      const int ch = (s / chunk) % C, tap = (s / chunk + b) % nch;
+      if (tap < taps) D[(size_t)b * ns + s] = kernels[(size_t)ch * taps + tap];
+    }
+  PtGuard pd, pb;
+  {
+    DevDoubles d(c, D.data(), D.size());
+    pd.p = encode(c, d.d, ns, g, shifted(c->hp.q[l], pt_shift), l, 1);
+  }
+  if (bias) {
+    std::vector<double> bs(ns);
+    for (int s = 0; s < ns; ++s) bs[s] = bias[(s / chunk) % C];
+    DevDoubles d(c, bs.data(), bs.size());
+    pb.p = encode(c, d.d, ns, 1, in_scale * pd.p->scale / (double)c->hp.q[l], l - 1);
+  }
+  *dp = pd.p;
+  *bp = pb.p;
+  pd.p = pb.p = nullptr;
+}
+
+he_status he_im2col_conv_bsgs_encode(he_context* c, const double* kernels, int C, int kh, int kw,
+                                     const double* bias, int chunk, int g, int pt_shift, int level,
+                                     double in_scale, he_plaintext** diags, he_plaintext** bias_pt) {
+  return guard([&] {
+    need_ctx(c);
+    need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
+    conv_bsgs_encode(c, kernels, C, kh, kw, bias, chunk, g, pt_shift, level, in_scale, diags, bias_pt);
+  });
+}
+
+he_status he_im2col_conv_bsgs_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags,
+                                 const he_plaintext* bias, int chunk, int g, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_pt(c, diags); need_out(out);
+    need(ct->size == 2, HE_SHAPE_MISMATCH, "conv needs a size-2 ciphertext");
+    need(ct->level >= 1, HE_LEVEL_EXHAUSTED, "the one-level conv consumes one level");
+    need(diags->qp, HE_INVALID_ARGUMENT, "diagonals must come from he_im2col_conv_bsgs_encode (QP form)");
+    need(diags->level == ct->level, HE_LEVEL_MISMATCH, "diagonals must be at the ciphertext level");
+    const int ns = c->N / 2;
+    need(chunk >= 1 && (chunk & (chunk - 1)) == 0 && ns % chunk == 0, HE_LAYOUT_MISMATCH,
+         "chunk must be a power of two dividing n_s");
+    need(g >= 1 && diags->B == g && (ns / chunk) % g == 0, HE_SHAPE_MISMATCH, "need g diagonals, g | n_s / chunk");
+    const int n2 = ns / chunk / g;
+    for (int b = 1; b < g; ++b) {
+      u32 gg;
+      need(galois_key(c, chunk * b, &gg) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * b");
+    }
+    for (int a = 1; a < n2; ++a) {
+      u32 gg;
+      need(galois_key(c, chunk * g * a, &gg) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * g * a");
+    }
+    if (bias) {
+      need_pt(c, bias);
+      need_plain_q(bias);
+      need(bias->B == 1, HE_SHAPE_MISMATCH, "bias is one plaintext");
+      need(bias->level == ct->level - 1, HE_LEVEL_MISMATCH, "bias at the rescaled level");
+      need(bias->scale == ct->scale * diags->scale / (double)c->hp.q[ct->level], HE_SCALE_MISMATCH,
+           "bias scale must equal the output scale");
+    }
+    *out = ct_conv_bsgs(c, ct, diags, bias, chunk, g);
+  });
+}
+
 he_status he_im2col_conv(he_context* c, const he_ciphertext* ct, const double* kernels, int C, int kh, int kw,
                          const double* bias, int chunk, int kernel_shift, int mask_shift, he_ciphertext** out) {
   return guard([&] {

@@ -1790,6 +1790,38 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
   }
 }
 
+// One-level im2col conv (oracle circuits.im2col_conv_bsgs): v = rescale(ModDown(
+// sum_{b<g} D_b (.) rot(x, chunk b))) with the g QP diagonals D_b = sum_c Mask_c (.) rot(K_c, chunk b)
+// (the baby-step kernel, one group), then the giant steps sum_{a<n2} rot(v, chunk g a) as a
+// unit-diagonal rotation sum, + bias.
+he_ciphertext* ct_conv_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
+                            const he_plaintext* bias, int chunk, int g) {
+  std::vector<he_ciphertext*> inner = bsgs_inner(c, x, diags, g, chunk);
+  he_ciphertext* v = inner[0];
+  he_ciphertext* r = nullptr;
+  try {
+    r = ct_rescale(c, v);
+    ct_free(v);
+    v = nullptr;
+    const int n2 = c->N / 2 / chunk / g;
+    if (n2 > 1) {
+      he_ciphertext* r2 = ct_rot_sum(c, r, n2, chunk * g);
+      ct_free(r);
+      r = r2;
+    }
+    if (bias) {
+      he_ciphertext* r2 = ct_add_plain(c, r, bias);
+      ct_free(r);
+      r = r2;
+    }
+  } catch (...) {
+    ct_free(v);
+    ct_free(r);
+    throw;
+  }
+  return r;
+}
+
 // ---- keygen (a2/a3, C9-C12) --------------------------------------------------
 static void make_ksk(he_context* c, u64* key, u64 pur_a, u64 pur_e, u64 objbase, u32 gal) {
   const int L = c->L, NP = c->NP, N = c->N;

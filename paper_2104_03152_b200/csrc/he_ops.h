@@ -48,6 +48,8 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
                                const he_plaintext* bias);
 he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
                        const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1 = 0);
+he_ciphertext* ct_conv_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
+                            const he_plaintext* bias, int chunk, int g);
 const u64* galois_key(he_context* c, int step, u32* gal_out);
 size_t wire_payload_bytes(he_context* c, const he_ciphertext* ct);
 void wire_pack(he_context* c, const he_ciphertext* ct, u64* out_dev);

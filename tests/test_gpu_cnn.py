@@ -22,8 +22,10 @@ pytestmark = pytest.mark.gpu
 def cfg4():
     from paper_2104_03152_b200 import Context
     from paper_2104_03152_b200.cnn import rotation_steps
-    steps = OC.cnn_rotation_steps(fold_n1=8)       # superset: log2 fold + hoisted fold + FC steps
-    assert steps == rotation_steps(fold_n1=8)
+    forms = [dict(), dict(fold_n1=8), dict(conv_g=8, fc_bsgs=True), dict(fc_bsgs=True)]
+    for f in forms:
+        assert OC.cnn_rotation_steps(**f) == rotation_steps(**f)
+    steps = sorted(set().union(*[rotation_steps(**f) for f in forms]))   # every conv / FC form
     o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
     o.keygen(steps)
     g = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
@@ -36,7 +38,7 @@ def inj(g, o, vecs, scale, level):
     return g.he_pt_from_int_coeffs(ms, scale, level)
 
 
-@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold"])
+@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold", "bsgs+conv8"])
 def test_cnn_layers_bit_exact(cfg4, lazy):
     """lazy=False: FC layers with one ModDown per rotation (oracle vec_mat); lazy=True: one
     ModDown per vec_mat (oracle vec_mat_lazy, QP diagonals); "bsgs": baby step n/4 with one lazy
@@ -44,25 +46,36 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
     o, g = cfg4
     w = cnn_weights(3)
     imgs = mnist_like_images(2, 4)
-    ns, q, plan = o.slots, o.q, OC.CNN_PLAN
-    o_in = [OC.cnn_encrypt_input(o, img, b) for b, img in enumerate(imgs)]
+    conv_g = 8 if lazy == "bsgs+conv8" else 0
+    ns, q, plan = o.slots, o.q, (OC.CNN_PLAN_BSGS if conv_g else OC.CNN_PLAN)
+    o_in = [OC.cnn_encrypt_input(o, img, b, plan) for b, img in enumerate(imgs)]
     lvl = o_in[0].level
     x = g.he_ct_import_words(np.stack([c.words for c in o_in]), lvl, o_in[0].scale)
     # conv (C18/C19)
-    K = [OC.conv_kernel_slots(w.conv_w[c].reshape(-1), 64, ns) for c in range(4)]
-    M = [OC.conv_mask_slots(c, 4, 64, ns) for c in range(4)]
-    gK = inj(g, o, K, float(q[lvl]) * 2.0 ** plan["conv_shift"], lvl)
-    gM = inj(g, o, M, float(q[lvl - 1]) * 2.0 ** plan["mask_shift"], lvl - 1)
-    s2 = (o_in[0].scale * gK.scale / q[lvl]) * gM.scale / q[lvl - 1]
-    gB = inj(g, o, [OC.conv_bias_slots(w.conv_b, 64, ns)], s2, lvl - 2)
-    n1 = 8 if lazy == "bsgs+fold" else 0
-    if n1:
-        x = g.he_im2col_conv_hoisted_pt(x, gK, gM, gB, 64, n1)
+    if conv_g:      # one-level conv: g QP diagonals, one rescale, giant-step rotation sum
+        ps = float(q[lvl]) * 2.0 ** plan["conv_shift"]
+        Dv = OC.conv_bsgs_diagonals(w.conv_w.reshape(4, -1), 64, ns, conv_g)
+        gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in Dv]), ps, lvl)
+        gB = inj(g, o, [OC.conv_bias_slots(w.conv_b, 64, ns)], o_in[0].scale * ps / q[lvl], lvl - 1)
+        x = g.he_im2col_conv_bsgs_pt(x, gD, gB, 64, conv_g)
+        ref = [OC.im2col_conv_bsgs(o, c, w.conv_w.reshape(4, -1), w.conv_b, 64, conv_g, plan["conv_shift"])
+               for c in o_in]
         lazy = "bsgs"
     else:
-        x = g.he_im2col_conv_pt(x, gK, gM, gB, 64)
-    ref = [OC.im2col_conv(o, c, w.conv_w.reshape(4, -1), w.conv_b, 64, plan["conv_shift"], plan["mask_shift"],
-                          fold_n1=n1) for c in o_in]
+        K = [OC.conv_kernel_slots(w.conv_w[c].reshape(-1), 64, ns) for c in range(4)]
+        M = [OC.conv_mask_slots(c, 4, 64, ns) for c in range(4)]
+        gK = inj(g, o, K, float(q[lvl]) * 2.0 ** plan["conv_shift"], lvl)
+        gM = inj(g, o, M, float(q[lvl - 1]) * 2.0 ** plan["mask_shift"], lvl - 1)
+        s2 = (o_in[0].scale * gK.scale / q[lvl]) * gM.scale / q[lvl - 1]
+        gB = inj(g, o, [OC.conv_bias_slots(w.conv_b, 64, ns)], s2, lvl - 2)
+        n1 = 8 if lazy == "bsgs+fold" else 0
+        if n1:
+            x = g.he_im2col_conv_hoisted_pt(x, gK, gM, gB, 64, n1)
+            lazy = "bsgs"
+        else:
+            x = g.he_im2col_conv_pt(x, gK, gM, gB, 64)
+        ref = [OC.im2col_conv(o, c, w.conv_w.reshape(4, -1), w.conv_b, 64, plan["conv_shift"],
+                              plan["mask_shift"], fold_n1=n1) for c in o_in]
     W = x.words()
     for b in range(2):
         assert np.array_equal(W[b], ref[b].words), ("conv", b)
@@ -108,14 +121,14 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         assert np.allclose(z[b], o.decode(o.decrypt(ref[b]), 10), rtol=1e-9, atol=1e-9)
 
 
-@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold"])
+@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold", "bsgs+conv8"])
 def test_cnn_all_gpu_tolerance(cfg4, lazy):
     """Own encode/encrypt/decrypt/decode: logits within 5e-3 abs of float64, argmax equal."""
     from paper_2104_03152_b200.cnn import EncryptedCNN
     o, g = cfg4
     w = cnn_weights(3)
-    net = EncryptedCNN(g, w, lazy=bool(lazy), bsgs=lazy in ("bsgs", "bsgs+fold"),
-                       fold_n1=8 if lazy == "bsgs+fold" else 0)
+    net = EncryptedCNN(g, w, lazy=bool(lazy), bsgs=lazy in ("bsgs", "bsgs+fold", "bsgs+conv8"),
+                       fold_n1=8 if lazy == "bsgs+fold" else 0, conv_g=8 if lazy == "bsgs+conv8" else 0)
     imgs = mnist_like_images(16, 4)
     logits = net.decrypt(net.forward(net.encrypt(imgs, 1000)))
     for b, img in enumerate(imgs):

@@ -149,16 +149,53 @@ def test_hoisted_fold_is_the_same_sum():
     assert np.allclose(s, ref, atol=1e-9)
 
 
+def mock_conv_bsgs(slots, kernels, bias, chunk, g):
+    """The one-level conv: v = sum_{b<g} D_b * rot(x, chunk b), then
+    sum_{a<n2} rot(v, chunk g a) + bias (slot simulator, rot = np.roll(., -k))."""
+    D = C.conv_bsgs_diagonals(kernels, chunk, NS, g)
+    v = sum(D[b] * np.roll(slots, -chunk * b) for b in range(g))
+    n2 = NS // chunk // g
+    return sum(np.roll(v, -chunk * g * a) for a in range(n2)) + C.conv_bias_slots(bias, chunk, NS)
+
+
+@pytest.mark.parametrize("g", [4, 8, 16, 64])
+def test_one_level_conv_is_the_same_conv(g):
+    """D_b = sum_c Mask_c * rot(K_c, chunk b) and Mask_c has period C chunks, so the baby-step /
+    giant-step form equals the paper's fold-then-mask conv (mock_conv, itself pinned against
+    torch conv2d above) whenever C | g; with g = 2 (C does not divide g) it does not."""
+    w = cnn_weights(3)
+    img = mnist_like_images(1, 4, start=2)[0]
+    slots = C.im2col_slots(img, 7, 7, 3, NS)
+    k = w.conv_w.reshape(4, -1)
+    ref = mock_conv(slots, k, w.conv_b, 64)
+    assert np.allclose(mock_conv_bsgs(slots, k, w.conv_b, 64, g), ref, atol=1e-9)
+    assert not np.allclose(mock_conv_bsgs(slots, k, w.conv_b, 64, 2), ref, atol=1e-3)
+
+
+def test_one_level_conv_diagonals_by_hand():
+    """conv_bsgs_diagonals against its definition on a tiny layout written out by hand: 16 slots,
+    chunk 2 (8 chunks), C = 2 channels of 3 taps, g = 2.  D_b[s] = kernel_c[tap] with
+    c = (s / 2) mod 2, tap = s / 2 + b (when < 3)."""
+    k = np.array([[1.0, 2.0, 3.0], [10.0, 20.0, 30.0]])
+    D = C.conv_bsgs_diagonals(k, 2, 16, 2)
+    # chunks 0..7 -> (channel, tap) for b = 0: (0,0) (1,1) (0,2) (1,-) (0,-) ...
+    assert D[0].tolist() == [1, 1, 20, 20, 3, 3, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0]
+    # b = 1: chunk q reads tap q + 1: (0,1) (1,2) (0,-) ...; chunk 7 wraps to tap 0 of channel 1
+    assert D[1].tolist() == [2, 2, 30, 30, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 10, 10]
+
+
 @pytest.mark.slow
 def test_oracle_cnn_fast_schedule_end_to_end():
-    """The oracle with the bench's evaluation schedule (hoisted conv fold, BSGS FC layers) meets the
-    same 5e-3 / argmax bar against the float network."""
+    """The oracle with the bench's evaluation schedule (one-level conv, BSGS FC layers, input one
+    level lower) meets the same 5e-3 / argmax bar against the float network."""
     from oracle.oracle import OracleContext
     w = cnn_weights(3)
     img = mnist_like_images(1, 4, start=9)[0]
     ctx = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-    ctx.keygen(C.cnn_rotation_steps(fold_n1=8))
-    out = C.cnn_forward(ctx, C.cnn_encrypt_input(ctx, img, 0), w, lazy=True, bsgs=True, fold_n1=8)
+    ctx.keygen(C.cnn_rotation_steps(conv_g=C.CONV_G, fc_bsgs=True))   # 77 keys
+    ct = C.cnn_encrypt_input(ctx, img, 0, C.CNN_PLAN_BSGS)
+    out = C.cnn_forward(ctx, ct, w, lazy=True, bsgs=True, conv_g=C.CONV_G)
+    assert ct.level == ctx.L - 2 and out.level == 0
     z = ctx.decode(ctx.decrypt(out), 10)
     ref = float_net_numpy(img, w)
     assert np.max(np.abs(z - ref)) < 5e-3 and np.argmax(z) == np.argmax(ref)
