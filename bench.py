@@ -109,7 +109,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2104_03152_b200 import Context, he_im2col_encode_batch
-    from paper_2104_03152_b200.cnn import CONV_G, EncryptedCNN, rotation_steps
+    from paper_2104_03152_b200.cnn import CONV_G, FC1_G, EncryptedCNN, rotation_steps
     from paper_2104_03152_b200.dist import gather_to_rank0, max_over_ranks, shard_indices
     from synthetic import CFG4, cnn_weights, mnist_like_images
 
@@ -120,8 +120,8 @@ def run_ours(args, rank, world, local_rank):
 
     ctx = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
     ctx.he_set_stream(stream)
-    ctx.he_keygen(rotation_steps(conv_g=CONV_G, fc_bsgs=True))
-    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed), conv_g=CONV_G)
+    ctx.he_keygen(rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
+    net = EncryptedCNN(ctx, cnn_weights(CFG4.seed), conv_g=CONV_G, fc1_g=FC1_G)
     ns = ctx.slots
 
     # this rank's shard of the image stream (image i depends only on (seed, i))
@@ -312,11 +312,11 @@ def oracle_sample(images: int = 1, start: int = 10_000):
     from concurrent.futures import ThreadPoolExecutor
     from oracle import circuits as OC
     from oracle.oracle import OracleContext
-    from paper_2104_03152_b200.cnn import CONV_G
+    from paper_2104_03152_b200.cnn import CONV_G, FC1_G
     from synthetic import CFG4, cnn_weights, mnist_like_images
     if "o" not in _ORACLE:   # keys are made once (excluded from timing, like the GPU arm)
         o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-        o.keygen(OC.cnn_rotation_steps(conv_g=CONV_G, fc_bsgs=True))
+        o.keygen(OC.cnn_rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
         _ORACLE["o"] = o
     o = _ORACLE["o"]
     w = cnn_weights(CFG4.seed)
@@ -325,8 +325,8 @@ def oracle_sample(images: int = 1, start: int = 10_000):
 
     def one(i):
         ct = OC.cnn_encrypt_input(o, imgs[i], 3_000_000 + start + i, OC.CNN_PLAN_BSGS)
-        # the same evaluation schedule as the GPU arm: one-level conv, BSGS FC layers
-        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True, bsgs=True, conv_g=CONV_G)), 10)
+        # the same evaluation schedule as the GPU arm: one-level conv, folded BSGS FC1, BSGS FC2
+        return o.decode(o.decrypt(OC.cnn_forward(o, ct, w, lazy=True, bsgs=True, conv_g=CONV_G, fc1_g=FC1_G)), 10)
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=min(images, cores)) as ex:
@@ -373,9 +373,10 @@ def main():
 
     config = {"workload": "BASELINE config 5 (config-4 CNN on seeded synthetic 28x28 images, sharded)",
               "network": "conv7x7s3x4 -> x^2 -> fc256x64 -> x^2 -> fc64x10 (PAPER.md:98)",
-              "ckks": "N=8192, primes [31,26x6,31] (input at level 5, scale 2^30), 77 Galois keys",
-              "evaluation": "conv: one level, 8 baby x 8 giant chunk steps; FC: BSGS (baby step n/4); "
-                            "every rotation sum with one lazy ModDown (DESIGN.md §3)",
+              "ckks": "N=8192, primes [31,26x6,31] (input at level 5, scale 2^30), 47 Galois keys",
+              "evaluation": "conv: one level, 8 baby x 8 giant chunk steps; FC1: 64 diagonals by BSGS "
+                            "(32 x 2) + fold 4; FC2: BSGS (16 x 4); every rotation sum with one lazy "
+                            "ModDown (DESIGN.md §3)",
               "batch_per_gpu": args.batch, "global_batch": args.batch * world,
               "step": "encode+encrypt+conv+square+fc1+square+fc2+decrypt+decode",
               "parallelism": f"dp{world} (independent images, no data-path collective)",

@@ -297,6 +297,21 @@ he_status he_vec_mat_encode_bsgs(he_context* ctx, const double* W, int n, int m,
                                  he_plaintext** diags, he_plaintext** bias_pt);
 he_status he_vec_mat_bsgs_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* diags, int g,
                              const he_plaintext* bias_pt, he_ciphertext** out);
+/* Folded baby-step/giant-step form for a replicated output (C17) with m | n
+ * (oracle vec_mat_bsgs_fold; the rectangular "hybrid" diagonal method): the
+ * replicated-output diagonals satisfy D_{k + m t} = rot(D_k, m t), so only the
+ * first m diagonals are encoded (BSGS order, g | m, m/g <= 4 groups), and
+ * he_vec_mat_pt / he_vec_mat_bsgs_pt finish the n-term sum with
+ * sum_{t < n/m} rot(., m t) as one hoisted rotation sum before the rescale.
+ * Needs Galois keys for 1..g-1, g k2 (k2 < m/g) and m t (t < n/m).  Same
+ * scales, bias and level use as he_vec_mat_encode with replicate_out = 1. */
+he_status he_vec_mat_encode_bsgs_fold(he_context* ctx, const double* W, int n, int m, const double* bias,
+                                      int pt_scale_shift, int level, double in_scale, int g,
+                                      he_plaintext** diags, he_plaintext** bias_pt);
+/* The folded evaluation with the shape given explicitly (diags = the first m
+ * diagonals in BSGS order, e.g. injected with he_pt_from_int_coeffs_qp). */
+he_status he_vec_mat_bsgs_fold_pt(he_context* ctx, const he_ciphertext* ct, const he_plaintext* diags, int g,
+                                  int n, int m, const he_plaintext* bias_pt, he_ciphertext** out);
 he_status he_im2col_conv_encode(he_context* ctx, const double* kernels, int n_channels, int kh, int kw,
                                 const double* bias, int chunk, int kernel_shift, int mask_shift,
                                 int level, double in_scale, he_plaintext** kernels_pt,

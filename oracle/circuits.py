@@ -265,19 +265,22 @@ CNN_PLAN = dict(in_log2=30, conv_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=
 # scale is the same 2^22 (2 (2 (30 - 2) - 26 - 4) - 26 - 4 = 22).
 CNN_PLAN_BSGS = dict(in_log2=30, conv_shift=-2, fc1_shift=-4, fc2_shift=-4, in_level_drop=1)
 CONV_G = 8          # baby steps of the one-level conv: 8 chunks x 8 giant steps
+FC1_G = 32          # baby steps of the folded FC1 (vec_mat_bsgs_fold): 32 x 2 groups, fold 4
 
 
 def cnn_rotation_steps(ns: int = 4096, chunk: int = 64, fold_n1: int = 0, conv_g: int = 0,
-                       fc_bsgs: bool = False) -> list:
+                       fc_bsgs: bool = False, fc1_g: int = 0) -> list:
     """A-rot: exactly the circuit's steps.  FC: 1..255 (FC2's 1..63 are a subset), or with
     fc_bsgs the baby steps 1..g-1 and giant steps g k2 of FC1 (n 256, g 64) and FC2 (n 64, g 16).
     Conv: the log2 fold steps chunk 2^r, or chunk b and chunk n1 a (hoisted fold, fold_n1), or
     chunk b and chunk g a (one-level conv, conv_g)."""
     if fc_bsgs:
-        steps = set()
-        for n in (256, 64):
-            g = n // 4
-            steps |= set(range(1, g)) | {g * k2 for k2 in range(1, (n + g - 1) // g)}
+        def bsgs(n, g):         # baby steps 1..g-1, giant steps g k2
+            return set(range(1, g)) | {g * k2 for k2 in range(1, (n + g - 1) // g)}
+        # FC1 (n 256 -> m 64): plain BSGS with g = n/4, or folded with g = fc1_g over the first m
+        # diagonals (giant g k2 < m) and the fold m t < n; FC2 (n 64): g = 16
+        fc1 = bsgs(64, fc1_g) | {64, 128, 192} if fc1_g else bsgs(256, 64)
+        steps = fc1 | bsgs(64, 16)
     else:
         steps = set(range(1, 256))
     n1 = conv_g or fold_n1
@@ -297,10 +300,11 @@ def cnn_encrypt_input(ctx: OracleContext, img: np.ndarray, stream_id: int, plan=
 
 
 def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False, bsgs: bool = False,
-                fold_n1: int = 0, conv_g: int = 0) -> OCt:
+                fold_n1: int = 0, conv_g: int = 0, fc1_g: int = 0) -> OCt:
     """The paper's network; lazy=True uses vec_mat_lazy for FC1/FC2, bsgs=True
     vec_mat_bsgs (baby step n/4); fold_n1 > 0 the hoisted conv fold; conv_g > 0 the one-level
-    conv (im2col_conv_bsgs, plan CNN_PLAN_BSGS, input from cnn_encrypt_input with that plan)."""
+    conv (im2col_conv_bsgs, plan CNN_PLAN_BSGS, input from cnn_encrypt_input with that plan);
+    fc1_g > 0 (with bsgs) FC1 as vec_mat_bsgs_fold with baby step fc1_g."""
     plan = plan or (CNN_PLAN_BSGS if conv_g else CNN_PLAN)
 
     def vm(x, W, b, rep, shift):
@@ -314,7 +318,10 @@ def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False, b
         x = im2col_conv(ctx, ct, w.conv_w.reshape(w.conv_w.shape[0], -1), w.conv_b, 64,
                         plan["conv_shift"], plan["mask_shift"], fold_n1=fold_n1)
     x = ctx.square(x)
-    x = vm(x, w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"])
+    if bsgs and fc1_g:
+        x = vec_mat_bsgs_fold(ctx, x, w.fc1_w.T, w.fc1_b, -plan["fc1_shift"], g=fc1_g)
+    else:
+        x = vm(x, w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"])
     x = ctx.square(x)
     x = vm(x, w.fc2_w.T, w.fc2_b, False, -plan["fc2_shift"])
     return x
@@ -451,4 +458,33 @@ def vec_mat_bsgs(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | 
     acc = ctx.rescale(acc)
     if bias is not None:
         acc = ctx.add_plain(acc, ctx.encode(vecmat_bias_slots(bias, ns, replicate_out), acc.scale, acc.level))
+    return acc
+
+
+def vec_mat_bsgs_fold(ctx: OracleContext, ct: OCt, W: np.ndarray, bias: np.ndarray | None,
+                      pt_scale_shift: int = 0, g: int = 32) -> OCt:
+    """vec_mat with replicated output (C17) when m | n: the diagonals are rotation-periodic,
+    D_{k + m t}[j] = W[(j + k + m t) mod n][j mod m] = rot(D_k, m t)[j], so
+        sum_{k < n} D_k (.) rot(x, k) = sum_{t < n/m} rot(y', m t),  y' = sum_{k < m} D_k (.) rot(x, k)
+    (the rectangular "hybrid" diagonal method).  y' by baby-step/giant-step over the first m
+    diagonals (g | m, m/g groups, as vec_mat_bsgs), then the n/m-term sum as one unit-diagonal
+    rotation sum (rot_sum, one lazy ModDown), one rescale, + bias."""
+    n, m = W.shape
+    assert n % m == 0 and m % g == 0
+    ns = ctx.slots
+    D = vecmat_diagonals(W, ns, True)[:m]
+    E = bsgs_diagonals(D, g)
+    lvl = ct.level
+    pscale = _shifted(ctx.q[lvl], -pt_scale_shift)
+    acc = None
+    for k2 in range(E.shape[0]):
+        Eqp = np.stack([ctx.coeffs_to_pt_qp(ctx.encode_coeffs(E[k2, k1], pscale)[1], lvl) for k1 in range(g)])
+        inner = OCt(ctx.vec_mat_lazy_acc(ct, Eqp), lvl, ct.scale * pscale)
+        if k2:
+            inner = ctx.rotate(inner, g * k2)
+        acc = inner if acc is None else ctx.add(acc, inner)
+    acc = rot_sum(ctx, acc, n // m, m)
+    acc = ctx.rescale(acc)
+    if bias is not None:
+        acc = ctx.add_plain(acc, ctx.encode(vecmat_bias_slots(bias, ns, True), acc.scale, acc.level))
     return acc

@@ -108,6 +108,9 @@ _SIGS = {
     "he_vec_mat_encode_bsgs": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                VPP, VPP],
     "he_vec_mat_bsgs_pt": [VP, VP, VP, C.c_int, VP, VPP],
+    "he_vec_mat_bsgs_fold_pt": [VP, VP, VP, C.c_int, C.c_int, C.c_int, VP, VPP],
+    "he_vec_mat_encode_bsgs_fold": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_double, C.c_int,
+                                    VPP, VPP],
     "he_vec_mat_encode_lazy": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
     "he_key_export": [VP, C.c_int, C.c_int32, U64P],
     "he_key_words": [VP, C.c_int],
@@ -420,11 +423,20 @@ class Context:
                          None if b is None else b.ctypes.data_as(DP), int(bool(replicate_out)),
                          int(pt_scale_shift))
 
-    def he_vec_mat_encode(self, W, bias, replicate_out, pt_scale_shift, level, in_scale, lazy=False, bsgs_g=0):
+    def he_vec_mat_encode(self, W, bias, replicate_out, pt_scale_shift, level, in_scale, lazy=False, bsgs_g=0,
+                          fold=False):
+        """fold=True (replicated output, m | n, bsgs_g | m): he_vec_mat_encode_bsgs_fold."""
         W = np.ascontiguousarray(W, dtype=np.float64)
         n, m = W.shape
         b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
         d, bp = C.c_void_p(), C.c_void_p()
+        if fold:
+            assert replicate_out and bsgs_g
+            _check(lib().he_vec_mat_encode_bsgs_fold(self.h, W.ctypes.data_as(DP), n, m,
+                                                     None if b is None else b.ctypes.data_as(DP),
+                                                     int(pt_scale_shift), level, float(in_scale), int(bsgs_g),
+                                                     C.byref(d), C.byref(bp)))
+            return Plaintext(self, d), (Plaintext(self, bp) if bp.value else None)
         if bsgs_g:
             _check(lib().he_vec_mat_encode_bsgs(self.h, W.ctypes.data_as(DP), n, m,
                                                 None if b is None else b.ctypes.data_as(DP), int(bool(replicate_out)),
@@ -450,6 +462,11 @@ class Context:
 
     def he_vec_mat_pt(self, ct, diags: Plaintext, bias: Plaintext | None = None) -> Ciphertext:
         return self._ct2(lib().he_vec_mat_pt, ct.h, diags.h, None if bias is None else bias.h)
+
+    def he_vec_mat_bsgs_fold_pt(self, ct, diags: Plaintext, g: int, n: int, m: int,
+                                bias: Plaintext | None = None) -> Ciphertext:
+        return self._ct2(lib().he_vec_mat_bsgs_fold_pt, ct.h, diags.h, int(g), int(n), int(m),
+                         None if bias is None else bias.h)
 
     def he_vec_mat_bsgs_pt(self, ct, diags: Plaintext, g: int, bias: Plaintext | None = None) -> Ciphertext:
         return self._ct2(lib().he_vec_mat_bsgs_pt, ct.h, diags.h, int(g), None if bias is None else bias.h)

@@ -21,6 +21,7 @@ PLAN = dict(in_log2=30, kernel_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=4)
 # lower, the conv plaintext is at q_l 2^conv_shift, FC1 at q_l 2^fc1_shift, FC2 at q_l 2^-fc2_shift.
 PLAN_BSGS = dict(in_log2=30, conv_shift=-2, fc1_shift=-4, fc2_shift=4, in_level_drop=1)
 CONV_G = 8          # one-level conv: 8 baby steps (chunks) x 8 giant steps
+FC1_G = 32          # folded FC1 (he_vec_mat_encode_bsgs_fold): baby step 32, 2 groups, fold 4
 CHUNK = 64          # next power of two >= 64 windows (C18)
 KH = KW = 7
 STRIDE = 3
@@ -30,15 +31,17 @@ FOLD_N1 = 8        # hoisted conv fold: 8 x 8 chunks
 
 
 def rotation_steps(ns: int = 4096, chunk: int = CHUNK, fold_n1: int = 0, conv_g: int = 0,
-                   fc_bsgs: bool = False) -> list:
+                   fc_bsgs: bool = False, fc1_g: int = 0) -> list:
     """A-rot, exactly the circuit's steps.  FC: 1..255, or with fc_bsgs the baby steps 1..g-1 and
     giant steps g k2 of FC1 (n 256, g 64) and FC2 (n 64, g 16).  Conv: chunk 2^r (log2 fold), or
     chunk b and chunk n1 a (hoisted fold) / chunk b and chunk g a (one-level conv)."""
     if fc_bsgs:
-        steps = set()
-        for n in (256, 64):
-            g = n // 4
-            steps |= set(range(1, g)) | {g * k2 for k2 in range(1, (n + g - 1) // g)}
+        def bsgs(n, g):         # baby steps 1..g-1, giant steps g k2
+            return set(range(1, g)) | {g * k2 for k2 in range(1, (n + g - 1) // g)}
+        # FC1 (n 256 -> m 64): plain BSGS with g = n/4, or folded with g = fc1_g over the first m
+        # diagonals (giant g k2 < m) and the fold m t < n; FC2 (n 64): g = 16
+        fc1 = bsgs(64, fc1_g) | {64, 128, 192} if fc1_g else bsgs(256, 64)
+        steps = fc1 | bsgs(64, 16)
     else:
         steps = set(range(1, 256))
     n1 = conv_g or fold_n1
@@ -57,11 +60,12 @@ class EncryptedCNN:
     """conv_w [4,1,7,7], conv_b [4], fc1_w [64,256], fc1_b [64], fc2_w [10,64], fc2_b [10] (PyTorch layouts)."""
 
     def __init__(self, ctx: Context, w, plan=None, lazy: bool = True, bsgs: bool = True, fold_n1: int = 0,
-                 conv_g: int = 0):
+                 conv_g: int = 0, fc1_g: int = 0):
         """FC layers: bsgs (default) = baby-step/giant-step with lazy ModDown (oracle vec_mat_bsgs,
         baby step n/4); lazy = one ModDown per vec_mat (oracle vec_mat_lazy); neither = one ModDown
-        per rotation (oracle vec_mat).  Conv: conv_g > 0 = the one-level conv (plan PLAN_BSGS),
-        else fold_n1 > 0 = the hoisted two-level fold, else the paper's log2 fold."""
+        per rotation (oracle vec_mat); bsgs with fc1_g > 0 = FC1 folded (oracle vec_mat_bsgs_fold,
+        baby step fc1_g).  Conv: conv_g > 0 = the one-level conv (plan PLAN_BSGS), else fold_n1 > 0
+        = the hoisted two-level fold, else the paper's log2 fold."""
         self.ctx, self.lazy, self.fold_n1, self.conv_g = ctx, lazy, fold_n1, conv_g
         self.plan = dict(plan or (PLAN_BSGS if conv_g else PLAN))
         self.bsgs = bsgs and lazy
@@ -83,9 +87,11 @@ class EncryptedCNN:
             lvl = self.top - 2
         s = s * s / ctx.q[lvl]          # square: tensor, relin, rescale
         lvl -= 1
-        g1 = np.asarray(w.fc1_w).shape[1] // 4 if self.bsgs else 0
+        fold = bool(self.bsgs and fc1_g)
+        g1 = fc1_g if fold else (np.asarray(w.fc1_w).shape[1] // 4 if self.bsgs else 0)
         self.fc1_d, self.fc1_b = ctx.he_vec_mat_encode(np.asarray(w.fc1_w).T, w.fc1_b, True,
-                                                       -self.plan["fc1_shift"], lvl, s, lazy=lazy, bsgs_g=g1)
+                                                       -self.plan["fc1_shift"], lvl, s, lazy=lazy, bsgs_g=g1,
+                                                       fold=fold)
         s = s * self.fc1_d.scale / ctx.q[lvl]
         lvl -= 1
         s = s * s / ctx.q[lvl]

@@ -886,6 +886,14 @@ he_status he_im2col_conv(he_context* c, const he_ciphertext* ct, const double* k
   });
 }
 
+static void need_vm_fold_keys(he_context* c, const he_plaintext* diags) {
+  for (int t = 1; t < diags->fold_n; ++t) {
+    u32 gg;
+    need(galois_key(c, diags->fold_step * t, &gg) != nullptr, HE_MISSING_GALOIS_KEY,
+         "missing Galois key for a fold step m t");
+  }
+}
+
 he_status he_vec_mat_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags,
                         const he_plaintext* bias_pt, he_ciphertext** out) {
   return guard([&] {
@@ -903,25 +911,29 @@ he_status he_vec_mat_pt(he_context* c, const he_ciphertext* ct, const he_plainte
       need(bias_pt->scale == ct->scale * diags->scale / (double)c->hp.q[ct->level], HE_SCALE_MISMATCH,
            "bias scale must equal the output scale");
     }
+    need_vm_fold_keys(c, diags);
     *out = ct_vec_mat(c, ct, diags, bias_pt);
   });
 }
 
 static void vecmat_encode(he_context* c, const double* W, int n, int m, const double* bias, int replicate_out,
                           int pt_scale_shift, int l, double in_scale, he_plaintext** dp, he_plaintext** bp,
-                          int qp = 0, int g = 0) {
+                          int qp = 0, int g = 0, bool fold = false) {
   need(W != nullptr, HE_INVALID_ARGUMENT, "null matrix");
   need(l >= 1 && l < c->L, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
   const int ns = c->N / 2;
   std::vector<double> D = vecmat_diagonals(W, n, m, ns, replicate_out != 0);
-  int items = n;
-  if (g > 0) {   // BSGS order: E[k2][k1] = rot(D_{k1 + g k2}, -g k2), zero past n
-    const int n2 = (n + g - 1) / g;
+  // folded form: D_{k + m t} = rot(D_k, m t) for replicated output, keep the first m diagonals
+  const int nd = fold ? m : n;
+  if (fold) D.resize((size_t)m * ns);
+  int items = nd;
+  if (g > 0) {   // BSGS order: E[k2][k1] = rot(D_{k1 + g k2}, -g k2), zero past nd
+    const int n2 = (nd + g - 1) / g;
     std::vector<double> E((size_t)n2 * g * ns, 0.0);
     for (int k2 = 0; k2 < n2; ++k2)
       for (int k1 = 0; k1 < g; ++k1) {
         const int k = k1 + g * k2;
-        if (k >= n) continue;
+        if (k >= nd) continue;
         for (int j = 0; j < ns; ++j) E[((size_t)k2 * g + k1) * ns + (j + g * k2) % ns] = D[(size_t)k * ns + j];
       }
     D.swap(E);
@@ -932,6 +944,10 @@ static void vecmat_encode(he_context* c, const double* W, int n, int m, const do
     DevDoubles d(c, D.data(), D.size());
     pd.p = encode(c, d.d, ns, items, shifted(c->hp.q[l], -pt_scale_shift), l, qp);
     pd.p->bsgs_g = g;
+    if (fold) {
+      pd.p->fold_n = n / m;
+      pd.p->fold_step = m;
+    }
   }
   if (bias) {
     std::vector<double> bs(ns, 0.0);
@@ -980,10 +996,23 @@ he_status he_vec_mat_encode_bsgs(he_context* c, const double* W, int n, int m, c
   });
 }
 
-he_status he_vec_mat_bsgs_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags, int g,
-                             const he_plaintext* bias_pt, he_ciphertext** out) {
+he_status he_vec_mat_encode_bsgs_fold(he_context* c, const double* W, int n, int m, const double* bias,
+                                      int pt_scale_shift, int level, double in_scale, int g, he_plaintext** diags,
+                                      he_plaintext** bias_pt) {
   return guard([&] {
-    need_ctx(c); need_ct(c, ct); need_pt(c, diags); need_out(out);
+    need_ctx(c);
+    need(diags && bias_pt, HE_INVALID_ARGUMENT, "null output pointer");
+    need(c->K > 0, HE_INVALID_PARAMS, "lazy ModDown needs special primes");
+    need(n >= 1 && m >= 1 && n % m == 0, HE_SHAPE_MISMATCH, "folded vec_mat needs m | n");
+    need(g >= 1 && m % g == 0 && m / g <= 4, HE_SHAPE_MISMATCH, "baby step g: g | m, at most 4 giant steps");
+    vecmat_encode(c, W, n, m, bias, 1, pt_scale_shift, level, in_scale, diags, bias_pt, 1, g, true);
+  });
+}
+
+static void vec_mat_bsgs_checks(he_context* c, const he_ciphertext* ct, const he_plaintext* diags, int g,
+                                const he_plaintext* bias_pt) {
+  {
+    need_ctx(c); need_ct(c, ct); need_pt(c, diags);
     need(diags->qp && c->K > 0, HE_LAYOUT_MISMATCH, "BSGS needs QP diagonals");
     need(ct->size == 2 && ct->level >= 1, HE_LEVEL_EXHAUSTED, "vec_mat needs a size-2 ciphertext with a level");
     need(diags->level == ct->level, HE_LEVEL_MISMATCH, "diagonals must be at the ciphertext level");
@@ -995,7 +1024,31 @@ he_status he_vec_mat_bsgs_pt(he_context* c, const he_ciphertext* ct, const he_pl
       need(bias_pt->scale == ct->scale * diags->scale / (double)c->hp.q[ct->level], HE_SCALE_MISMATCH,
            "bias scale must equal the output scale");
     }
+  }
+}
+
+he_status he_vec_mat_bsgs_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags, int g,
+                             const he_plaintext* bias_pt, he_ciphertext** out) {
+  return guard([&] {
+    need_out(out);
+    vec_mat_bsgs_checks(c, ct, diags, g, bias_pt);
+    need_vm_fold_keys(c, diags);
     *out = ct_vec_mat_bsgs(c, ct, diags, g, bias_pt);
+  });
+}
+
+he_status he_vec_mat_bsgs_fold_pt(he_context* c, const he_ciphertext* ct, const he_plaintext* diags, int g, int n,
+                                  int m, const he_plaintext* bias_pt, he_ciphertext** out) {
+  return guard([&] {
+    need_out(out);
+    vec_mat_bsgs_checks(c, ct, diags, g, bias_pt);
+    need(m >= 1 && n >= m && n % m == 0 && diags->B == ((m + g - 1) / g) * g, HE_SHAPE_MISMATCH,
+         "folded vec_mat: m | n and the diagonals hold the first m in BSGS order");
+    for (int t = 1; t < n / m; ++t) {
+      u32 gg;
+      need(galois_key(c, m * t, &gg) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step m t");
+    }
+    *out = ct_vec_mat_bsgs(c, ct, diags, g, bias_pt, n / m, m);
   });
 }
 

@@ -94,6 +94,7 @@ struct he_plaintext {
   int qp = 0;  // 1: also carries the K special limbs (data limbs first), for lazy-ModDown products
   uint32_t* dm = nullptr;  // small primes: cached Montgomery-form u32 copy (lazy vec_mat)
   int bsgs_g = 0;          // > 0: vec_mat diagonals in baby-step/giant-step order E[k2][k1], baby step g
+  int fold_n = 0, fold_step = 0;  // > 1: folded replicated-output vec_mat, sum_{t<fold_n} rot(., fold_step t)
 };
 
 namespace he {

@@ -1674,8 +1674,17 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
   return inner;
 }
 
+static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step);
+
+// diags->fold_n > 1 (he_vec_mat_encode_bsgs_fold, oracle vec_mat_bsgs_fold): the giant-step sum
+// covers the first m = fold_step diagonals; the replicated-output fold sum_{t<fold_n} rot(., m t)
+// (one hoisted unit-diagonal rotation sum) completes the n-term sum before the rescale.
 he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags, int g,
-                               const he_plaintext* bias) {
+                               const he_plaintext* bias, int fold_n, int fold_step) {
+  if (fold_n < 0) {
+    fold_n = diags->fold_n;
+    fold_step = diags->fold_step;
+  }
   const int G = diags->B / g;
   for (int k2 = 1; k2 < G; ++k2) {
     u32 gg;
@@ -1698,6 +1707,17 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
       ct_free(r);
       ct_free(acc);
       acc = s2;
+    }
+    if (fold_n > 1) {
+      he_ciphertext* f = nullptr;
+      try {
+        f = ct_rot_sum(c, acc, fold_n, fold_step);
+      } catch (...) {
+        ct_free(acc);
+        throw;
+      }
+      ct_free(acc);
+      acc = f;
     }
     he_ciphertext* res = ct_rescale(c, acc);
     ct_free(acc);

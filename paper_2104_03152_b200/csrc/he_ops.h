@@ -45,7 +45,7 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
 he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                           const he_plaintext* bias);
 he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags, int g,
-                               const he_plaintext* bias);
+                               const he_plaintext* bias, int fold_n = -1, int fold_step = 0);
 he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext* kernels,
                        const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1 = 0);
 he_ciphertext* ct_conv_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags,

@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 def cfg4():
     from paper_2104_03152_b200 import Context
     from paper_2104_03152_b200.cnn import rotation_steps
-    forms = [dict(), dict(fold_n1=8), dict(conv_g=8, fc_bsgs=True), dict(fc_bsgs=True)]
+    forms = [dict(), dict(fold_n1=8), dict(conv_g=8, fc_bsgs=True), dict(fc_bsgs=True),
+             dict(conv_g=8, fc_bsgs=True, fc1_g=32)]
     for f in forms:
         assert OC.cnn_rotation_steps(**f) == rotation_steps(**f)
     steps = sorted(set().union(*[rotation_steps(**f) for f in forms]))   # every conv / FC form
@@ -38,7 +39,7 @@ def inj(g, o, vecs, scale, level):
     return g.he_pt_from_int_coeffs(ms, scale, level)
 
 
-@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold", "bsgs+conv8"])
+@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold", "bsgs+conv8", "fast"])
 def test_cnn_layers_bit_exact(cfg4, lazy):
     """lazy=False: FC layers with one ModDown per rotation (oracle vec_mat); lazy=True: one
     ModDown per vec_mat (oracle vec_mat_lazy, QP diagonals); "bsgs": baby step n/4 with one lazy
@@ -46,7 +47,8 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
     o, g = cfg4
     w = cnn_weights(3)
     imgs = mnist_like_images(2, 4)
-    conv_g = 8 if lazy == "bsgs+conv8" else 0
+    conv_g = 8 if lazy in ("bsgs+conv8", "fast") else 0
+    fc1_g = 32 if lazy == "fast" else 0      # the bench's schedule: one-level conv + folded FC1
     ns, q, plan = o.slots, o.q, (OC.CNN_PLAN_BSGS if conv_g else OC.CNN_PLAN)
     o_in = [OC.cnn_encrypt_input(o, img, b, plan) for b, img in enumerate(imgs)]
     lvl = o_in[0].level
@@ -94,7 +96,12 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         Dv = OC.vecmat_diagonals(Wm, ns, rep)
         bs = ref[0].scale * ps / q[lvl]
         gb = inj(g, o, [OC.vecmat_bias_slots(bias, ns, rep)], bs, lvl - 1)
-        if lazy == "bsgs":
+        if name == "fc1" and fc1_g:
+            E = OC.bsgs_diagonals(Dv[:64], fc1_g).reshape(-1, ns)
+            gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in E]), ps, lvl)
+            x = g.he_vec_mat_bsgs_fold_pt(x, gD, fc1_g, 256, 64, gb)
+            ref = [OC.vec_mat_bsgs_fold(o, c, Wm, bias, shift, g=fc1_g) for c in ref]
+        elif lazy == "bsgs":
             gg = Wm.shape[0] // 4
             E = OC.bsgs_diagonals(Dv, gg).reshape(-1, ns)
             gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in E]), ps, lvl)
@@ -121,14 +128,15 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         assert np.allclose(z[b], o.decode(o.decrypt(ref[b]), 10), rtol=1e-9, atol=1e-9)
 
 
-@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold", "bsgs+conv8"])
+@pytest.mark.parametrize("lazy", [False, True, "bsgs", "bsgs+fold", "bsgs+conv8", "fast"])
 def test_cnn_all_gpu_tolerance(cfg4, lazy):
     """Own encode/encrypt/decrypt/decode: logits within 5e-3 abs of float64, argmax equal."""
     from paper_2104_03152_b200.cnn import EncryptedCNN
     o, g = cfg4
     w = cnn_weights(3)
-    net = EncryptedCNN(g, w, lazy=bool(lazy), bsgs=lazy in ("bsgs", "bsgs+fold", "bsgs+conv8"),
-                       fold_n1=8 if lazy == "bsgs+fold" else 0, conv_g=8 if lazy == "bsgs+conv8" else 0)
+    net = EncryptedCNN(g, w, lazy=bool(lazy), bsgs=lazy in ("bsgs", "bsgs+fold", "bsgs+conv8", "fast"),
+                       fold_n1=8 if lazy == "bsgs+fold" else 0, conv_g=8 if lazy in ("bsgs+conv8", "fast") else 0,
+                       fc1_g=32 if lazy == "fast" else 0)
     imgs = mnist_like_images(16, 4)
     logits = net.decrypt(net.forward(net.encrypt(imgs, 1000)))
     for b, img in enumerate(imgs):

@@ -184,17 +184,35 @@ def test_one_level_conv_diagonals_by_hand():
     assert D[1].tolist() == [2, 2, 30, 30, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 10, 10]
 
 
+def test_replicated_vecmat_fold_identity():
+    """Replicated-output diagonals are rotation-periodic, D_{k + m t} = rot(D_k, m t), so the first
+    m diagonals plus a fold over m t give x @ W replicated (the oracle's vec_mat_bsgs_fold), pinned
+    against numpy matmul with the slot simulator; a fold with the wrong step does not."""
+    rng = np.random.default_rng(3)
+    x, W = rng.normal(size=256), rng.normal(size=(256, 64))
+    D = C.vecmat_diagonals(W, NS, True)
+    for k in (0, 5, 63):
+        for t in (1, 3):
+            assert np.array_equal(D[k + 64 * t], np.roll(D[k], -64 * t))
+    xr = C.replicate(x, NS)
+    yp = sum(np.roll(xr, -k) * D[k] for k in range(64))
+    y = sum(np.roll(yp, -64 * t) for t in range(4))
+    assert np.allclose(y, np.tile(x @ W, NS // 64), atol=1e-9)
+    bad = sum(np.roll(yp, -32 * t) for t in range(4))
+    assert not np.allclose(bad, np.tile(x @ W, NS // 64), atol=1e-3)
+
+
 @pytest.mark.slow
 def test_oracle_cnn_fast_schedule_end_to_end():
-    """The oracle with the bench's evaluation schedule (one-level conv, BSGS FC layers, input one
-    level lower) meets the same 5e-3 / argmax bar against the float network."""
+    """The oracle with the bench's evaluation schedule (one-level conv, folded BSGS FC1, BSGS FC2,
+    input one level lower) meets the same 5e-3 / argmax bar against the float network."""
     from oracle.oracle import OracleContext
     w = cnn_weights(3)
     img = mnist_like_images(1, 4, start=9)[0]
     ctx = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-    ctx.keygen(C.cnn_rotation_steps(conv_g=C.CONV_G, fc_bsgs=True))   # 77 keys
+    ctx.keygen(C.cnn_rotation_steps(conv_g=C.CONV_G, fc_bsgs=True, fc1_g=C.FC1_G))   # 47 keys
     ct = C.cnn_encrypt_input(ctx, img, 0, C.CNN_PLAN_BSGS)
-    out = C.cnn_forward(ctx, ct, w, lazy=True, bsgs=True, conv_g=C.CONV_G)
+    out = C.cnn_forward(ctx, ct, w, lazy=True, bsgs=True, conv_g=C.CONV_G, fc1_g=C.FC1_G)
     assert ct.level == ctx.L - 2 and out.level == 0
     z = ctx.decode(ctx.decrypt(out), 10)
     ref = float_net_numpy(img, w)

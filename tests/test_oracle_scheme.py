@@ -366,3 +366,22 @@ def test_one_level_conv_oracle_pin():
     # fresh noise ~1.4e-5 per slot (N = 2^11, scale 2^30) times |k| <= 1 over 4 taps, plus rescale
     # and key-switch rounding: ~3e-5 measured for the paper's order
     assert np.max(np.abs(zn - ref)) < 2e-4 and np.max(np.abs(zo - ref)) < 2e-4
+
+
+def test_vec_mat_bsgs_fold_oracle_pin():
+    """Oracle vec_mat_bsgs_fold (n 64 -> m 16, g 8: 2 groups, fold 4) decrypts to x @ W replicated
+    (numpy) within CKKS noise and to the same values as the plain diagonal method (vec_mat)."""
+    from oracle import circuits as OC
+    c = OracleContext(11, (50, 40, 40, 50), 1, 9)
+    ns, n, m, g = 1024, 64, 16, 8
+    c.keygen(sorted(set(range(1, n)) | {16, 32, 48}))
+    rng = np.random.default_rng(11)
+    x, W, bias = rng.uniform(-1, 1, n), rng.normal(0, 0.2, (n, m)), rng.uniform(-0.5, 0.5, m)
+    ct = c.encrypt(c.encode(OC.replicate(x, ns), 2.0 ** 30, 2), 0)
+    f = OC.vec_mat_bsgs_fold(c, ct, W, bias, 0, g=g)
+    p = OC.vec_mat(c, ct, W, bias, True, 0)
+    assert f.level == p.level == 1 and f.scale == p.scale
+    ref = np.tile(x @ W + bias, ns // m)
+    zf, zp = c.decode(c.decrypt(f)), c.decode(c.decrypt(p))
+    # fresh noise ~1.4e-5 per slot times |W| summed over 64 terms, plus key-switch and rescale rounding
+    assert np.max(np.abs(zf - ref)) < 2e-4 and np.max(np.abs(zp - ref)) < 2e-4
