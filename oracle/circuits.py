@@ -266,6 +266,7 @@ CNN_PLAN = dict(in_log2=30, conv_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=
 CNN_PLAN_BSGS = dict(in_log2=30, conv_shift=-2, fc1_shift=-4, fc2_shift=-4, in_level_drop=1)
 CONV_G = 8          # baby steps of the one-level conv: 8 chunks x 8 giant steps
 FC1_G = 32          # baby steps of the folded FC1 (vec_mat_bsgs_fold): 32 x 2 groups, fold 4
+FC2_M = 16          # folded FC2: outputs padded to 16, 16 diagonals (one group), fold 4
 
 
 def cnn_rotation_steps(ns: int = 4096, chunk: int = 64, fold_n1: int = 0, conv_g: int = 0,
@@ -304,7 +305,8 @@ def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False, b
     """The paper's network; lazy=True uses vec_mat_lazy for FC1/FC2, bsgs=True
     vec_mat_bsgs (baby step n/4); fold_n1 > 0 the hoisted conv fold; conv_g > 0 the one-level
     conv (im2col_conv_bsgs, plan CNN_PLAN_BSGS, input from cnn_encrypt_input with that plan);
-    fc1_g > 0 (with bsgs) FC1 as vec_mat_bsgs_fold with baby step fc1_g."""
+    fc1_g > 0 (with bsgs) FC1 as vec_mat_bsgs_fold with baby step fc1_g and FC2 folded with its
+    outputs padded to FC2_M."""
     plan = plan or (CNN_PLAN_BSGS if conv_g else CNN_PLAN)
 
     def vm(x, W, b, rep, shift):
@@ -323,8 +325,25 @@ def cnn_forward(ctx: OracleContext, ct: OCt, w, plan=None, lazy: bool = False, b
     else:
         x = vm(x, w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"])
     x = ctx.square(x)
-    x = vm(x, w.fc2_w.T, w.fc2_b, False, -plan["fc2_shift"])
+    if bsgs and fc1_g:
+        # FC2 with its 10 outputs padded to 16 columns (zero weights and bias): the output is then
+        # replicated with period 16 | 64 and folds like FC1 (16 diagonals, fold 4); slots 0..9 hold
+        # the logits as before (DESIGN.md §3 'folded FC layers')
+        W2, b2 = pad_columns(w.fc2_w.T, w.fc2_b, FC2_M)
+        x = vec_mat_bsgs_fold(ctx, x, W2, b2, -plan["fc2_shift"], g=FC2_M)
+    else:
+        x = vm(x, w.fc2_w.T, w.fc2_b, False, -plan["fc2_shift"])
     return x
+
+
+def pad_columns(W: np.ndarray, b: np.ndarray, m: int):
+    """W (n x m0) and bias (m0) padded with zero columns / entries to m >= m0 outputs."""
+    n, m0 = W.shape
+    Wp = np.zeros((n, m))
+    Wp[:, :m0] = W
+    bp = np.zeros(m)
+    bp[:m0] = b
+    return Wp, bp
 
 
 # ------------------------------------------------------------ config 5b ---

@@ -22,6 +22,7 @@ PLAN = dict(in_log2=30, kernel_shift=0, mask_shift=-4, fc1_shift=0, fc2_shift=4)
 PLAN_BSGS = dict(in_log2=30, conv_shift=-2, fc1_shift=-4, fc2_shift=4, in_level_drop=1)
 CONV_G = 8          # one-level conv: 8 baby steps (chunks) x 8 giant steps
 FC1_G = 32          # folded FC1 (he_vec_mat_encode_bsgs_fold): baby step 32, 2 groups, fold 4
+FC2_M = 16          # folded FC2: outputs padded to 16 columns, 16 diagonals (one group), fold 4
 CHUNK = 64          # next power of two >= 64 windows (C18)
 KH = KW = 7
 STRIDE = 3
@@ -96,9 +97,17 @@ class EncryptedCNN:
         lvl -= 1
         s = s * s / ctx.q[lvl]
         lvl -= 1
-        g2 = np.asarray(w.fc2_w).shape[1] // 4 if self.bsgs else 0
-        self.fc2_d, self.fc2_b = ctx.he_vec_mat_encode(np.asarray(w.fc2_w).T, w.fc2_b, False,
-                                                       self.plan["fc2_shift"], lvl, s, lazy=lazy, bsgs_g=g2)
+        if fold:    # FC2 outputs padded to FC2_M zero columns: replicated with period 16, folded
+            W2 = np.zeros((np.asarray(w.fc2_w).shape[1], FC2_M))
+            W2[:, :np.asarray(w.fc2_w).shape[0]] = np.asarray(w.fc2_w).T
+            b2 = np.zeros(FC2_M)
+            b2[:len(w.fc2_b)] = w.fc2_b
+            self.fc2_d, self.fc2_b = ctx.he_vec_mat_encode(W2, b2, True, self.plan["fc2_shift"], lvl, s,
+                                                           lazy=lazy, bsgs_g=FC2_M, fold=True)
+        else:
+            g2 = np.asarray(w.fc2_w).shape[1] // 4 if self.bsgs else 0
+            self.fc2_d, self.fc2_b = ctx.he_vec_mat_encode(np.asarray(w.fc2_w).T, w.fc2_b, False,
+                                                           self.plan["fc2_shift"], lvl, s, lazy=lazy, bsgs_g=g2)
         self.n_out = int(np.asarray(w.fc2_w).shape[0])
 
     def im2col(self, imgs: np.ndarray) -> np.ndarray:

@@ -96,11 +96,17 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         Dv = OC.vecmat_diagonals(Wm, ns, rep)
         bs = ref[0].scale * ps / q[lvl]
         gb = inj(g, o, [OC.vecmat_bias_slots(bias, ns, rep)], bs, lvl - 1)
-        if name == "fc1" and fc1_g:
-            E = OC.bsgs_diagonals(Dv[:64], fc1_g).reshape(-1, ns)
+        if fc1_g:           # folded FC layers (FC2 padded to 16 outputs)
+            if name == "fc2":
+                Wm, bias = OC.pad_columns(Wm, bias, OC.FC2_M)
+                Dv = OC.vecmat_diagonals(Wm, ns, True)
+                gb = inj(g, o, [OC.vecmat_bias_slots(bias, ns, True)], bs, lvl - 1)
+            n_, m_ = Wm.shape
+            gg = fc1_g if name == "fc1" else OC.FC2_M
+            E = OC.bsgs_diagonals(Dv[:m_], gg).reshape(-1, ns)
             gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in E]), ps, lvl)
-            x = g.he_vec_mat_bsgs_fold_pt(x, gD, fc1_g, 256, 64, gb)
-            ref = [OC.vec_mat_bsgs_fold(o, c, Wm, bias, shift, g=fc1_g) for c in ref]
+            x = g.he_vec_mat_bsgs_fold_pt(x, gD, gg, n_, m_, gb)
+            ref = [OC.vec_mat_bsgs_fold(o, c, Wm, bias, shift, g=gg) for c in ref]
         elif lazy == "bsgs":
             gg = Wm.shape[0] // 4
             E = OC.bsgs_diagonals(Dv, gg).reshape(-1, ns)
