@@ -53,8 +53,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def cu(f):
         o = os.path.join(objdir, f + ".o")
+        extra = os.environ.get("HE_NVCC_EXTRA", "").split()   # experiments only (e.g. -DHE_NTT32_MINB=2)
         out = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                    "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr",
+                    "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr", *extra,
                     "-I", CSRC, "-c", os.path.join(CSRC, f), "-o", o])
         if verbose:
             sys.stderr.write(out)

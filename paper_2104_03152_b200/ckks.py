@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhe_ckks.so")
+# HE_CKKS_LIB: load another in-tree build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("HE_CKKS_LIB") or os.path.join(_HERE, "libhe_ckks.so")
 
 STATUS = {
     0: "OK", 1: "INVALID_PARAMS", 2: "PARAM_MISMATCH", 3: "DOMAIN_MISMATCH", 4: "LEVEL_MISMATCH",

@@ -269,16 +269,20 @@ __device__ __forceinline__ void ntt_pass32_io(u32 tid, const uint2* __restrict__
     u32 x[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) x[k] = ld(base + (k << LO));
+    // twiddle of the butterfly on bit b at index j: tw[2^s + (j >> (b + 1))], s = LOGN-1-b.  With
+    // j = hi << (LO+NB) | k << LO | lo, j >> (b+1) = (hi << (LO+NB-1-b)) | (k >> (b+1-LO)): one
+    // base pointer per stage and compile-time offsets (identical offsets share one load).
+    const u32 hi = g >> LO;
 #pragma unroll
     for (int ss = 0; ss < NB; ++ss) {
       const int b = INV ? LO + ss : LO + NB - 1 - ss;
       const int s = LOGN - 1 - b;
       const int half = INV ? 1 << ss : 1 << (NB - 1 - ss);
+      const uint2* tws = tw + (1u << s) + (hi << (LO + NB - 1 - b));
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if (k & half) continue;
-        const u32 j = base + (k << LO);
-        const uint2 w = __ldg(tw + (1u << s) + (j >> (LOGN - s)));
+        const uint2 w = __ldg(tws + (k >> (b + 1 - LO)));
         if (LAZY) {
           if (!INV) ct_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
           else gs_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
@@ -293,10 +297,45 @@ __device__ __forceinline__ void ntt_pass32_io(u32 tid, const uint2* __restrict__
   }
 }
 
+// Shared-memory pass.  base has zero bits in [LO, LO+NB), so base + (k << LO) is base | (k << LO)
+// and spad32(base + (k << LO)) = spad32(base) + (k << LO) + ((k << LO) >> 5): one padded base
+// pointer per group and compile-time offsets (LDS/STS with immediate offsets).
 template <int LOGN, bool INV, int LO, int NB, bool LAZY = false>
 __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __restrict__ tw, u32 q) {
-  ntt_pass32_io<LOGN, INV, LO, NB, LAZY>(
-      tid, tw, q, [&](u32 i) { return sm[spad32(i)]; }, [&](u32 i, u32 v) { sm[spad32(i)] = v; });
+  typedef NttGeom<LOGN, 1> G;
+  constexpr int NG = 1 << (G::R - NB);
+  constexpr int E = 1 << NB;
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    const u32 g = tid + gi * G::T;
+    const u32 base = ((g >> LO) << (LO + NB)) | (g & ((1u << LO) - 1u));
+    u32* p = sm + spad32(base);
+    u32 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = p[(k << LO) + ((k << LO) >> 5)];
+    const u32 hi = g >> LO;
+#pragma unroll
+    for (int ss = 0; ss < NB; ++ss) {
+      const int b = INV ? LO + ss : LO + NB - 1 - ss;
+      const int s = LOGN - 1 - b;
+      const int half = INV ? 1 << ss : 1 << (NB - 1 - ss);
+      const uint2* tws = tw + (1u << s) + (hi << (LO + NB - 1 - b));
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & half) continue;
+        const uint2 w = __ldg(tws + (k >> (b + 1 - LO)));
+        if (LAZY) {
+          if (!INV) ct_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
+          else gs_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
+        } else {
+          if (!INV) ct_bfly32(x[k], x[k + half], w.x, w.y, q);
+          else gs_bfly32(x[k], x[k + half], w.x, w.y, q);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) p[(k << LO) + ((k << LO) >> 5)] = x[k];
+  }
 }
 
 // Passes P0 .. PEND-1 (pass P covers bit group GP = INV ? P : NPASS-1-P).
@@ -364,7 +403,7 @@ __device__ __forceinline__ u32 ntt_reduce32(u32 v, u32 q) {
 template <int LOGN>
 struct NttGeom32 {
   static constexpr int SMEM = ((1 << LOGN) + (1 << LOGN) / 32) * 4;
-  static constexpr int MINB = (1 << LOGN) <= 8192 ? 3 : 2;
+  static constexpr int MINB = (1 << LOGN) <= 8192 ? 3 : 2;   // 3 CTAs/SM at N = 2^13 (MINB 2: -17%)
 };
 
 template <int LOGN, bool INV, class Job>
