@@ -224,11 +224,16 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
     # communication per inference: serialized encrypted input + encrypted logits of one image
-    one = ctx.he_encrypt(ctx.he_encode(slots_dev[0][:1], 2.0 ** net.plan["in_log2"], net.top), 7)
+    pt1 = ctx.he_encode(slots_dev[0][:1], 2.0 ** net.plan["in_log2"], net.top)
+    one = ctx.he_encrypt(pt1, 7)
     up = len(ctx.he_ct_serialize(one))
+    up_seeded = len(ctx.he_ct_serialize_seeded(ctx.he_encrypt_symmetric(pt1, 7, 0x5EED)))
     down = len(ctx.he_ct_serialize(net.forward(one)))
-    comm = {"input_bytes": up, "output_bytes": down, "total_bytes": up + down, "paper_total": "427 KB (PAPER.md:120)",
-            "format": "bit-packed NTT words, w_i = bit_length(q_i) (DESIGN.md §3 wire format)"}
+    comm = {"input_bytes": up, "output_bytes": down, "total_bytes": up + down,
+            "input_bytes_seeded_symmetric": up_seeded, "total_bytes_seeded": up_seeded + down,
+            "paper_total": "427 KB (PAPER.md:120)",
+            "format": "bit-packed NTT words, w_i = bit_length(q_i); seeded form = c0 + (a_seed, stream) "
+                      "(DESIGN.md §3 wire format)"}
     e2e = {"value": world * B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": B * ns * 8, "d2h_bytes_per_step": B * net.n_out * 8}
 

@@ -159,6 +159,16 @@ he_status he_decode_device(he_context* ctx, const he_plaintext* pt, double* out_
  * (v, e0, e1) from Philox stream `stream_id + b`.  Output scale/level = pt's. */
 he_status he_encrypt(he_context* ctx, const he_plaintext* pt, uint64_t stream_id,
                      he_ciphertext** out);
+/* Symmetric (secret-key) encryption (SURVEY 8(f) #3 "seeded symmetric
+ * encryption halves the upload"): item b gets
+ *   c1 = a,  a_i = Uniform(a_seed, stream (SYM_A, stream_id + b, i))   (C13 sampler)
+ *   c0 = -a s + e + m,  e = CDT(context seed, stream (SYM_E, stream_id + b, 0))   (C11)
+ * a_seed is PUBLIC (it travels in the seeded wire form; it must not be the
+ * context seed, which also derives the secret key).  The result is marked
+ * seeded: he_ct_serialize_seeded can omit c1.  Needs the secret key
+ * (HE_MISSING_KEY).  Output scale/level = pt's. */
+he_status he_encrypt_symmetric(he_context* ctx, const he_plaintext* pt, uint64_t stream_id, uint64_t a_seed,
+                               he_ciphertext** out);
 /* m = c0 + c1 s (+ c2 s^2).  Needs the secret key. */
 he_status he_decrypt(he_context* ctx, const he_ciphertext* ct, he_plaintext** out);
 
@@ -360,7 +370,14 @@ size_t he_key_words(const he_context* ctx, int kind);
 he_status he_ct_serialized_size(he_context* ctx, const he_ciphertext* ct, size_t* bytes);
 /* Write header + payload to dst (host, or device when on_device != 0). */
 he_status he_ct_serialize(he_context* ctx, const he_ciphertext* ct, void* dst, int on_device);
-/* Read a serialized ciphertext of len bytes; rejects a bad header, a wrong
+/* Seeded form of a fresh he_encrypt_symmetric ciphertext (HE_INVALID_ARGUMENT
+ * for any other ciphertext): magic "HECKKSS1", the same header fields with
+ * size 2, the 20-byte tail holding u64 a_seed, u64 stream_id, 4 zero bytes;
+ * the payload is c0 of every item only (half the bytes). */
+he_status he_ct_serialized_size_seeded(he_context* ctx, const he_ciphertext* ct, size_t* bytes);
+he_status he_ct_serialize_seeded(he_context* ctx, const he_ciphertext* ct, void* dst, int on_device);
+/* Read a serialized ciphertext of len bytes (either form; a seeded one gets
+ * its c1 regenerated on the device); rejects a bad header, a wrong
  * length or a residue >= its prime (HE_INVALID_ARGUMENT), other parameters
  * (HE_PARAM_MISMATCH). */
 he_status he_ct_deserialize(he_context* ctx, const void* src, int on_device, size_t len, he_ciphertext** out);

@@ -195,7 +195,8 @@ void philox_block(u64 seed, u64 sid, u64 block, u32 out[4]) {
 // C9 stream id: purpose<<56 | object<<16 | prime_index
 enum Purpose : u64 {
   P_S = 1, P_PK_A = 2, P_PK_E = 3, P_RLK_A = 4, P_RLK_E = 5,
-  P_GK_A = 6, P_GK_E = 7, P_ENC_V = 8, P_ENC_E0 = 9, P_ENC_E1 = 10
+  P_GK_A = 6, P_GK_E = 7, P_ENC_V = 8, P_ENC_E0 = 9, P_ENC_E1 = 10,
+  P_SYM_A = 11, P_SYM_E = 12   // symmetric encryption (DESIGN.md §3 reading "seeded symmetric")
 };
 u64 make_sid(u64 purpose, u64 object, u64 prime) {
   return (purpose << 56) | (object << 16) | prime;
@@ -795,6 +796,28 @@ void orc_encrypt(void* h, const uint64_t* pt, int level, uint64_t stream_id, uin
       c0[n] = addmod(addmod(mulmod(vt[n], b[n], qi), e0t[n], qi), pt[(size_t)i * N + n], qi);
       c1[n] = addmod(mulmod(vt[n], a[n], qi), e1t[n], qi);
     }
+  }
+}
+
+// Symmetric encryption (DESIGN.md §3 "seeded symmetric encryption"):
+// a_i = Uniform(a_seed, (P_SYM_A, stream_id, i)) -- the PUBLIC seed --, e = CDT(seed, (P_SYM_E,
+// stream_id, 0)); c0 = -a s + e + m, c1 = a (NTT domain, level l).
+void orc_encrypt_symmetric(void* h, const uint64_t* pt, int level, uint64_t stream_id, uint64_t a_seed,
+                           uint64_t* ct) {
+  Ctx* c = (Ctx*)h;
+  const int N = c->N, Lc = level + 1;
+  std::vector<i64> e(N);
+  sample_cdt(c->seed, make_sid(P_SYM_E, stream_id, 0), N, c->cdt.data(), (int)c->cdt.size(), e.data());
+  std::vector<u64> et(N);
+  for (int i = 0; i < Lc; ++i) {
+    const u64 qi = c->q[i];
+    u64* c0 = ct + (size_t)i * N;
+    u64* c1 = ct + ((size_t)Lc + i) * N;
+    sample_uniform(a_seed, make_sid(P_SYM_A, stream_id, (u64)i), qi, N, c1);
+    signed_to_ntt(*c, e.data(), i, et.data());
+    for (int n = 0; n < N; ++n)
+      c0[n] = addmod(addmod(negmod(mulmod(c1[n], c->s_ntt[(size_t)i * N + n], qi), qi), et[n], qi),
+                     pt[(size_t)i * N + n], qi);
   }
 }
 

@@ -83,6 +83,8 @@ def lib():
         L.orc_decode.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_double,
                                  ctypes.c_int, DP, DP]
         L.orc_encrypt.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_uint64, U64P]
+        L.orc_encrypt_symmetric.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                            U64P]
         L.orc_decrypt.argtypes = [ctypes.c_void_p, U64P, ctypes.c_int, ctypes.c_int, U64P]
         L.orc_pointwise.argtypes = [ctypes.c_void_p, ctypes.c_int, U64P, U64P, ctypes.c_int,
                                     ctypes.c_int, ctypes.c_int, U64P]
@@ -316,6 +318,13 @@ class OracleContext:
         out = np.zeros((2, pt.level + 1, self.N), dtype=np.uint64)
         w = _u64(pt.words)
         self.lib.orc_encrypt(self.h, _p(w, U64P), pt.level, stream_id, _p(out, U64P))
+        return OCt(out, pt.level, pt.scale)
+
+    def encrypt_symmetric(self, pt: OPt, stream_id: int, a_seed: int) -> OCt:
+        """c1 = a = Uniform(a_seed, (SYM_A, stream_id, i)), c0 = -a s + e + m."""
+        out = np.zeros((2, pt.level + 1, self.N), dtype=np.uint64)
+        w = _u64(pt.words)
+        self.lib.orc_encrypt_symmetric(self.h, _p(w, U64P), pt.level, stream_id, a_seed, _p(out, U64P))
         return OCt(out, pt.level, pt.scale)
 
     def decrypt(self, ct: OCt) -> OPt:

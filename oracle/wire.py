@@ -17,6 +17,7 @@ import numpy as np
 
 HEADER_BYTES = 64
 MAGIC = b"HECKKS01"
+MAGIC_SEEDED = b"HECKKSS1"
 
 
 def limb_widths(primes, level: int) -> list:
@@ -51,3 +52,16 @@ def pack(words: np.ndarray, primes, level: int, scale: float) -> bytes:
     hdr = MAGIC + struct.pack("<IIIIdQI", N.bit_length() - 1, B, size, level, float(scale), len(out), nl)
     hdr += bytes(HEADER_BYTES - len(hdr))
     return bytes(hdr) + bytes(out)
+
+
+def pack_seeded(c0_words: np.ndarray, primes, level: int, scale: float, a_seed: int, stream0: int) -> bytes:
+    """Seeded form of a fresh symmetric ciphertext: c0_words [B][level+1][N]; header
+    magic b"HECKKSS1", size field 2, the 20-byte tail = u64 a_seed | u64 stream0 | 4 zero bytes;
+    payload = the c0 limbs packed exactly as pack() packs a size-1 batch."""
+    B = c0_words.shape[0]
+    body = pack(c0_words.reshape(B, 1, level + 1, -1), primes, level, scale)[HEADER_BYTES:]
+    N = c0_words.shape[-1]
+    hdr = MAGIC_SEEDED + struct.pack("<IIIIdQIQQ", N.bit_length() - 1, B, 2, level, float(scale), len(body),
+                                     level + 1, a_seed, stream0)
+    hdr += bytes(HEADER_BYTES - len(hdr))
+    return bytes(hdr) + body

@@ -63,6 +63,7 @@ _SIGS = {
     "he_decode": [VP, VP, DP, SZ],
     "he_decode_device": [VP, VP, VP, SZ],
     "he_encrypt": [VP, VP, C.c_uint64, VPP],
+    "he_encrypt_symmetric": [VP, VP, C.c_uint64, C.c_uint64, VPP],
     "he_decrypt": [VP, VP, VPP],
     "he_add": [VP, VP, VP, VPP],
     "he_sub": [VP, VP, VP, VPP],
@@ -117,6 +118,8 @@ _SIGS = {
     "he_key_words": [VP, C.c_int],
     "he_ct_serialized_size": [VP, VP, C.POINTER(SZ)],
     "he_ct_serialize": [VP, VP, VP, C.c_int],
+    "he_ct_serialized_size_seeded": [VP, VP, C.POINTER(SZ)],
+    "he_ct_serialize_seeded": [VP, VP, VP, C.c_int],
     "he_ct_deserialize": [VP, VP, C.c_int, SZ, VPP],
     "he_ntt_forward": [VP, VP, SZ, C.c_int],
     "he_ntt_inverse": [VP, VP, SZ, C.c_int],
@@ -382,6 +385,12 @@ class Context:
         _check(lib().he_encrypt(self.h, pt.h, stream_id, C.byref(h)))
         return Ciphertext(self, h)
 
+    def he_encrypt_symmetric(self, pt: Plaintext, stream_id: int, a_seed: int) -> Ciphertext:
+        """Secret-key encryption with c1 drawn from the public seed a_seed (seeded wire form)."""
+        h = C.c_void_p()
+        _check(lib().he_encrypt_symmetric(self.h, pt.h, stream_id, a_seed, C.byref(h)))
+        return Ciphertext(self, h)
+
     def he_decrypt(self, ct: Ciphertext) -> Plaintext:
         h = C.c_void_p()
         _check(lib().he_decrypt(self.h, ct.h, C.byref(h)))
@@ -512,6 +521,13 @@ class Context:
         _check(lib().he_ct_serialized_size(self.h, ct.h, C.byref(n)))
         buf = C.create_string_buffer(n.value)
         _check(lib().he_ct_serialize(self.h, ct.h, buf, 0))
+        return buf.raw
+
+    def he_ct_serialize_seeded(self, ct: Ciphertext) -> bytes:
+        n = SZ()
+        _check(lib().he_ct_serialized_size_seeded(self.h, ct.h, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().he_ct_serialize_seeded(self.h, ct.h, buf, 0))
         return buf.raw
 
     def he_ct_deserialize(self, data: bytes) -> Ciphertext:

@@ -295,6 +295,18 @@ he_status he_encrypt(he_context* c, const he_plaintext* pt, uint64_t stream_id, 
   });
 }
 
+he_status he_encrypt_symmetric(he_context* c, const he_plaintext* pt, uint64_t stream_id, uint64_t a_seed,
+                               he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c);
+    need_pt(c, pt);
+    need_out(out);
+    need(c->has_sk, HE_MISSING_KEY, "symmetric encryption needs the secret key");
+    need(!pt->qp, HE_LAYOUT_MISMATCH, "plaintext must be on the data limbs only");
+    *out = encrypt_symmetric(c, pt, stream_id, a_seed);
+  });
+}
+
 he_status he_decrypt(he_context* c, const he_ciphertext* ct, he_plaintext** out) {
   return guard([&] {
     need_ctx(c);
@@ -1241,10 +1253,17 @@ struct WireHeader {
   double scale;
   uint64_t payload_bytes;
   uint32_t n_limbs;
-  char pad[20];
+  char pad[20];   // seeded form: u64 a_seed, u64 stream0, 4 zero bytes (unaligned: memcpy)
 };
 static_assert(sizeof(WireHeader) == 64, "wire header is 64 bytes");
 const char kMagic[8] = {'H', 'E', 'C', 'K', 'K', 'S', '0', '1'};
+const char kMagicSeeded[8] = {'H', 'E', 'C', 'K', 'K', 'S', 'S', '1'};
+
+size_t limb_bytes(he_context* c, int level) {
+  size_t b = 0;
+  for (int i = 0; i <= level; ++i) b += (size_t)c->N * c->hp.kbits[i] / 8;
+  return b;
+}
 }  // namespace
 
 he_status he_ct_serialized_size(he_context* c, const he_ciphertext* ct, size_t* bytes) {
@@ -1281,6 +1300,54 @@ he_status he_ct_serialize(he_context* c, const he_ciphertext* ct, void* dst, int
   });
 }
 
+he_status he_ct_serialized_size_seeded(he_context* c, const he_ciphertext* ct, size_t* bytes) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(bytes);
+    need(ct->seeded, HE_INVALID_ARGUMENT, "only fresh symmetric ciphertexts have a seeded form");
+    *bytes = sizeof(WireHeader) + limb_bytes(c, ct->level) * ct->B;
+  });
+}
+
+he_status he_ct_serialize_seeded(he_context* c, const he_ciphertext* ct, void* dst, int on_device) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, ct); need_out(dst);
+    need(ct->seeded, HE_INVALID_ARGUMENT, "only fresh symmetric ciphertexts have a seeded form");
+    WireHeader h;
+    memset(&h, 0, sizeof(h));
+    memcpy(h.magic, kMagicSeeded, 8);
+    h.log2N = c->logN;
+    h.B = ct->B;
+    h.size = 2;
+    h.level = ct->level;
+    h.scale = ct->scale;
+    h.payload_bytes = limb_bytes(c, ct->level) * ct->B;
+    h.n_limbs = ct->level + 1;
+    memcpy(h.pad, &ct->a_seed, 8);
+    memcpy(h.pad + 8, &ct->stream0, 8);
+    // c0 of every item as a size-1 batch, packed like he_ct_serialize
+    he_ciphertext* c0 = ct_new(c, ct->B, 1, ct->level, ct->scale);
+    try {
+      ct_copy_c0(c, ct, c0->d, false);
+      char* d = (char*)dst;
+      if (on_device) {
+        HE_CK(cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+        wire_pack(c, c0, (u64*)(d + sizeof(h)));
+        HE_CK(cudaStreamSynchronize(c->stream));   // h is on this stack frame
+      } else {
+        memcpy(d, &h, sizeof(h));
+        Scratch buf(c, h.payload_bytes);
+        wire_pack(c, c0, buf.as<u64>());
+        HE_CK(cudaMemcpyAsync(d + sizeof(h), buf.p, h.payload_bytes, cudaMemcpyDeviceToHost, c->stream));
+        HE_CK(cudaStreamSynchronize(c->stream));
+      }
+    } catch (...) {
+      ct_free(c0);
+      throw;
+    }
+    ct_free(c0);
+  });
+}
+
 he_status he_ct_deserialize(he_context* c, const void* src, int on_device, size_t len, he_ciphertext** out) {
   return guard([&] {
     need_ctx(c); need_out(out);
@@ -1292,16 +1359,40 @@ he_status he_ct_deserialize(he_context* c, const void* src, int on_device, size_
     } else {
       memcpy(&h, src, sizeof(h));
     }
-    need(memcmp(h.magic, kMagic, 8) == 0, HE_INVALID_ARGUMENT, "bad wire magic");
+    const bool seeded = memcmp(h.magic, kMagicSeeded, 8) == 0;
+    need(seeded || memcmp(h.magic, kMagic, 8) == 0, HE_INVALID_ARGUMENT, "bad wire magic");
     need((int)h.log2N == c->logN, HE_PARAM_MISMATCH, "ring degree differs from the context's");
-    need(h.size == 2 || h.size == 3, HE_SHAPE_MISMATCH, "size must be 2 or 3");
+    need(h.size == 2 || (!seeded && h.size == 3), HE_SHAPE_MISMATCH, "size must be 2 or 3 (seeded: 2)");
     need((int)h.level < c->L && h.n_limbs == h.level + 1 && h.B >= 1, HE_INVALID_ARGUMENT, "bad header");
     // payload length implied by the context's primes must match the header and the buffer
-    size_t expect = 0;
-    for (uint32_t i = 0; i <= h.level; ++i) expect += (size_t)c->N * c->hp.kbits[i] / 8;
-    expect *= (size_t)h.B * h.size;
+    const size_t expect = limb_bytes(c, (int)h.level) * h.B * (seeded ? 1 : h.size);
     need(expect == h.payload_bytes && len == sizeof(h) + expect, HE_INVALID_ARGUMENT, "wire length mismatch");
     const char* s = (const char*)src + sizeof(h);
+    if (seeded) {   // payload = c0 of every item; c1 regenerated from (a_seed, stream0)
+      u64 a_seed, stream0;
+      memcpy(&a_seed, h.pad, 8);
+      memcpy(&stream0, h.pad + 8, 8);
+      Scratch buf(c, expect);
+      if (on_device) HE_CK(cudaMemcpyAsync(buf.p, s, expect, cudaMemcpyDeviceToDevice, c->stream));
+      else HE_CK(cudaMemcpyAsync(buf.p, s, expect, cudaMemcpyHostToDevice, c->stream));
+      he_ciphertext* c0 = wire_unpack(c, buf.as<u64>(), h.B, 1, (int)h.level, h.scale);
+      he_ciphertext* ct = nullptr;
+      try {
+        ct = ct_new(c, h.B, 2, (int)h.level, h.scale);
+        ct->seeded = 1;
+        ct->a_seed = a_seed;
+        ct->stream0 = stream0;
+        ct_copy_c0(c, ct, c0->d, true);
+        sym_regen_c1(c, ct);
+      } catch (...) {
+        ct_free(c0);
+        ct_free(ct);
+        throw;
+      }
+      ct_free(c0);
+      *out = ct;
+      return;
+    }
     if (on_device) {
       *out = wire_unpack(c, (const u64*)s, h.B, (int)h.size, (int)h.level, h.scale);
     } else {

@@ -145,7 +145,8 @@ __device__ __forceinline__ u32 uint4_at(const uint4& v, int i) {
 // C9 stream id
 enum Purpose : u64 {
   PUR_S = 1, PUR_PK_A = 2, PUR_PK_E = 3, PUR_RLK_A = 4, PUR_RLK_E = 5,
-  PUR_GK_A = 6, PUR_GK_E = 7, PUR_ENC_V = 8, PUR_ENC_E0 = 9, PUR_ENC_E1 = 10
+  PUR_GK_A = 6, PUR_GK_E = 7, PUR_ENC_V = 8, PUR_ENC_E0 = 9, PUR_ENC_E1 = 10,
+  PUR_SYM_A = 11, PUR_SYM_E = 12   // symmetric encryption: a from a public seed, e from the context seed
 };
 __host__ __device__ __forceinline__ u64 stream_sid(u64 purpose, u64 object, u64 prime) {
   return (purpose << 56) | (object << 16) | prime;

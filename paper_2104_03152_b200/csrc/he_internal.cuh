@@ -84,6 +84,10 @@ struct he_ciphertext {
   int B, size, level;
   double scale;
   he::u64* d;  // [B][size][level+1][N]
+  // fresh symmetric ciphertext: c1 of item b is Uniform(a_seed, (PUR_SYM_A, stream0 + b, i)), so the
+  // seeded wire form can omit it (set by he_encrypt_symmetric / seeded deserialization only)
+  int seeded = 0;
+  he::u64 a_seed = 0, stream0 = 0;
 };
 
 struct he_plaintext {

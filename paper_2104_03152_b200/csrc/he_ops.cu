@@ -2040,6 +2040,75 @@ he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
   return ct;
 }
 
+// Symmetric encryption (DESIGN.md §3 "seeded symmetric encryption"):
+//   c1 = a,  a_i = Uniform(a_seed, (PUR_SYM_A, stream_id + b, i))  (NTT words, C13 sampler)
+//   c0 = -a s + e + m,  e = CDT(seed, (PUR_SYM_E, stream_id + b, 0))  (C11)
+__global__ void k_sym_combine(u64* __restrict__ ct, const u64* __restrict__ et, const u64* __restrict__ pt,
+                              size_t pt_bs, const u64* __restrict__ sk, const PrimeD* __restrict__ primes, int N,
+                              int Lc, size_t rows) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int b = (int)(r / Lc), i = (int)(r % Lc);
+    const PrimeD P = load_prime(primes, i);
+    const size_t LN = (size_t)Lc * N;
+    u64* c0 = ct + (size_t)b * 2 * LN + (size_t)i * N;
+    const u64* c1 = c0 + LN;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const u64 as = mul_mod(c1[n], sk[(size_t)i * N + n], P);
+      c0[n] = add_mod(sub_mod(et[r * N + n], as, P.q), pt[(size_t)b * pt_bs + (size_t)i * N + n], P.q);
+    }
+  }
+}
+
+void sym_regen_c1(he_context* c, he_ciphertext* ct) {
+  const int Lc = ct->level + 1;
+  const size_t LN = (size_t)Lc * c->N;
+  ProfScope ps_(c, "sample_uniform", 0.0, 0);
+  k_sample_uniform<<<dim3((c->N + 255) / 256, (unsigned)std::min<size_t>((size_t)ct->B * Lc, 65535)), 256, 0,
+                     c->stream>>>(ct->d + LN, 2 * LN, ct->B, Lc, c->N, ct->a_seed, PUR_SYM_A, ct->stream0,
+                                  c->d_primes);
+  check_launch(c);
+}
+
+// c0 of every item to / from a dense [B][Lc][N] buffer (the seeded wire payload).
+void ct_copy_c0(he_context* c, const he_ciphertext* ct, u64* dst, bool to_ct) {
+  const size_t LN = (size_t)(ct->level + 1) * c->N;
+  if (to_ct)
+    HE_CK(cudaMemcpy2DAsync(ct->d, 2 * LN * 8, dst, LN * 8, LN * 8, ct->B, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    HE_CK(cudaMemcpy2DAsync(dst, LN * 8, ct->d, 2 * LN * 8, LN * 8, ct->B, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+he_ciphertext* encrypt_symmetric(he_context* c, const he_plaintext* pt, u64 stream_id, u64 a_seed) {
+  const int Lc = pt->level + 1, B = pt->B;
+  he_ciphertext* ct = ct_new(c, B, 2, pt->level, pt->scale);
+  try {
+    ct->seeded = 1;
+    ct->a_seed = a_seed;
+    ct->stream0 = stream_id;
+    sym_regen_c1(c, ct);
+    Scratch e(c, (size_t)B * c->N * 8), et(c, (size_t)B * Lc * c->N * 8);
+    {
+      ProfScope ps_(c, "sample_small", 0.0, 0);
+      k_sample_small<<<dim3((c->N + 255) / 256, (unsigned)std::min(B, 65535)), 256, 0, c->stream>>>(
+          e.as<i64>(), c->N, B, c->seed, PUR_SYM_E, stream_id, 1, c->d_cdt);
+    }
+    check_launch(c);
+    signed_to_ntt(c, e.as<i64>(), et.as<u64>(), B, Lc);
+    const size_t rows = (size_t)B * Lc;
+    {
+      ProfScope ps_(c, "sym_combine", 0.0, 0);
+      k_sym_combine<<<rows_grid2(c, rows), 256, 0, c->stream>>>(ct->d, et.as<u64>(), pt->d,
+                                                                pt->B == 1 ? 0 : (size_t)Lc * c->N, c->d_sk,
+                                                                c->d_primes, c->N, Lc, rows);
+    }
+    check_launch(c);
+  } catch (...) {
+    ct_free(ct);
+    throw;
+  }
+  return ct;
+}
+
 he_plaintext* decrypt(he_context* c, const he_ciphertext* ct) {
   const int Lc = ct->level + 1;
   he_plaintext* pt = pt_new(c, ct->B, ct->level, ct->scale);

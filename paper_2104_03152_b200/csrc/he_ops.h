@@ -32,6 +32,9 @@ he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, dou
 he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level, int qp = 0);
 void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n);
 he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id);
+he_ciphertext* encrypt_symmetric(he_context* c, const he_plaintext* pt, u64 stream_id, u64 a_seed);
+void sym_regen_c1(he_context* c, he_ciphertext* ct);
+void ct_copy_c0(he_context* c, const he_ciphertext* ct, u64* dst, bool to_ct);
 he_plaintext* decrypt(he_context* c, const he_ciphertext* ct);
 
 he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b);  // 0 add, 1 sub

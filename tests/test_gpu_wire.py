@@ -75,3 +75,53 @@ def test_cnn_communication_per_inference():
     # the decrypted logits survive the round trip unchanged
     z = net.decrypt(g.he_ct_deserialize(down))
     assert np.array_equal(z, net.decrypt(ct_out))
+
+
+def test_symmetric_encrypt_bit_exact_and_seeded_wire():
+    """he_encrypt_symmetric == oracle encrypt_symmetric word for word (item b on stream id + b); the
+    seeded wire bytes == oracle/wire.pack_seeded (c0 only: half the full payload); deserializing them
+    regenerates c1 on the device (same words); non-fresh ciphertexts have no seeded form."""
+    from paper_2104_03152_b200 import Context, HEError
+    o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, 5)
+    o.keygen([])
+    g = Context(CFG4.logN, CFG4.bits, CFG4.n_special, 5)
+    g.he_keygen([])
+    level, B = 5, 3
+    zs = np.random.default_rng(8).uniform(-1, 1, (B, o.slots))
+    pts = [o.encode(z, 2.0 ** 30, level) for z in zs]
+    gct = g.he_encrypt_symmetric(g.he_pt_import_words(np.stack([p.words for p in pts]), level, 2.0 ** 30),
+                                 100, 777)
+    ref = [o.encrypt_symmetric(p, 100 + b, 777) for b, p in enumerate(pts)]
+    W = gct.words()
+    for b in range(B):
+        assert np.array_equal(W[b], ref[b].words), b
+    blob = g.he_ct_serialize_seeded(gct)
+    assert blob == wire.pack_seeded(np.stack([r.words[0] for r in ref]), o.q, level, 2.0 ** 30, 777, 100)
+    full = g.he_ct_serialize(gct)
+    assert len(blob) - 64 == (len(full) - 64) // 2
+    back = g.he_ct_deserialize(blob)
+    assert np.array_equal(back.words(), W) and back.level == level and back.scale == 2.0 ** 30
+    assert np.max(np.abs(g.he_decode(g.he_decrypt(back), o.slots) - zs)) < 1e-4
+    with pytest.raises(HEError):
+        g.he_ct_serialize_seeded(g.he_add(gct, gct))
+    with pytest.raises(HEError):
+        g.he_ct_serialize_seeded(g.he_ct_deserialize(full))
+
+
+def test_cnn_communication_seeded_input():
+    """The bench schedule (input at level 5) with a seeded symmetric upload: 8192 x (31 + 5 x 26)
+    bits up, 8192 x 31 bits x 2 down; the logits equal those of the public-key path's decryption."""
+    from paper_2104_03152_b200 import Context
+    from paper_2104_03152_b200.cnn import CONV_G, FC1_G, EncryptedCNN, rotation_steps
+    g = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    g.he_keygen(rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
+    net = EncryptedCNN(g, cnn_weights(3), conv_g=CONV_G, fc1_g=FC1_G)
+    img = mnist_like_images(1, 4)
+    pt = g.he_encode(net.im2col(img), 2.0 ** net.plan["in_log2"], net.top)
+    up = g.he_ct_serialize_seeded(g.he_encrypt_symmetric(pt, 0, 31337))
+    down = g.he_ct_serialize(net.forward(g.he_ct_deserialize(up)))
+    assert len(up) == 64 + 8192 * (31 + 5 * 26) // 8 == 64 + 164864
+    assert len(down) == 64 + 2 * 8192 * 31 // 8 == 64 + 63488
+    z = net.decrypt(g.he_ct_deserialize(down))
+    ref = net.decrypt(net.forward(net.encrypt(img, 0)))
+    assert np.max(np.abs(z - ref)) < 2e-3 and np.argmax(z) == np.argmax(ref)

@@ -385,3 +385,47 @@ def test_vec_mat_bsgs_fold_oracle_pin():
     zf, zp = c.decode(c.decrypt(f)), c.decode(c.decrypt(p))
     # fresh noise ~1.4e-5 per slot times |W| summed over 64 terms, plus key-switch and rescale rounding
     assert np.max(np.abs(zf - ref)) < 2e-4 and np.max(np.abs(zp - ref)) < 2e-4
+
+
+def test_symmetric_encrypt_oracle_pin():
+    """Oracle symmetric encryption: decrypt - m is the NTT of ONE small integer
+    polynomial e (the same in every limb, |e| within the CDT's range, std ~ sigma = 3.2); c1 depends
+    only on the public (a_seed, stream): another context seed (other secret key) gives the same c1,
+    another a_seed a different one; the ciphertext decodes to the message."""
+    c = OracleContext(10, (50, 40, 40), 1, 21)
+    c.keygen([])
+    z = np.random.default_rng(5).uniform(-1, 1, c.slots)
+    pt = c.encode(z, 2.0 ** 30, 1)
+    ct = c.encrypt_symmetric(pt, 7, 0xABCDEF)
+    d = c.decrypt(ct)
+    es = []
+    for i in range(2):
+        q = int(c.q[i])
+        diff = np.array([(int(a) - int(b)) % q for a, b in zip(d.words[i], pt.words[i])], dtype=np.uint64)
+        e = np.array([int(v) if int(v) <= q // 2 else int(v) - q for v in c.intt(i, diff)])
+        es.append(e)
+    assert np.array_equal(es[0], es[1])
+    assert np.max(np.abs(es[0])) <= 41 and 2.5 < np.std(es[0]) < 4.0
+    c2 = OracleContext(10, (50, 40, 40), 1, 22)
+    c2.keygen([])
+    ct2 = c2.encrypt_symmetric(c2.encode(z, 2.0 ** 30, 1), 7, 0xABCDEF)
+    assert np.array_equal(ct2.words[1], ct.words[1]) and not np.array_equal(ct2.words[0], ct.words[0])
+    assert not np.array_equal(c.encrypt_symmetric(pt, 7, 0xABCDEE).words[1], ct.words[1])
+    assert np.max(np.abs(c.decode(c.decrypt(ct)) - z)) < 1e-4
+
+
+def test_seeded_wire_reference_packer():
+    """oracle/wire.pack_seeded: header fields at their offsets (magic, size 2, a_seed and stream in
+    the tail) and a c0-only payload, half the full form's."""
+    import struct
+    from oracle import wire
+    rng = np.random.default_rng(2)
+    q = [1073479681, 1073184769]
+    c0 = np.stack([np.stack([rng.integers(0, qi, 64, dtype=np.uint64) for qi in q]) for _ in range(3)])
+    blob = wire.pack_seeded(c0, q, 1, 2.0 ** 20, 0x1122334455667788, 9)
+    assert blob[:8] == b"HECKKSS1"
+    log2n, B, size, level, scale, pay, nl, a_seed, stream = struct.unpack("<IIIIdQIQQ", blob[8:60])
+    assert (log2n, B, size, level, scale, nl) == (6, 3, 2, 1, 2.0 ** 20, 2)
+    assert (a_seed, stream) == (0x1122334455667788, 9) and blob[60:64] == bytes(4)
+    full = wire.pack(np.stack([c0, c0], axis=1), q, 1, 2.0 ** 20)
+    assert pay == len(blob) - 64 == (len(full) - 64) // 2 == 3 * 64 * 60 // 8
