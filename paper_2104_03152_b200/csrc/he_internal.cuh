@@ -193,7 +193,7 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
 
 template <int LOGN, bool INV, class Job>
 void launch_ntt32_t(he_context* c, const Job& job, int nblk) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   static bool configured = false;
   auto kern = k_ntt32<LOGN, INV, Job>;
   if (!configured) {

@@ -218,6 +218,23 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __r
 // entry 0 of the inverse table holds (N^{-1}, its companion).
 __device__ __forceinline__ u32 spad32(u32 i) { return i + (i >> 5); }
 
+// Geometry of the 32-bit engine: 2^R words per thread, T = N / 2^R threads, NPASS passes of R bits.
+// Measured at N = 2^13 (profiles/r01_ncu_summary.md): R = 4 with 3 CTAs/SM is the best of R 4/5 x
+// 2..5 CTAs/SM; the transforms are latency-bound (load -> passes -> store per CTA, ~35% issue
+// utilisation; twiddle loads cost ~10%), the next step is a persistent double-buffered kernel.
+#ifndef HE_NTT32_R
+#define HE_NTT32_R 0   // 0: the 64-bit engine's choice (R = 4 for N <= 2^14)
+#endif
+template <int LOGN>
+struct NttGeomS {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int LOGNL = LOGN;
+  static constexpr int NL = N;
+  static constexpr int R = HE_NTT32_R ? HE_NTT32_R : NttGeom<LOGN, 1>::R;
+  static constexpr int T = NL >> R;
+  static constexpr int NPASS = (LOGNL + R - 1) / R;
+};
+
 // Conditional subtraction as an unsigned min: x - q wraps above 2^31 when
 // x < q (all values < 2q < 2^32), so min(x, x - q) is the reduced value; one
 // VIADDMNMX instead of ISETP + SEL.
@@ -259,7 +276,7 @@ __device__ __forceinline__ void gs_bfly32_lazy(u32& x, u32& y, u32 w, u32 wsh, u
 // when fused, which saves a shared-memory round trip and a barrier.
 template <int LOGN, bool INV, int LO, int NB, bool LAZY, class LD, class ST>
 __device__ __forceinline__ void ntt_pass32_io(u32 tid, const uint2* __restrict__ tw, u32 q, LD ld, ST st) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   constexpr int NG = 1 << (G::R - NB);
   constexpr int E = 1 << NB;
 #pragma unroll
@@ -302,7 +319,7 @@ __device__ __forceinline__ void ntt_pass32_io(u32 tid, const uint2* __restrict__
 // pointer per group and compile-time offsets (LDS/STS with immediate offsets).
 template <int LOGN, bool INV, int LO, int NB, bool LAZY = false>
 __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __restrict__ tw, u32 q) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   constexpr int NG = 1 << (G::R - NB);
   constexpr int E = 1 << NB;
 #pragma unroll
@@ -339,9 +356,9 @@ __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __rest
 }
 
 // Passes P0 .. PEND-1 (pass P covers bit group GP = INV ? P : NPASS-1-P).
-template <int LOGN, bool INV, int P, bool LAZY = false, int PEND = NttGeom<LOGN, 1>::NPASS>
+template <int LOGN, bool INV, int P, bool LAZY = false, int PEND = NttGeomS<LOGN>::NPASS>
 __device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, u32 q) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   if constexpr (P < PEND) {
     constexpr int GP = INV ? P : G::NPASS - 1 - P;
     constexpr int LO = GP * G::R;
@@ -356,7 +373,7 @@ __device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, 
 // of the input in shared memory); result left in sm (lazy range when q < 2^30).
 template <int LOGN, class LD>
 __device__ __forceinline__ void ntt_fwd32_from(u32* sm, u32 tid, const uint2* tw, u32 q, LD ld) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   constexpr int LO = (G::NPASS - 1) * G::R, NB = G::LOGNL - LO;
   auto st = [&](u32 i, u32 v) { sm[spad32(i)] = v; };
   if (q < (1u << 30)) {
@@ -374,7 +391,7 @@ __device__ __forceinline__ void ntt_fwd32_from(u32* sm, u32 tid, const uint2* tw
 // scaled by N^{-1} (canonical), to st(i, v) instead of shared memory.
 template <int LOGN, class ST>
 __device__ __forceinline__ void ntt_inv32_to(u32* sm, u32 tid, const uint2* tw, u32 q, ST st) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   constexpr int LO = (G::NPASS - 1) * G::R, NB = G::LOGNL - LO;
   const uint2 ni = __ldg(tw);
   auto ld = [&](u32 i) { return sm[spad32(i)]; };
@@ -403,13 +420,16 @@ __device__ __forceinline__ u32 ntt_reduce32(u32 v, u32 q) {
 template <int LOGN>
 struct NttGeom32 {
   static constexpr int SMEM = ((1 << LOGN) + (1 << LOGN) / 32) * 4;
-  static constexpr int MINB = (1 << LOGN) <= 8192 ? 3 : 2;   // 3 CTAs/SM at N = 2^13 (MINB 2: -17%)
+#ifndef HE_NTT32_MINB
+#define HE_NTT32_MINB 3
+#endif
+  static constexpr int MINB = (1 << LOGN) <= 8192 ? HE_NTT32_MINB : 2;   // 3 CTAs/SM at N = 2^13 (2: -17%)
 };
 
 template <int LOGN, bool INV, class Job>
-__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T, NttGeom32<LOGN>::MINB)
+__global__ void __launch_bounds__(NttGeomS<LOGN>::T, NttGeom32<LOGN>::MINB)
 k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   extern __shared__ u32 sm32[];
   const u32 tid = threadIdx.x;
   const int blk = blockIdx.x;

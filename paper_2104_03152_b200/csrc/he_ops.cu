@@ -726,9 +726,9 @@ struct FusedArgs {
   u64* accx;           // [B][2][Lc+K][N]
 };
 template <int LOGN>
-__global__ void __launch_bounds__(NttGeom<LOGN, 1>::T, (1 << LOGN) <= 8192 ? 2 : 1)
+__global__ void __launch_bounds__(NttGeomS<LOGN>::T, (1 << LOGN) <= 8192 ? 2 : 1)
 k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all) {
-  typedef NttGeom<LOGN, 1> G;
+  typedef NttGeomS<LOGN> G;
   extern __shared__ u32 sm32[];
   u32* buf = sm32;                                  // NTT workspace (padded)
   u32* acc = sm32 + G::N + G::N / 32;               // [2][N]
@@ -1287,11 +1287,11 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
     kern<<<dim3(nt, B), T, smem, c->stream>>>(fa, c->d_primes, c->d_tw32);
   };
   switch (c->logN) {
-    case 10: launch(k_modup_ip32<10>, NttGeom<10, 1>::T); break;
-    case 11: launch(k_modup_ip32<11>, NttGeom<11, 1>::T); break;
-    case 12: launch(k_modup_ip32<12>, NttGeom<12, 1>::T); break;
-    case 13: launch(k_modup_ip32<13>, NttGeom<13, 1>::T); break;
-    default: launch(k_modup_ip32<14>, NttGeom<14, 1>::T); break;
+    case 10: launch(k_modup_ip32<10>, NttGeomS<10>::T); break;
+    case 11: launch(k_modup_ip32<11>, NttGeomS<11>::T); break;
+    case 12: launch(k_modup_ip32<12>, NttGeomS<12>::T); break;
+    case 13: launch(k_modup_ip32<13>, NttGeomS<13>::T); break;
+    default: launch(k_modup_ip32<14>, NttGeomS<14>::T); break;
   }
   check_launch(c);
   epi.accx = accx.as<u64>();
