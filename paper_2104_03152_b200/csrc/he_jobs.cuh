@@ -5,6 +5,41 @@
 
 namespace he {
 
+// ---- per-block binding for the 32-bit engine (k_ntt32) ----------------------
+// A job may provide bind32(blk, P) returning an object with load(n) / store(n, v): the block's
+// decomposition, row pointers and 32-bit constants are computed once per CTA instead of per
+// element.  k_ntt32 runs only on contexts whose primes are all < 2^31, so bound jobs use u32
+// arithmetic.  Jobs without bind32 go through JobAt (their per-element load/store).
+__device__ __forceinline__ u32 add32(u32 a, u32 b, u32 q) { return min(a + b, a + b - q); }
+__device__ __forceinline__ u32 sub32(u32 a, u32 b, u32 q) { return min(a - b, a - b + q); }
+__device__ __forceinline__ u32 red32(u32 x, u32 q, u32 mu32) {   // x mod q, mu32 = floor(2^32 / q)
+  const u32 r = x - __umulhi(x, mu32) * q;
+  return min(r, r - q);
+}
+__device__ __forceinline__ u32 mulsh32(u32 x, u32 w, u32 wsh, u32 q) {   // Shoup, x < 2^32, w < q
+  const u32 r = x * w - __umulhi(x, wsh) * q;
+  return min(r, r - q);
+}
+__device__ __forceinline__ u32 shoup_companion32(u32 w, u32 q) { return (u32)(((u64)w << 32) / q); }
+__device__ __forceinline__ u32 mu32_of(const PrimeD& P) { return (u32)(P.mu64 >> 32); }
+
+template <class Job>
+struct JobAt {
+  const Job& j;
+  int blk;
+  const PrimeD& P;
+  __device__ __forceinline__ u64 load(u32 i) const { return j.load(blk, i, P); }
+  __device__ __forceinline__ void store(u32 i, u64 v) const { j.store(blk, i, v, P); }
+};
+template <class Job>
+__device__ __forceinline__ auto bind_job(const Job& j, int blk, const PrimeD& P, int) -> decltype(j.bind32(blk, P)) {
+  return j.bind32(blk, P);
+}
+template <class Job>
+__device__ __forceinline__ JobAt<Job> bind_job(const Job& j, int blk, const PrimeD& P, long) {
+  return JobAt<Job>{j, blk, P};
+}
+
 // Plain transform of limbs: blk -> (item = blk / nl, limb = blk % nl), limb l
 // modulo prime l; items at strides src_bs / dst_bs words.
 struct JobLimbs {
@@ -19,6 +54,16 @@ struct JobLimbs {
   }
   __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
     dst[(size_t)(blk / nl) * dst_bs + (size_t)(blk % nl) * N + i] = v;
+  }
+  struct B32 {
+    const u64* s;
+    u64* d;
+    __device__ __forceinline__ u64 load(u32 i) const { return s[i]; }
+    __device__ __forceinline__ void store(u32 i, u64 v) const { d[i] = v; }
+  };
+  __device__ B32 bind32(int blk, const PrimeD&) const {
+    const size_t it = (size_t)(blk / nl), l = (size_t)(blk % nl);
+    return B32{src + it * src_bs + l * N, dst + it * dst_bs + l * N};
   }
 };
 
@@ -35,6 +80,16 @@ struct JobLimbsTo32 {
   }
   __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
     dst[(size_t)(blk / nl) * dst_bs + (size_t)(blk % nl) * N + i] = (u32)v;
+  }
+  struct B32 {
+    const u64* s;
+    u32* d;
+    __device__ __forceinline__ u64 load(u32 i) const { return s[i]; }
+    __device__ __forceinline__ void store(u32 i, u64 v) const { d[i] = (u32)v; }
+  };
+  __device__ B32 bind32(int blk, const PrimeD&) const {
+    const size_t it = (size_t)(blk / nl), l = (size_t)(blk % nl);
+    return B32{src + it * src_bs + l * N, dst + it * dst_bs + l * N};
   }
 };
 inline double alg_bytes(const JobLimbsTo32& j, int nblk) { return 12.0 * j.N * nblk; }
@@ -179,6 +234,19 @@ struct JobModUp32 {
     dec(blk, b, j, t);
     ext[(((size_t)b * Lc + j) * (Lc + K) + t) * N + i] = (u32)v;
   }
+  struct B32 {
+    const u32* c;
+    u32* e;
+    u32 qj, q, mut;
+    __device__ __forceinline__ u64 load(u32 i) const { return lift32(c[i], qj, q, mut); }
+    __device__ __forceinline__ void store(u32 i, u64 v) const { e[i] = (u32)v; }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    int b, j, t;
+    dec(blk, b, j, t);
+    return B32{coef + ((size_t)b * Lc + j) * N, ext + (((size_t)b * Lc + j) * (Lc + K) + t) * N,
+               (u32)__ldg(qtab + j), (u32)P.q, mu32_of(P)};
+  }
 };
 inline double alg_bytes(const JobModUp32& j, int nblk) {
   const int nt = j.Lc + j.K - 1;
@@ -265,6 +333,33 @@ struct JobKsSpecial {
     a.tb[((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N + n] =
         a.K == 1 ? y : mul_mod(y, __ldg(a.Phat_inv + k), P);
   }
+  // lazy ModDown with u32 accumulators and one special prime (the small-prime fused path)
+  struct B32 {
+    const JobKsSpecial* j;
+    int blk;
+    const PrimeD* P;
+    bool fast;
+    const u32* ax;
+    u64* tb;
+    u32 q, ph;
+    __device__ __forceinline__ u64 load(u32 n) const { return fast ? (u64)ax[n] : j->load(blk, n, *P); }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      if (fast) tb[n] = add32((u32)v, ph, q);
+      else j->store(blk, n, v, *P);
+    }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    int kk, b, part, k;
+    dec(blk, kk, b, part, k);
+    const bool fast = a.accx && a.accx32 && a.K == 1;
+    B32 r{this, blk, &P, fast, nullptr, nullptr, (u32)P.q, 0};
+    if (fast) {
+      r.ax = reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + a.Lc + k) * a.N;
+      r.tb = a.tb + ((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N;
+      r.ph = (u32)__ldg(a.Ph_mod + a.L + k);
+    }
+    return r;
+  }
 };
 
 // a9 data limbs: c_i = sum_k tb_k [P/p_k]_{q_i} - [P/2]_{q_i} (coefficient
@@ -312,6 +407,60 @@ struct JobKsData {
     const size_t o = (size_t)kk * a.out_ks + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N + n;
     if (a.acc_in) u = add_mod(u, a.acc_in[o], P.q);
     a.out[o] = u;
+  }
+  // lazy ModDown with u32 accumulators and one special prime (the small-prime fused path): the
+  // same arithmetic in u32 with the block's rows and constants bound once
+  struct B32 {
+    const JobKsData* j;
+    int blk;
+    const PrimeD* P;
+    bool fast, gather;
+    const u64* tb;
+    const u32* ax;
+    const u64* add;
+    const u64* D;
+    const u64* acc;
+    u64* out;
+    u32 q, mu32, ph, pinv, pinvsh, g;
+    int logN;
+    __device__ __forceinline__ u64 load(u32 n) const {
+      if (!fast) return j->load(blk, n, *P);
+      return sub32(red32((u32)tb[n], q, mu32), ph, q);
+    }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      if (!fast) {
+        j->store(blk, n, v, *P);
+        return;
+      }
+      u32 u = mulsh32(sub32(ax[n], (u32)v, q), pinv, pinvsh, q);
+      if (add) u = add32(u, (u32)add[gather ? galois_src(n, g, logN) : n], q);
+      if (D) u = (u32)mul_mod(u, D[n], *P);
+      if (acc) u = add32(u, (u32)acc[n], q);
+      out[n] = u;
+    }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    int kk, b, part, i;
+    dec(blk, kk, b, part, i);
+    const bool fast = a.accx && a.accx32 && a.K == 1;
+    B32 r{this, blk, &P, fast, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+          (u32)P.q, mu32_of(P), 0, 0, 0, 1, a.logN};
+    if (fast) {
+      const size_t LN = (size_t)a.Lc * a.N;
+      r.tb = a.tb + (((size_t)kk * a.B + b) * 2 + part) * a.N;
+      r.ax = reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N;
+      r.ph = (u32)__ldg(a.Ph_mod + i);
+      r.pinv = (u32)__ldg(a.Pinv_mod + i);
+      r.pinvsh = shoup_companion32(r.pinv, r.q);
+      r.g = a.gal[kk];
+      r.gather = a.add_gather && r.g != 1;
+      if (part < a.add_parts) r.add = a.addsrc + (size_t)b * a.add_bs + part * LN + (size_t)i * a.N;
+      if (a.D) r.D = a.D + (size_t)kk * a.D_ks + (size_t)i * a.N;
+      const size_t o = (size_t)kk * a.out_ks + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N;
+      if (a.acc_in) r.acc = a.acc_in + o;
+      r.out = a.out + o;
+    }
+    return r;
   }
 };
 
@@ -370,6 +519,24 @@ struct JobRescaleData {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
     const u64 t = sub_mod(src.at(r, i, n, P), v, P.q);
     out[((size_t)r * (Lc - 1) + i) * N + n] = mul_mod(t, __ldg(qinv + i), P);
+  }
+  struct B32 {
+    const RescaleSrc* src;
+    const PrimeD* P;
+    const u64* y;
+    u64* out;
+    int r, i;
+    u32 q, mu32, h, qi, qish;
+    __device__ __forceinline__ u64 load(u32 n) const { return sub32(red32((u32)y[n], q, mu32), h, q); }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      out[n] = mulsh32(sub32((u32)src->at(r, i, n, *P), (u32)v, q), qi, qish, q);
+    }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    const int r = blk / (Lc - 1), i = blk % (Lc - 1);
+    const u32 q = (u32)P.q, qi = (u32)__ldg(qinv + i);
+    return B32{&src, &P, y + (size_t)r * N, out + ((size_t)r * (Lc - 1) + i) * N, r, i, q, mu32_of(P),
+               (u32)__ldg(h + i), qi, shoup_companion32(qi, q)};
   }
 };
 

@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 
 #include "he_common.cuh"
+#include "he_jobs.cuh"
 
 namespace he {
 
@@ -437,14 +438,15 @@ k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw
   const PrimeD P = load_prime(primes, pi);
   const uint2* tw = tw_all + (size_t)pi * G::N;
   const u32 q = (u32)P.q;
-  for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)job.load(blk, i, P);
+  const auto jb = bind_job(job, blk, P, 0);   // block decomposition + constants, once per CTA
+  for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)jb.load(i);
   __syncthreads();
   ntt_run32<LOGN, INV>(sm32, tid, tw, q);
   const uint2 ni = __ldg(tw);
   for (u32 i = tid; i < G::NL; i += G::T) {
     u32 v = sm32[spad32(i)];
     v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
-    job.store(blk, i, (u64)v, P);
+    jb.store(i, (u64)v);
   }
 }
 
