@@ -8,6 +8,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <type_traits>
+#include <utility>
+#include <algorithm>
 
 #include "../../include/he_ckks.h"
 #include "he_common.cuh"
@@ -191,9 +194,45 @@ void launch_ntt_t(he_context* c, const Job& job, int nblk) {
   check_launch(c);
 }
 
+// Jobs with a single u32 input row (pipe_ok() on the host) run the persistent pipelined kernel.
+template <class J, class = void>
+struct has_raw32 : std::false_type {};
+template <class J>
+struct has_raw32<J, std::void_t<decltype(std::declval<const J&>().raw32(0))>> : std::true_type {};
+
+#ifndef HE_NTT32_PIPE
+#define HE_NTT32_PIPE 1
+#endif
+
+template <int LOGN, bool INV, class Job>
+void launch_ntt32_pipe(he_context* c, const Job& job, int nblk) {
+  typedef NttGeomS<LOGN> G;
+  static int grid = 0;
+  auto kern = k_ntt32_pipe<LOGN, INV, Job>;
+  if (!grid) {
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NttGeom32Pipe<LOGN>::SMEM));
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 0, sms = 0;
+    HE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, NttGeom32Pipe<LOGN>::SMEM));
+    HE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    grid = std::max(1, per_sm) * sms;
+  }
+  ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk,
+               c->prof_on ? alg_ops(job, nblk, LOGN) : 0.0);
+  kern<<<std::min(nblk, grid), G::T, NttGeom32Pipe<LOGN>::SMEM, c->stream>>>(
+      job, c->d_primes, INV ? c->d_itw32 : c->d_tw32, nblk);
+  check_launch(c);
+}
+
 template <int LOGN, bool INV, class Job>
 void launch_ntt32_t(he_context* c, const Job& job, int nblk) {
   typedef NttGeomS<LOGN> G;
+  if constexpr (has_raw32<Job>::value) {
+    if (nblk > 0 && HE_NTT32_PIPE && job.pipe_ok()) {
+      launch_ntt32_pipe<LOGN, INV>(c, job, nblk);
+      return;
+    }
+  }
   static bool configured = false;
   auto kern = k_ntt32<LOGN, INV, Job>;
   if (!configured) {

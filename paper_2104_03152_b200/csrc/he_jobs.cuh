@@ -239,8 +239,15 @@ struct JobModUp32 {
     u32* e;
     u32 qj, q, mut;
     __device__ __forceinline__ u64 load(u32 i) const { return lift32(c[i], qj, q, mut); }
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return lift32(x, qj, q, mut); }
     __device__ __forceinline__ void store(u32 i, u64 v) const { e[i] = (u32)v; }
   };
+  // pipelined transform (k_ntt32_pipe): the block's input is one u32 row
+  __host__ __device__ bool pipe_ok() const { return true; }
+  __host__ __device__ const u32* raw32(int blk) const {
+    const int nt = Lc + K - 1;
+    return coef + ((size_t)(blk / (Lc * nt)) * Lc + (blk % (Lc * nt)) / nt) * N;
+  }
   __device__ B32 bind32(int blk, const PrimeD& P) const {
     int b, j, t;
     dec(blk, b, j, t);
@@ -340,25 +347,32 @@ struct JobKsSpecial {
     const PrimeD* P;
     bool fast;
     const u32* ax;
-    u64* tb;
+    u32* tb;
     u32 q, ph;
     __device__ __forceinline__ u64 load(u32 n) const { return fast ? (u64)ax[n] : j->load(blk, n, *P); }
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return x; }
     __device__ __forceinline__ void store(u32 n, u64 v) const {
-      if (fast) tb[n] = add32((u32)v, ph, q);
+      if (fast) tb[n] = add32((u32)v, ph, q);   // fast path: tb holds u32 words (read by JobKsData)
       else j->store(blk, n, v, *P);
     }
   };
   __device__ B32 bind32(int blk, const PrimeD& P) const {
     int kk, b, part, k;
     dec(blk, kk, b, part, k);
-    const bool fast = a.accx && a.accx32 && a.K == 1;
+    const bool fast = pipe_ok();
     B32 r{this, blk, &P, fast, nullptr, nullptr, (u32)P.q, 0};
     if (fast) {
-      r.ax = reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + a.Lc + k) * a.N;
-      r.tb = a.tb + ((((size_t)kk * a.B + b) * 2 + part) * a.K + k) * a.N;
+      r.ax = raw32(blk);
+      r.tb = reinterpret_cast<u32*>(a.tb) + (((size_t)kk * a.B + b) * 2 + part) * a.N;
       r.ph = (u32)__ldg(a.Ph_mod + a.L + k);
     }
     return r;
+  }
+  // lazy ModDown with u32 accumulators and one special prime: input = one u32 accumulator row
+  __host__ __device__ bool pipe_ok() const { return a.accx && a.accx32 && a.K == 1; }
+  __host__ __device__ const u32* raw32(int blk) const {
+    const int b = (blk >> 1) % a.B, part = blk & 1;   // K == 1: blk = (kk B + b) 2 + part
+    return reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + a.Lc) * a.N;
   }
 };
 
@@ -415,7 +429,7 @@ struct JobKsData {
     int blk;
     const PrimeD* P;
     bool fast, gather;
-    const u64* tb;
+    const u32* tb;
     const u32* ax;
     const u64* add;
     const u64* D;
@@ -425,8 +439,9 @@ struct JobKsData {
     int logN;
     __device__ __forceinline__ u64 load(u32 n) const {
       if (!fast) return j->load(blk, n, *P);
-      return sub32(red32((u32)tb[n], q, mu32), ph, q);
+      return sub32(red32(tb[n], q, mu32), ph, q);
     }
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return sub32(red32(x, q, mu32), ph, q); }
     __device__ __forceinline__ void store(u32 n, u64 v) const {
       if (!fast) {
         j->store(blk, n, v, *P);
@@ -442,12 +457,12 @@ struct JobKsData {
   __device__ B32 bind32(int blk, const PrimeD& P) const {
     int kk, b, part, i;
     dec(blk, kk, b, part, i);
-    const bool fast = a.accx && a.accx32 && a.K == 1;
+    const bool fast = pipe_ok();
     B32 r{this, blk, &P, fast, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
           (u32)P.q, mu32_of(P), 0, 0, 0, 1, a.logN};
     if (fast) {
       const size_t LN = (size_t)a.Lc * a.N;
-      r.tb = a.tb + (((size_t)kk * a.B + b) * 2 + part) * a.N;
+      r.tb = raw32(blk);
       r.ax = reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N;
       r.ph = (u32)__ldg(a.Ph_mod + i);
       r.pinv = (u32)__ldg(a.Pinv_mod + i);
@@ -461,6 +476,12 @@ struct JobKsData {
       r.out = a.out + o;
     }
     return r;
+  }
+  // fast path input = one u32 row of tb (written by JobKsSpecial's fast store)
+  __host__ __device__ bool pipe_ok() const { return a.accx && a.accx32 && a.K == 1; }
+  __host__ __device__ const u32* raw32(int blk) const {
+    const int r = blk / a.Lc;   // (kk B + b) 2 + part
+    return reinterpret_cast<const u32*>(a.tb) + (size_t)r * a.N;
   }
 };
 

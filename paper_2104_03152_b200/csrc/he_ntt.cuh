@@ -450,4 +450,55 @@ k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw
   }
 }
 
+// ---- pipelined persistent variant (jobs with a single u32 input row: raw32 / load_raw) ----------
+// Each CTA loops over job blocks blk = blockIdx.x, blockIdx.x + gridDim.x, ...; while block k's
+// passes and epilogue run, cp.async streams block k+1's raw input row into a staging buffer, so
+// the load latency that a one-shot CTA exposes (load -> passes -> store) is overlapped.
+template <int LOGN>
+__device__ __forceinline__ void stage_row32(u32* stage, const u32* __restrict__ src, u32 tid) {
+  typedef NttGeomS<LOGN> G;
+  const u32 base = (u32)__cvta_generic_to_shared(stage);
+#pragma unroll
+  for (u32 c = tid; c < G::NL / 4; c += G::T)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(base + c * 16), "l"(src + c * 4));
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int LOGN>
+struct NttGeom32Pipe {
+  static constexpr int SMEM = NttGeom32<LOGN>::SMEM + (1 << LOGN) * 4;   // + staging row
+};
+
+template <int LOGN, bool INV, class Job>
+__global__ void __launch_bounds__(NttGeomS<LOGN>::T, NttGeom32<LOGN>::MINB)
+k_ntt32_pipe(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all, int nblk) {
+  typedef NttGeomS<LOGN> G;
+  extern __shared__ u32 sm32[];
+  u32* stage = sm32 + G::NL + G::NL / 32;
+  const u32 tid = threadIdx.x;
+  int blk = blockIdx.x;
+  if (blk >= nblk) return;
+  stage_row32<LOGN>(stage, job.raw32(blk), tid);
+  for (; blk < nblk; blk += gridDim.x) {
+    const int pi = job.prime(blk);
+    const PrimeD P = load_prime(primes, pi);
+    const uint2* tw = tw_all + (size_t)pi * G::N;
+    const u32 q = (u32)P.q;
+    const auto jb = job.bind32(blk, P);
+    cp_async_wait_all();
+    __syncthreads();   // staged row visible; the previous block's epilogue is done with sm32
+    for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)jb.load_raw(stage[i]);
+    __syncthreads();   // staging buffer free
+    if (blk + (int)gridDim.x < nblk) stage_row32<LOGN>(stage, job.raw32(blk + gridDim.x), tid);
+    ntt_run32<LOGN, INV>(sm32, tid, tw, q);
+    const uint2 ni = __ldg(tw);
+    for (u32 i = tid; i < G::NL; i += G::T) {
+      u32 v = sm32[spad32(i)];
+      v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
+      jb.store(i, (u64)v);
+    }
+  }
+}
+
 }  // namespace he
