@@ -44,7 +44,7 @@ UNIT = "images/s"
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from one `ncu --set full` capture of the
-# bench command (profiles/r01_ncu_summary.md), batch 256
+# bench command at its default batch (profiles/r01_ncu_summary.md)
 TRAFFIC = {}
 try:
     TRAFFIC = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
@@ -361,7 +361,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256, help="images per GPU per step")
+    ap.add_argument("--batch", type=int, default=512, help="images per GPU per step (BASELINE config 5: batch 512)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

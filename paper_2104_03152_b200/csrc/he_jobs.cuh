@@ -518,6 +518,19 @@ struct JobRescaleLast {
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     y[(size_t)blk * N + n] = add_mod(v, (P.q - 1) >> 1, P.q);
   }
+  // 32-bit engine: y holds u32 words (read by JobRescaleData's bound / pipelined load)
+  struct B32 {
+    const RescaleSrc* src;
+    const PrimeD* P;
+    u32* y;
+    int blk, l;
+    u32 q, h;
+    __device__ __forceinline__ u64 load(u32 n) const { return src->at(blk, l, n, *P); }
+    __device__ __forceinline__ void store(u32 n, u64 v) const { y[n] = add32((u32)v, h, q); }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    return B32{&src, &P, reinterpret_cast<u32*>(y) + (size_t)blk * N, blk, Lc - 1, (u32)P.q, (u32)((P.q - 1) >> 1)};
+  }
 };
 // a11 rescale, step 2: out_i = (x_i - NTT_i([y]_{q_i} - [h]_{q_i})) [q_l^{-1}]_{q_i}.
 struct JobRescaleData {
@@ -544,11 +557,12 @@ struct JobRescaleData {
   struct B32 {
     const RescaleSrc* src;
     const PrimeD* P;
-    const u64* y;
+    const u32* y;
     u64* out;
     int r, i;
     u32 q, mu32, h, qi, qish;
-    __device__ __forceinline__ u64 load(u32 n) const { return sub32(red32((u32)y[n], q, mu32), h, q); }
+    __device__ __forceinline__ u64 load(u32 n) const { return sub32(red32(y[n], q, mu32), h, q); }
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return sub32(red32(x, q, mu32), h, q); }
     __device__ __forceinline__ void store(u32 n, u64 v) const {
       out[n] = mulsh32(sub32((u32)src->at(r, i, n, *P), (u32)v, q), qi, qish, q);
     }
@@ -556,8 +570,12 @@ struct JobRescaleData {
   __device__ B32 bind32(int blk, const PrimeD& P) const {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
     const u32 q = (u32)P.q, qi = (u32)__ldg(qinv + i);
-    return B32{&src, &P, y + (size_t)r * N, out + ((size_t)r * (Lc - 1) + i) * N, r, i, q, mu32_of(P),
+    return B32{&src, &P, raw32(blk), out + ((size_t)r * (Lc - 1) + i) * N, r, i, q, mu32_of(P),
                (u32)__ldg(h + i), qi, shoup_companion32(qi, q)};
+  }
+  __host__ __device__ bool pipe_ok() const { return true; }
+  __host__ __device__ const u32* raw32(int blk) const {
+    return reinterpret_cast<const u32*>(y) + (size_t)(blk / (Lc - 1)) * N;
   }
 };
 
