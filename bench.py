@@ -380,12 +380,12 @@ def main():
               "network": "conv7x7s3x4 -> x^2 -> fc256x64 -> x^2 -> fc64x10 (PAPER.md:98)",
               "ckks": "N=8192, primes [31,26x6,31] (input at level 5, scale 2^30), 47 Galois keys",
               "evaluation": "conv: one level, 8 baby x 8 giant chunk steps; FC1: 64 diagonals by BSGS "
-                            "(32 x 2) + fold 4; FC2: BSGS (16 x 4); every rotation sum with one lazy "
+                            "(32 x 2) + fold 4; FC2 padded to 16 outputs: 16 diagonals + fold 4; every rotation sum with one lazy "
                             "ModDown (DESIGN.md §3)",
               "batch_per_gpu": args.batch, "global_batch": args.batch * world,
               "step": "encode+encrypt+conv+square+fc1+square+fc2+decrypt+decode",
               "parallelism": f"dp{world} (independent images, no data-path collective)",
-              "l2": "inputs larger than L2 (1.9 GB of Galois keys read every step)"}
+              "l2": "working set per step far larger than the 126 MB L2 (batch 512: 0.4 GB input ciphertexts, 0.7 GB conv ModUp digits, 0.17 GB u32 Galois keys), no flush"}
 
     if args.impl == "reference":
         r = run_reference(args, rank, world)
