@@ -117,3 +117,100 @@ def test_wide_ragged_batch_bit_exact(pair):
         oc = o.encrypt(pts[b], 1000 + b)
         assert np.array_equal(r[b], o.rotate(oc, 2).words), b
         assert np.array_equal(sq[b], o.square(oc).words), b
+
+
+# ---- the bench schedule's new entry points on a small context (both engines) --------------------
+@pytest.mark.parametrize("bits", [(50, 40, 40, 50), (31, 26, 26, 31)], ids=["64bit", "32bit"])
+def test_one_level_conv_small_ragged_bit_exact(bits):
+    """he_im2col_conv_bsgs_pt on N = 2^11 (16 chunks of 64), C = 4 channels of 2x2 kernels, g = 4
+    baby x 4 giant steps, a ragged batch of 3: word for word with oracle im2col_conv_bsgs, on the
+    64-bit and the 32-bit engine; plus its layout / level / key errors."""
+    from paper_2104_03152_b200 import Context, HEError
+    chunk, g_ = 64, 4
+    steps = sorted({chunk * b for b in range(1, g_)} | {chunk * g_ * a for a in range(1, 1024 // chunk // g_)})
+    o = OracleContext(11, bits, 1, 5)
+    o.keygen(steps)
+    g = Context(11, bits, 1, 5)
+    g.he_keygen(steps)
+    rng = np.random.default_rng(7)
+    k = rng.uniform(-1, 1, (4, 2, 2))
+    bias = rng.uniform(-0.5, 0.5, 4)
+    lvl = 2
+    zs = np.zeros((3, o.slots))
+    zs[:, : 4 * chunk] = rng.uniform(-1, 1, (3, 4 * chunk))
+    o_in = [o.encrypt(o.encode(z, 2.0 ** 24, lvl), 40 + b) for b, z in enumerate(zs)]
+    x = g.he_ct_import_words(np.stack([c.words for c in o_in]), lvl, 2.0 ** 24)
+    ps = float(o.q[lvl]) * 2.0 ** -2
+    Dv = OC.conv_bsgs_diagonals(k.reshape(4, -1), chunk, o.slots, g_)
+    gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in Dv]), ps, lvl)
+    gB = g.he_pt_from_int_coeffs(np.stack([o.encode_coeffs(OC.conv_bias_slots(bias, chunk, o.slots),
+                                                           2.0 ** 24 * ps / o.q[lvl])[1]]),
+                                 2.0 ** 24 * ps / o.q[lvl], lvl - 1)
+    y = g.he_im2col_conv_bsgs_pt(x, gD, gB, chunk, g_)
+    for b in range(3):
+        ref = OC.im2col_conv_bsgs(o, o_in[b], k.reshape(4, -1), bias, chunk, g_, -2)
+        assert np.array_equal(y.words()[b], ref.words), b
+        assert y.level == ref.level == lvl - 1 and y.scale == ref.scale
+    # errors: C does not divide g; diagonals at another level; a missing giant-step key
+    with pytest.raises(HEError) as e:
+        g.he_im2col_conv_bsgs_encode(k, bias, chunk, 2, -2, lvl, 2.0 ** 24)
+    assert e.value.name == "LAYOUT_MISMATCH"
+    x1 = g.he_ct_import_words(np.stack([c.words[:, :2] for c in o_in]), 1, 2.0 ** 24)
+    with pytest.raises(HEError) as e:
+        g.he_im2col_conv_bsgs_pt(x1, gD, None, chunk, g_)
+    assert e.value.name == "LEVEL_MISMATCH"
+    g2 = Context(11, bits, 1, 5)
+    g2.he_keygen(steps[:-1])
+    x2 = g2.he_ct_import_words(np.stack([c.words for c in o_in]), lvl, 2.0 ** 24)
+    gD2 = g2.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in Dv]), ps, lvl)
+    with pytest.raises(HEError) as e:
+        g2.he_im2col_conv_bsgs_pt(x2, gD2, None, chunk, g_)
+    assert e.value.name == "MISSING_GALOIS_KEY"
+
+
+@pytest.mark.parametrize("bits", [(50, 40, 40, 50), (31, 26, 26, 31)], ids=["64bit", "32bit"])
+def test_folded_vec_mat_small_ragged_bit_exact(bits):
+    """he_vec_mat_bsgs_fold_pt (n 64 -> m 16, g 8: 2 groups + fold 4) on N = 2^11 with a ragged
+    batch of 3: word for word with oracle vec_mat_bsgs_fold on both engines; the encode-side form
+    (he_vec_mat_encode_bsgs_fold + he_vec_mat_pt) decrypts to x @ W; m not dividing n is rejected."""
+    from paper_2104_03152_b200 import Context, HEError
+    n, m, gg = 64, 16, 8
+    steps = sorted(set(range(1, gg)) | {gg} | {m * t for t in range(1, n // m)})
+    o = OracleContext(11, bits, 1, 9)
+    o.keygen(steps)
+    g = Context(11, bits, 1, 9)
+    g.he_keygen(steps)
+    rng = np.random.default_rng(11)
+    W, bias = rng.normal(0, 0.2, (n, m)), rng.uniform(-0.5, 0.5, m)
+    xs = rng.uniform(-1, 1, (3, n))
+    lvl = 2
+    o_in = [o.encrypt(o.encode(OC.replicate(x, o.slots), 2.0 ** 30, lvl), 60 + b) for b, x in enumerate(xs)]
+    x = g.he_ct_import_words(np.stack([c.words for c in o_in]), lvl, 2.0 ** 30)
+    ps = float(o.q[lvl])
+    E = OC.bsgs_diagonals(OC.vecmat_diagonals(W, o.slots, True)[:m], gg).reshape(-1, o.slots)
+    gD = g.he_pt_from_int_coeffs_qp(np.stack([o.encode_coeffs(v, ps)[1] for v in E]), ps, lvl)
+    y = g.he_vec_mat_bsgs_fold_pt(x, gD, gg, n, m, None)
+    for b in range(3):
+        ref = OC.vec_mat_bsgs_fold(o, o_in[b], W, None, 0, g=gg)
+        assert np.array_equal(y.words()[b], ref.words), b
+    d, bp = g.he_vec_mat_encode(W, bias, True, 0, lvl, 2.0 ** 30, lazy=True, bsgs_g=gg, fold=True)
+    z = g.he_decode(g.he_decrypt(g.he_vec_mat_pt(x, d, bp)), o.slots)
+    # at scale 2^30 the key-switch noise of the 11 rotations is ~1e-5 per slot (~1e-3 at 2^24)
+    for b in range(3):
+        assert np.max(np.abs(z[b] - np.tile(xs[b] @ W + bias, o.slots // m))) < 1e-3
+    with pytest.raises(HEError) as e:
+        g.he_vec_mat_encode(W[:, :12], bias[:12], True, 0, lvl, 2.0 ** 30, lazy=True, bsgs_g=4, fold=True)
+    assert e.value.name == "SHAPE_MISMATCH"
+
+
+def test_symmetric_encryption_needs_the_secret_key():
+    from paper_2104_03152_b200 import Context, HEError
+    g = Context(10, (31, 26, 31), 1, 1)
+    g.he_keygen([])
+    pt = g.he_encode(np.ones((1, 4)), 2.0 ** 20, 1)
+    ct = g.he_encrypt_symmetric(pt, 0, 99)
+    assert np.max(np.abs(g.he_decode(g.he_decrypt(ct), 4) - 1.0)) < 1e-3
+    g.he_drop_secret_key()
+    with pytest.raises(HEError) as e:
+        g.he_encrypt_symmetric(pt, 0, 99)
+    assert e.value.name == "MISSING_KEY"
