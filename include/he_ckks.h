@@ -125,7 +125,8 @@ he_status he_context_cdt(const he_context* ctx, uint64_t* table_out);
 he_status he_set_stream(he_context* ctx, void* stream);
 /* (Switching streams first synchronizes the old one: the context caches freed device
  * scratch blocks by size and hands them to later work in stream order.) */
-/* Block until all work queued on the context's stream is done. */
+/* Block until all work queued on the context's stream is done; reports (and
+ * clears) an asynchronous he_encode_device overflow as HE_SCALE_OVERFLOW. */
 he_status he_sync(he_context* ctx);
 
 /* Key generation on the device: ternary
@@ -145,7 +146,12 @@ he_status he_drop_secret_key(he_context* ctx);
  * limbs 0..level and NTT'd.  Canonical-embedding IFFT in float64 on device. */
 he_status he_encode(he_context* ctx, const double* z, size_t n_per_item, size_t B, double scale,
                     int level, he_plaintext** out);
-/* Same, with z already in device memory. */
+/* Same, with z already in device memory, and ASYNCHRONOUS: it only enqueues
+ * work on the context's stream (a server pipeline never drains the device at
+ * an encode).  A |scale z| >= 2^62 overflow is then reported as
+ * HE_SCALE_OVERFLOW by the next he_sync or host-output he_decode on this
+ * context (the affected plaintext is undefined); the other argument checks
+ * still fail here. */
 he_status he_encode_device(he_context* ctx, const double* z_dev, size_t n_per_item, size_t B,
                            double scale, int level, he_plaintext** out);
 /* Decode the first n slots of every item into host out[B][n]: CRT compose,

@@ -161,6 +161,7 @@ he_status he_sync(he_context* c) {
   return guard([&] {
     need_ctx(c);
     HE_CK(cudaStreamSynchronize(c->stream));
+    take_err(c);
   });
 }
 
@@ -236,14 +237,14 @@ he_status he_drop_secret_key(he_context* c) {
 
 // ---------------------------------------------------------------- encode ---
 static void encode_common(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
-                          he_plaintext** out) {
+                          he_plaintext** out, bool check_now = true) {
   need_ctx(c);
   need_out(out);
   need(B >= 1, HE_INVALID_ARGUMENT, "B must be >= 1");
   need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
   need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
   need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
-  *out = encode(c, z_dev, n, B, scale, level);
+  *out = encode(c, z_dev, n, B, scale, level, 0, check_now);
 }
 
 he_status he_encode(he_context* c, const double* z, size_t n, size_t B, double scale, int level,
@@ -258,7 +259,7 @@ he_status he_encode(he_context* c, const double* z, size_t n, size_t B, double s
 
 he_status he_encode_device(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
                            he_plaintext** out) {
-  return guard([&] { encode_common(c, z_dev, n, B, scale, level, out); });
+  return guard([&] { encode_common(c, z_dev, n, B, scale, level, out, false); });
 }
 
 he_status he_decode(he_context* c, const he_plaintext* pt, double* out, size_t n) {
@@ -271,6 +272,7 @@ he_status he_decode(he_context* c, const he_plaintext* pt, double* out, size_t n
     decode(c, pt, d.as<double>(), n);
     HE_CK(cudaMemcpyAsync(out, d.p, (size_t)pt->B * n * 8, cudaMemcpyDeviceToHost, c->stream));
     HE_CK(cudaStreamSynchronize(c->stream));
+    take_err(c);
   });
 }
 

@@ -48,6 +48,7 @@ struct he_context {
   ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [NP][N] (w, floor(w 2^64 / q))
   uint2 *d_tw32 = nullptr, *d_itw32 = nullptr;      // [NP][N] (w, floor(w 2^32 / q)); small primes only
   he::u64* d_cdt = nullptr;
+  int* d_err = nullptr;   // sticky device-side error flag (asynchronous he_encode_device overflow)
   he::u64 *d_P_mod = nullptr, *d_Pinv_mod = nullptr, *d_Ph_mod = nullptr;
   he::u64 *d_Phat_inv = nullptr, *d_Phat_mod = nullptr;
   he::u64 *d_rs_qinv = nullptr, *d_rs_h = nullptr, *d_crt = nullptr;

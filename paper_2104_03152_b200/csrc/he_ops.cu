@@ -1,3 +1,5 @@
+#include <mutex>
+#include <unordered_map>
 // he_ops.cu — kernels and internal operations of the B200 CKKS hot path
 // (SURVEY.md §8(a) a1-a16).  Product code: shares nothing with oracle/.
 #include <algorithm>
@@ -57,6 +59,18 @@ void dfree(he_context* c, void* p) {
   c->free_bins[it->second].push_back(p);
   c->cached_bytes += it->second;
   c->live_bytes.erase(it);
+}
+
+// cudaFuncSetAttribute waits for the device when the kernel is in flight, so a per-call attribute
+// set inside a launch path drains the stream; each kernel's dynamic smem limit is raised once.
+static void smem_limit_once(const void* f, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[f];
+  if (have >= bytes) return;
+  HE_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
 }
 
 template <class T>
@@ -122,6 +136,7 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
     c->d_itw2 = upload(c, i2);
   }
   c->d_cdt = upload(c, hp.cdt);
+  c->d_err = upload(c, std::vector<int>(1, 0));
   c->d_P_mod = upload(c, hp.P_mod);
   c->d_Pinv_mod = upload(c, hp.Pinv_mod);
   c->d_Ph_mod = upload(c, hp.Ph_mod);
@@ -1059,7 +1074,7 @@ void ring_mul(he_context* c, const u64* a, const u64* b, u64* out, size_t items,
   const int nblk = (int)(items * nl);
   auto run = [&](auto kern, int T, int smem) {
     static_cast<void>(T);
-    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_limit_once((const void*)kern, smem);
     {
       ProfScope ps_(c, "ntt_mul_intt", alg_bytes(j, nblk), nblk, nblk * (2 * ntt_ops(c->N, c->logN) + c->N));
       kern<<<nblk, T, smem, c->stream>>>(j, c->d_primes, c->d_tw2, c->d_itw2);
@@ -1155,21 +1170,26 @@ he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plai
   const int B = std::max(a->B, p->B);
   he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale);
   const size_t LN = (size_t)Lc * c->N;
-  // copy all polys, then add the plaintext into poly 0 of every item
-  for (int b = 0; b < B; ++b) {
-    const u64* src = a->d + (a->B == 1 ? 0 : (size_t)b * a->size * LN);
-    HE_CK(cudaMemcpyAsync(o->d + (size_t)b * a->size * LN, src, a->size * LN * 8, cudaMemcpyDeviceToDevice,
-                          c->stream));
-  }
+  // poly 0 of every item: a + p (items as size-1 rows at stride size*LN) ...
   const size_t rows = (size_t)B * Lc;
-  // treat items as size-1 rows at stride size*LN
   {
     ProfScope ps_(c, "pw_add", 0.0, 0);
-    k_binop<OP_ADD><<<rows_grid2(c, rows), 256, 0, c->stream>>>(o->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
-                                                                a->size * LN, p->B == 1 ? 0 : LN, Lc, 0,
-                                                                a->size * LN);
+    k_binop<OP_ADD><<<rows_grid2(c, rows), 256, 0, c->stream>>>(a->d, p->d, o->d, c->d_primes, c->N, Lc, rows,
+                                                                a->B == 1 ? 0 : a->size * LN, p->B == 1 ? 0 : LN,
+                                                                Lc, 0, a->size * LN);
   }
   check_launch(c);
+  // ... and polys 1..size-1 copied: one strided copy (a per-item loop only to broadcast a single item)
+  if (a->size > 1) {
+    const size_t w = (size_t)(a->size - 1) * LN * 8, pitch = (size_t)a->size * LN * 8;
+    if (a->B == B) {
+      HE_CK(cudaMemcpy2DAsync(o->d + LN, pitch, a->d + LN, pitch, w, B, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      for (int b = 0; b < B; ++b)
+        HE_CK(cudaMemcpyAsync(o->d + (size_t)b * a->size * LN + LN, a->d + LN, w, cudaMemcpyDeviceToDevice,
+                              c->stream));
+    }
+  }
   return o;
 }
 
@@ -1279,7 +1299,7 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
   FusedArgs fa{c->N, c->logN, Lc, c->K, c->L, c->NP, g, coef.as<u32>(), dsrc, bs, key32, c->d_q, accx.as<u64>()};
   auto launch = [&](auto kern, int T) {
     const int smem = (int)((N + N / 32 + 2 * N) * 4);
-    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_limit_once((const void*)kern, smem);
     // algorithmic bytes: digits read once per item, key rows once per launch, accumulators written once
     const double bytes = 4.0 * N * B * Lc + 4.0 * N * B * 2 * nt + 4.0 * N * 2 * Lc * nt;
     const double ops = (double)B * (Lc * (nt - 1)) * ntt_ops((int)N, c->logN) + (double)B * nt * Lc * 2 * N;
@@ -1444,7 +1464,7 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
           const_cast<he_plaintext*>(diags)->dm = dmp;
         }
         auto launch = [&](auto kern) {
-          HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+          smem_limit_once((const void*)kern, (int)kMaxSmem);
           kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, k32t, diags->dm, c->d_primes);
         };
         switch (Lc) {
@@ -1627,7 +1647,7 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
                                               "vecmat_bsgs_L8"};
           ProfScope ps_(c, tags[Lc], bytes, B * nt, ops);
           auto launch = [&](auto kern) {
-            HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+            smem_limit_once((const void*)kern, (int)kMaxSmem);
             kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, g, kt, diags->dm, c->d_primes);
           };
 #define HE_BSGS_CASE(LCV)                                                        \
@@ -1965,26 +1985,32 @@ void keygen(he_context* c, const std::vector<int>& steps) {
 }
 
 // ---- encode / decode / encrypt / decrypt --------------------------------------
-he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp) {
+// check_now: read the overflow flag back (stream sync) and fail here; otherwise the kernel ORs it
+// into the context's sticky flag, reported by the next he_sync / host-output decode (take_err).
+he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp,
+                     bool check_now) {
   const int N = c->N, M = N / 2, logM = c->logN - 1;
   Scratch m(c, B * N * 8), flag(c, 4);
-  HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
+  if (check_now) HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
   const bool in_smem = M <= 8192;
   Scratch g(c, in_smem ? 8 : B * M * 16);
   const int smem = in_smem ? M * 16 : 0;
   if (smem > 48 * 1024)
-    HE_CK(cudaFuncSetAttribute(k_encode_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_limit_once((const void*)k_encode_fft, smem);
   {
     ProfScope ps_(c, "encode_fft", 0.0, 0);
-    k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m.as<i64>(), flag.as<int>(), c->d_slot_index,
+    k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m.as<i64>(),
+                                                        check_now ? flag.as<int>() : c->d_err, c->d_slot_index,
                                                         c->d_fft_w, c->d_zeta, N, logM,
                                                         in_smem ? nullptr : g.as<double2>());
   }
   check_launch(c);
-  int hflag = 0;
-  HE_CK(cudaMemcpyAsync(&hflag, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
-  HE_CK(cudaStreamSynchronize(c->stream));
-  if (hflag) throw HeError(HE_SCALE_OVERFLOW, "encode: |scale * z| >= 2^62");
+  if (check_now) {
+    int hflag = 0;
+    HE_CK(cudaMemcpyAsync(&hflag, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    HE_CK(cudaStreamSynchronize(c->stream));
+    if (hflag) throw HeError(HE_SCALE_OVERFLOW, "encode: |scale * z| >= 2^62");
+  }
   he_plaintext* pt = pt_new(c, (int)B, level, scale, qp);
   signed_to_ntt(c, m.as<i64>(), pt->d, B, pt_limbs(pt), level + 1);
   return pt;
@@ -2012,7 +2038,7 @@ void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n) {
   Scratch g(c, in_smem ? 8 : B * M * 16);
   const int smem = in_smem ? M * 16 : 0;
   if (smem > 48 * 1024)
-    HE_CK(cudaFuncSetAttribute(k_decode_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_limit_once((const void*)k_decode_fft, smem);
   {
     ProfScope ps_(c, "decode_fft", 0.0, 0);
     k_decode_fft<<<(unsigned)B, 512, smem, c->stream>>>(X.as<double>(), n, pt->scale, out_dev, c->d_slot_index,
@@ -2120,6 +2146,18 @@ he_plaintext* decrypt(he_context* c, const he_ciphertext* ct) {
   }
   check_launch(c);
   return pt;
+}
+
+// Sticky asynchronous errors: read and clear (the caller has synchronized or is about to).
+void take_err(he_context* c) {
+  int h = 0;
+  HE_CK(cudaMemcpyAsync(&h, c->d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+  HE_CK(cudaStreamSynchronize(c->stream));
+  if (h) {
+    HE_CK(cudaMemsetAsync(c->d_err, 0, 4, c->stream));
+    HE_CK(cudaStreamSynchronize(c->stream));
+    throw HeError(HE_SCALE_OVERFLOW, "an asynchronous he_encode_device saw |scale * z| >= 2^62");
+  }
 }
 
 int check_words(he_context* c, const u64* w, size_t items, int Lc) {

@@ -28,7 +28,9 @@ int check_words(he_context* c, const u64* w, size_t items, int Lc);
 
 // scheme
 void keygen(he_context* c, const std::vector<int>& steps);
-he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp = 0);
+he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp = 0,
+                     bool check_now = true);
+void take_err(he_context* c);
 he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level, int qp = 0);
 void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n);
 he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id);

@@ -107,6 +107,13 @@ def test_encode_errors(cfg1):
     with pytest.raises(HEError) as e:
         g.he_encode(np.full(8, 1e12), 2.0 ** 40, 2)
     assert e.value.name == "SCALE_OVERFLOW"
+    # device input is asynchronous: the overflow is reported (once) by the next he_sync
+    import torch
+    g.he_encode(torch.full((1, 8), 1e12, dtype=torch.float64, device="cuda"), 2.0 ** 40, 2)
+    with pytest.raises(HEError) as e:
+        g.he_sync()
+    assert e.value.name == "SCALE_OVERFLOW"
+    g.he_sync()
 
 
 # ---------------------------------------------------------- encrypt/decrypt ---
