@@ -1,6 +1,9 @@
 // he_jobs.cuh — load/store functors that fuse each CKKS step into the NTT
 // kernels of he_ntt.cuh (SURVEY.md §8(a) kernels K1-K7).  Product code.
 #pragma once
+#include <type_traits>
+#include <utility>
+
 #include "he_common.cuh"
 
 namespace he {
@@ -22,6 +25,11 @@ __device__ __forceinline__ u32 mulsh32(u32 x, u32 w, u32 wsh, u32 q) {   // Shou
 }
 __device__ __forceinline__ u32 shoup_companion32(u32 w, u32 q) { return (u32)(((u64)w << 32) / q); }
 __device__ __forceinline__ u32 mu32_of(const PrimeD& P) { return (u32)(P.mu64 >> 32); }
+
+template <class B, class = void>
+struct has_load4 : std::false_type {};
+template <class B>
+struct has_load4<B, std::void_t<decltype(std::declval<const B&>().load4(0u))>> : std::true_type {};
 
 template <class Job>
 struct JobAt {
@@ -163,6 +171,52 @@ struct JobEncrypt {
     } else {
       *c1 = add_mod(*c1, v, P.q);
     }
+  }
+  // 32-bit engine: load4(j) draws coefficients 4j..4j+3 from one Philox block (ternary) or two
+  // (CDT) instead of one block per coefficient; the store is u32 arithmetic on bound rows
+  struct B32 {
+    const PrimeD* P;
+    const u64* cdt;
+    u64 seed, sid;
+    u64* c0;
+    u64* c1;
+    const u64* pkb;
+    const u64* pka;
+    const u64* m;
+    u32 q;
+    int which;
+    __device__ __forceinline__ u32 res(i64 v) const { return v < 0 ? q - (u32)(-v) : (u32)v; }
+    __device__ __forceinline__ uint4 load4(u32 j) const {
+      if (which == 0) {
+        const uint4 b = philox_block(seed, sid, j);
+        auto t = [&](u32 w) { return res((i64)(((u64)w * 3u) >> 32) - 1); };
+        return make_uint4(t(b.x), t(b.y), t(b.z), t(b.w));
+      }
+      return make_uint4(res(sample_cdt(seed, sid, 4 * j, cdt)), res(sample_cdt(seed, sid, 4 * j + 1, cdt)),
+                        res(sample_cdt(seed, sid, 4 * j + 2, cdt)), res(sample_cdt(seed, sid, 4 * j + 3, cdt)));
+    }
+    __device__ __forceinline__ u64 load(u32 n) const {
+      return which == 0 ? res(sample_ternary(seed, sid, n)) : res(sample_cdt(seed, sid, n, cdt));
+    }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      if (which == 0) {
+        c0[n] = add32((u32)mul_mod(v, pkb[n], *P), (u32)m[n], q);
+        c1[n] = (u32)mul_mod(v, pka[n], *P);
+      } else if (which == 1) {
+        c0[n] = add32((u32)c0[n], (u32)v, q);
+      } else {
+        c1[n] = add32((u32)c1[n], (u32)v, q);
+      }
+    }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    const int b = blk / Lc, i = blk % Lc;
+    const size_t LN = (size_t)Lc * N;
+    const u64 obj = stream0 + (u64)b;
+    const u64 pur = which == 0 ? PUR_ENC_V : which == 1 ? PUR_ENC_E0 : PUR_ENC_E1;
+    u64* c0 = ct + (size_t)b * 2 * LN + (size_t)i * N;
+    return B32{&P, cdt, seed, stream_sid(pur, obj, 0), c0, c0 + LN, pk + (size_t)i * N, pk + ((size_t)L + i) * N,
+               pt + (size_t)b * pt_bs + (size_t)i * N, (u32)P.q, which};
   }
 };
 inline double alg_bytes(const JobEncrypt& j, int nblk) {

@@ -439,7 +439,17 @@ k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw
   const uint2* tw = tw_all + (size_t)pi * G::N;
   const u32 q = (u32)P.q;
   const auto jb = bind_job(job, blk, P, 0);   // block decomposition + constants, once per CTA
-  for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)jb.load(i);
+  if constexpr (has_load4<decltype(jb)>::value) {   // 4 consecutive words per call (shared draws)
+    for (u32 j = tid; j < G::NL / 4; j += G::T) {
+      const uint4 v = jb.load4(j);
+      sm32[spad32(4 * j)] = v.x;
+      sm32[spad32(4 * j + 1)] = v.y;
+      sm32[spad32(4 * j + 2)] = v.z;
+      sm32[spad32(4 * j + 3)] = v.w;
+    }
+  } else {
+    for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)jb.load(i);
+  }
   __syncthreads();
   ntt_run32<LOGN, INV>(sm32, tid, tw, q);
   const uint2 ni = __ldg(tw);
