@@ -270,9 +270,9 @@ he_status he_decode(he_context* c, const he_plaintext* pt, double* out, size_t n
     need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
     Scratch d(c, std::max<size_t>(1, (size_t)pt->B * n) * 8);
     decode(c, pt, d.as<double>(), n);
+    take_err(c);   // (syncs) an asynchronous encode error fails the call before out is written
     HE_CK(cudaMemcpyAsync(out, d.p, (size_t)pt->B * n * 8, cudaMemcpyDeviceToHost, c->stream));
     HE_CK(cudaStreamSynchronize(c->stream));
-    take_err(c);
   });
 }
 

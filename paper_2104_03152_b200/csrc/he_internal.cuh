@@ -205,6 +205,8 @@ struct has_raw32<J, std::void_t<decltype(std::declval<const J&>().raw32(0))>> : 
 #define HE_NTT32_PIPE 1
 #endif
 
+// Kernel attributes and the occupancy-sized grid are configured once per process: the library
+// runs one process per GPU, so the first device's values hold for all calls.
 template <int LOGN, bool INV, class Job>
 void launch_ntt32_pipe(he_context* c, const Job& job, int nblk) {
   typedef NttGeomS<LOGN> G;
