@@ -595,6 +595,10 @@ struct JobRescaleData {
   const u64* h;     // [Lc-1] (q_l-1)/2 mod q_i   (row l of rs_h)
   const u64* qinv;  // [Lc-1] q_l^{-1} mod q_i
   int N, Lc;
+  // optional fused bias (vec_mat): poly 0 of item r / size gets + bias[item * bias_bs + i * N + n]
+  const u64* bias = nullptr;
+  size_t bias_bs = 0;
+  int size = 2;
   __device__ int prime(int blk) const { return blk % (Lc - 1); }
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
     // [y]_{q_i} - [h]_{q_i}: h is added to every coefficient (C15), so it is
@@ -606,25 +610,31 @@ struct JobRescaleData {
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
     const u64 t = sub_mod(src.at(r, i, n, P), v, P.q);
-    out[((size_t)r * (Lc - 1) + i) * N + n] = mul_mod(t, __ldg(qinv + i), P);
+    u64 o = mul_mod(t, __ldg(qinv + i), P);
+    if (bias && r % size == 0) o = add_mod(o, bias[(size_t)(r / size) * bias_bs + (size_t)i * N + n], P.q);
+    out[((size_t)r * (Lc - 1) + i) * N + n] = o;
   }
   struct B32 {
     const RescaleSrc* src;
     const PrimeD* P;
     const u32* y;
     u64* out;
+    const u64* bias;   // bias row (poly 0 only) or null
     int r, i;
     u32 q, mu32, h, qi, qish;
     __device__ __forceinline__ u64 load(u32 n) const { return sub32(red32(y[n], q, mu32), h, q); }
     __device__ __forceinline__ u64 load_raw(u32 x) const { return sub32(red32(x, q, mu32), h, q); }
     __device__ __forceinline__ void store(u32 n, u64 v) const {
-      out[n] = mulsh32(sub32((u32)src->at(r, i, n, *P), (u32)v, q), qi, qish, q);
+      u32 o = mulsh32(sub32((u32)src->at(r, i, n, *P), (u32)v, q), qi, qish, q);
+      if (bias) o = add32(o, (u32)bias[n], q);
+      out[n] = o;
     }
   };
   __device__ B32 bind32(int blk, const PrimeD& P) const {
     const int r = blk / (Lc - 1), i = blk % (Lc - 1);
     const u32 q = (u32)P.q, qi = (u32)__ldg(qinv + i);
-    return B32{&src, &P, raw32(blk), out + ((size_t)r * (Lc - 1) + i) * N, r, i, q, mu32_of(P),
+    const u64* brow = bias && r % size == 0 ? bias + (size_t)(r / size) * bias_bs + (size_t)i * N : nullptr;
+    return B32{&src, &P, raw32(blk), out + ((size_t)r * (Lc - 1) + i) * N, brow, r, i, q, mu32_of(P),
                (u32)__ldg(h + i), qi, shoup_companion32(qi, q)};
   }
   __host__ __device__ bool pipe_ok() const { return true; }

@@ -1209,20 +1209,26 @@ he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphert
 
 // ---- rescale (a11, C15) ----------------------------------------------------
 // rows R of polynomials at level l (src: rows of x, or ct (.) K products) -> out [R][l][N]
-static void rescale_rows(he_context* c, const RescaleSrc& src, size_t R, int l, u64* out) {
+static void rescale_rows(he_context* c, const RescaleSrc& src, size_t R, int l, u64* out,
+                         const he_plaintext* bias = nullptr, int size = 2) {
   const int Lc = l + 1;
   Scratch y(c, R * c->N * 8);
   JobRescaleLast j1{src, y.as<u64>(), c->N, Lc};
   launch_ntt<true>(c, j1, (int)R);
   JobRescaleData j2{src, y.as<u64>(), out, c->d_rs_h + (size_t)l * c->L, c->d_rs_qinv + (size_t)l * c->L, c->N, Lc};
+  if (bias) {   // + bias on poly 0 (the same words as a following add_plain: modular addition is exact)
+    j2.bias = bias->d;
+    j2.bias_bs = bias->B == 1 ? 0 : (size_t)(Lc - 1) * c->N;
+    j2.size = size;
+  }
   launch_ntt<false>(c, j2, (int)(R * (Lc - 1)));
 }
 
-he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a) {
+he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a, const he_plaintext* bias) {
   const int l = a->level;
   he_ciphertext* o = ct_new(c, a->B, a->size, l - 1, a->scale / (double)c->hp.q[l]);
   RescaleSrc src{a->d, nullptr, 0, c->N, l + 1};
-  rescale_rows(c, src, (size_t)a->B * a->size, l, o->d);
+  rescale_rows(c, src, (size_t)a->B * a->size, l, o->d, bias, a->size);
   return o;
 }
 
@@ -1517,17 +1523,12 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
     he_ciphertext* acc = ct_vec_mat_lazy(c, x, diags, keys, gals);
     he_ciphertext* res = nullptr;
     try {
-      res = ct_rescale(c, acc);
+      res = ct_rescale(c, acc, bias);   // bias fused into the rescale's store
     } catch (...) {
       ct_free(acc);
       throw;
     }
     ct_free(acc);
-    if (bias) {
-      he_ciphertext* r2 = ct_add_plain(c, res, bias);
-      ct_free(res);
-      res = r2;
-    }
     return res;
   }
   // k = 0 term
@@ -1739,13 +1740,8 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
       ct_free(acc);
       acc = f;
     }
-    he_ciphertext* res = ct_rescale(c, acc);
+    he_ciphertext* res = ct_rescale(c, acc, bias);   // bias fused into the rescale's store
     ct_free(acc);
-    if (bias) {
-      he_ciphertext* r2 = ct_add_plain(c, res, bias);
-      ct_free(res);
-      res = r2;
-    }
     return res;
   } catch (...) {
     cleanup();
