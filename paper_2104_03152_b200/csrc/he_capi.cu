@@ -407,15 +407,7 @@ he_status he_square(he_context* c, const he_ciphertext* a, he_ciphertext** out) 
     need(a->size == 2, HE_SHAPE_MISMATCH, "square needs a size-2 ciphertext");
     need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
     need(a->level >= 1, HE_LEVEL_EXHAUSTED, "square needs a level to rescale");
-    he_ciphertext* t = ct_tensor(c, a, a);
-    he_ciphertext* r = nullptr;
-    try {
-      r = ct_relinearize(c, t);
-    } catch (...) {
-      ct_free(t);
-      throw;
-    }
-    ct_free(t);
+    he_ciphertext* r = ct_square_relin(c, a);   // tensor fused into the key switch when available
     try {
       *out = ct_rescale(c, r);
     } catch (...) {

@@ -82,9 +82,11 @@ struct JobLimbsTo32 {
   u32* dst;
   int N, nl;
   size_t src_bs, dst_bs;
+  int sq = 0;   // 1: transform src^2 (the square's d2 = x1^2, formed here instead of by a tensor)
   __device__ int prime(int blk) const { return blk % nl; }
-  __device__ u64 load(int blk, u32 i, const PrimeD&) const {
-    return src[(size_t)(blk / nl) * src_bs + (size_t)(blk % nl) * N + i];
+  __device__ u64 load(int blk, u32 i, const PrimeD& P) const {
+    const u64 v = src[(size_t)(blk / nl) * src_bs + (size_t)(blk % nl) * N + i];
+    return sq ? mul_mod(v, v, P) : v;
   }
   __device__ void store(int blk, u32 i, u64 v, const PrimeD&) const {
     dst[(size_t)(blk / nl) * dst_bs + (size_t)(blk % nl) * N + i] = (u32)v;
@@ -92,12 +94,14 @@ struct JobLimbsTo32 {
   struct B32 {
     const u64* s;
     u32* d;
-    __device__ __forceinline__ u64 load(u32 i) const { return s[i]; }
+    const PrimeD* P;
+    int sq;
+    __device__ __forceinline__ u64 load(u32 i) const { return sq ? mul_mod(s[i], s[i], *P) : s[i]; }
     __device__ __forceinline__ void store(u32 i, u64 v) const { d[i] = (u32)v; }
   };
-  __device__ B32 bind32(int blk, const PrimeD&) const {
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
     const size_t it = (size_t)(blk / nl), l = (size_t)(blk % nl);
-    return B32{src + it * src_bs + l * N, dst + it * dst_bs + l * N};
+    return B32{src + it * src_bs + l * N, dst + it * dst_bs + l * N, &P, sq};
   }
 };
 inline double alg_bytes(const JobLimbsTo32& j, int nblk) { return 12.0 * j.N * nblk; }
@@ -344,6 +348,10 @@ struct KsArgs {
   // accx32: the accumulator words are u32 (small-prime fused key switch)
   const u64* accx;
   int accx32;
+  // square (he_square): poly 0 gets + x0^2 and poly 1 + 2 x0 x1 from x = sq_src (item stride
+  // sq_bs, 2 polys), i.e. the tensor's d0 / d1 formed in the epilogue instead of read
+  const u64* sq_src = nullptr;
+  size_t sq_bs = 0;
 };
 
 __device__ __forceinline__ u64 accx_word(const KsArgs& a, size_t i) {
@@ -471,6 +479,12 @@ struct JobKsData {
     const size_t LN = (size_t)a.Lc * a.N;
     if (part < a.add_parts)
       u = add_mod(u, a.addsrc[(size_t)b * a.add_bs + part * LN + (size_t)i * a.N + (a.add_gather ? sn : n)], P.q);
+    if (a.sq_src) {
+      const u64 x0 = a.sq_src[(size_t)b * a.sq_bs + (size_t)i * a.N + n];
+      const u64 x1 = a.sq_src[(size_t)b * a.sq_bs + LN + (size_t)i * a.N + n];
+      const u64 t = part == 0 ? mul_mod(x0, x0, P) : mul_mod(x0, x1, P);
+      u = add_mod(u, part == 0 ? t : add_mod(t, t, P.q), P.q);
+    }
     if (a.D) u = mul_mod(u, a.D[(size_t)kk * a.D_ks + (size_t)i * a.N + n], P);
     const size_t o = (size_t)kk * a.out_ks + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N + n;
     if (a.acc_in) u = add_mod(u, a.acc_in[o], P.q);
@@ -489,6 +503,8 @@ struct JobKsData {
     const u64* D;
     const u64* acc;
     u64* out;
+    const u64* sq0;   // square: x0 row of this limb (poly 0: + x0^2; poly 1 with sq1 = x1: + 2 x0 x1)
+    const u64* sq1;
     u32 q, mu32, ph, pinv, pinvsh, g;
     int logN;
     __device__ __forceinline__ u64 load(u32 n) const {
@@ -503,6 +519,10 @@ struct JobKsData {
       }
       u32 u = mulsh32(sub32(ax[n], (u32)v, q), pinv, pinvsh, q);
       if (add) u = add32(u, (u32)add[gather ? galois_src(n, g, logN) : n], q);
+      if (sq0) {
+        const u32 t = (u32)mul_mod(sq0[n], sq1 ? sq1[n] : sq0[n], *P);
+        u = add32(u, sq1 ? add32(t, t, q) : t, q);
+      }
       if (D) u = (u32)mul_mod(u, D[n], *P);
       if (acc) u = add32(u, (u32)acc[n], q);
       out[n] = u;
@@ -512,7 +532,7 @@ struct JobKsData {
     int kk, b, part, i;
     dec(blk, kk, b, part, i);
     const bool fast = pipe_ok();
-    B32 r{this, blk, &P, fast, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+    B32 r{this, blk, &P, fast, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
           (u32)P.q, mu32_of(P), 0, 0, 0, 1, a.logN};
     if (fast) {
       const size_t LN = (size_t)a.Lc * a.N;
@@ -528,6 +548,10 @@ struct JobKsData {
       const size_t o = (size_t)kk * a.out_ks + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N;
       if (a.acc_in) r.acc = a.acc_in + o;
       r.out = a.out + o;
+      if (a.sq_src) {
+        r.sq0 = a.sq_src + (size_t)b * a.sq_bs + (size_t)i * a.N;
+        if (part == 1) r.sq1 = r.sq0 + LN;
+      }
     }
     return r;
   }

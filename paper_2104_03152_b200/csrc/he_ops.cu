@@ -739,6 +739,7 @@ struct FusedArgs {
   const u32* key32;    // [L][2][NP][N] Montgomery form
   const u64* qtab;
   u64* accx;           // [B][2][Lc+K][N]
+  int sq = 0;          // 1: the digits are dsrc^2 (square: d2 = x1^2 formed on load)
 };
 template <int LOGN>
 __global__ void __launch_bounds__(NttGeomS<LOGN>::T, (1 << LOGN) <= 8192 ? 2 : 1)
@@ -760,7 +761,10 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
   for (int j = 0; j < a.Lc; ++j) {
     if (j == t) {
       const u64* src = a.dsrc + (size_t)b * a.dsrc_bs + (size_t)j * G::N;
-      for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)src[i];
+      if (a.sq)
+        for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)mul_mod(src[i], src[i], P);
+      else
+        for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)src[i];
     } else {
       const u32* src = a.coef + ((size_t)b * a.Lc + j) * G::N;
       const u32 qj = (u32)__ldg(a.qtab + j);
@@ -1294,15 +1298,16 @@ static void ks_launch(he_context* c, KsArgs& a) {
 static bool fused_ks_ok(he_context* c) { return c->small_primes && c->d_tw32 && c->logN <= 14; }
 
 static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, const u32* key32, u32 g,
-                     KsArgs& epi) {
+                     KsArgs& epi, int sq = 0) {
   const size_t N = c->N;
   const int nt = Lc + c->K;
   Scratch coef(c, (size_t)B * Lc * N * 4), accx(c, (size_t)B * 2 * nt * N * 4);
   {
-    JobLimbsTo32 j{dsrc, coef.as<u32>(), c->N, Lc, bs, (size_t)Lc * N};
+    JobLimbsTo32 j{dsrc, coef.as<u32>(), c->N, Lc, bs, (size_t)Lc * N, sq};
     launch_ntt<true>(c, j, B * Lc);
   }
-  FusedArgs fa{c->N, c->logN, Lc, c->K, c->L, c->NP, g, coef.as<u32>(), dsrc, bs, key32, c->d_q, accx.as<u64>()};
+  FusedArgs fa{c->N, c->logN, Lc, c->K, c->L, c->NP, g, coef.as<u32>(), dsrc, bs, key32, c->d_q, accx.as<u64>(),
+               sq};
   auto launch = [&](auto kern, int T) {
     const int smem = (int)((N + N / 32 + 2 * N) * 4);
     smem_limit_once((const void*)kern, smem);
@@ -1332,6 +1337,39 @@ const u64* galois_key(he_context* c, int step, u32* gal_out) {
   if (it == c->gk.end()) return nullptr;
   *gal_out = (u32)g;
   return it->second;
+}
+
+// Square + relinearize without the tensor: with the fused key switch, d2 = x1^2 is formed where
+// the digits are loaded (INTT and own-digit load) and d0 = x0^2, d1 = 2 x0 x1 in the ModDown
+// epilogue; the words equal ct_relinearize(ct_tensor(x, x)).  Other contexts take that path.
+he_ciphertext* ct_square_relin(he_context* c, const he_ciphertext* x) {
+  if (!(fused_ks_ok(c) && c->d_rlk32)) {
+    he_ciphertext* t = ct_tensor(c, x, x);
+    he_ciphertext* r = nullptr;
+    try {
+      r = ct_relinearize(c, t);
+    } catch (...) {
+      ct_free(t);
+      throw;
+    }
+    ct_free(t);
+    return r;
+  }
+  const int Lc = x->level + 1;
+  const size_t LN = (size_t)Lc * c->N;
+  he_ciphertext* o = ct_new(c, x->B, 2, x->level, x->scale * x->scale);
+  KsArgs k = ks_base(c, x->B, Lc, nullptr, nullptr, 0);
+  k.out = o->d;
+  k.out_bs = 2 * LN;
+  k.sq_src = x->d;
+  k.sq_bs = 2 * LN;
+  try {
+    ks_fused(c, x->d + LN, 2 * LN, x->B, Lc, c->d_rlk32, 1, k, 1);
+  } catch (...) {
+    ct_free(o);
+    throw;
+  }
+  return o;
 }
 
 he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a) {

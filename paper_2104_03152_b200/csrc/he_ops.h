@@ -46,6 +46,7 @@ he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plai
 he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphertext* y);
 he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a, const he_plaintext* bias = nullptr);
 he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a);
+he_ciphertext* ct_square_relin(he_context* c, const he_ciphertext* x);
 he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool add_input);
 he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                           const he_plaintext* bias);
