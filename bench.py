@@ -196,17 +196,15 @@ def run_ours(args, rank, world, local_rank):
                      "share": round(v[1] / tot, 3)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
 
     # --- e2e through the public API from pinned host images ---
-    # Every step: client im2col of the step's images (host, into pinned memory), H2D of the slot
-    # vectors, he_encode (device input: asynchronous), encrypt, forward, decrypt, he_decode into
-    # device memory and the D2H of the logits into pinned host memory, all enqueued on the context's
-    # stream; the H2D goes on a copy stream ordered by an event.  Depth-2 pipeline: the host waits
-    # for step i-1's logits only after enqueuing step i, then runs the im2col and H2D of step i+1
-    # while the device computes step i, so the device never drains between steps (each step's
-    # inputs and logits still cross PCIe inside the timed region).
+    # Every step, through the C-ABI host-buffer calls: client im2col of the step's images into
+    # page-locked memory, he_encode from that HOST buffer (its H2D copy runs on the context stream
+    # inside the call), encrypt, forward, decrypt, he_decode_async into page-locked HOST logits (the
+    # D2H copy is enqueued by the call).  Depth-2 pipeline: the host waits for step i-1's logits only
+    # after enqueuing step i, and runs step i+1's im2col while the device computes step i, so the
+    # device never drains between steps (each step's inputs and logits still cross PCIe inside the
+    # timed region).  Buffer k = i % 2 is reused only after step i-2 was waited for.
     pinned = [torch.from_numpy(imgs).pin_memory() for imgs in imgs_host]
     slot_buf = [torch.empty((B, ns), dtype=torch.float64).pin_memory() for _ in range(2)]
-    slot_dev2 = [torch.empty((B, ns), dtype=torch.float64, device=dev) for _ in range(2)]
-    logits_dev2 = [torch.empty((B, net.n_out), dtype=torch.float64, device=dev) for _ in range(2)]
     logits_pin = [torch.empty((B, net.n_out), dtype=torch.float64).pin_memory() for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]
     logits_host = np.zeros((B, net.n_out))
@@ -214,36 +212,23 @@ def run_ours(args, rank, world, local_rank):
     def im2col(i):
         he_im2col_encode_batch(pinned[i % n_batches].numpy(), 7, 7, 3, ns, out=slot_buf[i % 2].numpy())
 
-    copy_stream = torch.cuda.Stream(dev)
-    copied = [torch.cuda.Event() for _ in range(2)]
-
-    def h2d(i):   # step i's slot vectors on the copy stream (overlaps the previous step's compute)
-        k = i % 2
-        with torch.cuda.stream(copy_stream):
-            slot_dev2[k].copy_(slot_buf[k], non_blocking=True)
-            copied[k].record(copy_stream)
-
     def e2e_loop(first, count):
         im2col(first)
-        h2d(first)
         for i in range(first, first + count):
             k = i % 2
-            stream.wait_event(copied[k])                                                        # H2D done
-            pt = ctx.he_encode(slot_dev2[k], 2.0 ** net.plan["in_log2"], net.top)
+            pt = ctx.he_encode(slot_buf[k].numpy(), 2.0 ** net.plan["in_log2"], net.top)      # H2D inside
             dec = ctx.he_decrypt(net.forward(ctx.he_encrypt(pt, 2_000_000 + i * B)))
-            ctx.he_decode(dec, net.n_out, out=logits_dev2[k])
-            logits_pin[k].copy_(logits_dev2[k], non_blocking=True)                              # D2H
+            ctx.he_decode_async(dec, logits_pin[k].numpy(), net.n_out)                         # D2H inside
             done[k].record(stream)
             if i > first:
                 done[1 - k].synchronize()                       # step i-1 (and its buffers) finished
                 logits_host[:] = logits_pin[1 - k].numpy()
             if i + 1 < first + count:
                 im2col(i + 1)                                   # host work overlapping step i
-                h2d(i + 1)
         last = (first + count - 1) % 2
         done[last].synchronize()
         logits_host[:] = logits_pin[last].numpy()
-        ctx.he_sync()                                           # reports an asynchronous encode error
+        ctx.he_sync()
 
     e2e_loop(0, args.warmup)
     barrier()
@@ -267,6 +252,10 @@ def run_ours(args, rank, world, local_rank):
     e2e = {"value": world * B * args.steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": B * ns * 8, "d2h_bytes_per_step": B * net.n_out * 8}
 
+    check, cpu = None, None
+    if rank == 0 and not args.no_check:
+        check, cpu = bench_check(ctx, net, shard(n_batches), 3_000_000, dev, cpu_leg=(world == 1))
+
     extra = {}
     if rank == 0 and not args.no_extra:
         extra = micro_extra(ctx, stream, dev)
@@ -276,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
 
     extra["communication_cfg4"] = comm
     return dict(value=value, ms=ms, launches=launches, clocks=clk.summary(), roofline=roofline,
-                breakdown=breakdown, e2e=e2e, extra=extra)
+                breakdown=breakdown, e2e=e2e, extra=extra, check=check, cpu=cpu)
 
 
 def micro_extra(ctx_cnn, stream, dev):
@@ -340,6 +329,109 @@ def micro_extra(ctx_cnn, stream, dev):
 _ORACLE = {}
 
 
+def float_logits_torch(imgs, w):
+    """The paper's network in float64 with torch.nn.functional on the CPU (a library
+    pin of the plaintext network, independent of oracle/ and of the CUDA path)."""
+    import torch
+    t = lambda a: torch.tensor(np.asarray(a), dtype=torch.float64)
+    x = torch.nn.functional.conv2d(t(imgs)[:, None], t(w.conv_w), t(w.conv_b), stride=3)
+    x = x.flatten(1) ** 2
+    x = torch.nn.functional.linear(x, t(w.fc1_w), t(w.fc1_b)) ** 2
+    return torch.nn.functional.linear(x, t(w.fc2_w), t(w.fc2_b)).numpy()
+
+
+def oracle_context():
+    from oracle import circuits as OC
+    from oracle.oracle import OracleContext
+    from paper_2104_03152_b200.cnn import CONV_G, FC1_G
+    from synthetic import CFG4
+    if "o" not in _ORACLE:   # keys are made once (excluded from timing, like the GPU arm)
+        o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+        o.keygen(OC.cnn_rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
+        _ORACLE["o"] = o
+    return _ORACLE["o"]
+
+
+def bench_check(ctx, net, imgs, stream0, dev, items=None, cpu_leg=True):
+    """Correctness of the bench's own launch geometry (one batch of B images, the same calls and
+    launch configuration as the timed step), outside every timed region:
+      * items (default first, middle, last): their input plaintexts are the ORACLE's integer
+        encodings injected into the device-encoded batch (C7: encode is float-sensitive), the batch
+        is encrypted (stream stream0 + b) and evaluated on the GPU; the oracle encrypts and evaluates
+        the same items with the same stream ids; the output ciphertext words must be equal;
+      * all B decrypted logits within 5e-3 of the float64 network (torch.nn.functional) with equal
+        argmax (north_star).
+    The oracle runs here as the cpu_baseline leg (rank 0): the items in parallel on the host cores,
+    timed; returns (check, cpu_baseline)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import circuits as OC
+    from paper_2104_03152_b200.cnn import CONV_G, FC1_G
+    from paper_2104_03152_b200.ckks import he_im2col_encode_batch
+    from synthetic import CFG4, cnn_weights
+    B, ns, N = len(imgs), ctx.slots, ctx.N
+    items = items or sorted({0, B // 2, B - 1})
+    scale, top = 2.0 ** net.plan["in_log2"], net.top
+    slots = he_im2col_encode_batch(imgs, 7, 7, 3, ns)
+    o = oracle_context()
+    w = cnn_weights(CFG4.seed)
+    ms = np.stack([o.encode_coeffs(slots[s], scale)[1] for s in items])
+    # GPU: device encode of the batch, rows `items` replaced by the injected oracle encodings
+    pt = ctx.he_encode(torch.from_numpy(slots).to(dev), scale, top)
+    words = torch.empty((B, top + 1, N), dtype=torch.int64, device=dev)
+    ctx.he_pt_export_words(pt, words)
+    inj = torch.empty((len(items), top + 1, N), dtype=torch.int64, device=dev)
+    ctx.he_pt_export_words(ctx.he_pt_from_int_coeffs(ms, scale, top), inj)
+    words[items] = inj
+    pt = ctx.he_pt_import_words(words, top, scale)
+    out = net.forward(ctx.he_encrypt(pt, stream0))
+    logits = ctx.he_decode(ctx.he_decrypt(out), net.n_out)
+    gw = out.words()
+    ctx.he_sync()
+    # oracle on the items (cpu_baseline leg)
+    plan = OC.CNN_PLAN_BSGS
+
+    def one(k):
+        s = items[k]
+        ct = o.encrypt(o.coeffs_to_pt(ms[k], top, scale), stream0 + s)
+        y = OC.cnn_forward(o, ct, w, plan, lazy=True, bsgs=True, conv_g=CONV_G, fc1_g=FC1_G)
+        return y, o.decode(o.decrypt(y), net.n_out)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(len(items), os.cpu_count() or 1)) as ex:
+        res = list(ex.map(one, range(len(items))))
+    dt = time.perf_counter() - t0
+    exact = [bool(np.array_equal(gw[s], res[k][0].words)) for k, s in enumerate(items)]
+    ref = float_logits_torch(imgs, w)
+    err = np.max(np.abs(logits - ref), axis=1)
+    am = int(np.sum(np.argmax(logits, 1) == np.argmax(ref, 1)))
+    check = {"batch": B, "geometry": "the timed step's calls and launch configuration (B images per call)",
+             "bitexact_items": [int(s) for s in items], "bitexact": f"{sum(exact)}/{len(items)}",
+             "bitexact_ok": all(exact),
+             "oracle_logit_err_vs_gpu": float(max(np.max(np.abs(logits[s] - res[k][1])) for k, s in enumerate(items))),
+             "max_logit_err": float(np.max(err)), "median_logit_err": float(np.median(err)),
+             "within_5e-3": f"{int(np.sum(err < 5e-3))}/{B}", "argmax_equal": f"{am}/{B}",
+             "tolerance_ok": bool(np.max(err) < 5e-3 and am == B),
+             "reference": "float64 network via torch.nn.functional (CPU); bit-exact items vs oracle/ with the "
+                          "oracle's integer encodings injected (C7)"}
+    cpu = None
+    if cpu_leg:
+        cpu = {"value": len(items) / dt, "unit": UNIT, "cores": min(len(items), os.cpu_count() or 1),
+               "kind": "oracle", "cpu_model": cpu_model(),
+               "sample": f"{len(items)} images (items {items} of the checked batch): encrypt + forward + decrypt "
+                         f"through the CPU oracle, one per host thread, {dt:.1f} s"}
+    return check, cpu
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def oracle_sample(images: int = 1, start: int = 10_000):
     """Oracle CNN (encrypt + forward + decrypt, the GPU arm's evaluation schedule) on
     `images` independent images, in parallel over host threads (the oracle's C calls release the
@@ -349,11 +441,7 @@ def oracle_sample(images: int = 1, start: int = 10_000):
     from oracle.oracle import OracleContext
     from paper_2104_03152_b200.cnn import CONV_G, FC1_G
     from synthetic import CFG4, cnn_weights, mnist_like_images
-    if "o" not in _ORACLE:   # keys are made once (excluded from timing, like the GPU arm)
-        o = OracleContext(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
-        o.keygen(OC.cnn_rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
-        _ORACLE["o"] = o
-    o = _ORACLE["o"]
+    o = oracle_context()
     w = cnn_weights(CFG4.seed)
     imgs = mnist_like_images(images, 4, start=start)
     cores = os.cpu_count() or 1
@@ -394,7 +482,7 @@ def main():
     ap.add_argument("--batch", type=int, default=512, help="images per GPU per step (BASELINE config 5: batch 512)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the correctness check (and the cpu_baseline leg)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -422,7 +510,7 @@ def main():
         if rank == 0:
             line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
                     "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms"],
-                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
                     "data": "synthetic", "config": dict(config, batch_per_gpu=r["per_step"],
                                                         global_batch=r["per_step"],
                                                         reference=f"CPU oracle (oracle/), {r['per_step']} images "
@@ -439,16 +527,11 @@ def main():
 
     r = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            v, cores, dt = oracle_sample(1)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                   "sample": f"1 image (encrypt + forward + decrypt) through the CPU oracle, {dt:.1f} s"}
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": config, "clocks": r["clocks"], "gpu_launches": r["launches"],
-                "e2e": r["e2e"], "roofline": r["roofline"], "cpu_baseline": cpu,
+                "check": r["check"], "e2e": r["e2e"], "roofline": r["roofline"], "cpu_baseline": r["cpu"],
                 "breakdown": r["breakdown"], "extra": r["extra"],
                 "paper_context": "TenSEAL/SEAL CPU: 1456.29 ms/img (8 vCPU), 887.06 ms/img (16 vCPU), PAPER.md:113"}
         print(json.dumps(line), flush=True)

@@ -146,6 +146,14 @@ he_status he_drop_secret_key(he_context* ctx);
  * limbs 0..level and NTT'd.  Canonical-embedding IFFT in float64 on device. */
 he_status he_encode(he_context* ctx, const double* z, size_t n_per_item, size_t B, double scale,
                     int level, he_plaintext** out);
+/* (he_encode) The C7 bound is checked on the host before any work is queued:
+ * HE_SCALE_OVERFLOW when scale (2/N) sum_j |z_j| >= 2^62 (1 - 2^-20) for some
+ * item, or a value is not finite; the bound dominates every |m_i|, so no
+ * device readback is needed and the call returns after enqueuing the H2D copy
+ * and the encode kernels on the context's stream.  z is read by that copy:
+ * pageable memory may be reused when the call returns; page-locked memory
+ * (cudaHostAlloc, torch pin_memory) must stay unchanged until the stream has
+ * passed the call (he_sync, or an event recorded on the stream). */
 /* Same, with z already in device memory, and ASYNCHRONOUS: it only enqueues
  * work on the context's stream (a server pipeline never drains the device at
  * an encode).  A |scale z| >= 2^62 overflow is then reported as
@@ -157,6 +165,12 @@ he_status he_encode_device(he_context* ctx, const double* z_dev, size_t n_per_it
 /* Decode the first n slots of every item into host out[B][n]: CRT compose,
  * centre, float64, FFT, divide by the plaintext's scale (C6). */
 he_status he_decode(he_context* ctx, const he_plaintext* pt, double* out, size_t n);
+/* Same, ASYNCHRONOUS: enqueues the decode and the device-to-host copy into
+ * host out[B][n] on the context's stream and returns.  out is valid once the
+ * stream has passed the call (he_sync, or an event recorded on the stream);
+ * with page-locked out the copy overlaps later work (the e2e pipeline of
+ * bench.py).  A pending he_encode_device overflow is reported by he_sync. */
+he_status he_decode_async(he_context* ctx, const he_plaintext* pt, double* out, size_t n);
 /* Same, writing device memory out_dev[B][n]. */
 he_status he_decode_device(he_context* ctx, const he_plaintext* pt, double* out_dev, size_t n);
 

@@ -62,6 +62,7 @@ _SIGS = {
     "he_encode_device": [VP, VP, SZ, SZ, C.c_double, C.c_int, VPP],
     "he_decode": [VP, VP, DP, SZ],
     "he_decode_device": [VP, VP, VP, SZ],
+    "he_decode_async": [VP, VP, VP, SZ],
     "he_encrypt": [VP, VP, C.c_uint64, VPP],
     "he_encrypt_symmetric": [VP, VP, C.c_uint64, C.c_uint64, VPP],
     "he_decrypt": [VP, VP, VPP],
@@ -265,6 +266,12 @@ class Context:
         _check(lib().he_context_primes(h, pr.ctypes.data_as(U64P), ps.ctypes.data_as(U64P)))
         self.primes, self.psis = pr, ps
         self.q = [int(x) for x in pr]
+        self._stream = None
+        try:
+            import torch
+            self._device = torch.cuda.current_device() if torch.cuda.is_available() else None
+        except Exception:
+            self._device = None
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -286,6 +293,31 @@ class Context:
         """stream: a torch.cuda.Stream (or raw cudaStream_t int)."""
         s = getattr(stream, "cuda_stream", stream)
         _check(lib().he_set_stream(self.h, C.c_void_p(int(s) if s else 0)))
+        # kept so device inputs of asynchronous calls can be tied to this stream (record_stream)
+        self._stream = stream if hasattr(stream, "cuda_stream") else None
+
+    def _dev_input(self, t, what: str):
+        """A device float64 input read asynchronously on the context stream: checked for dtype and
+        device, made contiguous, and recorded on the context stream so torch's caching allocator does
+        not hand its memory to other work before the library's kernels have read it."""
+        import torch
+        if t.dtype != torch.float64:
+            raise HEError(17, f"{what}: device input must be float64, got {t.dtype}")
+        if self._device is not None and t.device.index != self._device:
+            raise HEError(17, f"{what}: tensor on cuda:{t.device.index}, context on cuda:{self._device}")
+        t = t.contiguous()
+        st = getattr(self, "_stream", None)
+        if st is not None and st.cuda_stream != torch.cuda.current_stream(t.device).cuda_stream:
+            t.record_stream(st)
+        return t
+
+    def _dev_output(self, out, shape, what: str):
+        import torch
+        if out.dtype != torch.float64 or tuple(out.shape) != tuple(shape) or not out.is_contiguous():
+            raise HEError(17, f"{what}: out must be a contiguous float64 tensor of shape {tuple(shape)}, "
+                              f"got {out.dtype} {tuple(out.shape)}")
+        if self._device is not None and out.device.index != self._device:
+            raise HEError(17, f"{what}: out on cuda:{out.device.index}, context on cuda:{self._device}")
 
     def he_sync(self) -> None:
         _check(lib().he_sync(self.h))
@@ -324,8 +356,7 @@ class Context:
         """z: [B][n] (or [n]) float64 host array, or a CUDA float64 tensor."""
         h = C.c_void_p()
         if _is_dev(z):
-            z2 = z if z.dim() == 2 else z.reshape(1, -1)
-            z2 = z2.contiguous()
+            z2 = self._dev_input(z if z.dim() == 2 else z.reshape(1, -1), "he_encode")
             _check(lib().he_encode_device(self.h, _ptr(z2), z2.shape[1], z2.shape[0], float(scale), level,
                                           C.byref(h)))
         else:
@@ -338,11 +369,22 @@ class Context:
         n = self.slots if n is None else n
         B = pt.B
         if out is not None and _is_dev(out):
+            self._dev_output(out, (B, n), "he_decode")
             _check(lib().he_decode_device(self.h, pt.h, _ptr(out), n))
             return out
+        if out is not None:
+            raise HEError(17, "he_decode: out must be a CUDA tensor (host results are returned)")
         res = np.zeros((B, n), dtype=np.float64)
         _check(lib().he_decode(self.h, pt.h, res.ctypes.data_as(DP), n))
         return res
+
+    def he_decode_async(self, pt: Plaintext, out, n: int) -> None:
+        """Enqueue decode + D2H into host `out` [B][n] float64 (a pinned torch tensor or numpy
+        array); valid after he_sync or an event recorded on the context stream."""
+        B = pt.B
+        if _is_dev(out) or tuple(out.shape) != (B, n) or str(out.dtype) not in ("torch.float64", "float64"):
+            raise HEError(17, f"he_decode_async: out must be a host float64 [{B}][{n}] buffer")
+        _check(lib().he_decode_async(self.h, pt.h, _ptr(out), n))
 
     def he_pt_from_int_coeffs(self, m, scale: float, level: int) -> Plaintext:
         m2 = np.ascontiguousarray(np.atleast_2d(np.asarray(m, dtype=np.int64)))
@@ -357,6 +399,20 @@ class Context:
         _check(lib().he_pt_from_int_coeffs_qp(self.h, m2.ctypes.data_as(I64P), m2.shape[0], float(scale), level,
                                               C.byref(h)))
         return Plaintext(self, h)
+
+    def he_pt_export_words(self, pt: Plaintext, out) -> None:
+        """Plaintext words [B][limbs][N] into `out` (a device int64/uint64 tensor or a host uint64 array)."""
+        if out.dtype not in (np.uint64,) and str(out.dtype) not in ("torch.int64", "torch.uint64"):
+            raise HEError(17, "he_pt_export_words: out must hold 64-bit words")
+        if int(np.prod(out.shape)) != pt.B * pt.limbs * self.N:
+            raise HEError(17, "he_pt_export_words: out has the wrong number of words")
+        _check(lib().he_pt_export_words(self.h, pt.h, _ptr(out), _is_dev(out)))
+
+    def he_ct_export_words(self, ct: Ciphertext, out) -> None:
+        """Ciphertext words [B][size][level+1][N] into `out` (device int64/uint64 tensor or host uint64 array)."""
+        if int(np.prod(out.shape)) != ct.B * ct.size * (ct.level + 1) * self.N:
+            raise HEError(17, "he_ct_export_words: out has the wrong number of words")
+        _check(lib().he_ct_export_words(self.h, ct.h, _ptr(out), _is_dev(out)))
 
     def he_pt_import_words(self, w, level: int, scale: float) -> Plaintext:
         h = C.c_void_p()
@@ -555,6 +611,9 @@ def he_im2col_encode_batch(imgs, kh: int, kw: int, stride: int, n_slots: int, ou
     B, H, W = imgs.shape
     if out is None:
         out = np.zeros((B, n_slots), dtype=np.float64)
+    elif (not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != (B, n_slots)
+          or not out.flags.c_contiguous):
+        raise HEError(17, f"he_im2col_encode_batch: out must be a C-contiguous float64 array of shape {(B, n_slots)}")
     _check(lib().he_im2col_encode_batch(imgs.ctypes.data_as(DP), B, H, W, kh, kw, stride, n_slots,
                                         out.ctypes.data_as(DP)))
     return out

@@ -247,13 +247,34 @@ static void encode_common(he_context* c, const double* z_dev, size_t n, size_t B
   *out = encode(c, z_dev, n, B, scale, level, 0, check_now);
 }
 
+// C7 bound, checked on the host before anything is enqueued: |m_i| <= scale (2/N) sum_j |z_j|, so
+// when that bound is below 2^62 (with a 2^-20 relative margin for the FFT's rounding) no
+// coefficient can overflow and the encode needs no device-to-host readback.
+static void host_overflow_check(const he_context* c, const double* z, size_t n, size_t B, double scale) {
+  const double lim = 4611686018427387904.0 * (1.0 - 1.0 / 1048576.0);
+  const double k = 2.0 * scale / (double)c->N;
+  for (size_t b = 0; b < B; ++b) {
+    double s = 0.0;
+    const double* zb = z + b * n;
+    for (size_t j = 0; j < n; ++j) s += std::fabs(zb[j]);
+    need(std::isfinite(s) && k * s < lim, HE_SCALE_OVERFLOW,
+         "encode: scale (2/N) sum |z| >= 2^62 (a coefficient may overflow), or a value is not finite");
+  }
+}
+
 he_status he_encode(he_context* c, const double* z, size_t n, size_t B, double scale, int level,
                     he_plaintext** out) {
   return guard([&] {
     need_ctx(c);
     need(z != nullptr || n == 0, HE_INVALID_ARGUMENT, "null input");
+    need(B >= 1, HE_INVALID_ARGUMENT, "B must be >= 1");
+    need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+    need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
+    host_overflow_check(c, z, n, B, scale);
+    // H2D on the context stream (asynchronous from pinned memory), then the encode kernels; the
+    // host bound above already excludes an overflow, so nothing is read back
     DevDoubles d(c, z, n * B);
-    encode_common(c, d.d, n, B, scale, level, out);
+    encode_common(c, d.d, n, B, scale, level, out, false);
   });
 }
 
@@ -273,6 +294,18 @@ he_status he_decode(he_context* c, const he_plaintext* pt, double* out, size_t n
     take_err(c);   // (syncs) an asynchronous encode error fails the call before out is written
     HE_CK(cudaMemcpyAsync(out, d.p, (size_t)pt->B * n * 8, cudaMemcpyDeviceToHost, c->stream));
     HE_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+he_status he_decode_async(he_context* c, const he_plaintext* pt, double* out, size_t n) {
+  return guard([&] {
+    need_ctx(c);
+    need_pt(c, pt);
+    need_out(out);
+    need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+    Scratch d(c, std::max<size_t>(1, (size_t)pt->B * n) * 8);
+    decode(c, pt, d.as<double>(), n);
+    HE_CK(cudaMemcpyAsync(out, d.p, (size_t)pt->B * n * 8, cudaMemcpyDeviceToHost, c->stream));
   });
 }
 
@@ -680,7 +713,6 @@ static void conv_checks(he_context* c, const he_ciphertext* ct, int C, int taps,
   need(chunk >= 1 && (chunk & (chunk - 1)) == 0 && chunk <= ns && ns % chunk == 0, HE_LAYOUT_MISMATCH,
        "chunk must be a power of two dividing n_s");
   need((size_t)taps * chunk <= (size_t)ns, HE_LAYOUT_MISMATCH, "taps x chunk exceeds the slots");
-  need(c->has_rlk || true, HE_MISSING_KEY, "");
 }
 
 static he_status conv_pt_impl(he_context* c, const he_ciphertext* ct, const he_plaintext* kernels,

@@ -43,6 +43,9 @@ struct he_context {
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
   bool small_primes = false;  // every prime < 2^31: 64-bit lazy sums of 62-bit products
+  // test knob (env HE_PIPE_GRID_CAP at context creation): caps the persistent NTT grid so that the
+  // multi-block prefetch loop of k_ntt32_pipe runs at small batch sizes too (tests only; 0 = off)
+  int pipe_grid_cap = 0;
   // device tables
   he::PrimeD* d_primes = nullptr;
   ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [NP][N] (w, floor(w 2^64 / q))
@@ -222,7 +225,9 @@ void launch_ntt32_pipe(he_context* c, const Job& job, int nblk) {
   }
   ProfScope ps(c, Job::kName, c->prof_on ? alg_bytes(job, nblk) : 0.0, nblk,
                c->prof_on ? alg_ops(job, nblk, LOGN) : 0.0);
-  kern<<<std::min(nblk, grid), G::T, NttGeom32Pipe<LOGN>::SMEM, c->stream>>>(
+  int gr = std::min(nblk, grid);
+  if (c->pipe_grid_cap > 0) gr = std::min(gr, c->pipe_grid_cap);
+  kern<<<gr, G::T, NttGeom32Pipe<LOGN>::SMEM, c->stream>>>(
       job, c->d_primes, INV ? c->d_itw32 : c->d_tw32, nblk);
   check_launch(c);
 }

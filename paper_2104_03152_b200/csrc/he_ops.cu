@@ -4,6 +4,7 @@
 // (SURVEY.md §8(a) a1-a16).  Product code: shares nothing with oracle/.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "he_internal.cuh"
@@ -90,12 +91,26 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
   c->K = hp.K;
   c->NP = hp.L + hp.K;
   c->seed = seed;
+  if (const char* cap = getenv("HE_PIPE_GRID_CAP")) c->pipe_grid_cap = atoi(cap);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
     throw HeError(HE_CUDA_ERROR, "no CUDA device available (the library has no CPU fallback)");
   }
   HE_CK(cudaGetDevice(&c->device));
+  {
+    // Kernel attributes (dynamic smem opt-in) and occupancy-sized persistent grids are configured
+    // once per process (he_internal.cuh launch helpers), which holds for one device per process
+    // (one process per GPU).  A second device would miss those attributes, so it is
+    // refused here instead of failing later at a launch.
+    static std::mutex mu;
+    static int first_device = -1;
+    std::lock_guard<std::mutex> lk(mu);
+    if (first_device < 0) first_device = c->device;
+    if (first_device != c->device)
+      throw HeError(HE_INVALID_PARAMS, "contexts on more than one CUDA device in one process are not supported "
+                                       "(one process per GPU)");
+  }
   std::vector<PrimeD> pd(c->NP);
   for (int t = 0; t < c->NP; ++t) {
     PrimeD& p = pd[t];
@@ -1654,8 +1669,9 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
     }
   }
   const size_t smem = ((size_t)Lc + 1) * N * 4;
+  // the fused kernel indexes the keygen tables d_step_key32 / d_step_gal (n_s + 1 entries) at k step
   const bool fused = c->small_primes && keys32.size() == (size_t)g && smem <= kMaxSmem && Lc <= 8 && G <= 4 &&
-                     N % (LAZY_SM_T * 2) == 0 && B <= 65535;
+                     N % (LAZY_SM_T * 2) == 0 && B <= 65535 && (size_t)(g - 1) * step <= N / 2;
   std::vector<he_ciphertext*> inner(G, nullptr);
   auto cleanup = [&] {
     for (auto* p : inner) ct_free(p);

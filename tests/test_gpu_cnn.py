@@ -44,9 +44,39 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
     """lazy=False: FC layers with one ModDown per rotation (oracle vec_mat); lazy=True: one
     ModDown per vec_mat (oracle vec_mat_lazy, QP diagonals); "bsgs": baby step n/4 with one lazy
     ModDown per giant step (oracle vec_mat_bsgs)."""
-    o, g = cfg4
+    _layers_bit_exact(*cfg4, lazy, 2)
+
+
+@pytest.fixture(scope="module")
+def cfg4_capped(cfg4):
+    """A second GPU context whose persistent pipelined NTT (k_ntt32_pipe) runs on at most 8 CTAs
+    (HE_PIPE_GRID_CAP), so every CTA loops over several blocks and the staged-prefetch path
+    (cp.async of block k+1's row while block k computes) runs for every pipelined job type
+    (ModUp32, KsSpecial, KsData, RescaleData) even at a small batch."""
+    import os
+    from paper_2104_03152_b200 import Context
+    from paper_2104_03152_b200.cnn import rotation_steps
+    o, _ = cfg4
+    os.environ["HE_PIPE_GRID_CAP"] = "8"
+    try:
+        g = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    finally:
+        del os.environ["HE_PIPE_GRID_CAP"]
+    g.he_keygen(sorted(set(rotation_steps(conv_g=8, fc_bsgs=True, fc1_g=32)) | set(rotation_steps())
+                       | set(rotation_steps(conv_g=8, fc_bsgs=True))))
+    return o, g
+
+
+@pytest.mark.parametrize("lazy", ["fast", "bsgs+conv8", False])
+def test_cnn_layers_bit_exact_multiblock_pipe(cfg4_capped, lazy):
+    """The bench schedule (and two others) word for word after every layer, with the pipelined
+    NTT forced into its multi-block loop (that loop only ran when nblk > grid)."""
+    _layers_bit_exact(*cfg4_capped, lazy, 3)
+
+
+def _layers_bit_exact(o, g, lazy, nimg):
     w = cnn_weights(3)
-    imgs = mnist_like_images(2, 4)
+    imgs = mnist_like_images(nimg, 4)
     conv_g = 8 if lazy in ("bsgs+conv8", "fast") else 0
     fc1_g = 32 if lazy == "fast" else 0      # the bench's schedule: one-level conv + folded FC1
     ns, q, plan = o.slots, o.q, (OC.CNN_PLAN_BSGS if conv_g else OC.CNN_PLAN)
@@ -79,14 +109,14 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
         ref = [OC.im2col_conv(o, c, w.conv_w.reshape(4, -1), w.conv_b, 64, plan["conv_shift"],
                               plan["mask_shift"], fold_n1=n1) for c in o_in]
     W = x.words()
-    for b in range(2):
+    for b in range(nimg):
         assert np.array_equal(W[b], ref[b].words), ("conv", b)
     assert x.scale == ref[0].scale and x.level == ref[0].level
     # square
     x = g.he_square(x)
     ref = [o.square(c) for c in ref]
     W = x.words()
-    for b in range(2):
+    for b in range(nimg):
         assert np.array_equal(W[b], ref[b].words), ("square1", b)
     # FC1 (replicated output) and FC2
     for name, Wm, bias, rep, shift in [("fc1", w.fc1_w.T, w.fc1_b, True, -plan["fc1_shift"]),
@@ -122,7 +152,7 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
             vm = OC.vec_mat_lazy if lazy else OC.vec_mat
             ref = [vm(o, c, Wm, bias, rep, shift) for c in ref]
         W = x.words()
-        for b in range(2):
+        for b in range(nimg):
             assert np.array_equal(W[b], ref[b].words), (name, b)
         if name == "fc1":
             x = g.he_square(x)
@@ -130,7 +160,7 @@ def test_cnn_layers_bit_exact(cfg4, lazy):
     assert x.level == 0
     # decrypt + decode of the bit-exact result vs the oracle's
     z = g.he_decode(g.he_decrypt(x), 10)
-    for b in range(2):
+    for b in range(nimg):
         assert np.allclose(z[b], o.decode(o.decrypt(ref[b]), 10), rtol=1e-9, atol=1e-9)
 
 

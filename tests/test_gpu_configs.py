@@ -35,9 +35,14 @@ def test_cfg3_rotations_and_mul_bit_exact():
     W = gct.words()
     for b in range(B):
         assert np.array_equal(W[b], octs[b].words)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(B) as ex:    # every item of the batch (the oracle's C calls release the GIL)
+        orot = {s: list(ex.map(lambda b: o.rotate(octs[b], s).words, range(B))) for s in steps}
     for s in steps:
         r = g.he_rotate(gct, s)
-        assert np.array_equal(r.words()[0], o.rotate(octs[0], s).words), s
+        Wr = r.words()
+        for b in range(B):
+            assert np.array_equal(Wr[b], orot[s][b]), (s, b)
         dec = g.he_decode(g.he_decrypt(r), o.slots)
         for b in range(B):
             assert np.max(np.abs(dec[b] - np.roll(z[b], -s))) < 1e-6, (s, b)
@@ -90,3 +95,39 @@ def test_cfg5b_deep_chain_bit_exact():
     # and 16 rescales is ~1e-7 at 2^40 (fresh ~340 sqrt(N) / 2^40, rounding ~42 sqrt(N) / 2^40 per
     # rescale), and the four rotate-and-adds sum 16 copies -> ~1-2e-6; DESIGN.md §3 R3
     assert np.max(np.abs(dec - y)) < 1e-5
+
+
+def test_cfg5b_deep_chain_batch_512_sampled_bit_exact():
+    """The cfg5b chain at the bench's batch (512 ciphertexts, BASELINE config 5): items 0 and 511
+    word for word against the oracle (their plaintexts injected; the rest encoded on the GPU)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2104_03152_b200 import Context
+    steps = [1, 2, 4, 8]
+    o = OracleContext(CFG5B.logN, CFG5B.bits, CFG5B.n_special, CFG5B.seed)
+    o.keygen(steps)
+    g = Context(CFG5B.logN, CFG5B.bits, CFG5B.n_special, CFG5B.seed)
+    g.he_keygen(steps)
+    B, lvl, items = 512, o.L - 1, [0, 511]
+    z = messages(B, o.slots, seed=CFG5B.seed + 1)
+    P = deep_chain_plaintexts(16, o.slots, seed=CFG5B.seed)
+    dev = torch.device("cuda", 0)
+    pt = g.he_encode(torch.from_numpy(z).to(dev), 2.0 ** 40, lvl)
+    words = torch.empty((B, lvl + 1, o.N), dtype=torch.int64, device=dev)
+    g.he_pt_export_words(pt, words)
+    opts = [o.encode(z[s], 2.0 ** 40, lvl) for s in items]
+    words[items] = torch.from_numpy(np.stack([p.words for p in opts]).view(np.int64)).to(dev)
+    ct = g.he_encrypt(g.he_pt_import_words(words, lvl, 2.0 ** 40), 0)
+    for t in range(16):
+        l = ct.level
+        _, m = o.encode_coeffs(P[t], float(o.q[l]))
+        ct = g.he_rescale(g.he_mul_plain(ct, g.he_pt_from_int_coeffs(m, float(o.q[l]), l)))
+    for s in steps:
+        ct = g.he_add(ct, g.he_rotate(ct, s))
+    out = torch.empty((B, 2, ct.level + 1, o.N), dtype=torch.int64, device=dev)
+    g.he_ct_export_words(ct, out)
+    got = out[items].cpu().numpy().view(np.uint64)
+    with ThreadPoolExecutor(len(items)) as ex:
+        ref = list(ex.map(lambda k: OC.deep_chain(o, o.encrypt(opts[k], items[k]), P).words, range(len(items))))
+    for k in range(len(items)):
+        assert np.array_equal(got[k], ref[k]), items[k]

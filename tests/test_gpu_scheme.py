@@ -347,6 +347,13 @@ def test_small_prime_keyswitch_paths_bit_exact(small):
             w = g.he_rescale(gx).words()
             for b in range(3):
                 assert np.array_equal(w[b], o.rescale(OCt(x[b], lvl, 1.0)).words), (lvl, b)
+        # fused square (ct_square_relin: d2 = x1^2 on the digit loads, d0 / d1 in the ModDown
+        # epilogue) at every level, batch 1 and 3, against the oracle's tensor -> relinearize
+        for Bq in ((1, 3) if lvl >= 1 else ()):
+            xs = x[:Bq]
+            w = g.he_square(g.he_ct_import_words(xs, lvl, 1.0)).words()
+            for b in range(Bq):
+                assert np.array_equal(w[b], o.square(OCt(xs[b], lvl, 1.0)).words), ("square", lvl, Bq, b)
     z = messages(2, o.slots, seed=3)
     lvl = o.L - 1
     cts = [oracle_ct(o, z[b], 2.0 ** 26, lvl, b) for b in range(2)]
