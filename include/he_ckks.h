@@ -129,6 +129,21 @@ he_status he_set_stream(he_context* ctx, void* stream);
  * clears) an asynchronous he_encode_device overflow as HE_SCALE_OVERFLOW. */
 he_status he_sync(he_context* ctx);
 
+/* Device memory from the caller (SURVEY.md §8(b) "Creation/ownership": torch's
+ * caching allocator in the Python binding).  After this call every ciphertext,
+ * plaintext and scratch block of ctx is obtained as alloc(bytes, stream, user)
+ * and returned as free(ptr, bytes, stream, user), where stream is the
+ * context's cudaStream_t: a block freed on that stream may be reused by work
+ * queued later on it (stream-ordered semantics, as torch's allocator gives).
+ * alloc returns NULL on failure (-> HE_OUT_OF_MEMORY).  The context's cached
+ * internal blocks are released first (synchronizes the stream).  Blocks that
+ * were obtained before the call keep their origin and are returned to it.  The
+ * parameter tables and keys stay library-owned (cudaMalloc at creation and
+ * he_keygen).  alloc = free = NULL restores the internal pool. */
+typedef void* (*he_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*he_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
+he_status he_set_allocator(he_context* ctx, he_alloc_fn alloc, he_free_fn free, void* user);
+
 /* Key generation on the device: ternary
  * secret s, public key (-a s + e, a) over the data limbs, relinearisation key
  * for s^2 and one Galois key per distinct element of `rot_steps` (each step
@@ -138,6 +153,12 @@ he_status he_keygen(he_context* ctx, const int32_t* rot_steps, size_t n_steps);
 /* Drop the secret key (the "public" context of S:311-318): decrypt then fails
  * with HE_MISSING_KEY. */
 he_status he_drop_secret_key(he_context* ctx);
+/* The "public" context a client hands to the server (PAPER.md:32,
+ * 35): a NEW context with the same parameters and seed and device copies of
+ * the public, relinearisation and Galois keys, without the secret key (decrypt
+ * and symmetric encryption fail with HE_MISSING_KEY).  Free it with
+ * he_context_free; ctx is unchanged.  The copy runs on ctx's stream. */
+he_status he_make_public(he_context* ctx, he_context** out);
 
 /* ---- encode / decode (C6/C7) -------------------------- */
 /* Encode B real vectors of n_per_item <= n_s values each (host array
@@ -212,6 +233,20 @@ he_status he_relinearize(he_context* ctx, const he_ciphertext* a, he_ciphertext*
 he_status he_rescale(he_context* ctx, const he_ciphertext* a, he_ciphertext** out);
 /* rotate left by k (Galois automorphism 5^k + key switch). */
 he_status he_rotate(he_context* ctx, const he_ciphertext* a, int32_t k, he_ciphertext** out);
+
+/* In-place forms for the hot loop: a <- op(a, ...), same
+ * checks and results as the forms above.  add / sub / add_plain / mul_plain
+ * write into a's storage (no allocation) when a's batch is the larger one;
+ * rescale / rotate / square change the limb layout, so a's storage is
+ * replaced (its old block returns to the pool in stream order).  On error a is
+ * unchanged. */
+he_status he_add_inplace(he_context* ctx, he_ciphertext* a, const he_ciphertext* b);
+he_status he_sub_inplace(he_context* ctx, he_ciphertext* a, const he_ciphertext* b);
+he_status he_add_plain_inplace(he_context* ctx, he_ciphertext* a, const he_plaintext* p);
+he_status he_mul_plain_inplace(he_context* ctx, he_ciphertext* a, const he_plaintext* p);
+he_status he_rescale_inplace(he_context* ctx, he_ciphertext* a);
+he_status he_rotate_inplace(he_context* ctx, he_ciphertext* a, int32_t k);
+he_status he_square_inplace(he_context* ctx, he_ciphertext* a);
 
 /* Drop limbs above `level` (level <= ct level): the ciphertext mod Q_level
  * decrypts to the same message; scale unchanged.  Used to align levels. */
@@ -367,6 +402,12 @@ he_status he_pt_import_words(he_context* ctx, const uint64_t* src, int on_device
  * and NTT on device (C7 injection of an exactly-rounded encoding). */
 he_status he_pt_from_int_coeffs(he_context* ctx, const int64_t* m, size_t B, double scale, int level,
                                 he_plaintext** out);
+/* The inverse of he_pt_from_int_coeffs (test/injection): the
+ * plaintext's integer polynomials m[B][N] (host), i.e. INTT of the data limbs,
+ * CRT composition mod Q_level and centring into (-Q/2, Q/2].  Fails with
+ * HE_SCALE_OVERFLOW when a coefficient is outside the int64 range (then m is
+ * not written).  For a QP plaintext the data limbs are used. */
+he_status he_pt_to_int_coeffs(he_context* ctx, const he_plaintext* pt, int64_t* m);
 /* Same with the K special limbs appended (a QP plaintext, limbs 0..level then
  * p_0..p_{K-1}), for he_vec_mat_pt's lazy-ModDown form. */
 he_status he_pt_from_int_coeffs_qp(he_context* ctx, const int64_t* m, size_t B, double scale, int level,

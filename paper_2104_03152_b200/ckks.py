@@ -58,6 +58,16 @@ _SIGS = {
     "he_sync": [VP],
     "he_keygen": [VP, C.POINTER(C.c_int32), SZ],
     "he_drop_secret_key": [VP],
+    "he_make_public": [VP, VPP],
+    "he_set_allocator": [VP, VP, VP, VP],
+    "he_pt_to_int_coeffs": [VP, VP, I64P],
+    "he_add_inplace": [VP, VP, VP],
+    "he_sub_inplace": [VP, VP, VP],
+    "he_add_plain_inplace": [VP, VP, VP],
+    "he_mul_plain_inplace": [VP, VP, VP],
+    "he_rescale_inplace": [VP, VP],
+    "he_rotate_inplace": [VP, VP, C.c_int32],
+    "he_square_inplace": [VP, VP],
     "he_encode": [VP, DP, SZ, SZ, C.c_double, C.c_int, VPP],
     "he_encode_device": [VP, VP, SZ, SZ, C.c_double, C.c_int, VPP],
     "he_decode": [VP, VP, DP, SZ],
@@ -247,15 +257,22 @@ class Ciphertext:
         return C.cast(p, C.c_void_p).value or 0
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
 class Context:
     """he_context_create + the calls that take a context, under the C names."""
 
-    def __init__(self, logN: int, bits, n_special: int, seed: int, scale_log2: float = 0.0):
-        bits = [int(b) for b in bits]
-        arr = (C.c_int * len(bits))(*bits)
-        p = he_params(logN, len(bits), arr, n_special, scale_log2, 0)
-        h = C.c_void_p()
-        _check(lib().he_context_create(C.byref(p), seed, C.byref(h)))
+    def __init__(self, logN: int, bits, n_special: int, seed: int, scale_log2: float = 0.0, _handle=None):
+        if _handle is None:
+            bits = [int(b) for b in bits]
+            arr = (C.c_int * len(bits))(*bits)
+            p = he_params(logN, len(bits), arr, n_special, scale_log2, 0)
+            h = C.c_void_p()
+            _check(lib().he_context_create(C.byref(p), seed, C.byref(h)))
+        else:
+            h = _handle
         self.h = h
         lg, L, K = C.c_int(), C.c_int(), C.c_int()
         _check(lib().he_context_info(h, C.byref(lg), C.byref(L), C.byref(K)))
@@ -343,6 +360,50 @@ class Context:
     def he_drop_secret_key(self) -> None:
         _check(lib().he_drop_secret_key(self.h))
 
+    def he_make_public(self) -> "Context":
+        """A new context with copies of the public / relinearisation / Galois keys and no secret key."""
+        h = C.c_void_p()
+        _check(lib().he_make_public(self.h, C.byref(h)))
+        pub = Context(0, (), 0, 0, _handle=h)
+        pub._stream = self._stream
+        return pub
+
+    def he_set_allocator(self, alloc=None, free=None) -> None:
+        """Install a device allocator: alloc(bytes, stream_ptr) -> device pointer (int),
+        free(ptr, bytes, stream_ptr).  he_set_allocator_torch() installs torch's caching allocator.
+        With no arguments the internal pool is restored."""
+        if alloc is None:
+            self._alloc_cbs = None
+            _check(lib().he_set_allocator(self.h, None, None, None))
+            return
+
+        def a(nbytes, stream, user):
+            try:
+                return int(alloc(int(nbytes), int(stream or 0)))
+            except Exception:
+                return 0
+
+        def f(ptr, nbytes, stream, user):
+            try:
+                free(int(ptr), int(nbytes), int(stream or 0))
+            except Exception:
+                pass
+        cbs = (ALLOC_FN(a), FREE_FN(f))
+        _check(lib().he_set_allocator(self.h, C.cast(cbs[0], C.c_void_p), C.cast(cbs[1], C.c_void_p), None))
+        self._alloc_cbs = cbs   # the C side holds raw function pointers: keep the thunks alive
+
+    def he_set_allocator_torch(self) -> None:
+        """Device memory from torch's caching allocator (stream-ordered on the context stream)."""
+        import torch
+        dev = self._device if self._device is not None else torch.cuda.current_device()
+
+        def alloc(nbytes, stream):
+            return torch.cuda.caching_allocator_alloc(nbytes, dev, stream if stream else None)
+
+        def free(ptr, nbytes, stream):
+            torch.cuda.caching_allocator_delete(ptr)
+        self.he_set_allocator(alloc, free)
+
     def he_key_export(self, kind: int, step: int = 0) -> np.ndarray:
         n = int(lib().he_key_words(self.h, kind))
         out = np.zeros(n, dtype=np.uint64)
@@ -414,6 +475,12 @@ class Context:
             raise HEError(17, "he_ct_export_words: out has the wrong number of words")
         _check(lib().he_ct_export_words(self.h, ct.h, _ptr(out), _is_dev(out)))
 
+    def he_pt_to_int_coeffs(self, pt: Plaintext) -> np.ndarray:
+        """Signed integer coefficients m[B][N] of a plaintext (INTT, CRT, centred)."""
+        out = np.zeros((pt.B, self.N), dtype=np.int64)
+        _check(lib().he_pt_to_int_coeffs(self.h, pt.h, out.ctypes.data_as(I64P)))
+        return out
+
     def he_pt_import_words(self, w, level: int, scale: float) -> Plaintext:
         h = C.c_void_p()
         if _is_dev(w):
@@ -468,6 +535,19 @@ class Context:
     def he_relinearize(self, a): return self._ct2(lib().he_relinearize, a.h)
     def he_rescale(self, a): return self._ct2(lib().he_rescale, a.h)
     def he_rotate(self, a, k: int): return self._ct2(lib().he_rotate, a.h, int(k))
+
+    # in-place forms: a <- op(a, ...) (the handle is kept; returns a)
+    def _ip(self, fn, a, *args):
+        _check(fn(self.h, a.h, *args))
+        return a
+
+    def he_add_inplace(self, a, b): return self._ip(lib().he_add_inplace, a, b.h)
+    def he_sub_inplace(self, a, b): return self._ip(lib().he_sub_inplace, a, b.h)
+    def he_add_plain_inplace(self, a, p): return self._ip(lib().he_add_plain_inplace, a, p.h)
+    def he_mul_plain_inplace(self, a, p): return self._ip(lib().he_mul_plain_inplace, a, p.h)
+    def he_rescale_inplace(self, a): return self._ip(lib().he_rescale_inplace, a)
+    def he_rotate_inplace(self, a, k: int): return self._ip(lib().he_rotate_inplace, a, int(k))
+    def he_square_inplace(self, a): return self._ip(lib().he_square_inplace, a)
 
     def he_mod_switch_to(self, a, level: int): return self._ct2(lib().he_mod_switch_to, a.h, int(level))
     def he_dot(self, a, b, n: int): return self._ct2(lib().he_dot, a.h, b.h, int(n))

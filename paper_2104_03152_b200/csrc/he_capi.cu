@@ -235,6 +235,22 @@ he_status he_drop_secret_key(he_context* c) {
   });
 }
 
+he_status he_make_public(he_context* c, he_context** out) {
+  return guard([&] {
+    need_ctx(c);
+    need_out(out);
+    *out = context_make_public(c);
+  });
+}
+
+he_status he_set_allocator(he_context* c, he_alloc_fn alloc, he_free_fn free_fn, void* user) {
+  return guard([&] {
+    need_ctx(c);
+    need((alloc == nullptr) == (free_fn == nullptr), HE_INVALID_ARGUMENT, "alloc and free must both be set or both NULL");
+    set_allocator(c, alloc, free_fn, user);
+  });
+}
+
 // ---------------------------------------------------------------- encode ---
 static void encode_common(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
                           he_plaintext** out, bool check_now = true) {
@@ -424,6 +440,86 @@ he_status he_relinearize(he_context* c, const he_ciphertext* a, he_ciphertext** 
     need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
     *out = ct_relinearize(c, a);
   });
+}
+
+// ---- in-place forms (SURVEY 8(b) "_inplace variants exist for the hot loop") -------------------
+// add / sub / add_plain / mul_plain write into a's storage (no allocation) when a holds the larger
+// batch; rescale / rotate / square produce a new limb layout, so a's storage is replaced (the old
+// block returns to the pool in stream order) and the handle stays the caller's.
+static void adopt(he_ciphertext* a, he_ciphertext* r) {
+  std::swap(a->B, r->B);
+  std::swap(a->size, r->size);
+  std::swap(a->level, r->level);
+  std::swap(a->scale, r->scale);
+  std::swap(a->d, r->d);
+  a->seeded = 0;
+  ct_free(r);
+}
+
+he_status he_add_inplace(he_context* c, he_ciphertext* a, const he_ciphertext* b) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_ct(c, b);
+    need_same(a, b, true);
+    if (a->B >= b->B) ct_binop(c, 0, a, b, a);
+    else adopt(a, ct_binop(c, 0, a, b));
+    a->seeded = 0;
+  });
+}
+
+he_status he_sub_inplace(he_context* c, he_ciphertext* a, const he_ciphertext* b) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_ct(c, b);
+    need_same(a, b, true);
+    if (a->B >= b->B) ct_binop(c, 1, a, b, a);
+    else adopt(a, ct_binop(c, 1, a, b));
+    a->seeded = 0;
+  });
+}
+
+he_status he_add_plain_inplace(he_context* c, he_ciphertext* a, const he_plaintext* p) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_pt(c, p);
+    need_plain_q(p);
+    need(a->level == p->level, HE_LEVEL_MISMATCH, "levels differ");
+    need(a->scale == p->scale, HE_SCALE_MISMATCH, "scales differ");
+    need_batch(a->B, p->B);
+    if (a->B >= p->B) ct_add_plain(c, a, p, a);
+    else adopt(a, ct_add_plain(c, a, p));
+    a->seeded = 0;
+  });
+}
+
+he_status he_mul_plain_inplace(he_context* c, he_ciphertext* a, const he_plaintext* p) {
+  return guard([&] {
+    need_ctx(c); need_ct(c, a); need_pt(c, p);
+    need_plain_q(p);
+    need(a->level == p->level, HE_LEVEL_MISMATCH, "levels differ");
+    need_batch(a->B, p->B);
+    if (a->B >= p->B) ct_mul_plain(c, a, p, a);
+    else adopt(a, ct_mul_plain(c, a, p));
+    a->seeded = 0;
+  });
+}
+
+he_status he_rescale_inplace(he_context* c, he_ciphertext* a) {
+  he_ciphertext* r = nullptr;
+  const he_status st = he_rescale(c, a, &r);
+  if (st == HE_OK) adopt(a, r);
+  return st;
+}
+
+he_status he_rotate_inplace(he_context* c, he_ciphertext* a, int32_t k) {
+  he_ciphertext* r = nullptr;
+  const he_status st = he_rotate(c, a, k, &r);
+  if (st == HE_OK) adopt(a, r);
+  return st;
+}
+
+he_status he_square_inplace(he_context* c, he_ciphertext* a) {
+  he_ciphertext* r = nullptr;
+  const he_status st = he_square(c, a, &r);
+  if (st == HE_OK) adopt(a, r);
+  return st;
 }
 
 he_status he_rescale(he_context* c, const he_ciphertext* a, he_ciphertext** out) {
@@ -1215,6 +1311,16 @@ he_status he_pt_from_int_coeffs(he_context* c, const int64_t* m, size_t B, doubl
     Scratch d(c, B * c->N * 8);
     HE_CK(cudaMemcpyAsync(d.p, m, B * c->N * 8, cudaMemcpyHostToDevice, c->stream));
     *out = pt_from_int(c, d.as<i64>(), B, scale, level);
+  });
+}
+
+he_status he_pt_to_int_coeffs(he_context* c, const he_plaintext* pt, int64_t* m) {
+  return guard([&] {
+    need_ctx(c); need_pt(c, pt); need_out(m);
+    Scratch d(c, (size_t)pt->B * c->N * 8);
+    pt_to_int(c, pt, d.as<i64>());
+    HE_CK(cudaMemcpyAsync(m, d.p, (size_t)pt->B * c->N * 8, cudaMemcpyDeviceToHost, c->stream));
+    HE_CK(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -79,6 +79,13 @@ struct he_context {
   std::map<size_t, std::vector<void*>> free_bins;
   std::map<void*, size_t> live_bytes;
   size_t cached_bytes = 0;
+  // caller-installed allocator (he_set_allocator): ciphertext, plaintext and scratch blocks come
+  // from alloc(bytes, stream, user) and go back through free(ptr, bytes, stream, user) in stream
+  // order (torch's caching allocator in the Python binding); user_owned marks those blocks
+  he_alloc_fn user_alloc = nullptr;
+  he_free_fn user_free = nullptr;
+  void* user_ctx = nullptr;
+  std::map<void*, bool> user_owned;
   // opt-in profiler: CUDA events around every NTT-family launch
   struct ProfRec { const char* tag; cudaEvent_t a, b; double bytes; int blocks; double ops; };
   bool prof_on = false;

@@ -30,6 +30,13 @@ void trim_cache(he_context* c) {
 
 void* dalloc(he_context* c, size_t bytes) {
   const size_t sz = bin_size(bytes);
+  if (c->user_alloc) {
+    void* p = c->user_alloc(sz, (void*)c->stream, c->user_ctx);
+    if (!p) throw HeError(HE_OUT_OF_MEMORY, "the installed allocator returned NULL");
+    c->live_bytes[p] = sz;
+    c->user_owned[p] = true;
+    return p;
+  }
   auto it = c->free_bins.find(sz);
   if (it != c->free_bins.end() && !it->second.empty()) {
     void* p = it->second.back();
@@ -57,6 +64,13 @@ void dfree(he_context* c, void* p) {
   if (!p) return;
   auto it = c->live_bytes.find(p);
   if (it == c->live_bytes.end()) return;
+  auto uo = c->user_owned.find(p);
+  if (uo != c->user_owned.end()) {   // back to the caller's allocator, in stream order
+    c->user_owned.erase(uo);
+    c->user_free(p, it->second, (void*)c->stream, c->user_ctx);
+    c->live_bytes.erase(it);
+    return;
+  }
   c->free_bins[it->second].push_back(p);
   c->cached_bytes += it->second;
   c->live_bytes.erase(it);
@@ -176,8 +190,19 @@ void context_destroy(he_context* c) {
   if (c->d_rlk) cudaFree(c->d_rlk);
   if (c->d_rlk32) cudaFree(c->d_rlk32);
   trim_cache(c);
-  for (auto& kv : c->live_bytes) cudaFree(kv.first);
+  for (auto& kv : c->live_bytes) {
+    if (c->user_owned.count(kv.first)) c->user_free(kv.first, kv.second, (void*)c->stream, c->user_ctx);
+    else cudaFree(kv.first);
+  }
   c->live_bytes.clear();
+  c->user_owned.clear();
+}
+
+void set_allocator(he_context* c, he_alloc_fn alloc, he_free_fn free_fn, void* user) {
+  trim_cache(c);   // cached blocks of the internal pool go back to the driver (stream synchronized)
+  c->user_alloc = alloc;
+  c->user_free = free_fn;
+  c->user_ctx = user;
 }
 
 // ============================================================== handles ===
@@ -636,6 +661,138 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
 // E[k2][k1]; P (.) c0 is staged so the c0 term joins before the diagonal:
 //   acc_p[k2] += E[k2][k1] (ip_p + [p = 0] P c0[pi_k1(n)]).
 // accx: [G][B][2][Lc+K][N] u32.  Two coefficients per thread (8-byte vectors).
+//
+// Two reduction schedules, chosen per CTA from its target prime q (uniform branch):
+// * LAZY (LC q < 2^32 and g q < 2^32, e.g. every 26-bit prime of BASELINE config 4): the LC
+//   digit products of one inner product are summed in 64 bits (each < q^2) and reduced by ONE
+//   Montgomery REDC (T < LC q^2 < q 2^32, so the result is < 2q); the G diagonal products are
+//   accumulated in 64 bits over all g baby steps (sum < g q^2 < 2^64) and reduced once at the
+//   end (acc < g q^2 < q 2^32).  Keys and diagonals are stored as k 2^32 mod q, so each REDC
+//   removes exactly the one factor 2^32 its products carry: the results are the same residues.
+// * PAIRED (q up to 2^31): one REDC per pair of products and per diagonal product (x0 k0' +
+//   x1 k1' < 2 q^2 < q 2^32), the sums kept reduced.
+template <int LC, int G, bool LAZY>
+__device__ __forceinline__ void bsgs_tile(const LazyArgs& a, int g, const u32* const* __restrict__ keys32,
+                                          const u32* __restrict__ dm, const u32* xs, const u32* c0p, int t, int b,
+                                          int nt, bool data, u32 q, u32 qi, u32 Pm, u32 keyrow, u32 kpart, u32 kdig,
+                                          size_t gstride, u32 n0) {
+  constexpr int V = 2;
+  typedef typename std::conditional<LAZY, u64, u32>::type acc_t;
+  acc_t acc0[G][V], acc1[G][V];
+#pragma unroll
+  for (int k2 = 0; k2 < G; ++k2) {
+    const uint2 d0 = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + (size_t)t * a.N + n0));
+    const u32 dd[V] = {d0.x, d0.y};
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      if (data) {   // k1 = 0: P E[k2][0] (.) c
+        const u32 pc1 = redc32((u64)xs[t * a.N + n0 + e] * Pm, q, qi);
+        if (LAZY) {
+          acc0[k2][e] = (u64)dd[e] * c0p[n0 + e];
+          acc1[k2][e] = (u64)dd[e] * pc1;
+        } else {
+          acc0[k2][e] = redc32((u64)dd[e] * c0p[n0 + e], q, qi);
+          acc1[k2][e] = redc32((u64)dd[e] * pc1, q, qi);
+        }
+      } else {
+        acc0[k2][e] = acc1[k2][e] = 0;
+      }
+    }
+  }
+  for (int k = 1; k < g; ++k) {
+    const u32 gal = __ldg(a.gal + k * a.step);
+    const u32* key = keys32[k * a.step] + keyrow + n0;
+    u32 sn[V], y0[V], y1[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) sn[e] = galois_src(n0 + e, gal, a.logN);
+    if (LAZY) {
+      u64 T0[V], T1[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) T0[e] = T1[e] = 0;
+#pragma unroll
+      for (int j = 0; j < LC; ++j) {
+        const uint2 kb = __ldg(reinterpret_cast<const uint2*>(key + j * kdig));
+        const uint2 ka = __ldg(reinterpret_cast<const uint2*>(key + j * kdig + kpart));
+        const u32 bv[V] = {kb.x, kb.y}, av[V] = {ka.x, ka.y};
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const u32 x = xs[j * a.N + sn[e]];
+          T0[e] += (u64)x * bv[e];
+          T1[e] += (u64)x * av[e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        y0[e] = redc32(T0[e], q, qi);
+        if (data) y0[e] = addq(y0[e], c0p[sn[e]], q);
+        y1[e] = redc32(T1[e], q, qi);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        y0[e] = data ? c0p[sn[e]] : 0u;
+        y1[e] = 0;
+      }
+#pragma unroll
+      for (int j = 0; j < LC; j += 2) {
+        const uint2 kb0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig));
+        const uint2 ka0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig + kpart));
+        uint2 kb1 = make_uint2(0, 0), ka1 = make_uint2(0, 0);
+        if (j + 1 < LC) {
+          kb1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig));
+          ka1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig + kpart));
+        }
+        const u32 b0[V] = {kb0.x, kb0.y}, a0[V] = {ka0.x, ka0.y}, b1[V] = {kb1.x, kb1.y}, a1[V] = {ka1.x, ka1.y};
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const u32 x0 = xs[j * a.N + sn[e]];
+          u64 s0 = (u64)x0 * b0[e], s1 = (u64)x0 * a0[e];
+          if (j + 1 < LC) {
+            const u32 x1 = xs[(j + 1) * a.N + sn[e]];
+            s0 += (u64)x1 * b1[e];
+            s1 += (u64)x1 * a1[e];
+          }
+          y0[e] = addq(y0[e], redc32(s0, q, qi), q);
+          y1[e] = addq(y1[e], redc32(s1, q, qi), q);
+        }
+      }
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < G; ++k2) {
+      const uint2 dv = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + ((size_t)k * nt + t) * a.N + n0));
+      const u32 dd[V] = {dv.x, dv.y};
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        if (LAZY) {
+          acc0[k2][e] += (u64)dd[e] * y0[e];
+          acc1[k2][e] += (u64)dd[e] * y1[e];
+        } else {
+          acc0[k2][e] = addq(acc0[k2][e], redc32((u64)dd[e] * y0[e], q, qi), q);
+          acc1[k2][e] = addq(acc1[k2][e], redc32((u64)dd[e] * y1[e], q, qi), q);
+        }
+      }
+    }
+  }
+  u32* out = reinterpret_cast<u32*>(a.accx);
+#pragma unroll
+  for (int k2 = 0; k2 < G; ++k2) {
+    u32 r0[V], r1[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      if (LAZY) {
+        r0[e] = redc32(acc0[k2][e], q, qi);
+        r1[e] = redc32(acc1[k2][e], q, qi);
+      } else {
+        r0[e] = (u32)acc0[k2][e];
+        r1[e] = (u32)acc1[k2][e];
+      }
+    }
+    const size_t base = ((((size_t)k2 * gridDim.y + b) * 2) * nt + t) * a.N + n0;
+    *reinterpret_cast<uint2*>(out + base) = make_uint2(r0[0], r0[1]);
+    *reinterpret_cast<uint2*>(out + base + (size_t)nt * a.N) = make_uint2(r1[0], r1[1]);
+  }
+}
+
 template <int LC, int G>
 __global__ void __launch_bounds__(LAZY_SM_T, 1)
 k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
@@ -668,74 +825,13 @@ k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, con
   __syncthreads();
   const u32 keyrow = tp * N, kpart = NP * N, kdig = 2 * NP * N;
   const size_t gstride = (size_t)g * nt * N;   // between giant-step groups in dm
+  const bool lazy = (u64)LC * q < (1ULL << 32) && (u64)g * q < (1ULL << 32);
   for (u32 tile = 0; tile < N; tile += LAZY_SM_T * V) {
     const u32 n0 = tile + threadIdx.x * V;
-    u32 acc0[G][V], acc1[G][V];
-#pragma unroll
-    for (int k2 = 0; k2 < G; ++k2) {
-      const uint2 d0 = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + (size_t)t * N + n0));
-      const u32 dd[V] = {d0.x, d0.y};
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        if (data) {   // k1 = 0: P E[k2][0] (.) c
-          acc0[k2][e] = redc32((u64)dd[e] * c0p[n0 + e], q, qi);
-          acc1[k2][e] = redc32((u64)dd[e] * redc32((u64)xs[t * N + n0 + e] * Pm, q, qi), q, qi);
-        } else {
-          acc0[k2][e] = acc1[k2][e] = 0;
-        }
-      }
-    }
-    for (int k = 1; k < g; ++k) {
-      const u32 gal = __ldg(a.gal + k * a.step);
-      const u32* key = keys32[k * a.step] + keyrow + n0;
-      u32 sn[V], y0[V], y1[V];
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        sn[e] = galois_src(n0 + e, gal, a.logN);
-        y0[e] = data ? c0p[sn[e]] : 0u;
-        y1[e] = 0;
-      }
-#pragma unroll
-      for (int j = 0; j < LC; j += 2) {
-        const uint2 kb0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig));
-        const uint2 ka0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig + kpart));
-        uint2 kb1 = make_uint2(0, 0), ka1 = make_uint2(0, 0);
-        if (j + 1 < LC) {
-          kb1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig));
-          ka1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig + kpart));
-        }
-        const u32 b0[V] = {kb0.x, kb0.y}, a0[V] = {ka0.x, ka0.y}, b1[V] = {kb1.x, kb1.y}, a1[V] = {ka1.x, ka1.y};
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          const u32 x0 = xs[j * N + sn[e]];
-          u64 s0 = (u64)x0 * b0[e], s1 = (u64)x0 * a0[e];
-          if (j + 1 < LC) {
-            const u32 x1 = xs[(j + 1) * N + sn[e]];
-            s0 += (u64)x1 * b1[e];
-            s1 += (u64)x1 * a1[e];
-          }
-          y0[e] = addq(y0[e], redc32(s0, q, qi), q);
-          y1[e] = addq(y1[e], redc32(s1, q, qi), q);
-        }
-      }
-#pragma unroll
-      for (int k2 = 0; k2 < G; ++k2) {
-        const uint2 dv = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + ((size_t)k * nt + t) * N + n0));
-        const u32 dd[V] = {dv.x, dv.y};
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          acc0[k2][e] = addq(acc0[k2][e], redc32((u64)dd[e] * y0[e], q, qi), q);
-          acc1[k2][e] = addq(acc1[k2][e], redc32((u64)dd[e] * y1[e], q, qi), q);
-        }
-      }
-    }
-    u32* out = reinterpret_cast<u32*>(a.accx);
-#pragma unroll
-    for (int k2 = 0; k2 < G; ++k2) {
-      const size_t base = ((((size_t)k2 * gridDim.y + b) * 2) * nt + t) * N + n0;
-      *reinterpret_cast<uint2*>(out + base) = make_uint2(acc0[k2][0], acc0[k2][1]);
-      *reinterpret_cast<uint2*>(out + base + (size_t)nt * N) = make_uint2(acc1[k2][0], acc1[k2][1]);
-    }
+    if (lazy)
+      bsgs_tile<LC, G, true>(a, g, keys32, dm, xs, c0p, t, b, nt, data, q, qi, Pm, keyrow, kpart, kdig, gstride, n0);
+    else
+      bsgs_tile<LC, G, false>(a, g, keys32, dm, xs, c0p, t, b, nt, data, q, qi, Pm, keyrow, kpart, kdig, gstride, n0);
   }
 }
 
@@ -1012,7 +1108,8 @@ __global__ void k_decode_fft(const double* __restrict__ X, size_t n, double scal
 // CRT compose (a13): X = sum_i [x_i Qhat_i^{-1}]_{q_i} Qhat_i mod Q, centred, to double.
 constexpr int CRT_MAXW = 40;
 __global__ void k_crt_compose(const u64* __restrict__ coef, double* __restrict__ X, const u64* __restrict__ crt,
-                              const PrimeD* __restrict__ primes, int N, int Lc, size_t total) {
+                              const PrimeD* __restrict__ primes, int N, int Lc, size_t total,
+                              i64* __restrict__ Xi = nullptr, int* ovf = nullptr) {
   const u64* Qhat_inv = crt;
   const u64* Qhat = crt + Lc;
   const u64* Q = Qhat + (size_t)Lc * Lc;
@@ -1072,6 +1169,13 @@ __global__ void k_crt_compose(const u64* __restrict__ coef, double* __restrict__
         borrow = (Q[w] < acc[w] + borrow) || (acc[w] + borrow < acc[w]) ? 1 : 0;
         acc[w] = d;
       }
+    }
+    if (Xi) {   // exact centred integer (|X| < 2^63), else flagged
+      bool fits = acc[0] < (1ULL << 63);
+      for (int w = 1; w < Lc; ++w) fits = fits && acc[w] == 0;
+      if (!fits) atomicOr(ovf, 1);
+      Xi[idx] = fits ? (gt ? -(i64)acc[0] : (i64)acc[0]) : 0;
+      continue;
     }
     for (int w = Lc - 1; w >= 0; --w) v = v * 18446744073709551616.0 + (double)acc[w];
     X[idx] = gt ? -v : v;
@@ -1134,9 +1238,9 @@ void signed_to_ntt(he_context* c, const i64* poly, u64* dst, size_t items, int n
 }
 
 // ---- arithmetic -----------------------------------------------------------
-he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b) {
+he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b, he_ciphertext* into) {
   const int B = std::max(a->B, b->B), Lc = a->level + 1;
-  he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale);
+  he_ciphertext* o = into ? into : ct_new(c, B, a->size, a->level, a->scale);
   const size_t rows = (size_t)B * a->size * Lc, LN = (size_t)Lc * c->N;
   const size_t a_bs = a->B == 1 ? 0 : a->size * LN, b_bs = b->B == 1 ? 0 : b->size * LN;
   // b indexed like a: pass b_limb_bs = LN with b pointer per part
@@ -1169,10 +1273,12 @@ he_ciphertext* ct_negate(he_context* c, const he_ciphertext* a) {
   return o;
 }
 
-he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p) {
+he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext* into) {
   const int Lc = a->level + 1;
   const int B = std::max(a->B, p->B);
-  he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale * p->scale);
+  const double scale = a->scale * p->scale;
+  he_ciphertext* o = into ? into : ct_new(c, B, a->size, a->level, scale);
+  o->scale = scale;
   const size_t LN = (size_t)Lc * c->N, rows = (size_t)B * a->size * Lc;
   {
     ProfScope ps_(c, "pw_mul", 0.0, 0);
@@ -1184,10 +1290,10 @@ he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plai
   return o;
 }
 
-he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p) {
+he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext* into) {
   const int Lc = a->level + 1;
   const int B = std::max(a->B, p->B);
-  he_ciphertext* o = ct_new(c, B, a->size, a->level, a->scale);
+  he_ciphertext* o = into ? into : ct_new(c, B, a->size, a->level, a->scale);
   const size_t LN = (size_t)Lc * c->N;
   // poly 0 of every item: a + p (items as size-1 rows at stride size*LN) ...
   const size_t rows = (size_t)B * Lc;
@@ -1199,7 +1305,7 @@ he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plai
   }
   check_launch(c);
   // ... and polys 1..size-1 copied: one strided copy (a per-item loop only to broadcast a single item)
-  if (a->size > 1) {
+  if (a->size > 1 && o != a) {
     const size_t w = (size_t)(a->size - 1) * LN * 8, pitch = (size_t)a->size * LN * 8;
     if (a->B == B) {
       HE_CK(cudaMemcpy2DAsync(o->d + LN, pitch, a->d + LN, pitch, w, B, cudaMemcpyDeviceToDevice, c->stream));
@@ -1939,6 +2045,35 @@ static void make_ksk(he_context* c, u64* key, u64 pur_a, u64 pur_e, u64 objbase,
   check_launch(c);
 }
 
+// per-step device tables (Galois element and key pointers for every step 0..n_s)
+void build_step_tables(he_context* c) {
+  const int N = c->N;
+  {
+    const int ns = N / 2;
+    std::vector<u32> sg(ns + 1);
+    std::vector<const u64*> sk(ns + 1, nullptr);
+    std::vector<const u32*> sk32(ns + 1, nullptr);
+    for (int k = 0; k <= ns; ++k) {
+      const u64 g = galois_element(N, k == 0 ? ns : k);
+      sg[k] = (u32)g;
+      auto it = c->gk.find(g);
+      if (it != c->gk.end()) sk[k] = it->second;
+      auto it32 = c->gk32.find(g);
+      if (it32 != c->gk32.end()) sk32[k] = it32->second;
+    }
+    sg[0] = 1;
+    HE_CK(cudaMalloc(&c->d_step_gal, sg.size() * 4));
+    HE_CK(cudaMalloc(&c->d_step_key, sk.size() * sizeof(u64*)));
+    HE_CK(cudaMalloc(&c->d_step_key32, sk32.size() * sizeof(u32*)));
+    HE_CK(cudaMemcpy(c->d_step_gal, sg.data(), sg.size() * 4, cudaMemcpyHostToDevice));
+    HE_CK(cudaMemcpy(c->d_step_key, sk.data(), sk.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+    HE_CK(cudaMemcpy(c->d_step_key32, sk32.data(), sk32.size() * sizeof(u32*), cudaMemcpyHostToDevice));
+    c->owned.push_back(c->d_step_gal);
+    c->owned.push_back((void*)c->d_step_key);
+    c->owned.push_back((void*)c->d_step_key32);
+  }
+}
+
 void keygen(he_context* c, const std::vector<int>& steps) {
   const int L = c->L, NP = c->NP, N = c->N;
   HE_CK(cudaMalloc(&c->d_sk, (size_t)NP * N * 8));
@@ -2007,31 +2142,61 @@ void keygen(he_context* c, const std::vector<int>& steps) {
       }
     }
   }
-  {   // per-step device tables
-    const int ns = N / 2;
-    std::vector<u32> sg(ns + 1);
-    std::vector<const u64*> sk(ns + 1, nullptr);
-    std::vector<const u32*> sk32(ns + 1, nullptr);
-    for (int k = 0; k <= ns; ++k) {
-      const u64 g = galois_element(N, k == 0 ? ns : k);
-      sg[k] = (u32)g;
-      auto it = c->gk.find(g);
-      if (it != c->gk.end()) sk[k] = it->second;
-      auto it32 = c->gk32.find(g);
-      if (it32 != c->gk32.end()) sk32[k] = it32->second;
-    }
-    sg[0] = 1;
-    HE_CK(cudaMalloc(&c->d_step_gal, sg.size() * 4));
-    HE_CK(cudaMalloc(&c->d_step_key, sk.size() * sizeof(u64*)));
-    HE_CK(cudaMalloc(&c->d_step_key32, sk32.size() * sizeof(u32*)));
-    HE_CK(cudaMemcpy(c->d_step_gal, sg.data(), sg.size() * 4, cudaMemcpyHostToDevice));
-    HE_CK(cudaMemcpy(c->d_step_key, sk.data(), sk.size() * sizeof(u64*), cudaMemcpyHostToDevice));
-    HE_CK(cudaMemcpy(c->d_step_key32, sk32.data(), sk32.size() * sizeof(u32*), cudaMemcpyHostToDevice));
-    c->owned.push_back(c->d_step_gal);
-    c->owned.push_back((void*)c->d_step_key);
-    c->owned.push_back((void*)c->d_step_key32);
-  }
+  build_step_tables(c);
   HE_CK(cudaStreamSynchronize(c->stream));
+}
+
+// he_make_public: a new context with the same parameters and seed holding copies of
+// the public, relinearisation and Galois keys and no secret key.
+he_context* context_make_public(he_context* c) {
+  he_context* p = new he_context();
+  try {
+    context_init(p, c->hp, c->seed);
+    p->stream = c->stream;
+    p->pipe_grid_cap = c->pipe_grid_cap;
+    const size_t N = c->N, L = c->L, NP = c->NP, kw = L * 2 * NP * N;
+    auto dup = [&](const void* src, size_t bytes) -> void* {
+      void* d = nullptr;
+      HE_CK(cudaMalloc(&d, bytes));
+      HE_CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+      return d;
+    };
+    if (c->d_pk) p->d_pk = (u64*)dup(c->d_pk, 2 * L * N * 8);
+    if (c->d_rlk) p->d_rlk = (u64*)dup(c->d_rlk, kw * 8);
+    if (c->d_rlk32) p->d_rlk32 = (u32*)dup(c->d_rlk32, kw * 4);
+    for (auto& kv : c->gk) p->gk[kv.first] = (u64*)dup(kv.second, kw * 8);
+    for (auto& kv : c->gk32) p->gk32[kv.first] = (u32*)dup(kv.second, kw * 4);
+    p->has_pk = c->has_pk;
+    p->has_rlk = c->has_rlk;
+    p->has_sk = false;
+    if (c->d_step_gal) build_step_tables(p);
+    HE_CK(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    context_destroy(p);
+    delete p;
+    throw;
+  }
+  return p;
+}
+
+// Signed integer coefficients of a plaintext (he_pt_to_int_coeffs): INTT, CRT compose, centre;
+// fails with HE_SCALE_OVERFLOW when a centred coefficient is outside the int64 range.
+void pt_to_int(he_context* c, const he_plaintext* pt, i64* out_dev) {
+  const int N = c->N, Lc = pt->level + 1;
+  const size_t B = pt->B;
+  Scratch coef(c, B * Lc * N * 8), flag(c, 4);
+  HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
+  const size_t pstride = (size_t)pt_limbs(pt) * N;
+  ntt_rows(c, pt->d, coef.as<u64>(), B, Lc, pstride, (size_t)Lc * N, true);
+  const size_t total = B * N;
+  k_crt_compose<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, c->stream>>>(
+      coef.as<u64>(), nullptr, c->d_crt + c->hp.crt_off[pt->level], c->d_primes, N, Lc, total, out_dev,
+      flag.as<int>());
+  check_launch(c);
+  int h = 0;
+  HE_CK(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  HE_CK(cudaStreamSynchronize(c->stream));
+  if (h) throw HeError(HE_SCALE_OVERFLOW, "pt_to_int_coeffs: a coefficient is outside the int64 range");
 }
 
 // ---- encode / decode / encrypt / decrypt --------------------------------------

@@ -12,6 +12,9 @@ inline size_t pt_words(const he_plaintext* p) { return (size_t)p->B * pt_limbs(p
 
 void context_init(he_context* c, const HostParams& hp, u64 seed);
 void context_destroy(he_context* c);
+he_context* context_make_public(he_context* c);
+void set_allocator(he_context* c, he_alloc_fn alloc, he_free_fn free_fn, void* user);
+void build_step_tables(he_context* c);
 
 he_ciphertext* ct_new(he_context* c, int B, int size, int level, double scale);
 he_plaintext* pt_new(he_context* c, int B, int level, double scale, int qp = 0);
@@ -33,16 +36,19 @@ he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, dou
 void take_err(he_context* c);
 he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level, int qp = 0);
 void decode(he_context* c, const he_plaintext* pt, double* out_dev, size_t n);
+void pt_to_int(he_context* c, const he_plaintext* pt, i64* out_dev);
 he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id);
 he_ciphertext* encrypt_symmetric(he_context* c, const he_plaintext* pt, u64 stream_id, u64 a_seed);
 void sym_regen_c1(he_context* c, he_ciphertext* ct);
 void ct_copy_c0(he_context* c, const he_ciphertext* ct, u64* dst, bool to_ct);
 he_plaintext* decrypt(he_context* c, const he_ciphertext* ct);
 
-he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b);  // 0 add, 1 sub
+// into: write the result into that ciphertext (in-place forms; into == a with a->B >= the other batch)
+he_ciphertext* ct_binop(he_context* c, int op, const he_ciphertext* a, const he_ciphertext* b,
+                        he_ciphertext* into = nullptr);  // 0 add, 1 sub
 he_ciphertext* ct_negate(he_context* c, const he_ciphertext* a);
-he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p);
-he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p);
+he_ciphertext* ct_mul_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext* into = nullptr);
+he_ciphertext* ct_add_plain(he_context* c, const he_ciphertext* a, const he_plaintext* p, he_ciphertext* into = nullptr);
 he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphertext* y);
 he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a, const he_plaintext* bias = nullptr);
 he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a);
