@@ -259,13 +259,33 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     if rank == 0 and not args.no_extra:
         extra = micro_extra(ctx, stream, dev)
+        if world == 1:   # BASELINE.md / SURVEY §8(d) CPU-oracle subsets of configs 1, 2, 3, 5b (~40 s)
+            from bench_configs import cpu_oracle_subsets
+            extra["cpu_oracle_subsets"] = cpu_oracle_subsets()
 
     # result collection to rank 0 (outside the timed region): NCCL gather of the logits
     gather_to_rank0(logits_dev)
+    # client-server data plane: rank 0 encrypts a global batch, scatters
+    # the ciphertext words over NCCL, every rank evaluates its block, the level-0 words are gathered
+    # back; they must equal, bit for bit, rank 0's own single-GPU evaluation of the whole batch
+    dist_check = None
+    if world > 1:
+        from paper_2104_03152_b200.dist import client_server_round
+        Bc = 4
+        imgs_c = mnist_like_images(world * Bc, 4, start=50_000) if rank == 0 else None
+        logits_c, words_c, _ = client_server_round(ctx, net, imgs_c, 4_000_000, dev)
+        if rank == 0:
+            slots_c = he_im2col_encode_batch(imgs_c, 7, 7, 3, ns)
+            ref = net.forward(ctx.he_encrypt(ctx.he_encode(slots_c, 2.0 ** net.plan["in_log2"], net.top),
+                                             4_000_000))
+            rw = torch.empty_like(words_c)
+            ctx.he_ct_export_words(ref, rw)
+            dist_check = {"ranks": world, "images": world * Bc, "collectives": "scatter (input words) + gather "
+                          "(level-0 words), NCCL", "bitwise_equal_single_gpu": bool(torch.equal(rw, words_c))}
 
     extra["communication_cfg4"] = comm
     return dict(value=value, ms=ms, launches=launches, clocks=clk.summary(), roofline=roofline,
-                breakdown=breakdown, e2e=e2e, extra=extra, check=check, cpu=cpu)
+                breakdown=breakdown, e2e=e2e, extra=extra, check=check, cpu=cpu, dist_check=dist_check)
 
 
 def micro_extra(ctx_cnn, stream, dev):
@@ -531,7 +551,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": config, "clocks": r["clocks"], "gpu_launches": r["launches"],
-                "check": r["check"], "e2e": r["e2e"], "roofline": r["roofline"], "cpu_baseline": r["cpu"],
+                "check": r["check"], "dist_check": r["dist_check"], "e2e": r["e2e"], "roofline": r["roofline"], "cpu_baseline": r["cpu"],
                 "breakdown": r["breakdown"], "extra": r["extra"],
                 "paper_context": "TenSEAL/SEAL CPU: 1456.29 ms/img (8 vCPU), 887.06 ms/img (16 vCPU), PAPER.md:113"}
         print(json.dumps(line), flush=True)

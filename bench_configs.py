@@ -100,3 +100,76 @@ def table45_ops(stream, timer, batch: int = 1):
         s = timer(f, reps=20)
         out[k] = {"ms": round(s * 1e3, 4), "paper_ms": PAPER_T45_MS[k]}
     return out
+
+
+# ------------------------------------------------ CPU oracle subsets ---
+def cpu_oracle_subsets():
+    """BASELINE.md / SURVEY §8(d) "Oracle timing": the CPU oracle (oracle/, test infrastructure,
+    never tuned) on bounded subsets of configs 1, 2, 3 and 5b, timed on this host's cores (std::thread
+    over independent items, as the oracle is written).  A baseline for context, not the target."""
+    import os
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import circuits as OC
+    from oracle.oracle import OracleContext
+    from synthetic import CFG1, CFG2_PRIME_BITS, CFG3, CFG5B, deep_chain_plaintexts, messages, vecmat_inputs
+    cores = os.cpu_count() or 1
+    out = {"cores": cores, "note": "CPU oracle baseline, not the target"}
+    try:
+        out["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:
+        out["cpu_model"] = "unknown"
+
+    def pmap(fn, n):
+        with ThreadPoolExecutor(max_workers=min(n, cores)) as ex:
+            return list(ex.map(fn, range(n)))
+
+    # config 1: one encrypted vec_mat (encrypt + 63 rotations + decrypt), batch 1 (keys excluded)
+    o = OracleContext(CFG1.logN, CFG1.bits, CFG1.n_special, CFG1.seed)
+    o.keygen(list(range(1, 64)))
+    x, W = vecmat_inputs(CFG1.seed)
+    t0 = time.perf_counter()
+    ct = o.encrypt(o.encode(OC.replicate(x, o.slots), 2.0 ** 40, o.L - 1), 0)
+    o.decode(o.decrypt(OC.vec_mat(o, ct, W, None, False)), 10)
+    dt = time.perf_counter() - t0
+    out["cfg1_vec_mat"] = {"sample": "1 vec_mat (x 64 replicated, W 64x10), encrypt..decrypt, 1 thread",
+                           "seconds": round(dt, 3), "vec_mats_per_s": round(1 / dt, 4)}
+    del o
+    # config 2: forward NTT of N=16384, L=8, B=64 (512 limb transforms), threads over limbs
+    N, L, B = 1 << 14, 8, 64
+    o = OracleContext(14, CFG2_PRIME_BITS(L), 0, 1)
+    rng = np.random.default_rng(1)
+    limbs = [rng.integers(0, int(o.q[l % L]), N, dtype=np.uint64) for l in range(B * L)]
+    t0 = time.perf_counter()
+    pmap(lambda i: o.ntt(i % L, limbs[i]), B * L)
+    dt = time.perf_counter() - t0
+    out["cfg2_ntt"] = {"sample": "forward NTT, N=16384, L=8, B=64", "seconds": round(dt, 3),
+                       "GBps_16NLB": round(16 * N * L * B / dt / 1e9, 4), "threads": min(B * L, cores)}
+    del o, limbs
+    # config 3: 4 ciphertexts x 14 rotations + 1 mul/relin/rescale
+    o = OracleContext(CFG3.logN, CFG3.bits, CFG3.n_special, CFG3.seed)
+    steps = [1 << r for r in range(14)]
+    o.keygen(steps)
+    z = messages(4, o.slots, seed=CFG3.seed)
+    cts = [o.encrypt(o.encode(z[b], 2.0 ** 50, o.L - 1), b) for b in range(4)]
+    t0 = time.perf_counter()
+    pmap(lambda i: o.rotate(cts[i // 14], steps[i % 14]), 4 * 14)
+    dt = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    o.rescale(o.relinearize(o.tensor(cts[0], cts[1])))
+    dm = time.perf_counter() - t1
+    out["cfg3_keyswitch"] = {"sample": "4 ciphertexts x 14 rotations (threads over rotations) + 1 mul+relin+rescale",
+                             "rotation_seconds": round(dt, 3), "rotations_per_s": round(56 / dt, 3),
+                             "mul_relin_rescale_seconds": round(dm, 3), "threads": min(56, cores)}
+    del o, cts
+    # config 5b: one ciphertext through the deep chain (16 x mul_plain + rescale, 4 rotate-and-add)
+    o = OracleContext(CFG5B.logN, CFG5B.bits, CFG5B.n_special, CFG5B.seed)
+    o.keygen([1, 2, 4, 8])
+    P = deep_chain_plaintexts(16, o.slots, seed=CFG5B.seed)
+    ct = o.encrypt(o.encode(messages(1, o.slots, seed=CFG5B.seed)[0], 2.0 ** 40, o.L - 1), 0)
+    t0 = time.perf_counter()
+    OC.deep_chain(o, ct, P)
+    dt = time.perf_counter() - t0
+    out["cfg5b_deep_chain"] = {"sample": "1 ciphertext, N=32768, 18+2 primes, 1 thread", "seconds": round(dt, 3),
+                               "ciphertexts_per_s": round(1 / dt, 5)}
+    return out

@@ -660,7 +660,15 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
 // giant-step groups with their own (pre-rotated, Montgomery u32) diagonals
 // E[k2][k1]; P (.) c0 is staged so the c0 term joins before the diagonal:
 //   acc_p[k2] += E[k2][k1] (ip_p + [p = 0] P c0[pi_k1(n)]).
-// accx: [G][B][2][Lc+K][N] u32.  Two coefficients per thread (8-byte vectors).
+// accx: [G][B][2][Lc+K][N] u32.
+//
+// Image-pair / half-ring tiling.  Every rotation element g = 5^k is 1 mod 4, so the NTT-domain
+// automorphism pi_g (a8) keeps the top index bit: 2 brv(pi(n)) + 1 = g (2 brv(n) + 1) mod 2N agrees
+// with 2 brv(n) + 1 mod 4, i.e. bit 0 of brv, the top bit of n.  A CTA therefore owns one half of
+// the ring (top bit h) and needs only that half of the digits - and with the smem of one full-ring
+// image it holds the halves of IB = 2 images, so every key row and diagonal it loads serves both
+// images (half the key traffic and half the key / diagonal / galois_src instructions per image).
+// CTA (t, h, pair): target limb t, coefficients [h N/2, (h+1) N/2), images IB pair + {0, 1}.
 //
 // Two reduction schedules, chosen per CTA from its target prime q (uniform branch):
 // * LAZY (LC q < 2^32 and g q < 2^32, e.g. every 26-bit prime of BASELINE config 4): the LC
@@ -671,168 +679,159 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
 //   removes exactly the one factor 2^32 its products carry: the results are the same residues.
 // * PAIRED (q up to 2^31): one REDC per pair of products and per diagonal product (x0 k0' +
 //   x1 k1' < 2 q^2 < q 2^32), the sums kept reduced.
-template <int LC, int G, bool LAZY>
-__device__ __forceinline__ void bsgs_tile(const LazyArgs& a, int g, const u32* const* __restrict__ keys32,
-                                          const u32* __restrict__ dm, const u32* xs, const u32* c0p, int t, int b,
-                                          int nt, bool data, u32 q, u32 qi, u32 Pm, u32 keyrow, u32 kpart, u32 kdig,
-                                          size_t gstride, u32 n0) {
-  constexpr int V = 2;
+template <int LC, int G, int IB, bool LAZY>
+__device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, const u32* const* __restrict__ keys32,
+                                            const u32* __restrict__ dm, const u32* xs, const u32* c0p, int t,
+                                            int b0, int nimg, int nt, bool data, u32 q, u32 qi, u32 Pm, u32 keyrow,
+                                            u32 kpart, u32 kdig, size_t gstride, u32 h0, u32 NH) {
   typedef typename std::conditional<LAZY, u64, u32>::type acc_t;
-  acc_t acc0[G][V], acc1[G][V];
-#pragma unroll
-  for (int k2 = 0; k2 < G; ++k2) {
-    const uint2 d0 = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + (size_t)t * a.N + n0));
-    const u32 dd[V] = {d0.x, d0.y};
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      if (data) {   // k1 = 0: P E[k2][0] (.) c
-        const u32 pc1 = redc32((u64)xs[t * a.N + n0 + e] * Pm, q, qi);
-        if (LAZY) {
-          acc0[k2][e] = (u64)dd[e] * c0p[n0 + e];
-          acc1[k2][e] = (u64)dd[e] * pc1;
-        } else {
-          acc0[k2][e] = redc32((u64)dd[e] * c0p[n0 + e], q, qi);
-          acc1[k2][e] = redc32((u64)dd[e] * pc1, q, qi);
-        }
-      } else {
-        acc0[k2][e] = acc1[k2][e] = 0;
-      }
-    }
-  }
-  for (int k = 1; k < g; ++k) {
-    const u32 gal = __ldg(a.gal + k * a.step);
-    const u32* key = keys32[k * a.step] + keyrow + n0;
-    u32 sn[V], y0[V], y1[V];
-#pragma unroll
-    for (int e = 0; e < V; ++e) sn[e] = galois_src(n0 + e, gal, a.logN);
-    if (LAZY) {
-      u64 T0[V], T1[V];
-#pragma unroll
-      for (int e = 0; e < V; ++e) T0[e] = T1[e] = 0;
-#pragma unroll
-      for (int j = 0; j < LC; ++j) {
-        const uint2 kb = __ldg(reinterpret_cast<const uint2*>(key + j * kdig));
-        const uint2 ka = __ldg(reinterpret_cast<const uint2*>(key + j * kdig + kpart));
-        const u32 bv[V] = {kb.x, kb.y}, av[V] = {ka.x, ka.y};
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          const u32 x = xs[j * a.N + sn[e]];
-          T0[e] += (u64)x * bv[e];
-          T1[e] += (u64)x * av[e];
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        y0[e] = redc32(T0[e], q, qi);
-        if (data) y0[e] = addq(y0[e], c0p[sn[e]], q);
-        y1[e] = redc32(T1[e], q, qi);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        y0[e] = data ? c0p[sn[e]] : 0u;
-        y1[e] = 0;
-      }
-#pragma unroll
-      for (int j = 0; j < LC; j += 2) {
-        const uint2 kb0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig));
-        const uint2 ka0 = __ldg(reinterpret_cast<const uint2*>(key + j * kdig + kpart));
-        uint2 kb1 = make_uint2(0, 0), ka1 = make_uint2(0, 0);
-        if (j + 1 < LC) {
-          kb1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig));
-          ka1 = __ldg(reinterpret_cast<const uint2*>(key + (j + 1) * kdig + kpart));
-        }
-        const u32 b0[V] = {kb0.x, kb0.y}, a0[V] = {ka0.x, ka0.y}, b1[V] = {kb1.x, kb1.y}, a1[V] = {ka1.x, ka1.y};
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          const u32 x0 = xs[j * a.N + sn[e]];
-          u64 s0 = (u64)x0 * b0[e], s1 = (u64)x0 * a0[e];
-          if (j + 1 < LC) {
-            const u32 x1 = xs[(j + 1) * a.N + sn[e]];
-            s0 += (u64)x1 * b1[e];
-            s1 += (u64)x1 * a1[e];
-          }
-          y0[e] = addq(y0[e], redc32(s0, q, qi), q);
-          y1[e] = addq(y1[e], redc32(s1, q, qi), q);
-        }
-      }
-    }
+  for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T) {
+    const u32 n = h0 + l;
+    acc_t acc0[IB][G], acc1[IB][G];
 #pragma unroll
     for (int k2 = 0; k2 < G; ++k2) {
-      const uint2 dv = __ldg(reinterpret_cast<const uint2*>(dm + k2 * gstride + ((size_t)k * nt + t) * a.N + n0));
-      const u32 dd[V] = {dv.x, dv.y};
+      const u32 d = __ldg(dm + k2 * gstride + (size_t)t * a.N + n);
 #pragma unroll
-      for (int e = 0; e < V; ++e) {
-        if (LAZY) {
-          acc0[k2][e] += (u64)dd[e] * y0[e];
-          acc1[k2][e] += (u64)dd[e] * y1[e];
+      for (int i = 0; i < IB; ++i) {
+        if (data) {   // k1 = 0: P E[k2][0] (.) c
+          const u32 pc1 = redc32((u64)xs[(i * LC + t) * NH + l] * Pm, q, qi);
+          const u32 pc0 = c0p[i * NH + l];
+          if (LAZY) {
+            acc0[i][k2] = (u64)d * pc0;
+            acc1[i][k2] = (u64)d * pc1;
+          } else {
+            acc0[i][k2] = redc32((u64)d * pc0, q, qi);
+            acc1[i][k2] = redc32((u64)d * pc1, q, qi);
+          }
         } else {
-          acc0[k2][e] = addq(acc0[k2][e], redc32((u64)dd[e] * y0[e], q, qi), q);
-          acc1[k2][e] = addq(acc1[k2][e], redc32((u64)dd[e] * y1[e], q, qi), q);
+          acc0[i][k2] = acc1[i][k2] = 0;
         }
       }
     }
-  }
-  u32* out = reinterpret_cast<u32*>(a.accx);
-#pragma unroll
-  for (int k2 = 0; k2 < G; ++k2) {
-    u32 r0[V], r1[V];
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
+    for (int k = 1; k < g; ++k) {
+      const u32 gal = __ldg(a.gal + k * a.step);
+      const u32* key = keys32[k * a.step] + keyrow + n;
+      const u32 sl = galois_src(n, gal, a.logN) - h0;   // same half (see above)
+      u32 y0[IB], y1[IB];
       if (LAZY) {
-        r0[e] = redc32(acc0[k2][e], q, qi);
-        r1[e] = redc32(acc1[k2][e], q, qi);
+        u64 T0[IB], T1[IB];
+#pragma unroll
+        for (int i = 0; i < IB; ++i) T0[i] = T1[i] = 0;
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
+          const u32 kb = __ldg(key + j * kdig), ka = __ldg(key + j * kdig + kpart);
+#pragma unroll
+          for (int i = 0; i < IB; ++i) {
+            const u32 x = xs[(i * LC + j) * NH + sl];
+            T0[i] += (u64)x * kb;
+            T1[i] += (u64)x * ka;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < IB; ++i) {
+          y0[i] = redc32(T0[i], q, qi);
+          if (data) y0[i] = addq(y0[i], c0p[i * NH + sl], q);
+          y1[i] = redc32(T1[i], q, qi);
+        }
       } else {
-        r0[e] = (u32)acc0[k2][e];
-        r1[e] = (u32)acc1[k2][e];
+#pragma unroll
+        for (int i = 0; i < IB; ++i) {
+          y0[i] = data ? c0p[i * NH + sl] : 0u;
+          y1[i] = 0;
+        }
+#pragma unroll
+        for (int j = 0; j < LC; j += 2) {
+          const u32 kb0 = __ldg(key + j * kdig), ka0 = __ldg(key + j * kdig + kpart);
+          const u32 kb1 = j + 1 < LC ? __ldg(key + (j + 1) * kdig) : 0u;
+          const u32 ka1 = j + 1 < LC ? __ldg(key + (j + 1) * kdig + kpart) : 0u;
+#pragma unroll
+          for (int i = 0; i < IB; ++i) {
+            const u32 x0 = xs[(i * LC + j) * NH + sl];
+            u64 s0 = (u64)x0 * kb0, s1 = (u64)x0 * ka0;
+            if (j + 1 < LC) {
+              const u32 x1 = xs[(i * LC + j + 1) * NH + sl];
+              s0 += (u64)x1 * kb1;
+              s1 += (u64)x1 * ka1;
+            }
+            y0[i] = addq(y0[i], redc32(s0, q, qi), q);
+            y1[i] = addq(y1[i], redc32(s1, q, qi), q);
+          }
+        }
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < G; ++k2) {
+        const u32 d = __ldg(dm + k2 * gstride + ((size_t)k * nt + t) * a.N + n);
+#pragma unroll
+        for (int i = 0; i < IB; ++i) {
+          if (LAZY) {
+            acc0[i][k2] += (u64)d * y0[i];
+            acc1[i][k2] += (u64)d * y1[i];
+          } else {
+            acc0[i][k2] = addq(acc0[i][k2], redc32((u64)d * y0[i], q, qi), q);
+            acc1[i][k2] = addq(acc1[i][k2], redc32((u64)d * y1[i], q, qi), q);
+          }
+        }
       }
     }
-    const size_t base = ((((size_t)k2 * gridDim.y + b) * 2) * nt + t) * a.N + n0;
-    *reinterpret_cast<uint2*>(out + base) = make_uint2(r0[0], r0[1]);
-    *reinterpret_cast<uint2*>(out + base + (size_t)nt * a.N) = make_uint2(r1[0], r1[1]);
+    u32* out = reinterpret_cast<u32*>(a.accx);
+#pragma unroll
+    for (int i = 0; i < IB; ++i) {
+      if (i < nimg) {
+#pragma unroll
+        for (int k2 = 0; k2 < G; ++k2) {
+          const size_t base = ((((size_t)k2 * B + b0 + i) * 2) * nt + t) * a.N + n;
+          out[base] = LAZY ? redc32(acc0[i][k2], q, qi) : (u32)acc0[i][k2];
+          out[base + (size_t)nt * a.N] = LAZY ? redc32(acc1[i][k2], q, qi) : (u32)acc1[i][k2];
+        }
+      }
+    }
   }
 }
 
-template <int LC, int G>
+template <int LC, int G, int IB>
 __global__ void __launch_bounds__(LAZY_SM_T, 1)
-k_vecmat_bsgs_mont(LazyArgs a, int g, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
-                   const PrimeD* __restrict__ primes) {
-  constexpr int V = 2;
-  extern __shared__ u32 xs[];
-  const int t = blockIdx.x, b = blockIdx.y, nt = LC + a.K;
+k_vecmat_bsgs_hp(LazyArgs a, int g, int B, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
+                 const PrimeD* __restrict__ primes) {
+  extern __shared__ u32 xs[];   // [IB][LC][N/2] digits of this half, then c0p [IB][N/2]
+  const int t = blockIdx.x, nt = LC + a.K;
+  const u32 NH = (u32)a.N / 2, h0 = blockIdx.y * NH;
+  const int b0 = blockIdx.z * IB, nimg = min(IB, B - b0);
   const int tp = t < LC ? t : a.L + (t - LC);
   const PrimeD P = load_prime(primes, tp);
   const u32 q = (u32)P.q, qi = mont_neg_inv(q);
   const u32 N = a.N, NP = a.NP;
-  const u64* c0 = a.ct + (size_t)b * 2 * LC * N;
-  const u64* c1 = c0 + (size_t)LC * N;
   const bool data = t < LC;
   const u32 Pm = (u32)((((u64)__ldg(a.P_mod + tp)) << 32) % q);
+  u32* c0p = xs + IB * LC * NH;
+  for (int i = 0; i < IB; ++i) {
+    const int b = b0 + (i < nimg ? i : 0);   // a missing second image repeats the first (never stored)
+    const u64* c0 = a.ct + (size_t)b * 2 * LC * N;
+    const u64* c1 = c0 + (size_t)LC * N;
 #pragma unroll
-  for (int j = 0; j < LC; ++j) {
-    if (t == j || !a.ext32) {
-      const u64* src = (t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N;
-      for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) xs[j * N + i] = (u32)src[i];
-    } else {
-      const u32* src = a.ext32 + (((size_t)b * LC + j) * nt + t) * N;
-      for (u32 i = threadIdx.x * 4; i < N; i += LAZY_SM_T * 4)
-        *reinterpret_cast<uint4*>(xs + j * N + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+    for (int j = 0; j < LC; ++j) {
+      u32* dst = xs + (i * LC + j) * NH;
+      if (t == j || !a.ext32) {
+        const u64* src = ((t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N) + h0;
+        for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T) dst[l] = (u32)src[l];
+      } else {
+        const u32* src = a.ext32 + (((size_t)b * LC + j) * nt + t) * N + h0;
+        for (u32 l = threadIdx.x * 4; l < NH; l += LAZY_SM_T * 4)
+          *reinterpret_cast<uint4*>(dst + l) = __ldg(reinterpret_cast<const uint4*>(src + l));
+      }
     }
+    if (data)
+      for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T)
+        c0p[i * NH + l] = redc32((u64)(u32)c0[(size_t)t * N + h0 + l] * Pm, q, qi);
   }
-  u32* c0p = xs + LC * N;   // P c0[t] (plain residues)
-  if (data)
-    for (u32 i = threadIdx.x; i < N; i += LAZY_SM_T) c0p[i] = redc32((u64)(u32)c0[(size_t)t * N + i] * Pm, q, qi);
   __syncthreads();
   const u32 keyrow = tp * N, kpart = NP * N, kdig = 2 * NP * N;
   const size_t gstride = (size_t)g * nt * N;   // between giant-step groups in dm
-  const bool lazy = (u64)LC * q < (1ULL << 32) && (u64)g * q < (1ULL << 32);
-  for (u32 tile = 0; tile < N; tile += LAZY_SM_T * V) {
-    const u32 n0 = tile + threadIdx.x * V;
-    if (lazy)
-      bsgs_tile<LC, G, true>(a, g, keys32, dm, xs, c0p, t, b, nt, data, q, qi, Pm, keyrow, kpart, kdig, gstride, n0);
-    else
-      bsgs_tile<LC, G, false>(a, g, keys32, dm, xs, c0p, t, b, nt, data, q, qi, Pm, keyrow, kpart, kdig, gstride, n0);
-  }
+  if ((u64)LC * q < (1ULL << 32) && (u64)g * q < (1ULL << 32))
+    bsgs_hp_run<LC, G, IB, true>(a, g, B, keys32, dm, xs, c0p, t, b0, nimg, nt, data, q, qi, Pm, keyrow, kpart,
+                                 kdig, gstride, h0, NH);
+  else
+    bsgs_hp_run<LC, G, IB, false>(a, g, B, keys32, dm, xs, c0p, t, b0, nimg, nt, data, q, qi, Pm, keyrow, kpart,
+                                  kdig, gstride, h0, NH);
 }
 
 // Fused ModUp + key inner product for small primes (a9 without materialising
@@ -1807,21 +1806,28 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
                                               "vecmat_bsgs_L4", "vecmat_bsgs_L5", "vecmat_bsgs_L6", "vecmat_bsgs_L7",
                                               "vecmat_bsgs_L8"};
           ProfScope ps_(c, tags[Lc], bytes, B * nt, ops);
+          // half-ring CTAs with image pairs (k_vecmat_bsgs_hp): same smem as one full-ring image
+          const int IBv = B >= 2 ? 2 : 1;
+          const size_t smem_hp = (size_t)IBv * (Lc + 1) * (N / 2) * 4;
+          const dim3 grid(nt, 2, (unsigned)((B + IBv - 1) / IBv));
           auto launch = [&](auto kern) {
             smem_limit_once((const void*)kern, (int)kMaxSmem);
-            kern<<<dim3(nt, B), LAZY_SM_T, smem, c->stream>>>(la, g, kt, diags->dm, c->d_primes);
+            kern<<<grid, LAZY_SM_T, smem_hp, c->stream>>>(la, g, B, kt, diags->dm, c->d_primes);
           };
+#define HE_BSGS_G(LCV, IBV)                                                      \
+    if (G == 1) launch(k_vecmat_bsgs_hp<LCV, 1, IBV>);                           \
+    else if (G == 2) launch(k_vecmat_bsgs_hp<LCV, 2, IBV>);                      \
+    else if (G == 3) launch(k_vecmat_bsgs_hp<LCV, 3, IBV>);                      \
+    else launch(k_vecmat_bsgs_hp<LCV, 4, IBV>);
 #define HE_BSGS_CASE(LCV)                                                        \
   case LCV:                                                                      \
-    if (G == 1) launch(k_vecmat_bsgs_mont<LCV, 1>);                              \
-    else if (G == 2) launch(k_vecmat_bsgs_mont<LCV, 2>);                         \
-    else if (G == 3) launch(k_vecmat_bsgs_mont<LCV, 3>);                         \
-    else launch(k_vecmat_bsgs_mont<LCV, 4>);                                     \
+    if (IBv == 2) { HE_BSGS_G(LCV, 2) } else { HE_BSGS_G(LCV, 1) }               \
     break;
           switch (Lc) {
             HE_BSGS_CASE(1) HE_BSGS_CASE(2) HE_BSGS_CASE(3) HE_BSGS_CASE(4)
             HE_BSGS_CASE(5) HE_BSGS_CASE(6) HE_BSGS_CASE(7) default: HE_BSGS_CASE(8)
           }
+#undef HE_BSGS_G
 #undef HE_BSGS_CASE
         }
         check_launch(c);

@@ -49,3 +49,39 @@ def test_sharding_gloo(world):
     order = np.argsort(idx)
     ref = np.sin(np.arange(3 * 5 * world)[:, None] * np.arange(1, 11)[None, :])
     assert np.array_equal(res[order], ref)
+
+
+def _worker_words(rank, world, port, q):
+    """Client (rank 0) scatters ciphertext words, every rank returns its block, rank 0 gathers."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2104_03152_b200.dist import gather_blocks_to_rank0, scatter_from_rank0
+        B, shape = 3, (2, 4, 16)
+        rng = np.random.default_rng(7)
+        full = torch.from_numpy(rng.integers(0, 2 ** 62, (world * B, *shape), dtype=np.int64))
+        mine = scatter_from_rank0(full if rank == 0 else None, (B, *shape), torch.int64, "cpu")
+        ok_block = bool(torch.equal(mine, full[rank * B:(rank + 1) * B]))
+        back = gather_blocks_to_rank0(mine + rank * 0)
+        oks = gather_to_rank0(torch.tensor([int(ok_block)]))
+        if rank == 0:
+            q.put((bool(torch.equal(back, full)), [int(o.item()) for o in oks]))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_client_scatter_gather_words_gloo():
+    """SURVEY §8(e) data plane: rank r receives exactly the contiguous block r of the client's
+    ciphertext words and the gathered blocks reassemble the client's array bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker_words, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    same, oks = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert same and oks == [1, 1]
