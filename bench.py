@@ -35,12 +35,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "encrypted 28x28 CNN inferences/s/box"
-# ALU roofline of the integer kernels: a 32-bit Shoup/Montgomery modular
-# butterfly needs >= 3 FMA-pipe (IMAD.HI, IMAD, IMAD) and >= 5 ALU-pipe (2 IADD3, 3 min-based
-# conditional subtractions) instructions; the ALU pipe (64 lanes/clk/SM) binds first:
-# 64 / 5 = 12.8 modular ops/clk/SM x 148 SMs x 1.965 GHz (max SM clock, held under this load).
-ALU_PEAK_GOPS = 12.8 * 148 * 1.965
 UNIT = "images/s"
+
+# Integer roofline.  The integer pipes' peak rates are MEASURED on this pool's B200
+# (profiles/int_peak.cu -> profiles/r02/int_peak.json: IMAD / IADD3 / VIADDMNMX 64 lanes/clk/SM,
+# IMAD.HI 32), and the dominant kernel's instruction mix is MEASURED by ncu (profiles/r02/pipe_mix.json,
+# from the `ncu --set full` capture of that kernel in the bench step: its busiest integer pipe and that
+# pipe's utilisation u at the captured duration d).  The kernel's integer peak is the modular-op rate
+# at which that pipe would be 100% busy with the same mix: alg_ops / (d u); frac = live rate / peak.
+
+
+def _load_json(rel):
+    try:
+        return json.load(open(os.path.join(ROOT, rel)))
+    except Exception:
+        return None
+
+
+INT_PEAK = _load_json("profiles/r02/int_peak.json")
+PIPE_MIX = _load_json("profiles/r02/pipe_mix.json") or {}
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from one `ncu --set full` capture of the
@@ -184,13 +197,24 @@ def run_ours(args, rank, world, local_rank):
     sec = t_ms / n_l / 1e3
     gbs = (alg_b / n_l) / sec / 1e9 if t_ms > 0 else 0.0
     gops = (alg_ops / n_l) / sec / 1e9 if t_ms > 0 else 0.0
-    roofline = {"bound": "alu", "kernel": top, "achieved": round(gops, 1), "peak": round(ALU_PEAK_GOPS, 1),
-                "unit": "Gmodop/s", "frac": round(gops / ALU_PEAK_GOPS, 4), "traffic": TRAFFIC.get(top),
+    mix = PIPE_MIX.get(top)
+    if mix:   # measured instruction mix of this kernel (ncu) -> its integer peak
+        peak_gops = mix["alg_ops_per_launch"] / (mix["ncu_duration_s"] * mix["busiest_pipe_util"]) / 1e9
+        peak_src = (f"integer pipes measured (profiles/r02/int_peak.json); kernel mix measured by ncu "
+                    f"(profiles/r02/pipe_mix.json: busiest pipe {mix['busiest_pipe']} at "
+                    f"{100 * mix['busiest_pipe_util']:.1f}% over {1e6 * mix['ncu_duration_s']:.0f} us) -> "
+                    f"the modop rate that saturates that pipe")
+    else:     # no capture of this kernel yet: the measured shoup32 modmul rate (4 FMA-pipe slots)
+        r = (INT_PEAK or {}).get("ops", {}).get("shoup32_modmul", {}).get("lane_steps_per_clk_per_sm", 15.8)
+        peak_gops = r * 148 * 1.965
+        peak_src = "measured shoup32 modmul rate (profiles/r02/int_peak.json) x 148 SMs x 1.965 GHz"
+    roofline = {"bound": "alu", "kernel": top, "achieved": round(gops, 1), "peak": round(peak_gops, 1),
+                "unit": "Gmodop/s", "frac": round(gops / peak_gops, 4), "traffic": TRAFFIC.get(top),
                 "alg_ops_per_launch": alg_ops / n_l, "alg_bytes_per_launch": alg_b / n_l,
                 "hbm_achieved_GBps": round(gbs, 1), "hbm_peak_GBps": peaks["hbm_gbs"],
                 "hbm_frac": round(gbs / peaks["hbm_gbs"], 4),
                 "share_of_step": round(t_ms / tot, 3), "us_per_launch": round(sec * 1e6, 2),
-                "peak_source": "ALU: derived (DESIGN.md §5: 12.8 modular ops/clk/SM x 148 x 1.965 GHz); HBM: "
+                "peak_source": peak_src + "; HBM: "
                                + ("MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback")}
     breakdown = {k: {"launches_per_step": v[0] / 2, "ms_per_step": round(v[1] / 2, 3),
                      "share": round(v[1] / tot, 3)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}

@@ -15,7 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libhe_ckks.so")
+# HE_LIB_OUT: build an experiment variant elsewhere (with HE_NVCC_EXTRA flags); the product is LIB
+LIB = os.environ.get("HE_LIB_OUT") or os.path.join(HERE, "libhe_ckks.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["he_ops.cu", "he_capi.cu"]
@@ -46,7 +47,8 @@ def _run(cmd):
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if LIB.endswith("/libhe_ckks.so") and os.path.dirname(LIB) == HERE
+                          else "build_" + os.path.basename(LIB).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     from concurrent.futures import ThreadPoolExecutor

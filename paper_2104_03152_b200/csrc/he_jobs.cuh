@@ -27,6 +27,12 @@ __device__ __forceinline__ u32 shoup_companion32(u32 w, u32 q) { return (u32)(((
 __device__ __forceinline__ u32 mu32_of(const PrimeD& P) { return (u32)(P.mu64 >> 32); }
 
 template <class B, class = void>
+struct has_store4 : std::false_type {};
+template <class B>
+struct has_store4<B, std::void_t<decltype(std::declval<const B&>().store4(0u, 0u, (const u32*)nullptr))>>
+    : std::true_type {};
+
+template <class B, class = void>
 struct has_load4 : std::false_type {};
 template <class B>
 struct has_load4<B, std::void_t<decltype(std::declval<const B&>().load4(0u))>> : std::true_type {};
@@ -497,6 +503,36 @@ struct JobKsData {
     int blk;
     const PrimeD* P;
     bool fast, gather;
+    // 4 outputs (n0 + u st): every operand load of the 4 is issued before the arithmetic, so the
+    // epilogue's global loads overlap instead of serialising behind the stores
+    __device__ __forceinline__ void store4(u32 n0, u32 st, const u32* v) const {
+      if (!fast || D || acc) {   // (the plaintext-factor / accumulating forms: one output at a time)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) store(n0 + u * st, v[u]);
+        return;
+      }
+      u32 axv[4], adv[4] = {0, 0, 0, 0}, s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const u32 n = n0 + u * st;
+        axv[u] = ax[n];
+        if (add) adv[u] = (u32)add[gather ? galois_src(n, g, logN) : n];
+        if (sq0) {
+          s0[u] = (u32)sq0[n];
+          s1[u] = sq1 ? (u32)sq1[n] : s0[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        u32 r = mulsh32(sub32(axv[u], v[u], q), pinv, pinvsh, q);
+        if (add) r = add32(r, adv[u], q);
+        if (sq0) {
+          const u32 t = (u32)mul_mod(s0[u], s1[u], *P);
+          r = add32(r, sq1 ? add32(t, t, q) : t, q);
+        }
+        out[n0 + u * st] = r;
+      }
+    }
     const u32* tb;
     const u32* ax;
     const u64* add;
@@ -646,6 +682,20 @@ struct JobRescaleData {
     const u64* bias;   // bias row (poly 0 only) or null
     int r, i;
     u32 q, mu32, h, qi, qish;
+    __device__ __forceinline__ void store4(u32 n0, u32 st, const u32* v) const {
+      u32 xv[4], bv[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xv[u] = (u32)src->at(r, i, n0 + u * st, *P);
+        if (bias) bv[u] = (u32)bias[n0 + u * st];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        u32 o = mulsh32(sub32(xv[u], v[u], q), qi, qish, q);
+        if (bias) o = add32(o, bv[u], q);
+        out[n0 + u * st] = o;
+      }
+    }
     __device__ __forceinline__ u64 load(u32 n) const { return sub32(red32(y[n], q, mu32), h, q); }
     __device__ __forceinline__ u64 load_raw(u32 x) const { return sub32(red32(x, q, mu32), h, q); }
     __device__ __forceinline__ void store(u32 n, u64 v) const {

@@ -28,7 +28,11 @@ struct NttGeom {
   static constexpr int N = 1 << LOGN;
   static constexpr int LOGNL = LOGN - (CL == 2 ? 1 : 0);  // bits owned by one CTA
   static constexpr int NL = 1 << LOGNL;
-  static constexpr int R = LOGNL - 10 > 4 ? LOGNL - 10 : 4;  // log2 words per thread
+#ifndef HE_NTT64_R14
+#define HE_NTT64_R14 4
+#endif
+  // log2 words per thread (a 2^14 limb per CTA: HE_NTT64_R14, 4 = 1024 threads x 16 words)
+  static constexpr int R = LOGNL == 14 ? HE_NTT64_R14 : (LOGNL - 10 > 4 ? LOGNL - 10 : 4);
   static constexpr int T = NL >> R;                            // threads per CTA
   // CTAs per SM the register budget is sized for (shared memory allows 3 at N=2^13)
   static constexpr int MINB = NL <= 8192 ? 2 : 1;
@@ -69,35 +73,23 @@ __device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const ulon
     u64 x[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) x[k] = sm[spad(base + (k << LO))];
-    if (!INV) {
+    // twiddle of the butterfly on bit b at index j = gbase | hi << (LO+NB) | k << LO | lo:
+    // tw[2^s + (j >> (b+1))], s = LOGN-1-b, and j >> (b+1) = (gbase >> (b+1)) + (hi << (LO+NB-1-b)) +
+    // (k >> (b+1-LO)): one base pointer per stage and compile-time offsets, so the butterflies of a
+    // group that share a twiddle share one load
+    const u32 hi = g >> LO;
 #pragma unroll
-      for (int ss = 0; ss < NB; ++ss) {
-        const int b = LO + NB - 1 - ss;   // local == global bit being paired
-        const int s = LOGN - 1 - b;       // stage index
-        const int half = 1 << (NB - 1 - ss);
+    for (int ss = 0; ss < NB; ++ss) {
+      const int b = INV ? LO + ss : LO + NB - 1 - ss;   // local == global bit being paired
+      const int s = LOGN - 1 - b;                        // stage index
+      const int half = INV ? 1 << ss : 1 << (NB - 1 - ss);
+      const ulonglong2* tws = tw + (1u << s) + (gbase >> (b + 1)) + (hi << (LO + NB - 1 - b));
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          if (k & half) continue;
-          const u32 j = gbase + base + (k << LO);
-          const u32 ti = (1u << s) + (j >> (LOGN - s));
-          const ulonglong2 w = __ldg(tw + ti);
-          ct_bfly(x[k], x[k + half], w.x, w.y, q, two_q);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int ss = 0; ss < NB; ++ss) {
-        const int b = LO + ss;
-        const int s = LOGN - 1 - b;
-        const int half = 1 << ss;
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-          if (k & half) continue;
-          const u32 j = gbase + base + (k << LO);
-          const u32 ti = (1u << s) + (j >> (LOGN - s));
-          const ulonglong2 w = __ldg(tw + ti);
-          gs_bfly(x[k], x[k + half], w.x, w.y, q, two_q);
-        }
+      for (int k = 0; k < E; ++k) {
+        if (k & half) continue;
+        const ulonglong2 w = __ldg(tws + (k >> (b + 1 - LO)));
+        if (!INV) ct_bfly(x[k], x[k + half], w.x, w.y, q, two_q);
+        else gs_bfly(x[k], x[k + half], w.x, w.y, q, two_q);
       }
     }
 #pragma unroll
@@ -418,6 +410,30 @@ __device__ __forceinline__ u32 ntt_reduce32(u32 v, u32 q) {
   return min(v, v - q);
 }
 
+// Final scaling (inverse) or reduction (forward) of the transform in sm and the job's store; jobs
+// with store4 get 4 outputs per call (their operand loads batched ahead of the arithmetic).
+template <int LOGN, bool INV, class JB>
+__device__ __forceinline__ void ntt32_epilogue(const JB& jb, const u32* sm, u32 tid, uint2 ni, u32 q) {
+  typedef NttGeomS<LOGN> G;
+  if constexpr (has_store4<JB>::value && (G::NL / G::T) % 4 == 0) {
+    for (u32 i0 = tid; i0 < G::NL; i0 += 4 * G::T) {
+      u32 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const u32 x = sm[spad32(i0 + u * G::T)];
+        v[u] = INV ? shoup32(x, ni.x, ni.y, q) : ntt_reduce32(x, q);
+      }
+      jb.store4(i0, G::T, v);
+    }
+  } else {
+    for (u32 i = tid; i < G::NL; i += G::T) {
+      u32 v = sm[spad32(i)];
+      v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
+      jb.store(i, (u64)v);
+    }
+  }
+}
+
 template <int LOGN>
 struct NttGeom32 {
   static constexpr int SMEM = ((1 << LOGN) + (1 << LOGN) / 32) * 4;
@@ -453,11 +469,7 @@ k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw
   __syncthreads();
   ntt_run32<LOGN, INV>(sm32, tid, tw, q);
   const uint2 ni = __ldg(tw);
-  for (u32 i = tid; i < G::NL; i += G::T) {
-    u32 v = sm32[spad32(i)];
-    v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
-    jb.store(i, (u64)v);
-  }
+  ntt32_epilogue<LOGN, INV>(jb, sm32, tid, ni, q);
 }
 
 // ---- pipelined persistent variant (jobs with a single u32 input row: raw32 / load_raw) ----------
@@ -503,11 +515,7 @@ k_ntt32_pipe(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict
     if (blk + (int)gridDim.x < nblk) stage_row32<LOGN>(stage, job.raw32(blk + gridDim.x), tid);
     ntt_run32<LOGN, INV>(sm32, tid, tw, q);
     const uint2 ni = __ldg(tw);
-    for (u32 i = tid; i < G::NL; i += G::T) {
-      u32 v = sm32[spad32(i)];
-      v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
-      jb.store(i, (u64)v);
-    }
+    ntt32_epilogue<LOGN, INV>(jb, sm32, tid, ni, q);
   }
 }
 
