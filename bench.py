@@ -341,9 +341,12 @@ def micro_extra(ctx_cnn, stream, dev):
     s_i = t(lambda: c2.he_ntt_inverse(a, B, L))
     s_m = t(lambda: c2.he_ntt_mul_intt(a, b, o, B, L))
     nbytes = 16 * N * L * B
+    peaks = load_peaks()
     out["ntt_cfg2"] = {"shape": "N=16384 L=8 B=256 (4.3 GB/s basis: 16 N L B bytes)",
                        "fwd_GBps": round(nbytes / s_f / 1e9, 1), "inv_GBps": round(nbytes / s_i / 1e9, 1),
-                       "fused_fwd_mul_inv_GBps": round(24 * N * L * B / s_m / 1e9, 1)}
+                       "fused_fwd_mul_inv_GBps": round(24 * N * L * B / s_m / 1e9, 1),
+                       "roofline": roofline_block("ntt_cfg2_fwd", nbytes / s_f / 1e9, 0.5 * N * 14 * L * B / s_f / 1e9,
+                                                  peaks)}
     del a, b, o
     # config 3: N=16384, 8 data + 2 special 50-bit primes, 256 ciphertexts, rotations by 2^r and ct x ct
     c3 = Context(CFG3.logN, CFG3.bits, CFG3.n_special, CFG3.seed)
@@ -354,9 +357,24 @@ def micro_extra(ctx_cnn, stream, dev):
     z = torch.from_numpy(messages(Bc, c3.slots, seed=CFG3.seed)).to(dev)
     ct = c3.he_encrypt(c3.he_encode(z, 2.0 ** 50, c3.L - 1), 0)
     s_rot = t(lambda: [c3.he_rotate(ct, s) for s in steps], reps=2)
+    # kernel breakdown of one batch of rotations (the in-library profiler: CUDA events per launch)
+    c3.he_profile_enable(True)
+    for s_ in steps:
+        c3.he_rotate(ct, s_)
+    torch.cuda.synchronize(dev)
+    prof3 = c3.he_profile_read()
+    c3.he_profile_enable(False)
+    tot3 = sum(v[1] for v in prof3.values()) or 1.0
+    top3 = max(prof3, key=lambda k: prof3[k][1])
+    p3 = (prof3[top3] + [0.0] * 5)[:5]
+    rot_break = {k: round(v[1] / tot3, 3) for k, v in sorted(prof3.items(), key=lambda kv: -kv[1][1])}
     s_mul = t(lambda: c3.he_rescale(c3.he_relinearize(c3.he_mul(ct, ct))), reps=3)
     out["keyswitch_cfg3"] = {"shape": "N=16384, 8+2 x 50-bit primes, 256 ciphertexts, top level",
                              "rotations_per_s": round(Bc * len(steps) / s_rot, 1),
+                             "rotation_breakdown": rot_break,
+                             "roofline": roofline_block("cfg3_" + top3, (p3[2] / p3[0]) / (p3[1] / p3[0] / 1e3) / 1e9,
+                                                        (p3[4] / p3[0]) / (p3[1] / p3[0] / 1e3) / 1e9, peaks,
+                                                        kernel=top3, share=p3[1] / tot3),
                              "mul_relin_rescale_per_s": round(Bc / s_mul, 1)}
     del c3, ct
     # config 1: one encrypted vec-mat (x 64 values replicated, W 64x10), batch 1: latency
@@ -367,6 +385,22 @@ def micro_extra(ctx_cnn, stream, dev):
     # PAPER.md Tables 4-5 op set at the paper's parameters (latency, one ciphertext)
     out["ops_table45"] = table45_ops(stream, t)
     return out
+
+
+def roofline_block(tag, gbs, gops, peaks, kernel=None, share=None):
+    """Roofline of a secondary metric's dominant kernel: HBM fraction of the algorithmic bytes, and the
+    integer-pipe fraction from the ncu-measured mix of that kernel (profiles/r02/pipe_mix.json entry
+    `tag`: the modop rate at which its busiest pipe saturates), when captured."""
+    r = {"kernel": kernel or tag, "hbm_achieved_GBps": round(gbs, 1), "hbm_peak_GBps": peaks["hbm_gbs"],
+         "hbm_frac": round(gbs / peaks["hbm_gbs"], 4), "alu_achieved_Gmodops": round(gops, 1)}
+    if share is not None:
+        r["share_of_batch"] = round(share, 3)
+    mix = PIPE_MIX.get(tag)
+    if mix:
+        peak = mix["alg_ops_per_launch"] / (mix["ncu_duration_s"] * mix["busiest_pipe_util"]) / 1e9
+        r.update({"bound": "alu", "alu_peak_Gmodops": round(peak, 1), "alu_frac": round(gops / peak, 4),
+                  "busiest_pipe": mix["busiest_pipe"], "peak_source": "ncu mix (profiles/r02/pipe_mix.json)"})
+    return r
 
 
 # ------------------------------------------------------- oracle (CPU) ---

@@ -262,6 +262,9 @@ void launch_ntt32_t(he_context* c, const Job& job, int nblk) {
   check_launch(c);
 }
 
+#ifndef HE_NTT64_CL14
+#define HE_NTT64_CL14 2   // CTAs per 2^14-word limb on the 64-bit engine: a 2-CTA DSMEM cluster (2 per SM; +8% at cfg2)
+#endif
 template <bool INV, class Job>
 void launch_ntt(he_context* c, const Job& job, int nblk) {
   if (c->small_primes && c->d_tw32 && c->logN <= 14) {
@@ -278,7 +281,7 @@ void launch_ntt(he_context* c, const Job& job, int nblk) {
     case 11: launch_ntt_t<11, 1, INV>(c, job, nblk); break;
     case 12: launch_ntt_t<12, 1, INV>(c, job, nblk); break;
     case 13: launch_ntt_t<13, 1, INV>(c, job, nblk); break;
-    case 14: launch_ntt_t<14, 1, INV>(c, job, nblk); break;
+    case 14: launch_ntt_t<14, HE_NTT64_CL14, INV>(c, job, nblk); break;
     case 15: launch_ntt_t<15, 2, INV>(c, job, nblk); break;
     default: throw HeError(HE_INVALID_PARAMS, "unsupported log2N");
   }

@@ -436,6 +436,19 @@ struct JobKsSpecial {
     }
     return r;
   }
+  // pipelined kernel (pipe_ok): the fast form only, without the generic fallback's registers
+  struct P32 {
+    u32* tb;
+    u32 q, ph;
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return x; }
+    __device__ __forceinline__ void store(u32 n, u64 v) const { tb[n] = add32((u32)v, ph, q); }
+  };
+  __device__ P32 bind_pipe(int blk, const PrimeD& P) const {
+    int kk, b, part, k;
+    dec(blk, kk, b, part, k);
+    return P32{reinterpret_cast<u32*>(a.tb) + (((size_t)kk * a.B + b) * 2 + part) * a.N, (u32)P.q,
+               (u32)__ldg(a.Ph_mod + a.L + k)};
+  }
   // lazy ModDown with u32 accumulators and one special prime: input = one u32 accumulator row
   __host__ __device__ bool pipe_ok() const { return a.accx && a.accx32 && a.K == 1; }
   __host__ __device__ const u32* raw32(int blk) const {
@@ -591,7 +604,72 @@ struct JobKsData {
     }
     return r;
   }
-  // fast path input = one u32 row of tb (written by JobKsSpecial's fast store)
+  // pipelined kernel (pipe_ok, accx mode: no plaintext factor D): the fast form only
+  struct P32 {
+    const u32* ax;
+    const u64* add;
+    const u64* acc;
+    u64* out;
+    const u64* sq0;
+    const u64* sq1;
+    const PrimeD* P;
+    u32 q, mu32, ph, pinv, pinvsh, g;
+    int logN;
+    bool gather;
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return sub32(red32(x, q, mu32), ph, q); }
+    __device__ __forceinline__ u32 fin(u32 n, u32 v, u32 axv, u32 adv, u32 s0, u32 s1, u32 acv) const {
+      u32 r = mulsh32(sub32(axv, v, q), pinv, pinvsh, q);
+      if (add) r = add32(r, adv, q);
+      if (sq0) {
+        const u32 t = (u32)mul_mod(s0, s1, *P);
+        r = add32(r, sq1 ? add32(t, t, q) : t, q);
+      }
+      if (acc) r = add32(r, acv, q);
+      return r;
+    }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      const u32 s0 = sq0 ? (u32)sq0[n] : 0u;
+      out[n] = fin(n, (u32)v, ax[n], add ? (u32)add[gather ? galois_src(n, g, logN) : n] : 0u, s0,
+                   sq1 ? (u32)sq1[n] : s0, acc ? (u32)acc[n] : 0u);
+    }
+    // 4 outputs n0 + u st: the operand loads of all 4 are issued before the arithmetic
+    __device__ __forceinline__ void store4(u32 n0, u32 st, const u32* v) const {
+      u32 axv[4], adv[4] = {0, 0, 0, 0}, s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0}, acv[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const u32 n = n0 + u * st;
+        axv[u] = ax[n];
+        if (add) adv[u] = (u32)add[gather ? galois_src(n, g, logN) : n];
+        if (sq0) {
+          s0[u] = (u32)sq0[n];
+          s1[u] = sq1 ? (u32)sq1[n] : s0[u];
+        }
+        if (acc) acv[u] = (u32)acc[n];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) out[n0 + u * st] = fin(n0 + u * st, v[u], axv[u], adv[u], s0[u], s1[u], acv[u]);
+    }
+  };
+  __device__ P32 bind_pipe(int blk, const PrimeD& P) const {
+    int kk, b, part, i;
+    dec(blk, kk, b, part, i);
+    const size_t LN = (size_t)a.Lc * a.N;
+    P32 r{reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N, nullptr,
+          nullptr, nullptr, nullptr, nullptr, &P, (u32)P.q, mu32_of(P), (u32)__ldg(a.Ph_mod + i),
+          (u32)__ldg(a.Pinv_mod + i), 0, a.gal[kk], a.logN, false};
+    r.pinvsh = shoup_companion32(r.pinv, r.q);
+    r.gather = a.add_gather && r.g != 1;
+    if (part < a.add_parts) r.add = a.addsrc + (size_t)b * a.add_bs + part * LN + (size_t)i * a.N;
+    const size_t o = (size_t)kk * a.out_ks + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N;
+    if (a.acc_in) r.acc = a.acc_in + o;
+    r.out = a.out + o;
+    if (a.sq_src) {
+      r.sq0 = a.sq_src + (size_t)b * a.sq_bs + (size_t)i * a.N;
+      if (part == 1) r.sq1 = r.sq0 + LN;
+    }
+    return r;
+  }
+  // fast path input = one u32 row of tb (written by JobKsSpecial's fast store); accx mode has no D
   __host__ __device__ bool pipe_ok() const { return a.accx && a.accx32 && a.K == 1; }
   __host__ __device__ const u32* raw32(int blk) const {
     const int r = blk / a.Lc;   // (kk B + b) 2 + part

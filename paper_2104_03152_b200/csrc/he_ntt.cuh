@@ -487,6 +487,103 @@ __device__ __forceinline__ void stage_row32(u32* stage, const u32* __restrict__ 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// Jobs may give the pipelined kernel a lighter binding (bind_pipe: the fast form only).
+template <class Job>
+__device__ __forceinline__ auto bind_pipe_job(const Job& j, int blk, const PrimeD& P, int)
+    -> decltype(j.bind_pipe(blk, P)) {
+  return j.bind_pipe(blk, P);
+}
+template <class Job>
+__device__ __forceinline__ auto bind_pipe_job(const Job& j, int blk, const PrimeD& P, long)
+    -> decltype(j.bind32(blk, P)) {
+  return j.bind32(blk, P);
+}
+
+// The first pass of a block reads its input straight from the staged row (no copy into sm32 and
+// no extra barrier): forward = the top bit group (the 1-bit pass at N = 2^13), inverse = bits
+// [0, R).  Ends with the barrier after which the staging buffer may be refilled.
+template <int LOGN, bool INV, bool LAZY, class JB>
+__device__ __forceinline__ void ntt32_pipe_block(const JB& jb, u32* sm, const u32* stage, u32 tid,
+                                                 const uint2* tw, u32 q) {
+  typedef NttGeomS<LOGN> G;
+  constexpr int LO = INV ? 0 : (G::NPASS - 1) * G::R;
+  constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+  auto ld = [&](u32 i) { return (u32)jb.load_raw(stage[i]); };
+  auto st = [&](u32 i, u32 v) { sm[spad32(i)] = v; };
+  ntt_pass32_io<LOGN, INV, LO, NB, LAZY>(tid, tw, q, ld, st);
+  __syncthreads();
+}
+
+// Inverse: the last pass (the top bit group) fused with the N^{-1} scaling and the job's store.
+// Thread tid's outputs are n = tid + m T (m < 2^R) exactly as in ntt32_epilogue: group gi of the
+// pass holds m = gi + k NG (k < 2^NB), so four consecutive groups give store4 runs of 4.
+template <int LOGN, bool LAZY, class JB>
+__device__ __forceinline__ void ntt32_inv_last_store(const JB& jb, const u32* sm, u32 tid, const uint2* tw, u32 q) {
+  typedef NttGeomS<LOGN> G;
+  constexpr int LO = (G::NPASS - 1) * G::R, NB = G::LOGNL - LO, E = 1 << NB, NG = 1 << (G::R - NB);
+  const uint2 ni = __ldg(tw);
+#pragma unroll
+  for (int c = 0; c < NG / 4; ++c) {
+    u32 out[E][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u32 g = tid + (4 * c + j) * G::T;   // < 2^LO, so the group's base is g
+      u32 x[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) x[k] = sm[spad32(g + (k << LO))];
+#pragma unroll
+      for (int ss = 0; ss < NB; ++ss) {
+        const int b = LO + ss, s = LOGN - 1 - b, half = 1 << ss;
+        const uint2* tws = tw + (1u << s);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (k & half) continue;
+          const uint2 w = __ldg(tws + (k >> (b + 1 - LO)));
+          if (LAZY) gs_bfly32_lazy(x[k], x[k + half], w.x, w.y, q);
+          else gs_bfly32(x[k], x[k + half], w.x, w.y, q);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < E; ++k) out[k][j] = shoup32(x[k], ni.x, ni.y, q);
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const u32 n0 = tid + (4 * c + k * NG) * G::T;
+      if constexpr (has_store4<JB>::value) {
+        jb.store4(n0, G::T, out[k]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) jb.store(n0 + u * G::T, (u64)out[k][u]);
+      }
+    }
+  }
+}
+
+// The remaining passes of a pipelined block and its epilogue.
+template <int LOGN, bool INV, class JB>
+__device__ __forceinline__ void ntt32_pipe_rest(const JB& jb, u32* sm, u32 tid, const uint2* tw, u32 q) {
+  typedef NttGeomS<LOGN> G;
+  constexpr int LO_LAST = (G::NPASS - 1) * G::R, NB_LAST = G::LOGNL - LO_LAST;
+  constexpr bool FUSE_LAST = INV && G::NPASS >= 3 && (1 << (G::R - NB_LAST)) % 4 == 0;
+  if (!INV) {
+    if (q < (1u << 30)) ntt_passes32<LOGN, false, 1, true>(sm, tid, tw, q);
+    else ntt_passes32<LOGN, false, 1, false>(sm, tid, tw, q);
+    ntt32_epilogue<LOGN, false>(jb, sm, tid, __ldg(tw), q);
+  } else if constexpr (FUSE_LAST) {
+    if (q < (1u << 30)) {
+      ntt_passes32<LOGN, true, 1, true, G::NPASS - 1>(sm, tid, tw, q);
+      ntt32_inv_last_store<LOGN, true>(jb, sm, tid, tw, q);
+    } else {
+      ntt_passes32<LOGN, true, 1, false, G::NPASS - 1>(sm, tid, tw, q);
+      ntt32_inv_last_store<LOGN, false>(jb, sm, tid, tw, q);
+    }
+  } else {
+    if (q < (1u << 30)) ntt_passes32<LOGN, true, 1, true>(sm, tid, tw, q);
+    else ntt_passes32<LOGN, true, 1, false>(sm, tid, tw, q);
+    ntt32_epilogue<LOGN, true>(jb, sm, tid, __ldg(tw), q);
+  }
+}
+
 template <int LOGN>
 struct NttGeom32Pipe {
   static constexpr int SMEM = NttGeom32<LOGN>::SMEM + (1 << LOGN) * 4;   // + staging row
@@ -507,15 +604,14 @@ k_ntt32_pipe(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict
     const PrimeD P = load_prime(primes, pi);
     const uint2* tw = tw_all + (size_t)pi * G::N;
     const u32 q = (u32)P.q;
-    const auto jb = job.bind32(blk, P);
+    const auto jb = bind_pipe_job(job, blk, P, 0);
     cp_async_wait_all();
     __syncthreads();   // staged row visible; the previous block's epilogue is done with sm32
-    for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)jb.load_raw(stage[i]);
-    __syncthreads();   // staging buffer free
+    if (q < (1u << 30)) ntt32_pipe_block<LOGN, INV, true>(jb, sm32, stage, tid, tw, q);
+    else ntt32_pipe_block<LOGN, INV, false>(jb, sm32, stage, tid, tw, q);
+    // ntt32_pipe_block synchronised once the staged row was consumed (its first pass): prefetch
     if (blk + (int)gridDim.x < nblk) stage_row32<LOGN>(stage, job.raw32(blk + gridDim.x), tid);
-    ntt_run32<LOGN, INV>(sm32, tid, tw, q);
-    const uint2 ni = __ldg(tw);
-    ntt32_epilogue<LOGN, INV>(jb, sm32, tid, ni, q);
+    ntt32_pipe_rest<LOGN, INV>(jb, sm32, tid, tw, q);
   }
 }
 

@@ -1404,6 +1404,8 @@ static KsArgs ks_base(he_context* c, int B, int Lc, const u64* ext, const u64* d
 }
 
 static void ks_launch(he_context* c, KsArgs& a) {
+  // the accx-mode ModDown (pipelined, JobKsData::P32) has no plaintext-factor epilogue
+  if (a.accx && a.D) throw HeError(HE_INVALID_ARGUMENT, "internal: plaintext factor with an accx ModDown");
   Scratch tb(c, (size_t)a.KB * a.B * 2 * a.K * a.N * 8);
   a.tb = tb.as<u64>();
   JobKsSpecial js{a};
