@@ -364,16 +364,26 @@ __device__ __forceinline__ u64 accx_word(const KsArgs& a, size_t i) {
   return a.accx32 ? (u64)reinterpret_cast<const u32*>(a.accx)[i] : a.accx[i];
 }
 
-// Inner product over digits at target limb t for source position sn.
+// Inner product over digits at target limb t for source position sn.  The products (each < q^2)
+// are summed in 128 bits and reduced once per 8 terms (q < 2^60, so 8 q^2 < 2^123 and the high
+// word stays below q): hi 2^64 + lo = [hi (2^64 mod q)]_q + [lo]_q, one Barrett product and one
+// 64-bit reduction instead of a Barrett reduction per term.
 __device__ __forceinline__ u64 ks_inner(const KsArgs& a, int kk, int b, int part, int t, int tprime,
                                         u32 sn, u32 n, const PrimeD& P) {
   const u64* key = a.keys[kk];
   u64 acc = 0;
-  for (int j = 0; j < a.Lc; ++j) {
-    const u64 x = (t == j) ? a.dsrc[(size_t)b * a.dsrc_bs + (size_t)j * a.N + sn]
-                           : a.ext[(((size_t)b * a.Lc + j) * (a.Lc + a.K) + t) * a.N + sn];
-    const u64 k = key[(((size_t)j * 2 + part) * a.NP + tprime) * a.N + n];
-    acc = add_mod(acc, mul_mod(x, k, P), P.q);
+  for (int j0 = 0; j0 < a.Lc; j0 += 8) {
+    u64 lo = 0, hi = 0;
+    const int j1 = min(a.Lc, j0 + 8);
+    for (int j = j0; j < j1; ++j) {
+      const u64 x = (t == j) ? a.dsrc[(size_t)b * a.dsrc_bs + (size_t)j * a.N + sn]
+                             : a.ext[(((size_t)b * a.Lc + j) * (a.Lc + a.K) + t) * a.N + sn];
+      const u64 k = key[(((size_t)j * 2 + part) * a.NP + tprime) * a.N + n];
+      const u64 pl = x * k, ph = __umul64hi(x, k);
+      lo += pl;
+      hi += ph + (lo < pl);
+    }
+    acc = add_mod(acc, add_mod(mul_mod(hi, P.r64, P), reduce64(lo, P), P.q), P.q);
   }
   return acc;
 }

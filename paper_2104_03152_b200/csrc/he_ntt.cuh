@@ -35,14 +35,20 @@ struct NttGeom {
   static constexpr int R = LOGNL == 14 ? HE_NTT64_R14 : (LOGNL - 10 > 4 ? LOGNL - 10 : 4);
   static constexpr int T = NL >> R;                            // threads per CTA
   // CTAs per SM the register budget is sized for (shared memory allows 3 at N=2^13)
-  static constexpr int MINB = NL <= 8192 ? 2 : 1;
+#ifndef HE_NTT64_MINB
+#define HE_NTT64_MINB 2
+#endif
+  static constexpr int MINB = NL <= 8192 ? HE_NTT64_MINB : 1;
   static constexpr int NPASS = (LOGNL + R - 1) / R;
   static constexpr int SMEM = (NL + NL / 16) * 8;
 };
 
 __device__ __forceinline__ u32 spad(u32 i) { return i + (i >> 4); }
 
-// Cooley-Tukey butterfly, inputs/outputs in [0, 4q).
+// Cooley-Tukey butterfly, inputs/outputs in [0, 4q).  (An approximate-quotient Shoup product --
+// three 32-bit high products instead of the 64x64 high product, result in [0, 4q) -- was measured
+// slower in round 2: the extra 64-bit conditional subtraction and register pressure cost more than
+// the fmaheavy cycles it saves; cfg2 forward 955 vs 999 GB/s.)
 __device__ __forceinline__ void ct_bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q, u64 two_q) {
   u64 X = x >= two_q ? x - two_q : x;
   u64 T = mul_shoup_lazy(y, w, wsh, q);
