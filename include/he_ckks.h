@@ -183,6 +183,14 @@ he_status he_encode(he_context* ctx, const double* z, size_t n_per_item, size_t 
  * still fail here. */
 he_status he_encode_device(he_context* ctx, const double* z_dev, size_t n_per_item, size_t B,
                            double scale, int level, he_plaintext** out);
+/* The float64 values he_encode rounds (a parity hook for C7: the canonical-
+ * embedding IFFT's output before round_half_away), for host z[B][n_per_item]:
+ * out[B][N] (host), out[b][i] = scale (2/N) Re(...) for i < N/2 and the
+ * imaginary parts for i >= N/2, in the coefficient order of m.  Synchronous.
+ * Same argument checks as he_encode except the 2^62 bound (values are
+ * returned, not rounded). */
+he_status he_encode_unrounded(he_context* ctx, const double* z, size_t n_per_item, size_t B, double scale,
+                              double* out);
 /* Decode the first n slots of every item into host out[B][n]: CRT compose,
  * centre, float64, FFT, divide by the plaintext's scale (C6). */
 he_status he_decode(he_context* ctx, const he_plaintext* pt, double* out, size_t n);

@@ -70,6 +70,7 @@ _SIGS = {
     "he_square_inplace": [VP, VP],
     "he_encode": [VP, DP, SZ, SZ, C.c_double, C.c_int, VPP],
     "he_encode_device": [VP, VP, SZ, SZ, C.c_double, C.c_int, VPP],
+    "he_encode_unrounded": [VP, DP, SZ, SZ, C.c_double, DP],
     "he_decode": [VP, VP, DP, SZ],
     "he_decode_device": [VP, VP, VP, SZ],
     "he_decode_async": [VP, VP, VP, SZ],
@@ -425,6 +426,14 @@ class Context:
             _check(lib().he_encode(self.h, z2.ctypes.data_as(DP), z2.shape[1], z2.shape[0], float(scale),
                                    level, C.byref(h)))
         return Plaintext(self, h)
+
+    def he_encode_unrounded(self, z, scale: float):
+        """[B][N] float64: the coefficient values he_encode rounds (C7 parity hook)."""
+        z2 = np.ascontiguousarray(np.atleast_2d(np.asarray(z, dtype=np.float64)))
+        res = np.zeros((z2.shape[0], self.N), dtype=np.float64)
+        _check(lib().he_encode_unrounded(self.h, z2.ctypes.data_as(DP), z2.shape[1], z2.shape[0], float(scale),
+                                         res.ctypes.data_as(DP)))
+        return res
 
     def he_decode(self, pt: Plaintext, n: int | None = None, out=None):
         n = self.slots if n is None else n

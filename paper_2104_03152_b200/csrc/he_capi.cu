@@ -294,6 +294,22 @@ he_status he_encode(he_context* c, const double* z, size_t n, size_t B, double s
   });
 }
 
+he_status he_encode_unrounded(he_context* c, const double* z, size_t n, size_t B, double scale, double* out) {
+  return guard([&] {
+    need_ctx(c);
+    need_out(out);
+    need(z != nullptr || n == 0, HE_INVALID_ARGUMENT, "null input");
+    need(B >= 1, HE_INVALID_ARGUMENT, "B must be >= 1");
+    need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+    need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
+    DevDoubles d(c, z, n * B);
+    Scratch pre(c, B * (size_t)c->N * 8);
+    encode_unrounded(c, d.d, n, B, scale, pre.as<double>());
+    HE_CK(cudaMemcpyAsync(out, pre.p, B * (size_t)c->N * 8, cudaMemcpyDeviceToHost, c->stream));
+    HE_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 he_status he_encode_device(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
                            he_plaintext** out) {
   return guard([&] { encode_common(c, z_dev, n, B, scale, level, out, false); });

@@ -37,6 +37,14 @@ struct has_load4 : std::false_type {};
 template <class B>
 struct has_load4<B, std::void_t<decltype(std::declval<const B&>().load4(0u))>> : std::true_type {};
 
+// Words a thread of the NTT kernels keeps in flight in its HBM-facing loops (chunks that are not
+// interleaved, so registers stay bounded).  Jobs whose per-word load / store is itself a long
+// computation (the key-switch inner products) set kIoWords lower.
+template <class J, class = void>
+struct io_words_of { static constexpr int value = 8; };
+template <class J>
+struct io_words_of<J, std::void_t<decltype(J::kIoWords)>> { static constexpr int value = J::kIoWords; };
+
 template <class Job>
 struct JobAt {
   const Job& j;
@@ -392,6 +400,7 @@ __device__ __forceinline__ u64 ks_inner(const KsArgs& a, int kk, int b, int part
 // tb = [ (x + [P/2]_{p_k}) (P/p_k)^{-1} ]_{p_k}    (C15 y_k and its CRT weight)
 struct JobKsSpecial {
   static constexpr const char* kName = "ks_special";
+  static constexpr int kIoWords = 2;   // load = an Lc-term 64-bit inner product
   KsArgs a;
   __device__ void dec(int blk, int& kk, int& b, int& part, int& k) const {
     k = blk % a.K;
@@ -471,6 +480,7 @@ struct JobKsSpecial {
 // domain), NTT, then u = (IP_i - NTT(c_i)) P^{-1} and the epilogue.
 struct JobKsData {
   static constexpr const char* kName = "ks_data";
+  static constexpr int kIoWords = 2;   // store = an Lc-term 64-bit inner product + epilogue
   KsArgs a;
   __device__ void dec(int blk, int& kk, int& b, int& part, int& i) const {
     i = blk % a.Lc;

@@ -64,21 +64,33 @@ __device__ __forceinline__ void gs_bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q, u
   y = mul_shoup_lazy(V, w, wsh, q);
 }
 
-// One pass over local bits [LO, LO+NB): each thread loads 2^NB words per
-// group (2^(R-NB) groups), runs NB stages in registers, writes them back.
-template <int LOGN, int CL, bool INV, int LO, int NB>
-__device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const ulonglong2* __restrict__ tw,
-                                         u64 q, u64 two_q) {
+// One pass over local bits [LO, LO+NB): each thread reads 2^NB words per group through ld(i)
+// (2^(R-NB) groups), runs NB stages in registers and hands them to st(i, v).  ld / st are shared
+// memory for the inner passes; the first forward pass reads the job's input straight from HBM and
+// the last inverse pass scales by N^{-1} and writes the job's output (the top bit group: both
+// coalesced, consecutive threads own consecutive indices), which saves two shared-memory round trips
+// and two barriers per transform.
+// WORDS bounds the words a thread has in flight (its groups run in chunks of max(1, WORDS / 2^NB)
+// groups, chunks not interleaved): HBM-facing passes take 8 so that all of a chunk's loads are issued
+// together without spilling; shared-memory passes are fully unrolled.
+template <int LOGN, int CL, bool INV, int LO, int NB, int WORDS = 0, class LD, class ST>
+__device__ __forceinline__ void ntt_pass_io(u32 tid, u32 gbase, const ulonglong2* __restrict__ tw, u64 q,
+                                            u64 two_q, LD ld, ST st) {
   typedef NttGeom<LOGN, CL> G;
   constexpr int NG = 1 << (G::R - NB);
   constexpr int E = 1 << NB;
+  constexpr int CH0 = WORDS > E ? WORDS / E : 1;
+  constexpr int CH = (WORDS == 0 || CH0 > NG) ? NG : CH0;
+#pragma unroll 1
+  for (int c = 0; c < NG / CH; ++c)
 #pragma unroll
-  for (int gi = 0; gi < NG; ++gi) {
+  for (int gg = 0; gg < CH; ++gg) {
+    const int gi = c * CH + gg;
     const u32 g = tid + gi * G::T;
     const u32 base = ((g >> LO) << (LO + NB)) | (g & ((1u << LO) - 1u));
     u64 x[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = sm[spad(base + (k << LO))];
+    for (int k = 0; k < E; ++k) x[k] = ld(base + (k << LO));
     // twiddle of the butterfly on bit b at index j = gbase | hi << (LO+NB) | k << LO | lo:
     // tw[2^s + (j >> (b+1))], s = LOGN-1-b, and j >> (b+1) = (gbase >> (b+1)) + (hi << (LO+NB-1-b)) +
     // (k >> (b+1-LO)): one base pointer per stage and compile-time offsets, so the butterflies of a
@@ -99,57 +111,123 @@ __device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const ulon
       }
     }
 #pragma unroll
-    for (int k = 0; k < E; ++k) sm[spad(base + (k << LO))] = x[k];
+    for (int k = 0; k < E; ++k) st(base + (k << LO), x[k]);
   }
 }
 
-// Passes over the local problem: group p covers local bits [pR, min(pR+R, LOGNL)).
-template <int LOGN, int CL, bool INV, int P>
+template <int LOGN, int CL, bool INV, int LO, int NB>
+__device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const ulonglong2* __restrict__ tw,
+                                         u64 q, u64 two_q) {
+  ntt_pass_io<LOGN, CL, INV, LO, NB>(
+      tid, gbase, tw, q, two_q, [&](u32 i) { return sm[spad(i)]; }, [&](u32 i, u64 v) { sm[spad(i)] = v; });
+}
+
+// Passes P .. PEND-1 over the local problem: pass P covers bit group GP = INV ? P : NPASS-1-P,
+// local bits [GP R, min(GP R + R, LOGNL)); each ends with a barrier.
+template <int LOGN, int CL, bool INV, int P, int PEND = NttGeom<LOGN, CL>::NPASS>
 __device__ __forceinline__ void ntt_passes(u64* sm, u32 tid, u32 gbase, const ulonglong2* tw, u64 q,
                                            u64 two_q) {
   typedef NttGeom<LOGN, CL> G;
-  constexpr int GP = INV ? P : G::NPASS - 1 - P;  // forward runs top-down
-  constexpr int LO = GP * G::R;
-  constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-  ntt_pass<LOGN, CL, INV, LO, NB>(sm, tid, gbase, tw, q, two_q);
-  __syncthreads();
-  if constexpr (P + 1 < G::NPASS) ntt_passes<LOGN, CL, INV, P + 1>(sm, tid, gbase, tw, q, two_q);
-}
-
-// Cross-CTA stage (bit LOGN-1) of the 2-CTA cluster transform, through DSMEM.
-template <int LOGN, bool INV>
-__device__ __forceinline__ void ntt_cross_stage(u64* sm, u32 tid, const ulonglong2* tw, u64 q, u64 two_q) {
-  namespace cg = cooperative_groups;
-  typedef NttGeom<LOGN, 2> G;
-  cg::cluster_group cl = cg::this_cluster();
-  const u32 rank = cl.block_rank();
-  u64* s0 = cl.map_shared_rank(sm, 0);
-  u64* s1 = cl.map_shared_rank(sm, 1);
-  const ulonglong2 tw1 = __ldg(tw + 1);
-  const u64 w = tw1.x, wsh = tw1.y;
-  for (u32 i = rank * (G::NL / 2) + tid; i < (rank + 1) * (G::NL / 2); i += G::T) {
-    u64 x = s0[spad(i)], y = s1[spad(i)];
-    if (!INV) ct_bfly(x, y, w, wsh, q, two_q);
-    else gs_bfly(x, y, w, wsh, q, two_q);
-    s0[spad(i)] = x;
-    s1[spad(i)] = y;
+  if constexpr (P < PEND) {
+    constexpr int GP = INV ? P : G::NPASS - 1 - P;  // forward runs top-down
+    constexpr int LO = GP * G::R;
+    constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+    ntt_pass<LOGN, CL, INV, LO, NB>(sm, tid, gbase, tw, q, two_q);
+    __syncthreads();
+    ntt_passes<LOGN, CL, INV, P + 1, PEND>(sm, tid, gbase, tw, q, two_q);
   }
 }
 
+// Cluster barrier halves (release / acquire): a CTA must not exit while its peer still reads its
+// shared memory, and remote stores must be visible before the peer's next pass.
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::); }
 __device__ __forceinline__ void cluster_sync_all() {
+  cluster_arrive();
+  cluster_wait();
+}
+
+// Forward cross-CTA stage (bit LOGN-1) of the 2-CTA cluster transform fused with the job's loads:
+// CTA r owns the pairs (i, i + NL), i in [r NL/2, (r+1) NL/2); every load of a thread is issued
+// before the first butterfly, the two outputs go to local index i of CTA 0 and CTA 1 (DSMEM).
+template <int LOGN, class Job>
+__device__ __forceinline__ void ntt_cross_load(const Job& job, int blk, const PrimeD& P, u64* sm, u32 tid,
+                                               u32 rank, const ulonglong2* tw) {
   namespace cg = cooperative_groups;
-  cg::this_cluster().sync();
+  typedef NttGeom<LOGN, 2> G;
+  constexpr int PAIRS = G::NL / 2 / G::T;
+  cg::cluster_group cl = cg::this_cluster();
+  u64* s0 = cl.map_shared_rank(sm, 0);
+  u64* s1 = cl.map_shared_rank(sm, 1);
+  constexpr int W2 = io_words_of<Job>::value / 2 > 0 ? io_words_of<Job>::value / 2 : 1;
+  constexpr int CH = PAIRS < W2 ? PAIRS : W2;   // io_words_of<Job> words in flight per chunk
+  const ulonglong2 tw1 = __ldg(tw + 1);
+#pragma unroll 1
+  for (int c = 0; c < PAIRS / CH; ++c) {
+    u64 x[CH], y[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const u32 i = rank * (G::NL / 2) + tid + (c * CH + k) * G::T;
+      x[k] = job.load(blk, i, P);
+      y[k] = job.load(blk, i + G::NL, P);
+    }
+    if (c == 0) cluster_wait();   // the peer CTA is running (its shared memory exists): arrived at entry
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const u32 i = rank * (G::NL / 2) + tid + (c * CH + k) * G::T;
+      ct_bfly(x[k], y[k], tw1.x, tw1.y, P.q, P.two_q);
+      s0[spad(i)] = x[k];
+      s1[spad(i)] = y[k];
+    }
+  }
+}
+
+// Inverse cross-CTA stage fused with the N^{-1} scaling and the job's stores (global indices i and
+// i + NL).  Arrives on the cluster barrier once the peer's shared memory has been read.
+template <int LOGN, class Job>
+__device__ __forceinline__ void ntt_cross_store(const Job& job, int blk, const PrimeD& P, u64* sm, u32 tid,
+                                                u32 rank, const ulonglong2* tw) {
+  namespace cg = cooperative_groups;
+  typedef NttGeom<LOGN, 2> G;
+  constexpr int PAIRS = G::NL / 2 / G::T;
+  cg::cluster_group cl = cg::this_cluster();
+  const u64* s0 = cl.map_shared_rank(sm, 0);
+  const u64* s1 = cl.map_shared_rank(sm, 1);
+  const ulonglong2 tw1 = __ldg(tw + 1);
+  u64 x[PAIRS], y[PAIRS];
+#pragma unroll
+  for (int k = 0; k < PAIRS; ++k) {
+    const u32 i = rank * (G::NL / 2) + tid + k * G::T;
+    x[k] = s0[spad(i)];
+    y[k] = s1[spad(i)];
+  }
+  cluster_arrive();
+#pragma unroll
+  for (int k = 0; k < PAIRS; ++k) {
+    const u32 i = rank * (G::NL / 2) + tid + k * G::T;
+    gs_bfly(x[k], y[k], tw1.x, tw1.y, P.q, P.two_q);
+    job.store(blk, i, mul_shoup(x[k], P.ninv, P.ninvsh, P.q), P);
+    job.store(blk, i + G::NL, mul_shoup(y[k], P.ninv, P.ninvsh, P.q), P);
+  }
 }
 
 // Generic batched transform.  Job provides:
 //   int  prime(int blk)                           absolute prime index of limb blk
 //   u64  load(int blk, u32 i, const PrimeD&)      canonical input word i (natural index)
 //   void store(int blk, u32 i, u64 v, const PrimeD&)  canonical output word i
-// blk = blockIdx.x / CL.
+// blk = blockIdx.x / CL.  The launch uses exactly G::T threads, so every per-thread loop has a
+// compile-time trip count and is unrolled: all of a thread's HBM loads are in flight together
+// (round 2: the rolled loops serialised one DRAM latency per word).
+//   forward:  [CL=2: loads + cross stage -> DSMEM]  or  [CL=1: loads + top pass]  -> shared passes
+//             -> reduce + store (shared memory read back in coalesced order)
+//   inverse:  coalesced loads -> shared passes -> [CL=1: top pass + N^{-1} + store]
+//             or [CL=2: cross stage + N^{-1} + store]
 template <int LOGN, int CL, bool INV, class Job>
 __global__ void __launch_bounds__(NttGeom<LOGN, CL>::T, NttGeom<LOGN, CL>::MINB)
 k_ntt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __restrict__ tw_all) {
   typedef NttGeom<LOGN, CL> G;
+  constexpr int PER = G::NL / G::T;
+  constexpr int LO_TOP = (G::NPASS - 1) * G::R, NB_TOP = G::LOGNL - LO_TOP;
   extern __shared__ u64 sm[];
   const u32 tid = threadIdx.x;
   const int blk = blockIdx.x / CL;
@@ -158,27 +236,53 @@ k_ntt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __restrict__
   const int pi = job.prime(blk);
   const PrimeD P = load_prime(primes, pi);
   const ulonglong2* tw = tw_all + (size_t)pi * G::N;
-  for (u32 i = tid; i < G::NL; i += G::T) sm[spad(i)] = job.load(blk, gbase + i, P);
-  if (CL == 2) cluster_sync_all(); else __syncthreads();
-  if (CL == 2 && !INV) {
-    ntt_cross_stage<LOGN, false>(sm, tid, tw, P.q, P.two_q);
-    cluster_sync_all();
-  }
-  ntt_passes<LOGN, CL, INV, 0>(sm, tid, gbase, tw, P.q, P.two_q);
-  if (CL == 2 && INV) {
-    cluster_sync_all();
-    ntt_cross_stage<LOGN, true>(sm, tid, tw, P.q, P.two_q);
-    cluster_sync_all();
-  }
-  for (u32 i = tid; i < G::NL; i += G::T) {
-    u64 v = sm[spad(i)];
-    if (!INV) {
+  auto sld = [&](u32 i) { return sm[spad(i)]; };
+  auto sst = [&](u32 i, u64 v) { sm[spad(i)] = v; };
+  if constexpr (!INV) {
+    if constexpr (CL == 2) {
+      cluster_arrive();
+      ntt_cross_load<LOGN>(job, blk, P, sm, tid, rank, tw);
+      cluster_sync_all();
+      ntt_passes<LOGN, CL, false, 0>(sm, tid, gbase, tw, P.q, P.two_q);
+    } else {
+      ntt_pass_io<LOGN, CL, false, LO_TOP, NB_TOP, io_words_of<Job>::value>(
+          tid, gbase, tw, P.q, P.two_q, [&](u32 i) { return job.load(blk, i, P); }, sst);
+      __syncthreads();
+      ntt_passes<LOGN, CL, false, 1>(sm, tid, gbase, tw, P.q, P.two_q);
+    }
+    constexpr int CS = PER < io_words_of<Job>::value ? PER : io_words_of<Job>::value;
+#pragma unroll 1
+    for (int c = 0; c < PER / CS; ++c)
+#pragma unroll
+    for (int kk = 0; kk < CS; ++kk) {
+      const u32 i = tid + (c * CS + kk) * G::T;
+      u64 v = sm[spad(i)];
       v = v >= P.two_q ? v - P.two_q : v;
       v = v >= P.q ? v - P.q : v;
-    } else {
-      v = mul_shoup(v, P.ninv, P.ninvsh, P.q);
+      job.store(blk, gbase + i, v, P);
     }
-    job.store(blk, gbase + i, v, P);
+  } else {
+    constexpr int CH = PER < io_words_of<Job>::value ? PER : io_words_of<Job>::value;
+#pragma unroll 1
+    for (int c = 0; c < PER / CH; ++c) {
+      u64 v[CH];
+#pragma unroll
+      for (int k = 0; k < CH; ++k) v[k] = job.load(blk, gbase + tid + (c * CH + k) * G::T, P);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) sm[spad(tid + (c * CH + k) * G::T)] = v[k];
+    }
+    __syncthreads();
+    if constexpr (CL == 2) {
+      ntt_passes<LOGN, CL, true, 0>(sm, tid, gbase, tw, P.q, P.two_q);
+      cluster_sync_all();
+      ntt_cross_store<LOGN>(job, blk, P, sm, tid, rank, tw);
+      cluster_wait();   // the peer has read this CTA's shared memory
+    } else {
+      ntt_passes<LOGN, CL, true, 0, G::NPASS - 1>(sm, tid, gbase, tw, P.q, P.two_q);
+      ntt_pass_io<LOGN, CL, true, LO_TOP, NB_TOP, io_words_of<Job>::value>(
+          tid, gbase, tw, P.q, P.two_q, sld,
+          [&](u32 i, u64 v) { job.store(blk, i, mul_shoup(v, P.ninv, P.ninvsh, P.q), P); });
+    }
   }
 }
 
@@ -195,18 +299,28 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __r
   const int blk = blockIdx.x;
   const int pi = job.prime(blk);
   const PrimeD P = load_prime(primes, pi);
-  for (u32 i = tid; i < G::NL; i += G::T) sm[spad(i)] = job.load(blk, i, P);
+  constexpr int PER = G::NL / G::T;
+  constexpr int LO_TOP = (G::NPASS - 1) * G::R, NB_TOP = G::LOGNL - LO_TOP;
+  const ulonglong2* tw = tw_all + (size_t)pi * G::N;
+  const ulonglong2* itw = itw_all + (size_t)pi * G::N;
+  ntt_pass_io<LOGN, 1, false, LO_TOP, NB_TOP, 8>(
+      tid, 0, tw, P.q, P.two_q, [&](u32 i) { return job.load(blk, i, P); },
+      [&](u32 i, u64 v) { sm[spad(i)] = v; });
   __syncthreads();
-  ntt_passes<LOGN, 1, false, 0>(sm, tid, 0, tw_all + (size_t)pi * G::N, P.q, P.two_q);
-  for (u32 i = tid; i < G::NL; i += G::T) {
+  ntt_passes<LOGN, 1, false, 1>(sm, tid, 0, tw, P.q, P.two_q);
+#pragma unroll 4
+  for (int k = 0; k < PER; ++k) {
+    const u32 i = tid + k * G::T;
     u64 v = sm[spad(i)];
     v = v >= P.two_q ? v - P.two_q : v;
     v = v >= P.q ? v - P.q : v;
     sm[spad(i)] = mul_mod(v, job.factor(blk, i, P), P);
   }
   __syncthreads();
-  ntt_passes<LOGN, 1, true, 0>(sm, tid, 0, itw_all + (size_t)pi * G::N, P.q, P.two_q);
-  for (u32 i = tid; i < G::NL; i += G::T) job.store(blk, i, mul_shoup(sm[spad(i)], P.ninv, P.ninvsh, P.q), P);
+  ntt_passes<LOGN, 1, true, 0, G::NPASS - 1>(sm, tid, 0, itw, P.q, P.two_q);
+  ntt_pass_io<LOGN, 1, true, LO_TOP, NB_TOP, 8>(
+      tid, 0, itw, P.q, P.two_q, [&](u32 i) { return sm[spad(i)]; },
+      [&](u32 i, u64 v) { job.store(blk, i, mul_shoup(v, P.ninv, P.ninvsh, P.q), P); });
 }
 
 // ===================================================== 32-bit arithmetic ===
@@ -216,6 +330,10 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __r
 // (2q < 2^32, but 4q may not be).  Twiddle table entries are (w, floor(w 2^32 / q));
 // entry 0 of the inverse table holds (N^{-1}, its companion).
 __device__ __forceinline__ u32 spad32(u32 i) { return i + (i >> 5); }
+// words a thread keeps in flight in the HBM-facing loops of the 32-bit engine (chunks, as ntt_pass_io)
+#ifndef NTT32_IO_WORDS
+#define NTT32_IO_WORDS 8
+#endif
 
 // Geometry of the 32-bit engine: 2^R words per thread, T = N / 2^R threads, NPASS passes of R bits.
 // Measured at N = 2^13 (profiles/r01_ncu_summary.md): R = 4 with 3 CTAs/SM is the best of R 4/5 x
@@ -273,13 +391,18 @@ __device__ __forceinline__ void gs_bfly32_lazy(u32& x, u32& y, u32 w, u32 wsh, u
 // outputs through st(i, v): shared memory for the inner passes; the job's
 // load (first forward pass) or the final scaling + store (last inverse pass)
 // when fused, which saves a shared-memory round trip and a barrier.
-template <int LOGN, bool INV, int LO, int NB, bool LAZY, class LD, class ST>
+template <int LOGN, bool INV, int LO, int NB, bool LAZY, int WORDS = 0, class LD, class ST>
 __device__ __forceinline__ void ntt_pass32_io(u32 tid, const uint2* __restrict__ tw, u32 q, LD ld, ST st) {
   typedef NttGeomS<LOGN> G;
   constexpr int NG = 1 << (G::R - NB);
   constexpr int E = 1 << NB;
+  constexpr int CH0 = WORDS > E ? WORDS / E : 1;   // groups per chunk (as ntt_pass_io)
+  constexpr int CH = (WORDS == 0 || CH0 > NG) ? NG : CH0;
+#pragma unroll 1
+  for (int c = 0; c < NG / CH; ++c)
 #pragma unroll
-  for (int gi = 0; gi < NG; ++gi) {
+  for (int gg = 0; gg < CH; ++gg) {
+    const int gi = c * CH + gg;
     const u32 g = tid + gi * G::T;
     const u32 base = ((g >> LO) << (LO + NB)) | (g & ((1u << LO) - 1u));
     u32 x[E];
@@ -370,17 +493,17 @@ __device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, 
 
 // Forward transform whose first pass reads the input through ld(i) (no staging
 // of the input in shared memory); result left in sm (lazy range when q < 2^30).
-template <int LOGN, class LD>
+template <int LOGN, int WORDS = NTT32_IO_WORDS, class LD>
 __device__ __forceinline__ void ntt_fwd32_from(u32* sm, u32 tid, const uint2* tw, u32 q, LD ld) {
   typedef NttGeomS<LOGN> G;
   constexpr int LO = (G::NPASS - 1) * G::R, NB = G::LOGNL - LO;
   auto st = [&](u32 i, u32 v) { sm[spad32(i)] = v; };
   if (q < (1u << 30)) {
-    ntt_pass32_io<LOGN, false, LO, NB, true>(tid, tw, q, ld, st);
+    ntt_pass32_io<LOGN, false, LO, NB, true, WORDS>(tid, tw, q, ld, st);
     __syncthreads();
     ntt_passes32<LOGN, false, 1, true>(sm, tid, tw, q);
   } else {
-    ntt_pass32_io<LOGN, false, LO, NB, false>(tid, tw, q, ld, st);
+    ntt_pass32_io<LOGN, false, LO, NB, false, WORDS>(tid, tw, q, ld, st);
     __syncthreads();
     ntt_passes32<LOGN, false, 1, false>(sm, tid, tw, q);
   }
@@ -421,8 +544,11 @@ __device__ __forceinline__ u32 ntt_reduce32(u32 v, u32 q) {
 template <int LOGN, bool INV, class JB>
 __device__ __forceinline__ void ntt32_epilogue(const JB& jb, const u32* sm, u32 tid, uint2 ni, u32 q) {
   typedef NttGeomS<LOGN> G;
-  if constexpr (has_store4<JB>::value && (G::NL / G::T) % 4 == 0) {
-    for (u32 i0 = tid; i0 < G::NL; i0 += 4 * G::T) {
+  constexpr int PER = G::NL / G::T;   // the launch has exactly T threads: unrolled, loads batched
+  if constexpr (has_store4<JB>::value && PER % 4 == 0) {
+#pragma unroll 2
+    for (int c = 0; c < PER / 4; ++c) {
+      const u32 i0 = tid + 4 * c * G::T;
       u32 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -432,7 +558,9 @@ __device__ __forceinline__ void ntt32_epilogue(const JB& jb, const u32* sm, u32 
       jb.store4(i0, G::T, v);
     }
   } else {
-    for (u32 i = tid; i < G::NL; i += G::T) {
+#pragma unroll 4
+    for (int k = 0; k < PER; ++k) {
+      const u32 i = tid + k * G::T;
       u32 v = sm[spad32(i)];
       v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
       jb.store(i, (u64)v);
@@ -448,35 +576,6 @@ struct NttGeom32 {
 #endif
   static constexpr int MINB = (1 << LOGN) <= 8192 ? HE_NTT32_MINB : 2;   // 3 CTAs/SM at N = 2^13 (2: -17%)
 };
-
-template <int LOGN, bool INV, class Job>
-__global__ void __launch_bounds__(NttGeomS<LOGN>::T, NttGeom32<LOGN>::MINB)
-k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all) {
-  typedef NttGeomS<LOGN> G;
-  extern __shared__ u32 sm32[];
-  const u32 tid = threadIdx.x;
-  const int blk = blockIdx.x;
-  const int pi = job.prime(blk);
-  const PrimeD P = load_prime(primes, pi);
-  const uint2* tw = tw_all + (size_t)pi * G::N;
-  const u32 q = (u32)P.q;
-  const auto jb = bind_job(job, blk, P, 0);   // block decomposition + constants, once per CTA
-  if constexpr (has_load4<decltype(jb)>::value) {   // 4 consecutive words per call (shared draws)
-    for (u32 j = tid; j < G::NL / 4; j += G::T) {
-      const uint4 v = jb.load4(j);
-      sm32[spad32(4 * j)] = v.x;
-      sm32[spad32(4 * j + 1)] = v.y;
-      sm32[spad32(4 * j + 2)] = v.z;
-      sm32[spad32(4 * j + 3)] = v.w;
-    }
-  } else {
-    for (u32 i = tid; i < G::NL; i += G::T) sm32[spad32(i)] = (u32)jb.load(i);
-  }
-  __syncthreads();
-  ntt_run32<LOGN, INV>(sm32, tid, tw, q);
-  const uint2 ni = __ldg(tw);
-  ntt32_epilogue<LOGN, INV>(jb, sm32, tid, ni, q);
-}
 
 // ---- pipelined persistent variant (jobs with a single u32 input row: raw32 / load_raw) ----------
 // Each CTA loops over job blocks blk = blockIdx.x, blockIdx.x + gridDim.x, ...; while block k's
@@ -588,6 +687,63 @@ __device__ __forceinline__ void ntt32_pipe_rest(const JB& jb, u32* sm, u32 tid, 
     else ntt_passes32<LOGN, true, 1, false>(sm, tid, tw, q);
     ntt32_epilogue<LOGN, true>(jb, sm, tid, __ldg(tw), q);
   }
+}
+
+template <int LOGN, bool INV, class Job>
+__global__ void __launch_bounds__(NttGeomS<LOGN>::T, NttGeom32<LOGN>::MINB)
+k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw_all) {
+  typedef NttGeomS<LOGN> G;
+  extern __shared__ u32 sm32[];
+  const u32 tid = threadIdx.x;
+  const int blk = blockIdx.x;
+  const int pi = job.prime(blk);
+  const PrimeD P = load_prime(primes, pi);
+  const uint2* tw = tw_all + (size_t)pi * G::N;
+  const u32 q = (u32)P.q;
+  const auto jb = bind_job(job, blk, P, 0);   // block decomposition + constants, once per CTA
+  constexpr int PER = G::NL / G::T;            // the launch has exactly T threads: unrolled loops
+  if constexpr (has_load4<decltype(jb)>::value) {   // 4 consecutive words per call (shared draws)
+#pragma unroll 2
+    for (int k = 0; k < PER / 4; ++k) {
+      const u32 j = tid + k * G::T;
+      const uint4 v = jb.load4(j);
+      sm32[spad32(4 * j)] = v.x;
+      sm32[spad32(4 * j + 1)] = v.y;
+      sm32[spad32(4 * j + 2)] = v.z;
+      sm32[spad32(4 * j + 3)] = v.w;
+    }
+    __syncthreads();
+    ntt_run32<LOGN, INV>(sm32, tid, tw, q);
+  } else if constexpr (!INV) {
+    // first pass (the top bit group: coalesced) straight from the job's loads
+    ntt_fwd32_from<LOGN, io_words_of<Job>::value>(sm32, tid, tw, q, [&](u32 i) { return (u32)jb.load(i); });
+  } else {
+    constexpr int CH = PER < io_words_of<Job>::value ? PER : io_words_of<Job>::value;
+#pragma unroll 1
+    for (int c = 0; c < PER / CH; ++c) {
+      u32 v[CH];
+#pragma unroll
+      for (int k = 0; k < CH; ++k) v[k] = (u32)jb.load(tid + (c * CH + k) * G::T);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) sm32[spad32(tid + (c * CH + k) * G::T)] = v[k];
+    }
+    __syncthreads();
+    constexpr int NB_LAST = G::LOGNL - (G::NPASS - 1) * G::R;
+    if constexpr (G::NPASS >= 3 && (1 << (G::R - NB_LAST)) % 4 == 0) {
+      // last pass (the top bit group: coalesced) fused with N^{-1} and the job's store
+      if (q < (1u << 30)) {
+        ntt_passes32<LOGN, true, 0, true, G::NPASS - 1>(sm32, tid, tw, q);
+        ntt32_inv_last_store<LOGN, true>(jb, sm32, tid, tw, q);
+      } else {
+        ntt_passes32<LOGN, true, 0, false, G::NPASS - 1>(sm32, tid, tw, q);
+        ntt32_inv_last_store<LOGN, false>(jb, sm32, tid, tw, q);
+      }
+      return;
+    }
+    ntt_run32<LOGN, INV>(sm32, tid, tw, q);
+  }
+  const uint2 ni = __ldg(tw);
+  ntt32_epilogue<LOGN, INV>(jb, sm32, tid, ni, q);
 }
 
 template <int LOGN>

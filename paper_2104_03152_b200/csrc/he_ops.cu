@@ -1059,7 +1059,8 @@ __device__ void fft_inplace(double2* buf, int M, const double* __restrict__ w, d
 
 __global__ void k_encode_fft(const double* __restrict__ z, size_t n, double scale, i64* __restrict__ m_out,
                              int* overflow, const int* __restrict__ slot_index, const double* __restrict__ w,
-                             const double* __restrict__ zeta, int N, int logM, double2* gscratch) {
+                             const double* __restrict__ zeta, int N, int logM, double2* gscratch,
+                             double* __restrict__ pre_out = nullptr) {
   extern __shared__ double2 fbuf[];
   const int M = N / 2;
   const int b = blockIdx.x;
@@ -1076,6 +1077,10 @@ __global__ void k_encode_fft(const double* __restrict__ z, size_t n, double scal
     const double zr = zeta[2 * i], zi = -zeta[2 * i + 1];  // zeta^{-i}
     const double2 v = buf[i];
     const double re = c * (v.x * zr - v.y * zi), im = c * (v.x * zi + v.y * zr);
+    if (pre_out) {   // he_encode_unrounded: the values this kernel rounds
+      pre_out[(size_t)b * N + i] = re;
+      pre_out[(size_t)b * N + i + M] = im;
+    }
     if (!(fabs(re) < lim) || !(fabs(im) < lim)) {
       atomicOr(overflow, 1);
       m_out[(size_t)b * N + i] = 0;
@@ -2237,6 +2242,22 @@ he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, dou
   he_plaintext* pt = pt_new(c, (int)B, level, scale, qp);
   signed_to_ntt(c, m.as<i64>(), pt->d, B, pt_limbs(pt), level + 1);
   return pt;
+}
+
+// The encode kernel's coefficient values before rounding (he_encode_unrounded).
+void encode_unrounded(he_context* c, const double* z_dev, size_t n, size_t B, double scale, double* pre_dev) {
+  const int N = c->N, M = N / 2, logM = c->logN - 1;
+  Scratch m(c, B * N * 8), flag(c, 4);
+  HE_CK(cudaMemsetAsync(flag.p, 0, 4, c->stream));
+  const bool in_smem = M <= 8192;
+  Scratch g(c, in_smem ? 8 : B * M * 16);
+  const int smem = in_smem ? M * 16 : 0;
+  if (smem > 48 * 1024)
+    smem_limit_once((const void*)k_encode_fft, smem);
+  k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m.as<i64>(), flag.as<int>(),
+                                                      c->d_slot_index, c->d_fft_w, c->d_zeta, N, logM,
+                                                      in_smem ? nullptr : g.as<double2>(), pre_dev);
+  check_launch(c);
 }
 
 he_plaintext* pt_from_int(he_context* c, const i64* m_dev, size_t B, double scale, int level, int qp) {

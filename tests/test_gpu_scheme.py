@@ -71,15 +71,23 @@ def test_encode_within_C7_and_injection_exact(cfg1, scale_log2, n):
     scale = 2.0 ** scale_log2
     pt = g.he_encode(z, scale, 2)
     w = pt.words()
+    pre_g = g.he_encode_unrounded(z, scale)   # the device's values before rounding (C7 hook)
     for b in range(3):
         pre, m = o.encode_coeffs(z[b], scale)
+        # north_star: float64 encode within 1e-9 relative (to the coefficient vector's max-norm,
+        # the scale at which a float64 FFT's error is defined)
+        nrm = max(1.0, float(np.max(np.abs(pre))))
+        assert np.max(np.abs(pre_g[b] - pre)) <= 1e-9 * nrm
         # GPU integers: centred limb-0 residues of its own encoding
         c0 = o.intt(0, w[b, 0]).astype(object)
         q0 = o.q[0]
         mg = np.array([int(x) - q0 if int(x) > q0 // 2 else int(x) for x in c0], dtype=np.float64)
-        # every GPU integer rounds a value within 1e-9 (relative) of the oracle's pre-rounding value
-        assert np.all(np.abs(mg - pre) <= 0.5 + 1e-9 * np.maximum(np.abs(pre), 1.0) * 64)
-        assert np.mean(mg == m) > 0.999
+        # ... are exactly its pre-rounding values rounded half away from zero (C7)
+        assert np.array_equal(mg, np.sign(pre_g[b]) * np.floor(np.abs(pre_g[b]) + 0.5))
+        # ... and equal the oracle's integers except where the oracle's value is within the
+        # 1e-9 tolerance of a rounding tie
+        tie = np.abs(np.abs(pre - np.trunc(pre)) - 0.5) <= 1e-9 * nrm
+        assert np.array_equal(mg[~tie], m[~tie].astype(np.float64))
         # injection of the oracle's integers reproduces its plaintext words exactly
         inj = g.he_pt_from_int_coeffs(m, scale, 2).words()[0]
         assert np.array_equal(inj, o.coeffs_to_pt(m, 2, scale).words)
