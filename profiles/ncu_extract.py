@@ -1,6 +1,6 @@
 """Key metrics of every kernel in an ncu --set full report (ncu -i ... --page raw --csv).
 
-    python profiles/ncu_extract.py report.ncu-rep [--json out.json]
+    python profiles/ncu_extract.py report.ncu-rep|raw.csv [--json out.json]
 
 Prints duration, DRAM/L2 traffic, issue and pipe utilisations, the per-pipe warp-instruction counts
 (sm__inst_executed_pipe_*.sum, the instruction mix the ALU roofline of bench.py uses) and the top
@@ -21,6 +21,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
         "lts__t_bytes.sum.per_second", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -38,7 +41,10 @@ def num(v):
 
 def main():
     rep = sys.argv[1]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):   # an exported raw page (ncu -i rep --page raw --csv > x.csv)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
