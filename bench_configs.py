@@ -30,6 +30,41 @@ def cfg1_latency(stream, timer):
         y = run()[0]
         res["lazy_moddown" if lazy else "per_rotation_moddown"] = {
             "latency_ms": round(s * 1e3, 3), "max_abs_err_vs_xW": float(np.max(np.abs(y - x @ W)))}
+    # the same calls with device-resident input / output (pinned host copies inside the timed region),
+    # eager, and recorded once as a CUDA graph (he_graph_*) and replayed: batch-1 latency is launch-bound
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    D, _ = c.he_vec_mat_encode(W, None, False, 0, lvl, 2.0 ** 40, lazy=False)
+    z_pin = torch.from_numpy(xs[None].copy()).pin_memory()
+    o_pin = torch.empty((1, 10), dtype=torch.float64).pin_memory()
+    z_dev = torch.empty((1, c.slots), dtype=torch.float64, device=dev)
+    out = torch.empty((1, 10), dtype=torch.float64, device=dev)
+
+    def calls():
+        ct = c.he_encrypt(c.he_encode(z_dev, 2.0 ** 40, lvl), 0)
+        c.he_decode(c.he_decrypt(c.he_vec_mat_pt(ct, D)), 10, out=out)
+
+    def io(body):
+        def f():
+            with torch.cuda.stream(stream):
+                z_dev.copy_(z_pin, non_blocking=True)
+            body()
+            with torch.cuda.stream(stream):
+                o_pin.copy_(out, non_blocking=True)
+        return f
+    s_eager = timer(io(calls), reps=20)
+    n0 = c.he_launch_count()
+    calls()
+    n_eager = c.he_launch_count() - n0
+    c.he_graph_begin()
+    calls()
+    g = c.he_graph_end()
+    s_graph = timer(io(g.launch), reps=20)
+    torch.cuda.synchronize()
+    res["device_io_eager"] = {"latency_ms": round(s_eager * 1e3, 3), "kernels": n_eager}
+    res["device_io_cuda_graph"] = {"latency_ms": round(s_graph * 1e3, 3), "kernels": g.kernels,
+                                   "max_abs_err_vs_xW": float(np.max(np.abs(o_pin.numpy()[0] - x @ W)))}
+    g.free()
     res["shape"] = "N=8192 [60,40,40,60] scale 2^40, x 64 replicated, W 64x10, batch 1 (encode..decode)"
     return res
 

@@ -84,6 +84,7 @@ enum {
 typedef struct he_context he_context;
 typedef struct he_plaintext he_plaintext;
 typedef struct he_ciphertext he_ciphertext;
+typedef struct he_graph he_graph;
 
 /* Parameters (SURVEY.md §8(b) "Context/keys").
  *   log2N      ring degree exponent, 10..15 (N = 1024..32768).
@@ -475,8 +476,39 @@ he_status he_profile_enable(he_context* ctx, int on);
 he_status he_profile_read(he_context* ctx, char* buf, size_t len);
 
 /* Number of kernels this library has launched on ctx (for the bench's
- * gpu_launches claim). */
+ * gpu_launches claim; a he_graph_launch adds the kernels its graph holds). */
 uint64_t he_launch_count(const he_context* ctx);
+
+/* ---- CUDA-graph recording of a call sequence (batch-1 latency) --------- */
+/* A batch-1 evaluation (e.g. BASELINE config 1: encode, encrypt, vec_mat,
+ * decrypt, decode) is a few dozen short kernels whose launch overhead is most
+ * of its latency.  he_graph_begin starts recording every library call made on
+ * ctx (stream capture, relaxed mode, of a private stream that first waits for
+ * ctx's stream); the calls then enqueue nothing and only record.  Device
+ * memory any recorded call allocates (outputs and scratch) is owned by the
+ * graph: it is never handed to other work while the graph exists, so every
+ * replay writes the same addresses, and the handles returned during recording
+ * stay valid and hold the last replay's results (freeing them is allowed and
+ * deferred).  Blocks freed during recording that existed before it are
+ * released at he_graph_free.  Inputs the sequence reads (device buffers such as
+ * he_encode_device's z_dev, plaintexts, keys) must stay alive and may be
+ * rewritten between replays.  A recorded he_encrypt draws the same Philox
+ * stream on every replay (same randomness): record the server part only when
+ * fresh encryption randomness matters.
+ * Errors: he_graph_begin fails with HE_INVALID_ARGUMENT when ctx is already
+ * recording or profiling; calls that read back to the host (host-output
+ * decode, he_sync, exports) fail while recording (HE_CUDA_ERROR) and leave
+ * the recording unusable: he_graph_end then fails and releases what was
+ * recorded.  he_set_stream fails while recording. */
+he_status he_graph_begin(he_context* ctx);
+he_status he_graph_end(he_context* ctx, he_graph** out);
+/* Enqueue one replay on ctx's current stream (asynchronous). */
+he_status he_graph_launch(he_graph* g);
+/* Number of kernel launches one replay performs. */
+uint64_t he_graph_kernels(const he_graph* g);
+/* Release the graph and the memory it owns (handles created during recording
+ * must not be used afterwards; freeing them later is a no-op). */
+he_status he_graph_free(he_graph* g);
 
 #ifdef __cplusplus
 }

@@ -138,11 +138,16 @@ _SIGS = {
     "he_modmul": [VP, VP, VP, VP, SZ, C.c_int],
     "he_ntt_mul_intt": [VP, VP, VP, VP, SZ, C.c_int],
     "he_launch_count": [VP],
+    "he_graph_begin": [VP],
+    "he_graph_end": [VP, VPP],
+    "he_graph_launch": [VP],
+    "he_graph_kernels": [VP],
+    "he_graph_free": [VP],
     "he_profile_enable": [VP, C.c_int],
     "he_profile_read": [VP, C.c_char_p, SZ],
     "he_last_error": [],
 }
-_RESTYPES = {"he_key_words": C.c_size_t, "he_launch_count": C.c_uint64, "he_last_error": C.c_char_p}
+_RESTYPES = {"he_key_words": C.c_size_t, "he_launch_count": C.c_uint64, "he_graph_kernels": C.c_uint64, "he_last_error": C.c_char_p}
 
 _lib = None
 
@@ -184,6 +189,31 @@ def _is_dev(a) -> int:
 
 
 # ---------------------------------------------------------------- handles ---
+class Graph:
+    """A recorded call sequence (he_graph_*): launch() enqueues one replay on the context stream."""
+
+    def __init__(self, ctx, h):
+        self.ctx, self.h = ctx, h
+
+    def launch(self) -> None:
+        _check(lib().he_graph_launch(self.h))
+
+    @property
+    def kernels(self) -> int:
+        return int(lib().he_graph_kernels(self.h))
+
+    def free(self) -> None:
+        if self.h:
+            _check(lib().he_graph_free(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Plaintext:
     def __init__(self, ctx: "Context", h):
         self.ctx, self.h = ctx, h
@@ -342,6 +372,15 @@ class Context:
 
     def he_launch_count(self) -> int:
         return int(lib().he_launch_count(self.h))
+
+    def he_graph_begin(self) -> None:
+        """Record the following calls on this context into a CUDA graph (he_graph_end)."""
+        _check(lib().he_graph_begin(self.h))
+
+    def he_graph_end(self) -> "Graph":
+        h = C.c_void_p()
+        _check(lib().he_graph_end(self.h, C.byref(h)))
+        return Graph(self, h)
 
     def he_profile_enable(self, on: bool = True) -> None:
         _check(lib().he_profile_enable(self.h, int(bool(on))))

@@ -151,6 +151,7 @@ he_status he_context_cdt(const he_context* c, uint64_t* table_out) {
 he_status he_set_stream(he_context* c, void* stream) {
   return guard([&] {
     need_ctx(c);
+    need(c->rec == nullptr, HE_INVALID_ARGUMENT, "he_set_stream while recording a graph");
     // cached scratch blocks were last used on the old stream
     if ((cudaStream_t)stream != c->stream) HE_CK(cudaStreamSynchronize(c->stream));
     c->stream = (cudaStream_t)stream;
@@ -166,6 +167,104 @@ he_status he_sync(he_context* c) {
 }
 
 uint64_t he_launch_count(const he_context* c) { return c ? c->launches : 0; }
+
+// ---- CUDA-graph recording -------------------------------------------------------------------
+static void graph_release(he_context* c, const std::vector<void*>& owned, const std::vector<void*>& deferred) {
+  for (void* p : owned) {
+    c->graph_owned.erase(p);
+    c->live_bytes.erase(p);
+    cudaFree(p);
+  }
+  for (void* p : deferred) {   // pre-existing blocks: back to their allocator now
+    c->graph_owned.erase(p);
+    dfree(c, p);
+  }
+}
+
+he_status he_graph_begin(he_context* c) {
+  return guard([&] {
+    need_ctx(c);
+    need(c->rec == nullptr, HE_INVALID_ARGUMENT, "already recording a graph");
+    need(!c->prof_on, HE_INVALID_ARGUMENT, "he_graph_begin with the profiler enabled");
+    auto* r = new he_context::GraphRec();
+    try {
+      HE_CK(cudaStreamCreateWithFlags(&r->cap, cudaStreamNonBlocking));
+      cudaEvent_t ev;
+      HE_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      HE_CK(cudaEventRecord(ev, c->stream));
+      HE_CK(cudaStreamWaitEvent(r->cap, ev, 0));
+      HE_CK(cudaEventDestroy(ev));
+      HE_CK(cudaStreamBeginCapture(r->cap, cudaStreamCaptureModeRelaxed));
+    } catch (...) {
+      if (r->cap) cudaStreamDestroy(r->cap);
+      delete r;
+      throw;
+    }
+    r->orig = c->stream;
+    r->launches0 = c->launches;
+    c->rec = r;
+    c->stream = r->cap;
+  });
+}
+
+he_status he_graph_end(he_context* c, he_graph** out) {
+  return guard([&] {
+    need_ctx(c);
+    need_out(out);
+    need(c->rec != nullptr, HE_INVALID_ARGUMENT, "not recording a graph");
+    he_context::GraphRec* r = c->rec;
+    c->rec = nullptr;
+    c->stream = r->orig;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(r->cap, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaStreamDestroy(r->cap);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      HE_CK(cudaDeviceSynchronize());   // nothing recorded ran; the owned blocks are unreferenced
+      graph_release(c, r->owned, r->deferred);
+      delete r;
+      throw HeError(HE_CUDA_ERROR, std::string("graph capture failed (a call synchronised or read back "
+                                               "while recording?): ") + cudaGetErrorString(e));
+    }
+    auto* g = new he_graph();
+    g->ctx = c;
+    g->graph = graph;
+    g->exec = exec;
+    g->kernels = c->launches - r->launches0;
+    c->launches = r->launches0;   // recorded, not launched
+    g->owned = std::move(r->owned);
+    g->deferred = std::move(r->deferred);
+    delete r;
+    *out = g;
+  });
+}
+
+he_status he_graph_launch(he_graph* g) {
+  return guard([&] {
+    need(g != nullptr && g->ctx != nullptr, HE_INVALID_ARGUMENT, "null graph");
+    need(g->ctx->rec == nullptr, HE_INVALID_ARGUMENT, "he_graph_launch while recording");
+    HE_CK(cudaGraphLaunch(g->exec, g->ctx->stream));
+    g->ctx->launches += g->kernels;
+  });
+}
+
+uint64_t he_graph_kernels(const he_graph* g) { return g ? g->kernels : 0; }
+
+he_status he_graph_free(he_graph* g) {
+  return guard([&] {
+    if (!g) return;
+    he_context* c = g->ctx;
+    // replays in flight on the context stream may still use the graph's memory
+    HE_CK(cudaStreamSynchronize(c->stream));
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    graph_release(c, g->owned, g->deferred);
+    delete g;
+  });
+}
 
 he_status he_profile_enable(he_context* c, int on) {
   return guard([&] {

@@ -91,6 +91,24 @@ struct he_context {
   bool prof_on = false;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
+  // CUDA-graph recording (he_graph_begin / he_graph_end): while rec is set, c->stream is the capture
+  // stream, dalloc takes graph-owned blocks (cudaMalloc, relaxed capture) and dfree defers
+  struct GraphRec {
+    cudaStream_t cap = nullptr, orig = nullptr;
+    uint64_t launches0 = 0;
+    std::vector<void*> owned;     // allocated while recording: freed with the graph
+    std::vector<void*> deferred;  // pre-existing blocks freed while recording: released with the graph
+  };
+  GraphRec* rec = nullptr;
+  std::map<void*, bool> graph_owned;   // blocks owned by a live graph (dfree is a no-op for them)
+};
+
+struct he_graph {
+  he_context* ctx;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;
+  std::vector<void*> owned, deferred;
 };
 
 struct he_ciphertext {

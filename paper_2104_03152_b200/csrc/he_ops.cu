@@ -30,6 +30,19 @@ void trim_cache(he_context* c) {
 
 void* dalloc(he_context* c, size_t bytes) {
   const size_t sz = bin_size(bytes);
+  if (c->rec) {   // recording a graph: a block only the graph uses (cudaMalloc is legal in relaxed capture)
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw HeError(e == cudaErrorMemoryAllocation ? HE_OUT_OF_MEMORY : HE_CUDA_ERROR,
+                    std::string("cudaMalloc (graph): ") + cudaGetErrorString(e));
+    }
+    c->rec->owned.push_back(p);
+    c->graph_owned[p] = true;
+    c->live_bytes[p] = sz;
+    return p;
+  }
   if (c->user_alloc) {
     void* p = c->user_alloc(sz, (void*)c->stream, c->user_ctx);
     if (!p) throw HeError(HE_OUT_OF_MEMORY, "the installed allocator returned NULL");
@@ -64,6 +77,12 @@ void dfree(he_context* c, void* p) {
   if (!p) return;
   auto it = c->live_bytes.find(p);
   if (it == c->live_bytes.end()) return;
+  if (c->graph_owned.count(p)) return;   // released by he_graph_free
+  if (c->rec) {                            // recorded kernels may still read it: release with the graph
+    c->rec->deferred.push_back(p);
+    c->graph_owned[p] = true;
+    return;
+  }
   auto uo = c->user_owned.find(p);
   if (uo != c->user_owned.end()) {   // back to the caller's allocator, in stream order
     c->user_owned.erase(uo);
