@@ -131,9 +131,13 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     B = args.batch
 
+    import time
+    t_kg = time.perf_counter()
     ctx = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
     ctx.he_set_stream(stream)
     ctx.he_keygen(rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
+    torch.cuda.synchronize(dev)
+    keygen_s = time.perf_counter() - t_kg   # Table 2 "Key generation": context + keys (first call, cold)
     net = EncryptedCNN(ctx, cnn_weights(CFG4.seed), conv_g=CONV_G, fc1_g=FC1_G)
     ns = ctx.slots
 
@@ -283,6 +287,10 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     if rank == 0 and not args.no_extra:
         extra = micro_extra(ctx, stream, dev)
+        from bench_configs import table2_breakdown
+        extra["table2_cfg4"] = table2_breakdown(ctx, net, imgs_host[0], stream, keygen_s)
+        from bench_configs import paper_schedule_throughput
+        extra["paper_schedule_cfg4"] = paper_schedule_throughput(stream, imgs_host[0], float_logits_torch)
         if world == 1:   # BASELINE.md / SURVEY §8(d) CPU-oracle subsets of configs 1, 2, 3, 5b (~40 s)
             from bench_configs import cpu_oracle_subsets
             extra["cpu_oracle_subsets"] = cpu_oracle_subsets()

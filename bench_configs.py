@@ -208,3 +208,103 @@ def cpu_oracle_subsets():
     out["cfg5b_deep_chain"] = {"sample": "1 ciphertext, N=32768, 18+2 primes, 1 thread", "seconds": round(dt, 3),
                                "ciphertexts_per_s": round(1 / dt, 5)}
     return out
+
+
+# PAPER.md Table 2: the encrypted MNIST evaluation per operation, ms for ONE image on
+# c4.2xlarge (8 vCPU) / c4.4xlarge (16 vCPU)
+PAPER_T2_MS = {"key_generation": (940.01, 921.04), "input_preparation": (9.8, 9.8), "conv": (236.9, 237.98),
+               "square1": (8.47, 8.42), "fc1": (1084.65, 575.34), "square2": (4.29, 4.2), "fc2": (121.36, 70.36),
+               "full_forward": (1456.29, 887.06)}
+
+
+def table2_breakdown(ctx, net, imgs, stream, keygen_s, reps: int = 3):
+    """The paper's Table-2 rows on the device, at the bench's schedule: per-stage CUDA-event time of
+    the batch (imgs [B][28][28], the bench's batch) and of a single image, plus key generation (the
+    bench's own context + keygen, host wall clock) and the host im2col per image."""
+    import time
+    import torch
+    from paper_2104_03152_b200 import he_im2col_encode_batch
+    from paper_2104_03152_b200.cnn import CHUNK
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    slots = he_im2col_encode_batch(imgs, 7, 7, 3, ctx.slots)
+    prep_s = time.perf_counter() - t0
+    res = {"key_generation_ms": round(keygen_s * 1e3, 2),
+           "input_preparation_ms_per_image": round(prep_s * 1e3 / len(imgs), 4),
+           "paper_ms_per_image_8vcpu_16vcpu": PAPER_T2_MS}
+    stages = ["encode_encrypt", "conv", "square1", "fc1", "square2", "fc2", "decrypt_decode"]
+    for label, x_host in (("batch", slots), ("single_image", slots[:1])):
+        B = x_host.shape[0]
+        x = torch.from_numpy(x_host).to(dev)
+        out = torch.empty((B, net.n_out), dtype=torch.float64, device=dev)
+        tot = [0.0] * len(stages)
+        for r in range(reps + 1):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
+            c = ctx
+            ev[0].record(stream)
+            ct = c.he_encrypt(c.he_encode(x, 2.0 ** net.plan["in_log2"], net.top), 7_000_000 + r * B)
+            ev[1].record(stream)
+            y = c.he_im2col_conv_bsgs_pt(ct, net.conv_d, net.conv_b, CHUNK, net.conv_g)
+            ev[2].record(stream)
+            y = c.he_square(y)
+            ev[3].record(stream)
+            y = c.he_vec_mat_pt(y, net.fc1_d, net.fc1_b)
+            ev[4].record(stream)
+            y = c.he_square(y)
+            ev[5].record(stream)
+            y = c.he_vec_mat_pt(y, net.fc2_d, net.fc2_b)
+            ev[6].record(stream)
+            c.he_decode(c.he_decrypt(y), net.n_out, out=out)
+            ev[7].record(stream)
+            torch.cuda.synchronize(dev)
+            if r:
+                for k in range(len(stages)):
+                    tot[k] += ev[k].elapsed_time(ev[k + 1]) / reps
+        res[label] = {"images": B, "ms": {k: round(v, 4) for k, v in zip(stages, tot)},
+                      "full_forward_ms": round(sum(tot[1:6]), 4),
+                      "full_forward_us_per_image": round(1e3 * sum(tot[1:6]) / B, 3)}
+    return res
+
+
+def paper_schedule_throughput(stream, imgs, float_logits, steps: int = 2):
+    """The config-4 network at the PAPER's evaluation schedule: 2-level im2col
+    conv with the log2(N) rotate-and-add fold, square, FC1 / FC2 by the diagonal method with one
+    ModDown per rotation (255 + 63 rotations), input encrypted at the top level; 259 Galois keys.
+    The bench's default schedule (one-level conv, folded BSGS FC layers) computes the
+    same network; this is the like-for-like number for the paper's own form.  Device-timed images/s
+    over `steps` steps of the batch `imgs` after one warm-up step, and the max |logit - float64 net|."""
+    import torch
+    from paper_2104_03152_b200 import Context, he_im2col_encode_batch
+    from paper_2104_03152_b200.cnn import EncryptedCNN, rotation_steps
+    from synthetic import CFG4, cnn_weights
+    dev = torch.device("cuda", torch.cuda.current_device())
+    c = Context(CFG4.logN, CFG4.bits, CFG4.n_special, CFG4.seed)
+    c.he_set_stream(stream)
+    c.he_keygen(rotation_steps())
+    w = cnn_weights(CFG4.seed)
+    net = EncryptedCNN(c, w, lazy=False, bsgs=False)
+    B = len(imgs)
+    x = torch.from_numpy(he_im2col_encode_batch(imgs, 7, 7, 3, c.slots)).to(dev)
+    out = torch.empty((B, net.n_out), dtype=torch.float64, device=dev)
+
+    def step(i):
+        ct = c.he_encrypt(c.he_encode(x, 2.0 ** net.plan["in_log2"], net.top), 8_000_000 + i * B)
+        c.he_decode(c.he_decrypt(net.forward(ct)), net.n_out, out=out)
+    step(0)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        step(1 + i)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    s = e0.elapsed_time(e1) / 1e3 / steps
+    ref = float_logits(imgs, w)
+    err = float(np.max(np.abs(out.cpu().numpy() - ref)))
+    n_keys = len(rotation_steps())
+    del net, c
+    return {"schedule": "paper (PAPER.md:57-64): 2-level conv + log2 fold, per-rotation diagonal vec_mat",
+            "images_per_s": round(B / s, 1), "ms_per_batch": round(s * 1e3, 2), "batch": B,
+            "galois_keys": n_keys, "max_logit_err": err, "argmax_equal": int(np.sum(
+                np.argmax(out.cpu().numpy(), 1) == np.argmax(ref, 1)))}
+
