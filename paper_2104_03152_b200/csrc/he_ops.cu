@@ -812,9 +812,12 @@ __global__ void __launch_bounds__(LAZY_SM_T, 1)
 k_vecmat_bsgs_hp(LazyArgs a, int g, int B, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
                  const PrimeD* __restrict__ primes) {
   extern __shared__ u32 xs[];   // [IB][LC][N/2] digits of this half, then c0p [IB][N/2]
-  const int t = blockIdx.x, nt = LC + a.K;
+  // grid (image pairs, halves, targets): the image pairs vary fastest, so the CTAs resident together
+  // share one (target, half) and its key rows / diagonals stay in L2 (round 2; targets fastest
+  // re-read them from DRAM, ~2.8x the unique bytes)
+  const int t = blockIdx.z, nt = LC + a.K;
   const u32 NH = (u32)a.N / 2, h0 = blockIdx.y * NH;
-  const int b0 = blockIdx.z * IB, nimg = min(IB, B - b0);
+  const int b0 = blockIdx.x * IB, nimg = min(IB, B - b0);
   const int tp = t < LC ? t : a.L + (t - LC);
   const PrimeD P = load_prime(primes, tp);
   const u32 q = (u32)P.q, qi = mont_neg_inv(q);
@@ -1825,7 +1828,9 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
         LazyArgs la{c->N, c->logN, Lc, c->K, c->L, c->NP, g, nullptr, x->d, nullptr, nullptr, gt, c->d_P_mod,
                     accx.as<u64>(), step, ext};
         {
-          const double bytes = 8.0 * N * ((double)B * Lc * nt + 2.0 * B * Lc) + 4.0 * N * G * B * 2 * nt +
+          // unique bytes: u32 extended digits (t != j), the u64 own digit (c1) and c0 row, u32 accumulators
+          // written, u32 key rows of the g-1 baby steps, u32 diagonals
+          const double bytes = 4.0 * N * B * Lc * (nt - 1) + 8.0 * N * 2.0 * B * Lc + 4.0 * N * G * B * 2 * nt +
                                4.0 * N * ((double)(g - 1) * 2 * Lc * nt + (double)G * g * nt);
           const double ops = (double)B * (g - 1) * N * (nt * (2.0 * Lc + 2.0 * G) + Lc);
           static const char* const tags[9] = {"vecmat_bsgs", "vecmat_bsgs_L1", "vecmat_bsgs_L2", "vecmat_bsgs_L3",
@@ -1835,7 +1840,7 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
           // half-ring CTAs with image pairs (k_vecmat_bsgs_hp): same smem as one full-ring image
           const int IBv = B >= 2 ? 2 : 1;
           const size_t smem_hp = (size_t)IBv * (Lc + 1) * (N / 2) * 4;
-          const dim3 grid(nt, 2, (unsigned)((B + IBv - 1) / IBv));
+          const dim3 grid((unsigned)((B + IBv - 1) / IBv), 2, nt);
           auto launch = [&](auto kern) {
             smem_limit_once((const void*)kern, (int)kMaxSmem);
             kern<<<grid, LAZY_SM_T, smem_hp, c->stream>>>(la, g, B, kt, diags->dm, c->d_primes);
