@@ -748,8 +748,38 @@ k_ntt32(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict__ tw
 
 template <int LOGN>
 struct NttGeom32Pipe {
-  static constexpr int SMEM = NttGeom32<LOGN>::SMEM + (1 << LOGN) * 4;   // + staging row
+  static constexpr int SMEM = NttGeom32<LOGN>::SMEM + (1 << LOGN) * 4 + 16;   // + staging row + mbarrier
 };
+
+// One-thread bulk copies (TMA engine, cp.async.bulk) of a block's input row into the staging buffer,
+// completing on an mbarrier (round 2; HE_NTT32_TMA=0 keeps the per-thread cp.async form).
+#ifndef HE_NTT32_TMA
+#define HE_NTT32_TMA 1
+#endif
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_row_to_smem(u32* dst, const u32* src, u32 bytes, u64* bar) {
+  // generic-proxy reads of dst (the previous block's first pass) are ordered before the async writes
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
+  u32 ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
 
 template <int LOGN, bool INV, class Job>
 __global__ void __launch_bounds__(NttGeomS<LOGN>::T, NttGeom32<LOGN>::MINB)
@@ -760,19 +790,39 @@ k_ntt32_pipe(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict
   const u32 tid = threadIdx.x;
   int blk = blockIdx.x;
   if (blk >= nblk) return;
+#if HE_NTT32_TMA
+  u64* bar = reinterpret_cast<u64*>(stage + G::NL);   // 8-byte aligned: (2 NL + NL / 32) words
+  u32 phase = 0;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) bulk_row_to_smem(stage, job.raw32(blk), G::NL * 4, bar);
+#else
   stage_row32<LOGN>(stage, job.raw32(blk), tid);
+#endif
   for (; blk < nblk; blk += gridDim.x) {
     const int pi = job.prime(blk);
     const PrimeD P = load_prime(primes, pi);
     const uint2* tw = tw_all + (size_t)pi * G::N;
     const u32 q = (u32)P.q;
     const auto jb = bind_pipe_job(job, blk, P, 0);
+#if HE_NTT32_TMA
+    mbar_wait(bar, phase);   // the staged row has landed
+    phase ^= 1;
+#else
     cp_async_wait_all();
+#endif
     __syncthreads();   // staged row visible; the previous block's epilogue is done with sm32
     if (q < (1u << 30)) ntt32_pipe_block<LOGN, INV, true>(jb, sm32, stage, tid, tw, q);
     else ntt32_pipe_block<LOGN, INV, false>(jb, sm32, stage, tid, tw, q);
     // ntt32_pipe_block synchronised once the staged row was consumed (its first pass): prefetch
+#if HE_NTT32_TMA
+    if (tid == 0 && blk + (int)gridDim.x < nblk) bulk_row_to_smem(stage, job.raw32(blk + gridDim.x), G::NL * 4, bar);
+#else
     if (blk + (int)gridDim.x < nblk) stage_row32<LOGN>(stage, job.raw32(blk + gridDim.x), tid);
+#endif
     ntt32_pipe_rest<LOGN, INV>(jb, sm32, tid, tw, q);
   }
 }
