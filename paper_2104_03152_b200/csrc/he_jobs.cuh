@@ -32,6 +32,17 @@ template <class B>
 struct has_store4<B, std::void_t<decltype(std::declval<const B&>().store4(0u, 0u, (const u32*)nullptr))>>
     : std::true_type {};
 
+// Epilogue operand rows a pipelined block will read after its passes: one thread asks the TMA engine
+// to pull them into L2 when the block starts (cp.async.bulk.prefetch.L2), so the epilogue's loads hit
+// L2 instead of waiting on DRAM.  Rows are 16-byte aligned and N * 4 or N * 8 bytes.
+__device__ __forceinline__ void prefetch_l2(const void* p, u32 bytes) {
+  if (p) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+template <class B, class = void>
+struct has_prefetch : std::false_type {};
+template <class B>
+struct has_prefetch<B, std::void_t<decltype(std::declval<const B&>().prefetch(0u))>> : std::true_type {};
+
 template <class B, class = void>
 struct has_load4 : std::false_type {};
 template <class B>
@@ -652,6 +663,13 @@ struct JobKsData {
       out[n] = fin(n, (u32)v, ax[n], add ? (u32)add[gather ? galois_src(n, g, logN) : n] : 0u, s0,
                    sq1 ? (u32)sq1[n] : s0, acc ? (u32)acc[n] : 0u);
     }
+    __device__ __forceinline__ void prefetch(u32 N) const {
+      prefetch_l2(ax, N * 4);
+      prefetch_l2(add, N * 8);
+      prefetch_l2(acc, N * 8);
+      prefetch_l2(sq0, N * 8);
+      prefetch_l2(sq1, N * 8);
+    }
     // 4 outputs n0 + u st: the operand loads of all 4 are issued before the arithmetic
     __device__ __forceinline__ void store4(u32 n0, u32 st, const u32* v) const {
       u32 axv[4], adv[4] = {0, 0, 0, 0}, s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0}, acv[4] = {0, 0, 0, 0};
@@ -793,6 +811,10 @@ struct JobRescaleData {
         if (bias) o = add32(o, bv[u], q);
         out[n0 + u * st] = o;
       }
+    }
+    __device__ __forceinline__ void prefetch(u32 N) const {
+      if (!src->K) prefetch_l2(src->x + ((size_t)r * src->Lc + i) * N, N * 8);
+      prefetch_l2(bias, N * 8);
     }
     __device__ __forceinline__ u64 load(u32 n) const { return sub32(red32(y[n], q, mu32), h, q); }
     __device__ __forceinline__ u64 load_raw(u32 x) const { return sub32(red32(x, q, mu32), h, q); }

@@ -808,6 +808,12 @@ k_ntt32_pipe(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict
     const uint2* tw = tw_all + (size_t)pi * G::N;
     const u32 q = (u32)P.q;
     const auto jb = bind_pipe_job(job, blk, P, 0);
+#ifndef HE_NTT32_PREFETCH
+#define HE_NTT32_PREFETCH 1
+#endif
+    if constexpr (HE_NTT32_PREFETCH && has_prefetch<decltype(jb)>::value) {
+      if (tid == 0) jb.prefetch(G::NL);   // the epilogue's operand rows -> L2 while the passes run
+    }
 #if HE_NTT32_TMA
     mbar_wait(bar, phase);   // the staged row has landed
     phase ^= 1;
