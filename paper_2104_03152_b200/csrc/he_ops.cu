@@ -832,16 +832,20 @@ k_vecmat_bsgs_hp(LazyArgs a, int g, int B, const u32* const* __restrict__ keys32
 #pragma unroll
     for (int j = 0; j < LC; ++j) {
       u32* dst = xs + (i * LC + j) * NH;
+      // (loops unrolled by 4: a thread's row loads are issued together, not one DRAM latency each)
       if (t == j || !a.ext32) {
         const u64* src = ((t == j) ? c1 + (size_t)j * N : a.ext + (((size_t)b * LC + j) * nt + t) * N) + h0;
+#pragma unroll 4
         for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T) dst[l] = (u32)src[l];
       } else {
         const u32* src = a.ext32 + (((size_t)b * LC + j) * nt + t) * N + h0;
+#pragma unroll 4
         for (u32 l = threadIdx.x * 4; l < NH; l += LAZY_SM_T * 4)
           *reinterpret_cast<uint4*>(dst + l) = __ldg(reinterpret_cast<const uint4*>(src + l));
       }
     }
     if (data)
+#pragma unroll 4
       for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T)
         c0p[i * NH + l] = redc32((u64)(u32)c0[(size_t)t * N + h0 + l] * Pm, q, qi);
   }
@@ -892,11 +896,18 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
   const u32 mut = (u32)((1ULL << 32) / q);
   for (int j = 0; j < a.Lc; ++j) {
     if (j == t) {
+      // compile-time trip counts (the launch has exactly T threads): 8 loads in flight per chunk
       const u64* src = a.dsrc + (size_t)b * a.dsrc_bs + (size_t)j * G::N;
-      if (a.sq)
-        for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)mul_mod(src[i], src[i], P);
-      else
-        for (u32 i = tid; i < G::N; i += G::T) buf[spad32(i)] = (u32)src[i];
+      constexpr int PER = G::N / G::T, CH = PER < 8 ? PER : 8;
+#pragma unroll 1
+      for (int c = 0; c < PER / CH; ++c) {
+        u64 v[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) v[k] = src[tid + (c * CH + k) * G::T];
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+          buf[spad32(tid + (c * CH + k) * G::T)] = a.sq ? (u32)mul_mod(v[k], v[k], P) : (u32)v[k];
+      }
     } else {
       const u32* src = a.coef + ((size_t)b * a.Lc + j) * G::N;
       const u32 qj = (u32)__ldg(a.qtab + j);
@@ -905,8 +916,11 @@ k_modup_ip32(FusedArgs a, const PrimeD* __restrict__ primes, const uint2* __rest
       ntt_fwd32_from<LOGN>(buf, tid, tw, q, [&](u32 i) { return lift32(src[i], qj, q, mut); });
     }
     __syncthreads();
-    // 4 consecutive coefficients per step: 16-byte key loads and accumulator updates
-    for (u32 n0 = tid * 4; n0 < G::N; n0 += G::T * 4) {
+    // 4 consecutive coefficients per step: 16-byte key loads and accumulator updates (compile-time
+    // trip count: every step's key loads are issued together)
+#pragma unroll
+    for (int s4 = 0; s4 < G::N / (4 * G::T); ++s4) {
+      const u32 n0 = tid * 4 + s4 * 4 * G::T;
       const uint4 kb = __ldg(reinterpret_cast<const uint4*>(key + j * kdig + n0));
       const uint4 ka = __ldg(reinterpret_cast<const uint4*>(key + j * kdig + kpart + n0));
       uint4 a0 = *reinterpret_cast<uint4*>(acc + n0), a1 = *reinterpret_cast<uint4*>(acc + G::N + n0);
