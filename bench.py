@@ -153,8 +153,8 @@ def run_ours(args, rank, world, local_rank):
 
     def step_device(i):
         x = slots_dev[i % n_batches]
-        pt = ctx.he_encode(x, 2.0 ** net.plan["in_log2"], net.top)
-        ct = ctx.he_encrypt(pt, 1_000_000 + i * B)
+        # encode + encrypt in one call (he_encode_encrypt: the same words as he_encrypt(he_encode(x)))
+        ct = ctx.he_encode_encrypt(x, 2.0 ** net.plan["in_log2"], net.top, 1_000_000 + i * B)
         out = net.forward(ct)
         ctx.he_decode(ctx.he_decrypt(out), net.n_out, out=logits_dev)
 
@@ -244,8 +244,9 @@ def run_ours(args, rank, world, local_rank):
         im2col(first)
         for i in range(first, first + count):
             k = i % 2
-            pt = ctx.he_encode(slot_buf[k].numpy(), 2.0 ** net.plan["in_log2"], net.top)      # H2D inside
-            dec = ctx.he_decrypt(net.forward(ctx.he_encrypt(pt, 2_000_000 + i * B)))
+            ct = ctx.he_encode_encrypt(slot_buf[k].numpy(), 2.0 ** net.plan["in_log2"], net.top,
+                                       2_000_000 + i * B)                                       # H2D inside
+            dec = ctx.he_decrypt(net.forward(ct))
             ctx.he_decode_async(dec, logits_pin[k].numpy(), net.n_out)                         # D2H inside
             done[k].record(stream)
             if i > first:

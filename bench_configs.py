@@ -242,7 +242,7 @@ def table2_breakdown(ctx, net, imgs, stream, keygen_s, reps: int = 3):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
             c = ctx
             ev[0].record(stream)
-            ct = c.he_encrypt(c.he_encode(x, 2.0 ** net.plan["in_log2"], net.top), 7_000_000 + r * B)
+            ct = c.he_encode_encrypt(x, 2.0 ** net.plan["in_log2"], net.top, 7_000_000 + r * B)
             ev[1].record(stream)
             y = c.he_im2col_conv_bsgs_pt(ct, net.conv_d, net.conv_b, CHUNK, net.conv_g)
             ev[2].record(stream)

@@ -209,6 +209,18 @@ he_status he_decode_device(he_context* ctx, const he_plaintext* pt, double* out_
  * (v, e0, e1) from Philox stream `stream_id + b`.  Output scale/level = pt's. */
 he_status he_encrypt(he_context* ctx, const he_plaintext* pt, uint64_t stream_id,
                      he_ciphertext** out);
+/* Encode + public-key encryption in one call (a CKKSVector's creation,
+ * PAPER.md:35, 57): the ciphertext words equal
+ * he_encrypt(he_encode(z, scale, level), stream_id) exactly; the encoder's
+ * integer coefficients m feed the transform of e0 (c0 = NTT(v) b + NTT(e0 + m),
+ * the transform being linear mod q_i), so the plaintext's own transforms and
+ * its HBM round trip are skipped.  Host z[B][n_per_item] with he_encode's
+ * host-side C7 bound check and copy semantics; the _device form reads z_dev
+ * and reports an overflow asynchronously like he_encode_device. */
+he_status he_encode_encrypt(he_context* ctx, const double* z, size_t n_per_item, size_t B, double scale,
+                            int level, uint64_t stream_id, he_ciphertext** out);
+he_status he_encode_encrypt_device(he_context* ctx, const double* z_dev, size_t n_per_item, size_t B,
+                                   double scale, int level, uint64_t stream_id, he_ciphertext** out);
 /* Symmetric (secret-key) encryption (SURVEY 8(f) #3 "seeded symmetric
  * encryption halves the upload"): item b gets
  *   c1 = a,  a_i = Uniform(a_seed, stream (SYM_A, stream_id + b, i))   (C13 sampler)

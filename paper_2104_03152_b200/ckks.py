@@ -75,6 +75,8 @@ _SIGS = {
     "he_decode_device": [VP, VP, VP, SZ],
     "he_decode_async": [VP, VP, VP, SZ],
     "he_encrypt": [VP, VP, C.c_uint64, VPP],
+    "he_encode_encrypt": [VP, DP, SZ, SZ, C.c_double, C.c_int, C.c_uint64, VPP],
+    "he_encode_encrypt_device": [VP, VP, SZ, SZ, C.c_double, C.c_int, C.c_uint64, VPP],
     "he_encrypt_symmetric": [VP, VP, C.c_uint64, C.c_uint64, VPP],
     "he_decrypt": [VP, VP, VPP],
     "he_add": [VP, VP, VP, VPP],
@@ -554,6 +556,19 @@ class Context:
     def he_encrypt(self, pt: Plaintext, stream_id: int = 0) -> Ciphertext:
         h = C.c_void_p()
         _check(lib().he_encrypt(self.h, pt.h, stream_id, C.byref(h)))
+        return Ciphertext(self, h)
+
+    def he_encode_encrypt(self, z, scale: float, level: int, stream_id: int = 0) -> Ciphertext:
+        """he_encode + he_encrypt in one call (same words); z as in he_encode (host array or CUDA tensor)."""
+        h = C.c_void_p()
+        if _is_dev(z):
+            z2 = self._dev_input(z if z.dim() == 2 else z.reshape(1, -1), "he_encode_encrypt")
+            _check(lib().he_encode_encrypt_device(self.h, _ptr(z2), z2.shape[1], z2.shape[0], float(scale), level,
+                                                  stream_id, C.byref(h)))
+        else:
+            z2 = np.ascontiguousarray(np.atleast_2d(np.asarray(z, dtype=np.float64)))
+            _check(lib().he_encode_encrypt(self.h, z2.ctypes.data_as(DP), z2.shape[1], z2.shape[0], float(scale),
+                                           level, stream_id, C.byref(h)))
         return Ciphertext(self, h)
 
     def he_encrypt_symmetric(self, pt: Plaintext, stream_id: int, a_seed: int) -> Ciphertext:

@@ -116,8 +116,7 @@ class EncryptedCNN:
     def encrypt(self, imgs: np.ndarray, stream_id: int = 0):
         """Client side: im2col (host) -> encode -> encrypt, images [B][28][28]."""
         slots = self.im2col(np.asarray(imgs, dtype=np.float64))
-        pt = self.ctx.he_encode(slots, 2.0 ** self.plan["in_log2"], self.top)
-        return self.ctx.he_encrypt(pt, stream_id)
+        return self.ctx.he_encode_encrypt(slots, 2.0 ** self.plan["in_log2"], self.top, stream_id)
 
     def forward(self, ct):
         """Server side: conv -> square -> FC1 -> square -> FC2."""

@@ -461,6 +461,37 @@ he_status he_encrypt(he_context* c, const he_plaintext* pt, uint64_t stream_id, 
   });
 }
 
+static void encode_encrypt_common(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
+                                  uint64_t stream_id, he_ciphertext** out) {
+  need_ctx(c);
+  need_out(out);
+  need(B >= 1, HE_INVALID_ARGUMENT, "B must be >= 1");
+  need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+  need(level >= 0 && level < c->L, HE_LEVEL_MISMATCH, "level out of range");
+  need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
+  need(c->has_pk, HE_MISSING_KEY, "no public key (call he_keygen)");
+  *out = encode_encrypt(c, z_dev, n, B, scale, level, stream_id);
+}
+
+he_status he_encode_encrypt(he_context* c, const double* z, size_t n, size_t B, double scale, int level,
+                            uint64_t stream_id, he_ciphertext** out) {
+  return guard([&] {
+    need_ctx(c);
+    need(z != nullptr || n == 0, HE_INVALID_ARGUMENT, "null input");
+    need(B >= 1, HE_INVALID_ARGUMENT, "B must be >= 1");
+    need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
+    need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
+    host_overflow_check(c, z, n, B, scale);
+    DevDoubles d(c, z, n * B);
+    encode_encrypt_common(c, d.d, n, B, scale, level, stream_id, out);
+  });
+}
+
+he_status he_encode_encrypt_device(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
+                                   uint64_t stream_id, he_ciphertext** out) {
+  return guard([&] { encode_encrypt_common(c, z_dev, n, B, scale, level, stream_id, out); });
+}
+
 he_status he_encrypt_symmetric(he_context* c, const he_plaintext* pt, uint64_t stream_id, uint64_t a_seed,
                                he_ciphertext** out) {
   return guard([&] {

@@ -180,11 +180,16 @@ struct JobEncrypt {
   const u64* cdt;          // 20-entry table
   u64 seed, stream0;
   int N, Lc, L, which;
+  // fused encode + encrypt (he_encode_encrypt): the message's signed coefficients [B][N] instead of
+  // plaintext words; the e0 pass transforms e0 + m (NTT is linear, so c0 has the same words)
+  const i64* mco = nullptr;
   __device__ int prime(int blk) const { return blk % Lc; }
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const {
     const u64 obj = stream0 + (u64)(blk / Lc);
     if (which == 0) return from_signed(sample_ternary(seed, stream_sid(PUR_ENC_V, obj, 0), n), P);
-    return from_signed(sample_cdt(seed, stream_sid(which == 1 ? PUR_ENC_E0 : PUR_ENC_E1, obj, 0), n, cdt), P);
+    i64 e = sample_cdt(seed, stream_sid(which == 1 ? PUR_ENC_E0 : PUR_ENC_E1, obj, 0), n, cdt);
+    if (which == 1 && mco) e += mco[(size_t)(blk / Lc) * N + n];
+    return from_signed(e, P);
   }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const {
     const int b = blk / Lc, i = blk % Lc;
@@ -192,7 +197,7 @@ struct JobEncrypt {
     u64* c0 = ct + (size_t)b * 2 * LN + (size_t)i * N + n;
     u64* c1 = c0 + LN;
     if (which == 0) {
-      const u64 m = pt[(size_t)b * pt_bs + (size_t)i * N + n];
+      const u64 m = pt ? pt[(size_t)b * pt_bs + (size_t)i * N + n] : 0;
       *c0 = add_mod(mul_mod(v, pk[(size_t)i * N + n], P), m, P.q);
       *c1 = mul_mod(v, pk[((size_t)L + i) * N + n], P);
     } else if (which == 1) {
@@ -214,22 +219,31 @@ struct JobEncrypt {
     const u64* m;
     u32 q;
     int which;
+    const i64* mc;   // fused encode + encrypt: this item's message coefficients (e0 pass), else null
     __device__ __forceinline__ u32 res(i64 v) const { return v < 0 ? q - (u32)(-v) : (u32)v; }
+    // e0 + m (m up to 2^62 in magnitude): a full signed reduction
+    __device__ __forceinline__ u32 resm(i64 e, u32 n) const { return (u32)from_signed(e + mc[n], *P); }
     __device__ __forceinline__ uint4 load4(u32 j) const {
       if (which == 0) {
         const uint4 b = philox_block(seed, sid, j);
         auto t = [&](u32 w) { return res((i64)(((u64)w * 3u) >> 32) - 1); };
         return make_uint4(t(b.x), t(b.y), t(b.z), t(b.w));
       }
+      if (mc)
+        return make_uint4(resm(sample_cdt(seed, sid, 4 * j, cdt), 4 * j),
+                          resm(sample_cdt(seed, sid, 4 * j + 1, cdt), 4 * j + 1),
+                          resm(sample_cdt(seed, sid, 4 * j + 2, cdt), 4 * j + 2),
+                          resm(sample_cdt(seed, sid, 4 * j + 3, cdt), 4 * j + 3));
       return make_uint4(res(sample_cdt(seed, sid, 4 * j, cdt)), res(sample_cdt(seed, sid, 4 * j + 1, cdt)),
                         res(sample_cdt(seed, sid, 4 * j + 2, cdt)), res(sample_cdt(seed, sid, 4 * j + 3, cdt)));
     }
     __device__ __forceinline__ u64 load(u32 n) const {
-      return which == 0 ? res(sample_ternary(seed, sid, n)) : res(sample_cdt(seed, sid, n, cdt));
+      if (which == 0) return res(sample_ternary(seed, sid, n));
+      return mc ? resm(sample_cdt(seed, sid, n, cdt), n) : res(sample_cdt(seed, sid, n, cdt));
     }
     __device__ __forceinline__ void store(u32 n, u64 v) const {
       if (which == 0) {
-        c0[n] = add32((u32)mul_mod(v, pkb[n], *P), (u32)m[n], q);
+        c0[n] = m ? add32((u32)mul_mod(v, pkb[n], *P), (u32)m[n], q) : (u32)mul_mod(v, pkb[n], *P);
         c1[n] = (u32)mul_mod(v, pka[n], *P);
       } else if (which == 1) {
         c0[n] = add32((u32)c0[n], (u32)v, q);
@@ -245,7 +259,8 @@ struct JobEncrypt {
     const u64 pur = which == 0 ? PUR_ENC_V : which == 1 ? PUR_ENC_E0 : PUR_ENC_E1;
     u64* c0 = ct + (size_t)b * 2 * LN + (size_t)i * N;
     return B32{&P, cdt, seed, stream_sid(pur, obj, 0), c0, c0 + LN, pk + (size_t)i * N, pk + ((size_t)L + i) * N,
-               pt + (size_t)b * pt_bs + (size_t)i * N, (u32)P.q, which};
+               pt ? pt + (size_t)b * pt_bs + (size_t)i * N : nullptr, (u32)P.q, which,
+               mco && which == 1 ? mco + (size_t)b * N : nullptr};
   }
 };
 inline double alg_bytes(const JobEncrypt& j, int nblk) {

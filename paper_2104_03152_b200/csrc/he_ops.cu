@@ -2253,6 +2253,23 @@ void pt_to_int(he_context* c, const he_plaintext* pt, i64* out_dev) {
 // ---- encode / decode / encrypt / decrypt --------------------------------------
 // check_now: read the overflow flag back (stream sync) and fail here; otherwise the kernel ORs it
 // into the context's sticky flag, reported by the next he_sync / host-output decode (take_err).
+// k_encode_fft into m_dev [B][N] (int64); an overflow sets the context's sticky flag (he_sync reports it).
+void encode_coeffs(he_context* c, const double* z_dev, size_t n, size_t B, double scale, i64* m_dev) {
+  const int N = c->N, M = N / 2, logM = c->logN - 1;
+  const bool in_smem = M <= 8192;
+  Scratch g(c, in_smem ? 8 : B * M * 16);
+  const int smem = in_smem ? M * 16 : 0;
+  if (smem > 48 * 1024)
+    smem_limit_once((const void*)k_encode_fft, smem);
+  {
+    ProfScope ps_(c, "encode_fft", 0.0, 0);
+    k_encode_fft<<<(unsigned)B, 512, smem, c->stream>>>(z_dev, n, scale, m_dev, c->d_err, c->d_slot_index,
+                                                        c->d_fft_w, c->d_zeta, N, logM,
+                                                        in_smem ? nullptr : g.as<double2>());
+  }
+  check_launch(c);
+}
+
 he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp,
                      bool check_now) {
   const int N = c->N, M = N / 2, logM = c->logN - 1;
@@ -2340,6 +2357,29 @@ he_ciphertext* encrypt(he_context* c, const he_plaintext* pt, u64 stream_id) {
       JobEncrypt j{ct->d, c->d_pk, pt->d, pt->B == 1 ? 0 : (size_t)Lc * c->N, c->d_cdt, c->seed, stream_id,
                    c->N, Lc, c->L, w};
       launch_ntt<false>(c, j, B * Lc);
+    }
+  } catch (...) {
+    ct_free(ct);
+    throw;
+  }
+  return ct;
+}
+
+// Fused encode + public-key encryption (he_encode_encrypt): the canonical-embedding coefficients m
+// (k_encode_fft, int64) feed the e0 pass directly, c0 = NTT(v) b + NTT(e0 + m), c1 = NTT(v) a + NTT(e1):
+// the plaintext's own B * Lc transforms and its HBM round trip disappear; the words equal
+// encrypt(encode(z)) exactly (the transform is linear mod q_i).
+he_ciphertext* encode_encrypt(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
+                              u64 stream_id) {
+  const int Lc = level + 1;
+  Scratch m(c, B * c->N * 8);
+  encode_coeffs(c, z_dev, n, B, scale, m.as<i64>());
+  he_ciphertext* ct = ct_new(c, (int)B, 2, level, scale);
+  try {
+    for (int w = 0; w < 3; ++w) {
+      JobEncrypt j{ct->d, c->d_pk, nullptr, 0, c->d_cdt, c->seed, stream_id, c->N, Lc, c->L, w};
+      j.mco = m.as<i64>();
+      launch_ntt<false>(c, j, (int)B * Lc);
     }
   } catch (...) {
     ct_free(ct);

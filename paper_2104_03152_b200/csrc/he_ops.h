@@ -31,6 +31,9 @@ int check_words(he_context* c, const u64* w, size_t items, int Lc);
 
 // scheme
 void keygen(he_context* c, const std::vector<int>& steps);
+void encode_coeffs(he_context* c, const double* z_dev, size_t n, size_t B, double scale, i64* m_dev);
+he_ciphertext* encode_encrypt(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level,
+                              u64 stream_id);
 void encode_unrounded(he_context* c, const double* z_dev, size_t n, size_t B, double scale, double* pre_dev);
 he_plaintext* encode(he_context* c, const double* z_dev, size_t n, size_t B, double scale, int level, int qp = 0,
                      bool check_now = true);

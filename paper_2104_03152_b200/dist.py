@@ -89,7 +89,7 @@ def client_server_round(ctx, net, imgs_all, stream_id: int, device):
     full = None
     if rank == 0:
         slots = he_im2col_encode_batch(imgs_all, 7, 7, 3, ctx.slots)
-        ct = ctx.he_encrypt(ctx.he_encode(slots, 2.0 ** net.plan["in_log2"], top), stream_id)
+        ct = ctx.he_encode_encrypt(slots, 2.0 ** net.plan["in_log2"], top, stream_id)
         full = torch.empty((ct.B, 2, top + 1, N), dtype=torch.int64, device=device)
         ctx.he_ct_export_words(ct, full)
         torch.cuda.synchronize(device)

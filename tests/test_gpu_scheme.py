@@ -146,6 +146,24 @@ def test_encrypt_decrypt_bit_exact(which, tiny, cfg1):
     assert np.max(np.abs(vals - z)) < 1e-3
 
 
+@pytest.mark.parametrize("which", ["tiny", "cfg1", "small"])
+def test_encode_encrypt_equals_encode_then_encrypt(which, tiny, cfg1, small):
+    """he_encode_encrypt (m fed into the e0 transform) gives exactly the words of
+    he_encrypt(he_encode(z)) -- the transform is linear mod q_i -- host and device input, a ragged
+    batch, two levels, 64-bit and 32-bit engines."""
+    import torch
+    o, g = (tiny if which == "tiny" else cfg1 if which == "cfg1" else small[:2])
+    scale = 2.0 ** (26 if which == "small" else 30)
+    z = messages(5, o.slots // 2 + 3, seed=17)
+    for lvl in (o.L - 1, 1):
+        ref = g.he_encrypt(g.he_encode(z, scale, lvl), 300).words()
+        assert np.array_equal(g.he_encode_encrypt(z, scale, lvl, 300).words(), ref)
+        zd = torch.from_numpy(z).cuda()
+        assert np.array_equal(g.he_encode_encrypt(zd, scale, lvl, 300).words(), ref)
+    vals = g.he_decode(g.he_decrypt(g.he_encode_encrypt(z, scale, o.L - 1, 9)), z.shape[1])
+    assert np.max(np.abs(vals - z)) < (1e-2 if which == "small" else 1e-3)
+
+
 # ------------------------------------------------------------- arithmetic ---
 def test_pointwise_ops_bit_exact(tiny):
     o, g = tiny
