@@ -682,14 +682,8 @@ he_status he_square(he_context* c, const he_ciphertext* a, he_ciphertext** out) 
     need(a->size == 2, HE_SHAPE_MISMATCH, "square needs a size-2 ciphertext");
     need(c->has_rlk, HE_MISSING_KEY, "no relinearisation key");
     need(a->level >= 1, HE_LEVEL_EXHAUSTED, "square needs a level to rescale");
-    he_ciphertext* r = ct_square_relin(c, a);   // tensor fused into the key switch when available
-    try {
-      *out = ct_rescale(c, r);
-    } catch (...) {
-      ct_free(r);
-      throw;
-    }
-    ct_free(r);
+    // tensor fused into the key switch and the rescale into its ModDown when available
+    *out = ct_square_rescale(c, a);
   });
 }
 

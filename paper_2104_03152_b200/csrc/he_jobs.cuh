@@ -373,6 +373,7 @@ struct KsArgs {
   const u64* Pinv_mod;     // P^{-1} mod q_i     [NP]
   const u64* Phat_inv;     // (P/p_k)^{-1} mod p_k [K]
   const u64* Phat_mod;     // (P/p_k) mod q_t   [K][NP]
+  const u64* P_mod;        // P mod q_t         [NP] (ModDown fused with the rescale)
   // epilogue (KsData only): out_p = acc_in_p[n] + D (.) (u_p + [p < add_parts] addsrc_p[pi?(n)])
   u64* out;                // item b at out + kk*out_ks + b*out_bs + p*Lc*N + i*N
   size_t out_bs, out_ks;
@@ -730,6 +731,147 @@ struct JobKsData {
   }
 };
 
+// ---- ModDown fused with the rescale that follows it (small primes, one special prime, accx) --------
+// Sequentially (JobKsData then JobRescaleLast / JobRescaleData), limb i of the result is
+//   u_i = (ax_i - NTT(conv_i)) P^{-1} + E_i,   y = INTT(u_l) + (q_l - 1)/2,
+//   out_i = (u_i - NTT([y]_{q_i} - [h]_{q_i})) q_l^{-1}  (+ bias),
+// with E_i the ModDown epilogue's NTT-domain terms (gathered c0, square terms, accumulated input).
+// Both transforms are linear mod q_i, so with y'_i = [y]_{q_i} - [h]_{q_i}:
+//   INTT(u_l) = (INTT(ax_l + P E_l) - conv_l) P^{-1}                       (JobKsDrop: one INTT)
+//   out_i     = (ax_i + P E_i - NTT(conv_i + P y'_i)) (P q_l)^{-1}          (JobKsDataRs: one NTT)
+// -- the same residues as the two-step form, with Lc + 1 transforms per part instead of 2 Lc + 1.
+struct KsEpi32 {   // the epilogue terms E(n) of a bound block (as JobKsData::P32::fin adds them)
+  const u64* add;
+  const u64* acc;
+  const u64* sq0;
+  const u64* sq1;
+  u32 g;
+  int logN;
+  bool gather;
+  __device__ __forceinline__ u32 at(u32 n, u32 q, const PrimeD& P) const {
+    u32 e = add ? (u32)add[gather ? galois_src(n, g, logN) : n] : 0u;
+    if (sq0) {
+      const u32 t = (u32)mul_mod(sq0[n], sq1 ? sq1[n] : sq0[n], P);
+      e = add32(e, sq1 ? add32(t, t, q) : t, q);
+    }
+    if (acc) e = add32(e, (u32)acc[n], q);
+    return e;
+  }
+};
+__device__ __forceinline__ KsEpi32 bind_epi32(const KsArgs& a, int b, int part, int i) {
+  const size_t LN = (size_t)a.Lc * a.N;
+  KsEpi32 e{nullptr, nullptr, nullptr, nullptr, a.gal[0], a.logN, false};
+  e.gather = a.add_gather && e.g != 1;
+  if (part < a.add_parts) e.add = a.addsrc + (size_t)b * a.add_bs + part * LN + (size_t)i * a.N;
+  if (a.acc_in) e.acc = a.acc_in + (size_t)b * a.out_bs + part * LN + (size_t)i * a.N;
+  if (a.sq_src) {
+    e.sq0 = a.sq_src + (size_t)b * a.sq_bs + (size_t)i * a.N;
+    if (part == 1) e.sq1 = e.sq0 + LN;
+  }
+  return e;
+}
+
+// The dropped limb l = Lc - 1: y[b][part] = INTT(ax_l + P E_l) - conv_l) P^{-1} + (q_l - 1)/2 (u32 rows).
+struct JobKsDrop {
+  static constexpr const char* kName = "ks_rescale_drop";
+  KsArgs a;
+  u32* y;   // [B][2][N]
+  int N;
+  __device__ int prime(int) const { return a.Lc - 1; }
+  struct B32 {
+    KsEpi32 e;
+    const PrimeD* P;
+    const u32* ax;
+    const u32* tb;
+    u32* y;
+    u32 q, mu32, ph, pinv, pinvsh, pm, pmsh, h;
+    __device__ __forceinline__ u64 load(u32 n) const {
+      return add32(ax[n], mulsh32(e.at(n, q, *P), pm, pmsh, q), q);
+    }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      const u32 conv = sub32(red32(tb[n], q, mu32), ph, q);
+      y[n] = add32(mulsh32(sub32((u32)v, conv, q), pinv, pinvsh, q), h, q);
+    }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    const int b = blk >> 1, part = blk & 1, l = a.Lc - 1;
+    const u32 q = (u32)P.q, pinv = (u32)__ldg(a.Pinv_mod + l), pm = (u32)__ldg(a.P_mod + l);
+    return B32{bind_epi32(a, b, part, l), &P,
+               reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + l) * a.N,
+               reinterpret_cast<const u32*>(a.tb) + ((size_t)b * 2 + part) * a.N, y + ((size_t)b * 2 + part) * a.N,
+               q, mu32_of(P), (u32)__ldg(a.Ph_mod + l), pinv, shoup_companion32(pinv, q), pm,
+               shoup_companion32(pm, q), (u32)((P.q - 1) >> 1)};
+  }
+  // generic form (only small-prime contexts take this path; the 64-bit engine instantiates it)
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const { return bind32(blk, P).load(n); }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const { bind32(blk, P).store(n, v); }
+};
+
+// Data limbs i < l of the rescaled result: out_i = (ax_i + P E_i - NTT(conv_i + P y'_i)) (P q_l)^{-1} + bias.
+struct JobKsDataRs {
+  static constexpr const char* kName = "ks_rescale";
+  KsArgs a;
+  const u32* y;       // JobKsDrop's rows
+  u64* out;           // [B][2][Lc-1][N] (item stride out_bs)
+  size_t out_bs;
+  const u64* rs_h;    // row l of rs_h: (q_l - 1)/2 mod q_i
+  const u64* rs_qinv; // row l of rs_qinv: q_l^{-1} mod q_i
+  const u64* bias;    // nullable: poly 0 gets + bias[b * bias_bs + i * N + n]
+  size_t bias_bs;
+  int N;
+  __device__ int prime(int blk) const { return blk % (a.Lc - 1); }
+  struct B32 {
+    KsEpi32 e;
+    const PrimeD* P;
+    const u32* ax;
+    const u32* tb;
+    const u32* y;
+    u64* out;
+    const u64* bias;
+    u32 q, mu32, ph, hr, pm, pmsh, cinv, cinvsh;
+    __device__ __forceinline__ u64 load(u32 n) const {
+      const u32 conv = sub32(red32(tb[n], q, mu32), ph, q);
+      const u32 yy = sub32(red32(y[n], q, mu32), hr, q);
+      return add32(conv, mulsh32(yy, pm, pmsh, q), q);
+    }
+    __device__ __forceinline__ u32 fin(u32 n, u32 v, u32 axv, u32 ev, u32 bv) const {
+      const u32 w = add32(axv, mulsh32(ev, pm, pmsh, q), q);
+      u32 o = mulsh32(sub32(w, v, q), cinv, cinvsh, q);
+      return bias ? add32(o, bv, q) : o;
+    }
+    __device__ __forceinline__ void store(u32 n, u64 v) const {
+      out[n] = fin(n, (u32)v, ax[n], e.at(n, q, *P), bias ? (u32)bias[n] : 0u);
+    }
+    // 4 outputs n0 + u st: every operand load of the 4 is issued before the arithmetic
+    __device__ __forceinline__ void store4(u32 n0, u32 st, const u32* v) const {
+      u32 axv[4], ev[4], bv[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const u32 n = n0 + u * st;
+        axv[u] = ax[n];
+        ev[u] = e.at(n, q, *P);
+        if (bias) bv[u] = (u32)bias[n];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) out[n0 + u * st] = fin(n0 + u * st, v[u], axv[u], ev[u], bv[u]);
+    }
+  };
+  __device__ B32 bind32(int blk, const PrimeD& P) const {
+    const int i = blk % (a.Lc - 1), r = blk / (a.Lc - 1), b = r >> 1, part = r & 1;
+    const u32 q = (u32)P.q, pm = (u32)__ldg(a.P_mod + i);
+    const u32 cinv = (u32)mul_mod(__ldg(a.Pinv_mod + i), __ldg(rs_qinv + i), P);
+    return B32{bind_epi32(a, b, part, i), &P,
+               reinterpret_cast<const u32*>(a.accx) + (((size_t)b * 2 + part) * (a.Lc + a.K) + i) * a.N,
+               reinterpret_cast<const u32*>(a.tb) + (size_t)r * a.N, y + (size_t)r * a.N,
+               out + (size_t)b * out_bs + ((size_t)part * (a.Lc - 1) + i) * a.N,
+               bias && part == 0 ? bias + (size_t)b * bias_bs + (size_t)i * a.N : nullptr, q, mu32_of(P),
+               (u32)__ldg(a.Ph_mod + i), (u32)__ldg(rs_h + i), pm, shoup_companion32(pm, q), cinv,
+               shoup_companion32(cinv, q)};
+  }
+  __device__ u64 load(int blk, u32 n, const PrimeD& P) const { return bind32(blk, P).load(n); }
+  __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const { bind32(blk, P).store(n, v); }
+};
+
 // Rescale source: row r of x, or (conv, C18) the product ct_b (.) K_c formed on
 // the fly for row r = (b C + c) 2 + p, so the products never reach HBM.
 struct RescaleSrc {
@@ -881,6 +1023,8 @@ inline double alg_bytes(const JobKsData& j, int nblk) {
   return N8 * w;
 }
 inline double alg_bytes(const JobRescaleLast& j, int nblk) { return 16.0 * j.N * nblk; }
+inline double alg_bytes(const JobKsDrop& j, int nblk) { return 4.0 * j.N * nblk * 3 + 8.0 * j.N * nblk; }
+inline double alg_bytes(const JobKsDataRs& j, int nblk) { return 4.0 * j.N * nblk * 3 + 16.0 * j.N * nblk; }
 inline double alg_bytes(const JobRescaleData& j, int nblk) {
   return 8.0 * j.N * (2.0 * nblk + (double)nblk / (j.Lc - 1));
 }

@@ -1441,6 +1441,7 @@ static KsArgs ks_base(he_context* c, int B, int Lc, const u64* ext, const u64* d
   a.Pinv_mod = c->d_Pinv_mod;
   a.Phat_inv = c->d_Phat_inv;
   a.Phat_mod = c->d_Phat_mod;
+  a.P_mod = c->d_P_mod;
   return a;
 }
 
@@ -1455,13 +1456,33 @@ static void ks_launch(he_context* c, KsArgs& a) {
   launch_ntt<false>(c, jd, a.KB * a.B * 2 * a.Lc);
 }
 
+// ModDown fused with the rescale that follows it (JobKsDrop / JobKsDataRs, he_jobs.cuh): out holds
+// [B][2][Lc-1][N] words at item stride out_bs, + bias on poly 0.  The same words as ks_launch then
+// ct_rescale (exact: both transforms are linear), Lc + 1 transforms per part instead of 2 Lc + 1.
+static bool ks_rescale_ok(const KsArgs& a) {
+  return a.accx && a.accx32 && a.K == 1 && !a.D && a.KB == 1 && a.Lc >= 2;
+}
+static void ks_launch_rescale(he_context* c, KsArgs& a, u64* out, size_t out_bs, const he_plaintext* bias) {
+  Scratch tb(c, (size_t)a.B * 2 * a.K * a.N * 8), y(c, (size_t)a.B * 2 * a.N * 4);
+  a.tb = tb.as<u64>();
+  JobKsSpecial js{a};
+  launch_ntt<true>(c, js, a.B * 2 * a.K);
+  JobKsDrop jd{a, y.as<u32>(), a.N};
+  launch_ntt<true>(c, jd, a.B * 2);
+  const int l = a.Lc - 1;
+  JobKsDataRs jr{a, y.as<u32>(), out, out_bs, c->d_rs_h + (size_t)l * c->L, c->d_rs_qinv + (size_t)l * c->L,
+                 bias ? bias->d : nullptr, bias && bias->B != 1 ? (size_t)(a.Lc - 1) * a.N : 0, a.N};
+  launch_ntt<false>(c, jr, a.B * 2 * (a.Lc - 1));
+}
+
 // Fused small-prime key switch: INTT of the digit source, k_modup_ip32 (ModUp
 // and inner product without the extended digits in HBM), then the accx-mode
 // ModDown with the caller's epilogue (epi.out, addsrc, acc_in ...).
 static bool fused_ks_ok(he_context* c) { return c->small_primes && c->d_tw32 && c->logN <= 14; }
 
 static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, const u32* key32, u32 g,
-                     KsArgs& epi, int sq = 0) {
+                     KsArgs& epi, int sq = 0, u64* rs_out = nullptr, size_t rs_bs = 0,
+                     const he_plaintext* rs_bias = nullptr) {
   const size_t N = c->N;
   const int nt = Lc + c->K;
   Scratch coef(c, (size_t)B * Lc * N * 4), accx(c, (size_t)B * 2 * nt * N * 4);
@@ -1491,7 +1512,8 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
   epi.accx = accx.as<u64>();
   epi.accx32 = 1;
   epi.gal[0] = g;
-  ks_launch(c, epi);
+  if (rs_out) ks_launch_rescale(c, epi, rs_out, rs_bs, rs_bias);
+  else ks_launch(c, epi);
 }
 
 const u64* galois_key(he_context* c, int step, u32* gal_out) {
@@ -1528,6 +1550,37 @@ he_ciphertext* ct_square_relin(he_context* c, const he_ciphertext* x) {
   k.sq_bs = 2 * LN;
   try {
     ks_fused(c, x->d + LN, 2 * LN, x->B, Lc, c->d_rlk32, 1, k, 1);
+  } catch (...) {
+    ct_free(o);
+    throw;
+  }
+  return o;
+}
+
+// he_square on the fused path: square, relinearize and rescale with the rescale merged into the
+// ModDown (ks_launch_rescale); other contexts: ct_square_relin then ct_rescale.
+he_ciphertext* ct_square_rescale(he_context* c, const he_ciphertext* x) {
+  if (!(fused_ks_ok(c) && c->d_rlk32 && c->K == 1 && x->level >= 1)) {
+    he_ciphertext* r = ct_square_relin(c, x);
+    he_ciphertext* o = nullptr;
+    try {
+      o = ct_rescale(c, r);
+    } catch (...) {
+      ct_free(r);
+      throw;
+    }
+    ct_free(r);
+    return o;
+  }
+  const int Lc = x->level + 1;
+  const size_t LN = (size_t)Lc * c->N;
+  he_ciphertext* o = ct_new(c, x->B, 2, x->level - 1, x->scale * x->scale / (double)c->hp.q[x->level]);
+  KsArgs k = ks_base(c, x->B, Lc, nullptr, nullptr, 0);
+  k.out_bs = 2 * LN;   // (level-l strides of the epilogue terms)
+  k.sq_src = x->d;
+  k.sq_bs = 2 * LN;
+  try {
+    ks_fused(c, x->d + LN, 2 * LN, x->B, Lc, c->d_rlk32, 1, k, 1, o->d, 2 * (LN - c->N));
   } catch (...) {
     ct_free(o);
     throw;
@@ -1797,8 +1850,11 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
 // BSGS vec_mat: diags = G groups of g QP diagonals E[k2][k1].
 // Baby-step part: inner[k2] = ModDown(sum_{k1 < g} E[k2][k1] (.) rot(x, k1 step)) for the G
 // groups of diags (unrescaled, scale x.scale * diags.scale).
+// rescale (G == 1 only): inner[0] is returned rescaled (+ bias on poly 0), the rescale merged into
+// the ModDown on the fused path (ks_launch_rescale).
 static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
-                                              int g, int step) {
+                                              int g, int step, bool rescale = false,
+                                              const he_plaintext* bias = nullptr) {
   const int Lc = x->level + 1, B = x->B, nt = Lc + c->K, G = diags->B / g;
   const size_t N = c->N, LN = (size_t)Lc * N;
   std::vector<const u64*> keys(g);
@@ -1877,14 +1933,20 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
         }
         check_launch(c);
         for (int k2 = 0; k2 < G; ++k2) {
-          inner[k2] = ct_new(c, B, 2, x->level, x->scale * diags->scale);
           KsArgs a = ks_base(c, B, Lc, nullptr, nullptr, 0);
           a.gal[0] = 1;
           a.accx = reinterpret_cast<const u64*>(accx.as<u32>() + (size_t)k2 * B * 2 * nt * N);
           a.accx32 = 1;
-          a.out = inner[k2]->d;
           a.out_bs = 2 * LN;
-          ks_launch(c, a);
+          if (rescale && G == 1 && ks_rescale_ok(a)) {
+            inner[k2] = ct_new(c, B, 2, x->level - 1, x->scale * diags->scale / (double)c->hp.q[x->level]);
+            ks_launch_rescale(c, a, inner[k2]->d, 2 * (LN - N), bias);
+            rescale = false;   // done
+          } else {
+            inner[k2] = ct_new(c, B, 2, x->level, x->scale * diags->scale);
+            a.out = inner[k2]->d;
+            ks_launch(c, a);
+          }
         }
       } catch (...) {
         dfree(c, ext);
@@ -1899,6 +1961,12 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
         dfree(c, view.dm);
       }
     }
+    if (rescale) {   // not merged into the ModDown (other contexts): a separate rescale
+      if (G != 1) throw HeError(HE_INVALID_ARGUMENT, "internal: fused rescale with several giant-step groups");
+      he_ciphertext* r = ct_rescale(c, inner[0], bias);
+      ct_free(inner[0]);
+      inner[0] = r;
+    }
   } catch (...) {
     cleanup();
     throw;
@@ -1906,7 +1974,8 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
   return inner;
 }
 
-static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step);
+static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step, bool rescale = false,
+                                 const he_plaintext* bias = nullptr);
 
 // diags->fold_n > 1 (he_vec_mat_encode_bsgs_fold, oracle vec_mat_bsgs_fold): the giant-step sum
 // covers the first m = fold_step diagonals; the replicated-output fold sum_{t<fold_n} rot(., m t)
@@ -1922,6 +1991,10 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
     u32 gg;
     if (!galois_key(c, g * k2, &gg))
       throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for giant step " + std::to_string(g * k2));
+  }
+  if (G == 1 && fold_n <= 1) {   // one group, no fold: the rescale (+ bias) merged into the ModDown
+    std::vector<he_ciphertext*> one = bsgs_inner(c, x, diags, g, 1, true, bias);
+    return one[0];
   }
   std::vector<he_ciphertext*> inner = bsgs_inner(c, x, diags, g, 1);
   auto cleanup = [&] {
@@ -1940,16 +2013,16 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
       ct_free(acc);
       acc = s2;
     }
-    if (fold_n > 1) {
+    if (fold_n > 1) {   // the fold's ModDown carries the rescale (+ bias)
       he_ciphertext* f = nullptr;
       try {
-        f = ct_rot_sum(c, acc, fold_n, fold_step);
+        f = ct_rot_sum(c, acc, fold_n, fold_step, true, bias);
       } catch (...) {
         ct_free(acc);
         throw;
       }
       ct_free(acc);
-      acc = f;
+      return f;
     }
     he_ciphertext* res = ct_rescale(c, acc, bias);   // bias fused into the rescale's store
     ct_free(acc);
@@ -1966,8 +2039,10 @@ __global__ void k_fill_u64(u64* __restrict__ p, size_t n, u64 v) {
 
 // sum_{k < n} rot(x, k step) with ONE lazy ModDown: the baby-step machinery with unit
 // diagonals (the plaintext polynomial 1, whose NTT words are all 1); scale unchanged.
-static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step) {
+static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step, bool rescale,
+                                 const he_plaintext* bias) {
   if (n == 1) {
+    if (rescale) return ct_rescale(c, x, bias);
     he_ciphertext* o = ct_new(c, x->B, x->size, x->level, x->scale);
     HE_CK(cudaMemcpyAsync(o->d, x->d, ct_words(x) * 8, cudaMemcpyDeviceToDevice, c->stream));
     return o;
@@ -1977,7 +2052,7 @@ static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, i
   try {
     k_fill_u64<<<148 * 4, 256, 0, c->stream>>>(ones->d, pt_words(ones), 1);
     check_launch(c);
-    inner = bsgs_inner(c, x, ones, n, step);
+    inner = bsgs_inner(c, x, ones, n, step, rescale, bias);
   } catch (...) {
     pt_free(ones);
     throw;
@@ -2043,13 +2118,10 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
 // unit-diagonal rotation sum, + bias.
 he_ciphertext* ct_conv_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                             const he_plaintext* bias, int chunk, int g) {
-  std::vector<he_ciphertext*> inner = bsgs_inner(c, x, diags, g, chunk);
-  he_ciphertext* v = inner[0];
-  he_ciphertext* r = nullptr;
+  std::vector<he_ciphertext*> inner = bsgs_inner(c, x, diags, g, chunk, true);   // rescale merged
+  he_ciphertext* v = nullptr;
+  he_ciphertext* r = inner[0];
   try {
-    r = ct_rescale(c, v);
-    ct_free(v);
-    v = nullptr;
     const int n2 = c->N / 2 / chunk / g;
     if (n2 > 1) {
       he_ciphertext* r2 = ct_rot_sum(c, r, n2, chunk * g);

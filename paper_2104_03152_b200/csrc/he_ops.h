@@ -57,6 +57,7 @@ he_ciphertext* ct_tensor(he_context* c, const he_ciphertext* x, const he_ciphert
 he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a, const he_plaintext* bias = nullptr);
 he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a);
 he_ciphertext* ct_square_relin(he_context* c, const he_ciphertext* x);
+he_ciphertext* ct_square_rescale(he_context* c, const he_ciphertext* x);
 he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool add_input);
 he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                           const he_plaintext* bias);
