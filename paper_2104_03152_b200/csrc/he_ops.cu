@@ -1673,6 +1673,45 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
   return o;
 }
 
+// acc + rot(a, step) with the addition in the rotation's ModDown epilogue (fused small-prime key
+// switch: acc_in); other contexts: rotate, then add.
+static he_ciphertext* ct_rotate_acc(he_context* c, const he_ciphertext* a, int step, const he_ciphertext* acc) {
+  const int Lc = a->level + 1;
+  const size_t LN = (size_t)Lc * c->N;
+  u32 g = 0;
+  const u64* key = galois_key(c, step, &g);
+  if (!key) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
+  auto it32 = c->gk32.find(g);
+  if (!(fused_ks_ok(c) && it32 != c->gk32.end() && acc->level == a->level && acc->B == a->B && acc->size == 2)) {
+    he_ciphertext* r = ct_rotate(c, a, step, false);
+    he_ciphertext* s2 = nullptr;
+    try {
+      s2 = ct_binop(c, 0, acc, r);
+    } catch (...) {
+      ct_free(r);
+      throw;
+    }
+    ct_free(r);
+    return s2;
+  }
+  he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
+  KsArgs k = ks_base(c, a->B, Lc, nullptr, nullptr, 0);
+  k.out = o->d;
+  k.out_bs = 2 * LN;
+  k.addsrc = a->d;
+  k.add_bs = 2 * LN;
+  k.add_parts = 1;
+  k.add_gather = 1;
+  k.acc_in = acc->d;
+  try {
+    ks_fused(c, a->d + LN, 2 * LN, a->B, Lc, it32->second, g, k);
+  } catch (...) {
+    ct_free(o);
+    throw;
+  }
+  return o;
+}
+
 // vec_mat with pre-encoded diagonals (a14, C17): acc = sum_k rot(x, k) (.) D_k
 // with all rotations hoisted (one ModUp of c1 shared by every k), then one
 // rescale and the bias.
@@ -1854,7 +1893,8 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
 // the ModDown on the fused path (ks_launch_rescale).
 static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                                               int g, int step, bool rescale = false,
-                                              const he_plaintext* bias = nullptr) {
+                                              const he_plaintext* bias = nullptr,
+                                              const he_plaintext* add_pt = nullptr) {
   const int Lc = x->level + 1, B = x->B, nt = Lc + c->K, G = diags->B / g;
   const size_t N = c->N, LN = (size_t)Lc * N;
   std::vector<const u64*> keys(g);
@@ -1938,6 +1978,13 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
           a.accx = reinterpret_cast<const u64*>(accx.as<u32>() + (size_t)k2 * B * 2 * nt * N);
           a.accx32 = 1;
           a.out_bs = 2 * LN;
+          if (add_pt && G == 1 && !rescale) {   // + plaintext on poly 0 in the ModDown epilogue
+            a.addsrc = add_pt->d;
+            a.add_bs = add_pt->B == 1 ? 0 : LN;
+            a.add_parts = 1;
+            a.add_gather = 0;
+            add_pt = nullptr;   // done
+          }
           if (rescale && G == 1 && ks_rescale_ok(a)) {
             inner[k2] = ct_new(c, B, 2, x->level - 1, x->scale * diags->scale / (double)c->hp.q[x->level]);
             ks_launch_rescale(c, a, inner[k2]->d, 2 * (LN - N), bias);
@@ -1961,6 +2008,12 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
         dfree(c, view.dm);
       }
     }
+    if (add_pt) {   // not merged into the ModDown: a separate add_plain
+      if (G != 1 || rescale) throw HeError(HE_INVALID_ARGUMENT, "internal: epilogue add with several groups");
+      he_ciphertext* r = ct_add_plain(c, inner[0], add_pt);
+      ct_free(inner[0]);
+      inner[0] = r;
+    }
     if (rescale) {   // not merged into the ModDown (other contexts): a separate rescale
       if (G != 1) throw HeError(HE_INVALID_ARGUMENT, "internal: fused rescale with several giant-step groups");
       he_ciphertext* r = ct_rescale(c, inner[0], bias);
@@ -1975,7 +2028,7 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
 }
 
 static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step, bool rescale = false,
-                                 const he_plaintext* bias = nullptr);
+                                 const he_plaintext* bias = nullptr, const he_plaintext* add_pt = nullptr);
 
 // diags->fold_n > 1 (he_vec_mat_encode_bsgs_fold, oracle vec_mat_bsgs_fold): the giant-step sum
 // covers the first m = fold_step diagonals; the replicated-output fold sum_{t<fold_n} rot(., m t)
@@ -2004,12 +2057,16 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
     // giant steps: acc = sum_k2 rot(inner_k2, g k2)
     he_ciphertext* acc = inner[0];
     inner[0] = nullptr;
-    for (int k2 = 1; k2 < G; ++k2) {
-      he_ciphertext* r = ct_rotate(c, inner[k2], g * k2, false);
+    for (int k2 = 1; k2 < G; ++k2) {   // acc + rot(inner_k2, g k2), the add in the ModDown epilogue
+      he_ciphertext* s2 = nullptr;
+      try {
+        s2 = ct_rotate_acc(c, inner[k2], g * k2, acc);
+      } catch (...) {
+        ct_free(acc);
+        throw;
+      }
       ct_free(inner[k2]);
       inner[k2] = nullptr;
-      he_ciphertext* s2 = ct_binop(c, 0, acc, r);
-      ct_free(r);
       ct_free(acc);
       acc = s2;
     }
@@ -2040,9 +2097,10 @@ __global__ void k_fill_u64(u64* __restrict__ p, size_t n, u64 v) {
 // sum_{k < n} rot(x, k step) with ONE lazy ModDown: the baby-step machinery with unit
 // diagonals (the plaintext polynomial 1, whose NTT words are all 1); scale unchanged.
 static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, int step, bool rescale,
-                                 const he_plaintext* bias) {
+                                 const he_plaintext* bias, const he_plaintext* add_pt) {
   if (n == 1) {
     if (rescale) return ct_rescale(c, x, bias);
+    if (add_pt) return ct_add_plain(c, x, add_pt);
     he_ciphertext* o = ct_new(c, x->B, x->size, x->level, x->scale);
     HE_CK(cudaMemcpyAsync(o->d, x->d, ct_words(x) * 8, cudaMemcpyDeviceToDevice, c->stream));
     return o;
@@ -2052,7 +2110,7 @@ static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, i
   try {
     k_fill_u64<<<148 * 4, 256, 0, c->stream>>>(ones->d, pt_words(ones), 1);
     check_launch(c);
-    inner = bsgs_inner(c, x, ones, n, step, rescale, bias);
+    inner = bsgs_inner(c, x, ones, n, step, rescale, bias, add_pt);
   } catch (...) {
     pt_free(ones);
     throw;
@@ -2123,12 +2181,11 @@ he_ciphertext* ct_conv_bsgs(he_context* c, const he_ciphertext* x, const he_plai
   he_ciphertext* r = inner[0];
   try {
     const int n2 = c->N / 2 / chunk / g;
-    if (n2 > 1) {
-      he_ciphertext* r2 = ct_rot_sum(c, r, n2, chunk * g);
+    if (n2 > 1) {   // + bias in the rotation sum's ModDown epilogue
+      he_ciphertext* r2 = ct_rot_sum(c, r, n2, chunk * g, false, nullptr, bias);
       ct_free(r);
       r = r2;
-    }
-    if (bias) {
+    } else if (bias) {
       he_ciphertext* r2 = ct_add_plain(c, r, bias);
       ct_free(r);
       r = r2;
