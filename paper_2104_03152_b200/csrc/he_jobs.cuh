@@ -43,6 +43,11 @@ struct has_prefetch : std::false_type {};
 template <class B>
 struct has_prefetch<B, std::void_t<decltype(std::declval<const B&>().prefetch(0u))>> : std::true_type {};
 
+template <class J, class = void>
+struct has_gather_src : std::false_type {};
+template <class J>
+struct has_gather_src<J, std::void_t<decltype(std::declval<const J&>().gather_src(0u))>> : std::true_type {};
+
 template <class B, class = void>
 struct has_load4 : std::false_type {};
 template <class B>
@@ -276,6 +281,12 @@ struct JobModUp {
   u64* ext;
   const u64* qtab;   // device table of all primes
   int N, Lc, K, L;
+  // gal != 1: the extended digits are stored already permuted by the rotation, ext[n] = X[pi_g(n)]
+  // (gathered from shared memory in the transform's epilogue), so the inner product reads them
+  // coalesced (k_ks_ip64).  pi_g keeps the top index bit for g = 5^k (the halves of a 2-CTA limb).
+  u32 gal = 1;
+  int logN = 0;
+  __device__ __forceinline__ u32 gather_src(u32 n) const { return gal == 1 ? n : galois_src(n, gal, logN); }
   __device__ void dec(int blk, int& b, int& j, int& t) const {
     const int nt = Lc + K - 1;
     b = blk / (Lc * nt);

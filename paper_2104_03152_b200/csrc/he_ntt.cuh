@@ -256,7 +256,9 @@ k_ntt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __restrict__
 #pragma unroll
     for (int kk = 0; kk < CS; ++kk) {
       const u32 i = tid + (c * CS + kk) * G::T;
-      u64 v = sm[spad(i)];
+      u32 si = i;   // jobs storing a permuted transform read word gather_src(n) of their own half
+      if constexpr (has_gather_src<Job>::value) si = job.gather_src(gbase + i) - gbase;
+      u64 v = sm[spad(si)];
       v = v >= P.two_q ? v - P.two_q : v;
       v = v >= P.q ? v - P.q : v;
       job.store(blk, gbase + i, v, P);

@@ -1399,14 +1399,85 @@ he_ciphertext* ct_rescale(he_context* c, const he_ciphertext* a, const he_plaint
 
 // ---- key switching (a9/a10, C12/C15/C16) -------------------------------------
 // ModUp of the digit source (NTT words, item stride bs): returns ext [B][Lc][Lc+K][N].
-static u64* modup(he_context* c, const u64* dsrc, size_t bs, int B, int Lc) {
+static u64* modup(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, u32 gal = 1) {
   const size_t N = c->N;
   Scratch coef(c, (size_t)B * Lc * N * 8);
   ntt_rows(c, dsrc, coef.as<u64>(), B, Lc, bs, (size_t)Lc * N, true);
   u64* ext = dalloc_t<u64>(c, (size_t)B * Lc * (Lc + c->K) * N);
-  JobModUp j{coef.as<u64>(), ext, c->d_q, c->N, Lc, c->K, c->L};
+  JobModUp j{coef.as<u64>(), ext, c->d_q, c->N, Lc, c->K, c->L, gal, c->logN};
   launch_ntt<false>(c, j, B * Lc * (Lc + c->K - 1));
   return ext;
+}
+
+// Key inner products of a (non-hoisted) key switch as one coalesced pass (64-bit contexts): for every
+// item b, target limb t < Lc + K and position n,
+//   accx[b][p][t][n] = sum_j X_j[t][n] ksk[j][p][t][n],  p = 0, 1,
+// with X_j[t] the extended digit already permuted by pi_g (modup with gal) and, for t == j, the digit's
+// own NTT word at pi_g(n).  Both parts share every digit load; the ModDown then runs in accx mode.
+// Products (< q^2 < 2^120) are summed in 128 bits and reduced once per 8 terms (as ks_inner).
+__global__ void k_ks_ip64(const u64* __restrict__ ext, const u64* __restrict__ dsrc, size_t dsrc_bs,
+                          const u64* __restrict__ key, u64* __restrict__ accx, const PrimeD* __restrict__ primes,
+                          int N, int logN, int Lc, int K, int L, int NP, u32 gal, int ext_permuted) {
+  const int nt = Lc + K, t = blockIdx.y, b = blockIdx.z;
+  const int tp = t < Lc ? t : L + (t - Lc);
+  const PrimeD P = load_prime(primes, tp);
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const u32 sn = gal == 1 ? (u32)n : galois_src((u32)n, gal, logN);
+    u64 acc0 = 0, acc1 = 0;
+    for (int j0 = 0; j0 < Lc; j0 += 8) {
+      u64 lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+      const int j1 = min(Lc, j0 + 8);
+      for (int j = j0; j < j1; ++j) {
+        const u64 x = (t == j) ? __ldg(dsrc + (size_t)b * dsrc_bs + (size_t)j * N + sn)
+                               : __ldg(ext + (((size_t)b * Lc + j) * nt + t) * N + (ext_permuted ? (u32)n : sn));
+        const u64 k0 = __ldg(key + (((size_t)j * 2 + 0) * NP + tp) * N + n);
+        const u64 k1 = __ldg(key + (((size_t)j * 2 + 1) * NP + tp) * N + n);
+        u64 pl = x * k0, ph = __umul64hi(x, k0);
+        lo0 += pl;
+        hi0 += ph + (lo0 < pl);
+        pl = x * k1;
+        ph = __umul64hi(x, k1);
+        lo1 += pl;
+        hi1 += ph + (lo1 < pl);
+      }
+      acc0 = add_mod(acc0, add_mod(mul_mod(hi0, P.r64, P), reduce64(lo0, P), P.q), P.q);
+      acc1 = add_mod(acc1, add_mod(mul_mod(hi1, P.r64, P), reduce64(lo1, P), P.q), P.q);
+    }
+    accx[(((size_t)b * 2 + 0) * nt + t) * N + n] = acc0;
+    accx[(((size_t)b * 2 + 1) * nt + t) * N + n] = acc1;
+  }
+}
+
+static void ks_launch(he_context* c, KsArgs& a);
+// ModUp (permuted by gal) + k_ks_ip64 + the accx-mode ModDown with the caller's epilogue (64-bit path).
+static void ks_materialized(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, const u64* key, u32 g,
+                            KsArgs& epi) {
+  const size_t N = c->N;
+  const int nt = Lc + c->K;
+  // the 2-CTA transforms (N >= 2^14) can permute inside a half only: pi_g keeps the top index bit iff
+  // g = 1 mod 4 (every rotation element 5^k); otherwise the inner product gathers
+  const bool permute = g == 1 || g % 4 == 1 || c->logN < 14;
+  u64* ext = modup(c, dsrc, bs, B, Lc, permute ? g : 1);
+  try {
+    Scratch accx(c, (size_t)B * 2 * nt * N * 8);
+    {
+      const double bytes = 8.0 * N * ((double)B * Lc * nt + 2.0 * Lc * nt + 2.0 * B * nt);
+      ProfScope ps_(c, "ks_ip", bytes, B * nt, (double)B * nt * Lc * 2 * N);
+      k_ks_ip64<<<dim3((unsigned)((N + 255) / 256), (unsigned)nt, (unsigned)B), 256, 0, c->stream>>>(
+          ext, dsrc, bs, key, accx.as<u64>(), c->d_primes, (int)N, c->logN, Lc, c->K, c->L, c->NP, g,
+          permute ? 1 : 0);
+    }
+    check_launch(c);
+    epi.ext = nullptr;
+    epi.accx = accx.as<u64>();
+    epi.accx32 = 0;
+    epi.gal[0] = g;
+    ks_launch(c, epi);
+  } catch (...) {
+    dfree(c, ext);
+    throw;
+  }
+  dfree(c, ext);
 }
 
 // Small-prime ModUp: u32 digits and u32 extended digits ([B][Lc][Lc+K][N] u32).
@@ -1607,22 +1678,18 @@ he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a) {
     }
     return o;
   }
-  u64* ext = modup(c, a->d + 2 * LN, 3 * LN, a->B, Lc);
-  KsArgs k = ks_base(c, a->B, Lc, ext, a->d + 2 * LN, 3 * LN);
-  k.keys[0] = c->d_rlk;
-  k.gal[0] = 1;
+  KsArgs k = ks_base(c, a->B, Lc, nullptr, a->d + 2 * LN, 3 * LN);
   k.out = o->d;
   k.out_bs = 2 * LN;
   k.addsrc = a->d;
   k.add_bs = 3 * LN;
   k.add_parts = 2;
   try {
-    ks_launch(c, k);
+    ks_materialized(c, a->d + 2 * LN, 3 * LN, a->B, Lc, c->d_rlk, 1, k);
   } catch (...) {
-    dfree(c, ext);
+    ct_free(o);
     throw;
   }
-  dfree(c, ext);
   return o;
 }
 
@@ -1652,10 +1719,7 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
     }
     return o;
   }
-  u64* ext = modup(c, a->d + LN, 2 * LN, a->B, Lc);
-  KsArgs k = ks_base(c, a->B, Lc, ext, a->d + LN, 2 * LN);
-  k.keys[0] = key;
-  k.gal[0] = g;
+  KsArgs k = ks_base(c, a->B, Lc, nullptr, a->d + LN, 2 * LN);
   k.out = o->d;
   k.out_bs = 2 * LN;
   k.addsrc = a->d;
@@ -1664,12 +1728,11 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
   k.add_gather = 1;
   if (add_input) k.acc_in = a->d;
   try {
-    ks_launch(c, k);
+    ks_materialized(c, a->d + LN, 2 * LN, a->B, Lc, key, g, k);
   } catch (...) {
-    dfree(c, ext);
+    ct_free(o);
     throw;
   }
-  dfree(c, ext);
   return o;
 }
 
