@@ -55,6 +55,33 @@ __device__ __forceinline__ void step(uint32_t& x, uint32_t a, uint32_t b, uint64
     const uint32_t m = (uint32_t)s * 0x7ffdffffu;
     const uint32_t t = (uint32_t)((s + (uint64_t)m * 0x7ffe0001u) >> 32);
     x = min(t, t - 0x7ffe0001u);
+  } else if constexpr (OP == 9) {  // 64-bit Harvey Cooley-Tukey butterfly (the cfg2 / cfg3 NTT's step): the pair
+    // (w, x-as-64) in [0, 4q): X = w mod 2q; T = y*tw - hi64(y*twsh)*q; w' = X + T; y' = X - T + 2q
+    const uint64_t q = 0x0ffffffffffc0001ull, two_q = 2 * q;
+    const uint64_t tw = (uint64_t)a << 28 | b, twsh = (uint64_t)b << 32 | a;
+    uint64_t y = (uint64_t)x << 29 | x;
+    const uint64_t X = w >= two_q ? w - two_q : w;
+    const uint64_t T = y * tw - __umul64hi(y, twsh) * q;
+    w = X + T;
+    y = X - T + two_q;
+    x = (uint32_t)(y >> 13);
+  } else if constexpr (OP == 10) { // 32-bit strict Cooley-Tukey butterfly (31-bit primes: values in [0, q))
+    const uint32_t q = 0x7ffe0001u;
+    uint32_t y = (uint32_t)w;
+    const uint32_t r = y * a - __umulhi(y, b) * q;
+    const uint32_t T = min(r, r - q);
+    const uint32_t u = min(x + T, x + T - q);
+    y = min(x - T + q, x - T);
+    x = u;
+    w = y;
+  } else if constexpr (OP == 11) { // 32-bit lazy Cooley-Tukey butterfly (q < 2^30: values in [0, 4q))
+    const uint32_t q = 0x3ffc0001u;
+    uint32_t y = (uint32_t)w;
+    const uint32_t X = min(x, x - 2 * q);
+    const uint32_t T = y * a - __umulhi(y, b) * q;
+    x = X + T;
+    y = X - T + 2 * q;
+    w = y;
   }
 }
 
@@ -132,7 +159,10 @@ int main() {
   run<5>("LOP3", 2, sms, d_out, false);
   run<6>("shoup32_modmul", 0, sms, d_out, false);
   run<7>("umul64hi", 0, sms, d_out, false);
-  run<8>("mont_mac_pair_redc", 0, sms, d_out, true);
+  run<8>("mont_mac_pair_redc", 0, sms, d_out, false);
+  run<9>("ct_butterfly_64bit_harvey", 0, sms, d_out, false);
+  run<10>("ct_butterfly_32bit_strict", 0, sms, d_out, false);
+  run<11>("ct_butterfly_32bit_lazy", 0, sms, d_out, true);
   printf(" }\n}\n");
   g_stop = true;
   t.join();
