@@ -53,6 +53,9 @@ def _load_json(rel):
 
 
 INT_PEAK = _load_json("profiles/r02/int_peak.json")
+# dependent-free NTT butterfly chains (profiles/int_peak.cu ops 9-11): the integer roof of a transform
+INT_PEAK2 = _load_json("profiles/r02/int_peak_v2.json") or {}
+BFLY64_GPS = (INT_PEAK2.get("ops", {}).get("ct_butterfly_64bit_harvey", {}) or {}).get("G_lane_steps_per_s")
 PIPE_MIX = _load_json("profiles/r02/pipe_mix.json") or {}
 
 
@@ -355,7 +358,7 @@ def micro_extra(ctx_cnn, stream, dev):
                        "fwd_GBps": round(nbytes / s_f / 1e9, 1), "inv_GBps": round(nbytes / s_i / 1e9, 1),
                        "fused_fwd_mul_inv_GBps": round(24 * N * L * B / s_m / 1e9, 1),
                        "roofline": roofline_block("ntt_cfg2_fwd", nbytes / s_f / 1e9, 0.5 * N * 14 * L * B / s_f / 1e9,
-                                                  peaks)}
+                                                  peaks, bfly_peak=BFLY64_GPS)}
     del a, b, o
     # config 3: N=16384, 8 data + 2 special 50-bit primes, 256 ciphertexts, rotations by 2^r and ct x ct
     c3 = Context(CFG3.logN, CFG3.bits, CFG3.n_special, CFG3.seed)
@@ -396,7 +399,7 @@ def micro_extra(ctx_cnn, stream, dev):
     return out
 
 
-def roofline_block(tag, gbs, gops, peaks, kernel=None, share=None):
+def roofline_block(tag, gbs, gops, peaks, kernel=None, share=None, bfly_peak=None):
     """Roofline of a secondary metric's dominant kernel: HBM fraction of the algorithmic bytes, and the
     integer-pipe fraction from the ncu-measured mix of that kernel (profiles/r02/pipe_mix.json entry
     `tag`: the modop rate at which its busiest pipe saturates), when captured."""
@@ -409,6 +412,10 @@ def roofline_block(tag, gbs, gops, peaks, kernel=None, share=None):
         peak = mix["alg_ops_per_launch"] / (mix["ncu_duration_s"] * mix["busiest_pipe_util"]) / 1e9
         r.update({"bound": "alu", "alu_peak_Gmodops": round(peak, 1), "alu_frac": round(gops / peak, 4),
                   "busiest_pipe": mix["busiest_pipe"], "peak_source": "ncu mix (profiles/r02/pipe_mix.json)"})
+    elif bfly_peak:   # a plain transform: its modops are butterflies, the roof the measured butterfly rate
+        r.update({"bound": "alu", "alu_peak_Gmodops": round(bfly_peak, 1), "alu_frac": round(gops / bfly_peak, 4),
+                  "peak_source": "dependent-free 64-bit Harvey butterfly chain measured on B200 "
+                                 "(profiles/int_peak.cu -> profiles/r02/int_peak_v2.json)"})
     return r
 
 

@@ -175,7 +175,14 @@ he_status he_encode(he_context* ctx, const double* z, size_t n_per_item, size_t 
  * and the encode kernels on the context's stream.  z is read by that copy:
  * pageable memory may be reused when the call returns; page-locked memory
  * (cudaHostAlloc, torch pin_memory) must stay unchanged until the stream has
- * passed the call (he_sync, or an event recorded on the stream). */
+ * passed the call (he_sync, or an event recorded on the stream).
+ * Inputs of 1 MiB or more (a batch of slot vectors; he_encode and
+ * he_encode_encrypt) are copied on a copy stream of the context's own into one
+ * of two context-owned device buffers, and the context's stream waits for the
+ * copy: in a pipelined client loop the upload of batch i+1 then overlaps the
+ * kernels of batch i instead of queueing behind them.  Ordering as seen from
+ * the context's stream is unchanged.  Smaller inputs, and calls recorded into
+ * a CUDA graph, are copied on the context's stream itself. */
 /* Same, with z already in device memory, and ASYNCHRONOUS: it only enqueues
  * work on the context's stream (a server pipeline never drains the device at
  * an encode).  A |scale z| >= 2^62 overflow is then reported as
@@ -440,6 +447,14 @@ he_status he_pt_limbs(const he_plaintext* pt, int* limbs);
 he_status he_key_export(he_context* ctx, int kind, int32_t step, uint64_t* dst);
 /* Number of words he_key_export writes for `kind`. */
 size_t he_key_words(const he_context* ctx, int kind);
+/* Device bytes the context's public, relinearisation and Galois keys occupy right
+ * now.  Keys at rest: a context whose primes are all < 2^31 (the
+ * 32-bit engine, BASELINE config 4) keeps every switching key as 32-bit words in
+ * Montgomery form only, 4 bytes per residue; the 64-bit words of a key are built
+ * from them the first time something asks for them (he_key_export, the per-rotation
+ * he_vec_mat_pt form and the other unfused paths) and then stay.  Other contexts
+ * hold 64-bit words (8 bytes per residue).  0 for a null context. */
+size_t he_key_bytes(const he_context* ctx);
 
 /* ---- wire format ("427KB of communication") ----
  * A 64-byte header (magic "HECKKS01", u32 log2N, u32 B, u32 size, u32 level,

@@ -130,6 +130,7 @@ _SIGS = {
     "he_vec_mat_encode_lazy": [VP, DP, C.c_int, C.c_int, DP, C.c_int, C.c_int, C.c_int, C.c_double, VPP, VPP],
     "he_key_export": [VP, C.c_int, C.c_int32, U64P],
     "he_key_words": [VP, C.c_int],
+    "he_key_bytes": [VP],
     "he_ct_serialized_size": [VP, VP, C.POINTER(SZ)],
     "he_ct_serialize": [VP, VP, VP, C.c_int],
     "he_ct_serialized_size_seeded": [VP, VP, C.POINTER(SZ)],
@@ -149,7 +150,7 @@ _SIGS = {
     "he_profile_read": [VP, C.c_char_p, SZ],
     "he_last_error": [],
 }
-_RESTYPES = {"he_key_words": C.c_size_t, "he_launch_count": C.c_uint64, "he_graph_kernels": C.c_uint64, "he_last_error": C.c_char_p}
+_RESTYPES = {"he_key_words": C.c_size_t, "he_key_bytes": C.c_size_t, "he_launch_count": C.c_uint64, "he_graph_kernels": C.c_uint64, "he_last_error": C.c_char_p}
 
 _lib = None
 
@@ -445,6 +446,10 @@ class Context:
         def free(ptr, nbytes, stream):
             torch.cuda.caching_allocator_delete(ptr)
         self.he_set_allocator(alloc, free)
+
+    def he_key_bytes(self) -> int:
+        """Device bytes held by the public, relinearisation and Galois keys (keys at rest)."""
+        return int(lib().he_key_bytes(self.h))
 
     def he_key_export(self, kind: int, step: int = 0) -> np.ndarray:
         n = int(lib().he_key_words(self.h, kind))

@@ -59,6 +59,58 @@ struct DevDoubles {
   ~DevDoubles() { dfree(c, d); }
 };
 
+// A large host input of the encoder (a batch of slot vectors): uploaded on the context's copy stream
+// into one of two context-owned buffers, so that the copy of this call runs while the kernels of the
+// previous calls are still executing on c->stream (the host runs ahead of the device in a pipelined
+// client loop; on c->stream the copy would queue behind them and the device would idle for its
+// duration every step).  c->stream waits for the copy; the copy stream waits, before it refills a
+// buffer, for the event recorded after the kernels that read it were enqueued.  Small inputs and
+// calls recorded into a CUDA graph take the plain path (DevDoubles).
+struct DevDoublesOverlap {
+  he_context* c;
+  double* d = nullptr;
+  int k = -1;          // >= 0: upload buffer k; -1: a pool block (plain path)
+  static constexpr size_t kMinBytes = 1u << 20;
+  DevDoublesOverlap(he_context* c_, const double* h, size_t n) : c(c_) {
+    const size_t bytes = n * 8;
+    if (bytes < kMinBytes || c->rec) {
+      d = dalloc_t<double>(c, n);
+      if (n) HE_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
+      return;
+    }
+    auto& u = c->up;
+    if (!u.stream) {
+      HE_CK(cudaStreamCreateWithFlags(&u.stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        HE_CK(cudaEventCreateWithFlags(&u.done[i], cudaEventDisableTiming));
+        HE_CK(cudaEventCreateWithFlags(&u.free_[i], cudaEventDisableTiming));
+      }
+    }
+    k = u.next;
+    u.next ^= 1;
+    if (u.cap[k] < bytes) {   // (re)size: the buffer's readers must have finished
+      if (u.buf[k]) {
+        HE_CK(cudaEventSynchronize(u.free_[k]));
+        HE_CK(cudaFree(u.buf[k]));
+        u.buf[k] = nullptr;
+        u.cap[k] = 0;
+      }
+      HE_CK(cudaMalloc(&u.buf[k], bytes));
+      u.cap[k] = bytes;
+    } else {
+      HE_CK(cudaStreamWaitEvent(u.stream, u.free_[k], 0));   // (never recorded: no-op)
+    }
+    d = u.buf[k];
+    HE_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, u.stream));
+    HE_CK(cudaEventRecord(u.done[k], u.stream));
+    HE_CK(cudaStreamWaitEvent(c->stream, u.done[k], 0));
+  }
+  ~DevDoublesOverlap() {
+    if (k < 0) dfree(c, d);
+    else cudaEventRecord(c->up.free_[k], c->stream);   // the readers of buffer k are enqueued
+  }
+};
+
 struct PtGuard {
   he_plaintext* p = nullptr;
   ~PtGuard() { pt_free(p); }
@@ -388,7 +440,7 @@ he_status he_encode(he_context* c, const double* z, size_t n, size_t B, double s
     host_overflow_check(c, z, n, B, scale);
     // H2D on the context stream (asynchronous from pinned memory), then the encode kernels; the
     // host bound above already excludes an overflow, so nothing is read back
-    DevDoubles d(c, z, n * B);
+    DevDoublesOverlap d(c, z, n * B);
     encode_common(c, d.d, n, B, scale, level, out, false);
   });
 }
@@ -482,7 +534,7 @@ he_status he_encode_encrypt(he_context* c, const double* z, size_t n, size_t B, 
     need(n <= (size_t)c->N / 2, HE_TOO_MANY_VALUES, "more values than slots");
     need(scale > 0 && std::isfinite(scale), HE_INVALID_ARGUMENT, "scale must be positive");
     host_overflow_check(c, z, n, B, scale);
-    DevDoubles d(c, z, n * B);
+    DevDoublesOverlap d(c, z, n * B);
     encode_encrypt_common(c, d.d, n, B, scale, level, stream_id, out);
   });
 }
@@ -694,7 +746,7 @@ he_status he_rotate(he_context* c, const he_ciphertext* a, int32_t k, he_ciphert
     const int ns = c->N / 2;
     need(std::abs(k) <= ns, HE_INVALID_ROTATION, "|k| must be <= n_s");
     u32 g;
-    if (k % ns == 0 && !galois_key(c, k == 0 ? ns : k, &g)) {  // identity without a key: copy
+    if (k % ns == 0 && !has_galois_key(c, k == 0 ? ns : k, &g)) {  // identity without a key: copy
       he_ciphertext* o = ct_new(c, a->B, a->size, a->level, a->scale);
       HE_CK(cudaMemcpyAsync(o->d, a->d, ct_words(a) * 8, cudaMemcpyDeviceToDevice, c->stream));
       *out = o;
@@ -749,7 +801,7 @@ he_ciphertext* fold_sum(he_context* c, he_ciphertext* t, int n) {
 void need_fold_keys(he_context* c, int n) {
   for (int s = 1; s < n; s <<= 1) {
     u32 g;
-    need(galois_key(c, s, &g) != nullptr, HE_MISSING_GALOIS_KEY, "dot needs Galois keys for powers of two below n");
+    need(has_galois_key(c, s, &g), HE_MISSING_GALOIS_KEY, "dot needs Galois keys for powers of two below n");
   }
 }
 
@@ -970,11 +1022,11 @@ he_status he_im2col_conv_hoisted_pt(he_context* c, const he_ciphertext* ct, cons
     const int nc = c->N / 2 / chunk, n2 = nc / n1;
     for (int b = 1; b < n1; ++b) {
       u32 g;
-      need(galois_key(c, chunk * b, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * b");
+      need(has_galois_key(c, chunk * b, &g), HE_MISSING_GALOIS_KEY, "missing key for chunk * b");
     }
     for (int a = 1; a < n2; ++a) {
       u32 g;
-      need(galois_key(c, chunk * n1 * a, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * n1 * a");
+      need(has_galois_key(c, chunk * n1 * a, &g), HE_MISSING_GALOIS_KEY, "missing key for chunk * n1 * a");
     }
     he_status st = conv_pt_impl(c, ct, kernels, masks, bias, chunk, n1, out);
     if (st != HE_OK) throw HeError(st, he_last_error());
@@ -1004,7 +1056,7 @@ static he_status conv_pt_impl(he_context* c, const he_ciphertext* ct, const he_p
     if (fold_n1 == 0)
       for (int step = chunk; step < c->N / 2; step <<= 1) {
         u32 g;
-        need(galois_key(c, step, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
+        need(has_galois_key(c, step, &g), HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
       }
     *out = ct_conv(c, ct, kernels, masks, bias, chunk, fold_n1);
   });
@@ -1126,11 +1178,11 @@ he_status he_im2col_conv_bsgs_pt(he_context* c, const he_ciphertext* ct, const h
     const int n2 = ns / chunk / g;
     for (int b = 1; b < g; ++b) {
       u32 gg;
-      need(galois_key(c, chunk * b, &gg) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * b");
+      need(has_galois_key(c, chunk * b, &gg), HE_MISSING_GALOIS_KEY, "missing key for chunk * b");
     }
     for (int a = 1; a < n2; ++a) {
       u32 gg;
-      need(galois_key(c, chunk * g * a, &gg) != nullptr, HE_MISSING_GALOIS_KEY, "missing key for chunk * g * a");
+      need(has_galois_key(c, chunk * g * a, &gg), HE_MISSING_GALOIS_KEY, "missing key for chunk * g * a");
     }
     if (bias) {
       need_pt(c, bias);
@@ -1151,7 +1203,7 @@ he_status he_im2col_conv(he_context* c, const he_ciphertext* ct, const double* k
     conv_checks(c, ct, C, kh * kw, chunk);
     for (int step = chunk; step < c->N / 2; step <<= 1) {
       u32 g;
-      need(galois_key(c, step, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
+      need(has_galois_key(c, step, &g), HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step");
     }
     PtGuard pk, pm, pb;
     conv_encode(c, kernels, C, kh, kw, bias, chunk, kernel_shift, mask_shift, ct->level, ct->scale, &pk.p, &pm.p,
@@ -1163,7 +1215,7 @@ he_status he_im2col_conv(he_context* c, const he_ciphertext* ct, const double* k
 static void need_vm_fold_keys(he_context* c, const he_plaintext* diags) {
   for (int t = 1; t < diags->fold_n; ++t) {
     u32 gg;
-    need(galois_key(c, diags->fold_step * t, &gg) != nullptr, HE_MISSING_GALOIS_KEY,
+    need(has_galois_key(c, diags->fold_step * t, &gg), HE_MISSING_GALOIS_KEY,
          "missing Galois key for a fold step m t");
   }
 }
@@ -1320,7 +1372,7 @@ he_status he_vec_mat_bsgs_fold_pt(he_context* c, const he_ciphertext* ct, const 
          "folded vec_mat: m | n and the diagonals hold the first m in BSGS order");
     for (int t = 1; t < n / m; ++t) {
       u32 gg;
-      need(galois_key(c, m * t, &gg) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step m t");
+      need(has_galois_key(c, m * t, &gg), HE_MISSING_GALOIS_KEY, "missing Galois key for a fold step m t");
     }
     *out = ct_vec_mat_bsgs(c, ct, diags, g, bias_pt, n / m, m);
   });
@@ -1334,7 +1386,7 @@ he_status he_vec_mat(he_context* c, const he_ciphertext* ct, const double* W, in
     need(ct->level >= 1, HE_LEVEL_EXHAUSTED, "vec_mat consumes one level");
     for (int k = 1; k < n; ++k) {
       u32 g;
-      need(galois_key(c, k, &g) != nullptr, HE_MISSING_GALOIS_KEY, "missing Galois key for a diagonal rotation");
+      need(has_galois_key(c, k, &g), HE_MISSING_GALOIS_KEY, "missing Galois key for a diagonal rotation");
     }
     PtGuard pd, pb;
     vecmat_encode(c, W, n, m, bias, replicate_out, pt_scale_shift, ct->level, ct->scale, &pd.p, &pb.p);
@@ -1484,6 +1536,8 @@ he_status he_pt_limbs(const he_plaintext* pt, int* limbs) {
   });
 }
 
+size_t he_key_bytes(const he_context* c) { return c ? key_bytes(const_cast<he_context*>(c)) : 0; }
+
 size_t he_key_words(const he_context* c, int kind) {
   if (!c) return 0;
   const size_t N = c->N;
@@ -1503,7 +1557,7 @@ he_status he_key_export(he_context* c, int kind, int32_t step, uint64_t* dst) {
     switch (kind) {
       case 0: src = c->d_sk; break;
       case 1: src = c->d_pk; break;
-      case 2: src = c->d_rlk; break;
+      case 2: src = relin_key(c); break;
       case 3: {
         u32 g;
         src = galois_key(c, step, &g);

@@ -101,6 +101,17 @@ struct he_context {
   };
   GraphRec* rec = nullptr;
   std::map<void*, bool> graph_owned;   // blocks owned by a live graph (dfree is a no-op for them)
+  // Host-input upload path (he_encode / he_encode_encrypt with a host z): two context-owned device
+  // buffers filled on a copy stream of the context's own, so the H2D of call i+1 overlaps the kernels
+  // of call i on c->stream.  up_done[k]: copy k finished (c->stream waits for it); up_free[k]: the
+  // kernels that read buffer k were enqueued (the copy stream waits for it before refilling).
+  struct Upload {
+    cudaStream_t stream = nullptr;
+    double* buf[2] = {nullptr, nullptr};
+    size_t cap[2] = {0, 0};
+    cudaEvent_t done[2] = {nullptr, nullptr}, free_[2] = {nullptr, nullptr};
+    int next = 0;
+  } up;
 };
 
 struct he_graph {

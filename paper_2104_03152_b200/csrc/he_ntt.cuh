@@ -479,17 +479,34 @@ __device__ __forceinline__ void ntt_pass32(u32* sm, u32 tid, const uint2* __rest
   }
 }
 
-// Passes P0 .. PEND-1 (pass P covers bit group GP = INV ? P : NPASS-1-P).
-template <int LOGN, bool INV, int P, bool LAZY = false, int PEND = NttGeomS<LOGN>::NPASS>
-__device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, u32 q) {
+// Warp-local passes.  A full pass (NB = R: one group per thread, g = tid) over bits [LO, LO+R) with
+// LO + R <= 5 + R touches, for warp w, exactly the words [w 2^(5+R), (w+1) 2^(5+R)): word =
+// (tid >> 5) << (5+R) | ... for every LO <= 5.  Two consecutive such passes (and a warp-ordered
+// epilogue) exchange data inside one warp only, so __syncwarp() orders them and the warps of a CTA
+// drift apart instead of meeting at a block barrier (at N = 2^13: the passes over bits [7:4], [3:0]).
+#ifndef HE_NTT32_WARPSYNC
+#define HE_NTT32_WARPSYNC 1
+#endif
+template <int LOGN, bool INV, int P>
+struct Pass32 {
   typedef NttGeomS<LOGN> G;
+  static constexpr int GP = INV ? P : G::NPASS - 1 - P;
+  static constexpr int LO = GP * G::R;
+  static constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+  static constexpr bool WL = HE_NTT32_WARPSYNC && P >= 0 && P < G::NPASS && NB == G::R && LO <= 5 && G::T % 32 == 0;
+};
+
+// Passes P0 .. PEND-1 (pass P covers bit group GP = INV ? P : NPASS-1-P).  TAIL_WL: what follows the
+// last pass reads only the words of the thread's own warp region (ntt32_epilogue<.., WL = true>).
+template <int LOGN, bool INV, int P, bool LAZY = false, int PEND = NttGeomS<LOGN>::NPASS, bool TAIL_WL = false>
+__device__ __forceinline__ void ntt_passes32(u32* sm, u32 tid, const uint2* tw, u32 q) {
   if constexpr (P < PEND) {
-    constexpr int GP = INV ? P : G::NPASS - 1 - P;
-    constexpr int LO = GP * G::R;
-    constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-    ntt_pass32<LOGN, INV, LO, NB, LAZY>(sm, tid, tw, q);
-    __syncthreads();
-    ntt_passes32<LOGN, INV, P + 1, LAZY, PEND>(sm, tid, tw, q);
+    typedef Pass32<LOGN, INV, P> PS;
+    ntt_pass32<LOGN, INV, PS::LO, PS::NB, LAZY>(sm, tid, tw, q);
+    constexpr bool next_wl = (P + 1 < PEND) ? Pass32<LOGN, INV, (P + 1 < PEND ? P + 1 : P)>::WL : TAIL_WL;
+    if constexpr (PS::WL && next_wl) __syncwarp();
+    else __syncthreads();
+    ntt_passes32<LOGN, INV, P + 1, LAZY, PEND, TAIL_WL>(sm, tid, tw, q);
   }
 }
 
@@ -543,26 +560,30 @@ __device__ __forceinline__ u32 ntt_reduce32(u32 v, u32 q) {
 
 // Final scaling (inverse) or reduction (forward) of the transform in sm and the job's store; jobs
 // with store4 get 4 outputs per call (their operand loads batched ahead of the arithmetic).
-template <int LOGN, bool INV, class JB>
+// WL: warp w stores the words of its own region [w 32 PER, (w+1) 32 PER) (lane + 32 k: still one
+// coalesced 32-word run per instruction), so a warp-local last pass needs only __syncwarp() before it.
+template <int LOGN, bool INV, class JB, bool WL = false>
 __device__ __forceinline__ void ntt32_epilogue(const JB& jb, const u32* sm, u32 tid, uint2 ni, u32 q) {
   typedef NttGeomS<LOGN> G;
   constexpr int PER = G::NL / G::T;   // the launch has exactly T threads: unrolled, loads batched
+  constexpr u32 ST = WL ? 32u : (u32)G::T;
+  const u32 i00 = WL ? (tid >> 5) * (32u * PER) + (tid & 31u) : tid;
   if constexpr (has_store4<JB>::value && PER % 4 == 0) {
 #pragma unroll 2
     for (int c = 0; c < PER / 4; ++c) {
-      const u32 i0 = tid + 4 * c * G::T;
+      const u32 i0 = i00 + 4 * c * ST;
       u32 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const u32 x = sm[spad32(i0 + u * G::T)];
+        const u32 x = sm[spad32(i0 + u * ST)];
         v[u] = INV ? shoup32(x, ni.x, ni.y, q) : ntt_reduce32(x, q);
       }
-      jb.store4(i0, G::T, v);
+      jb.store4(i0, ST, v);
     }
   } else {
 #pragma unroll 4
     for (int k = 0; k < PER; ++k) {
-      const u32 i = tid + k * G::T;
+      const u32 i = i00 + k * ST;
       u32 v = sm[spad32(i)];
       v = INV ? shoup32(v, ni.x, ni.y, q) : ntt_reduce32(v, q);
       jb.store(i, (u64)v);
@@ -673,9 +694,10 @@ __device__ __forceinline__ void ntt32_pipe_rest(const JB& jb, u32* sm, u32 tid, 
   constexpr int LO_LAST = (G::NPASS - 1) * G::R, NB_LAST = G::LOGNL - LO_LAST;
   constexpr bool FUSE_LAST = INV && G::NPASS >= 3 && (1 << (G::R - NB_LAST)) % 4 == 0;
   if (!INV) {
-    if (q < (1u << 30)) ntt_passes32<LOGN, false, 1, true>(sm, tid, tw, q);
-    else ntt_passes32<LOGN, false, 1, false>(sm, tid, tw, q);
-    ntt32_epilogue<LOGN, false>(jb, sm, tid, __ldg(tw), q);
+    constexpr bool TWL = Pass32<LOGN, false, G::NPASS - 1>::WL;   // the last pass is warp-local: so is the epilogue
+    if (q < (1u << 30)) ntt_passes32<LOGN, false, 1, true, G::NPASS, TWL>(sm, tid, tw, q);
+    else ntt_passes32<LOGN, false, 1, false, G::NPASS, TWL>(sm, tid, tw, q);
+    ntt32_epilogue<LOGN, false, JB, TWL>(jb, sm, tid, __ldg(tw), q);
   } else if constexpr (FUSE_LAST) {
     if (q < (1u << 30)) {
       ntt_passes32<LOGN, true, 1, true, G::NPASS - 1>(sm, tid, tw, q);

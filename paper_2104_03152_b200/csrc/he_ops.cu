@@ -201,6 +201,16 @@ void context_init(he_context* c, const HostParams& hp, u64 seed) {
 
 void context_destroy(he_context* c) {
   cudaStreamSynchronize(c->stream);
+  if (c->up.stream) {
+    cudaStreamSynchronize(c->up.stream);
+    for (int k = 0; k < 2; ++k) {
+      if (c->up.buf[k]) cudaFree(c->up.buf[k]);
+      if (c->up.done[k]) cudaEventDestroy(c->up.done[k]);
+      if (c->up.free_[k]) cudaEventDestroy(c->up.free_[k]);
+    }
+    cudaStreamDestroy(c->up.stream);
+    c->up = he_context::Upload();
+  }
   for (void* p : c->owned) cudaFree(p);
   for (auto& kv : c->gk) cudaFree(kv.second);
   for (auto& kv : c->gk32) cudaFree(kv.second);
@@ -554,6 +564,9 @@ __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* _
 // are the exact residues, bit-identical to the generic path.  One CTA per
 // (target limb t, item b).
 constexpr int LAZY_SM_T = 1024, LAZY_SM_EPT = 2;
+#ifndef HE_BSGS_FIXED
+#define HE_BSGS_FIXED 1   // 0: always the runtime-geometry BSGS kernels (A/B experiments)
+#endif
 
 __device__ __forceinline__ u32 redc32(u64 T, u32 q, u32 qneg_inv) {
   const u32 m = (u32)T * qneg_inv;
@@ -698,18 +711,88 @@ k_vecmat_lazy_mont(LazyArgs a, const u32* const* __restrict__ keys32, const u32*
 //   removes exactly the one factor 2^32 its products carry: the results are the same residues.
 // * PAIRED (q up to 2^31): one REDC per pair of products and per diagonal product (x0 k0' +
 //   x1 k1' < 2 q^2 < q 2^32), the sums kept reduced.
-template <int LC, int G, int IB, bool LAZY>
+// * UNIT (rotation sums: every diagonal is the plaintext polynomial 1, G = 1): no diagonal loads or
+//   products.  acc_p = [data] P c_p + sum_k (ip_p,k + [p = 0] P c0[pi_k(n)]); in the lazy schedule the
+//   Montgomery-form inner products of ALL baby steps are summed in 64 bits (< g LC q^2 < q 2^32) and
+//   reduced by one REDC at the end, the P c terms summed as plain residues: the same residues as the
+//   general schedule with the diagonal 2^32 mod q (Montgomery 1), one REDC and one product fewer per
+//   baby step, part and coefficient.
+template <int LC, int G, int IB, bool LAZY, bool UNIT = false>
 __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, const u32* const* __restrict__ keys32,
                                             const u32* __restrict__ dm, const u32* xs, const u32* c0p, int t,
                                             int b0, int nimg, int nt, bool data, u32 q, u32 qi, u32 Pm, u32 keyrow,
-                                            u32 kpart, u32 kdig, size_t gstride, u32 h0, u32 NH) {
+                                            u32 kpart, u32 kdig, size_t gstride, u32 h0, u32 NH, u32 N, int logN) {
   typedef typename std::conditional<LAZY, u64, u32>::type acc_t;
+  if constexpr (UNIT) {
+    static_assert(G == 1, "rotation sums have one group");
+    for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T) {
+      const u32 n = h0 + l;
+      acc_t T0[IB], T1[IB];   // LAZY: 64-bit sums of Montgomery-form products; else reduced residues
+      u32 s0[IB], s1[IB];     // plain residues: P c0 terms of every step, P c1 of step 0
+#pragma unroll
+      for (int i = 0; i < IB; ++i) {
+        T0[i] = T1[i] = 0;
+        s0[i] = data ? c0p[i * NH + l] : 0u;
+        s1[i] = data ? redc32((u64)xs[(i * LC + t) * NH + l] * Pm, q, qi) : 0u;
+      }
+      for (int k = 1; k < g; ++k) {
+        const u32 gal = __ldg(a.gal + k * a.step);
+        const u32* key = keys32[k * a.step] + keyrow + n;
+        const u32 sl = galois_src(n, gal, logN) - h0;
+        if (LAZY) {
+#pragma unroll
+          for (int j = 0; j < LC; ++j) {
+            const u32 kb = __ldg(key + j * kdig), ka = __ldg(key + j * kdig + kpart);
+#pragma unroll
+            for (int i = 0; i < IB; ++i) {
+              const u32 x = xs[(i * LC + j) * NH + sl];
+              T0[i] += (u64)x * kb;
+              T1[i] += (u64)x * ka;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < LC; j += 2) {
+            const u32 kb0 = __ldg(key + j * kdig), ka0 = __ldg(key + j * kdig + kpart);
+            const u32 kb1 = j + 1 < LC ? __ldg(key + (j + 1) * kdig) : 0u;
+            const u32 ka1 = j + 1 < LC ? __ldg(key + (j + 1) * kdig + kpart) : 0u;
+#pragma unroll
+            for (int i = 0; i < IB; ++i) {
+              const u32 x0 = xs[(i * LC + j) * NH + sl];
+              u64 p0 = (u64)x0 * kb0, p1 = (u64)x0 * ka0;
+              if (j + 1 < LC) {
+                const u32 x1 = xs[(i * LC + j + 1) * NH + sl];
+                p0 += (u64)x1 * kb1;
+                p1 += (u64)x1 * ka1;
+              }
+              T0[i] = addq((u32)T0[i], redc32(p0, q, qi), q);
+              T1[i] = addq((u32)T1[i], redc32(p1, q, qi), q);
+            }
+          }
+        }
+        if (data) {
+#pragma unroll
+          for (int i = 0; i < IB; ++i) s0[i] = addq(s0[i], c0p[i * NH + sl], q);
+        }
+      }
+      u32* out = reinterpret_cast<u32*>(a.accx);
+#pragma unroll
+      for (int i = 0; i < IB; ++i) {
+        if (i < nimg) {
+          const size_t base = ((((size_t)b0 + i) * 2) * nt + t) * N + n;
+          out[base] = addq(LAZY ? redc32(T0[i], q, qi) : (u32)T0[i], s0[i], q);
+          out[base + (size_t)nt * N] = addq(LAZY ? redc32(T1[i], q, qi) : (u32)T1[i], s1[i], q);
+        }
+      }
+    }
+    return;
+  }
   for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T) {
     const u32 n = h0 + l;
     acc_t acc0[IB][G], acc1[IB][G];
 #pragma unroll
     for (int k2 = 0; k2 < G; ++k2) {
-      const u32 d = __ldg(dm + k2 * gstride + (size_t)t * a.N + n);
+      const u32 d = __ldg(dm + k2 * gstride + (size_t)t * N + n);
 #pragma unroll
       for (int i = 0; i < IB; ++i) {
         if (data) {   // k1 = 0: P E[k2][0] (.) c
@@ -730,7 +813,7 @@ __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, con
     for (int k = 1; k < g; ++k) {
       const u32 gal = __ldg(a.gal + k * a.step);
       const u32* key = keys32[k * a.step] + keyrow + n;
-      const u32 sl = galois_src(n, gal, a.logN) - h0;   // same half (see above)
+      const u32 sl = galois_src(n, gal, logN) - h0;   // same half (see above)
       u32 y0[IB], y1[IB];
       if (LAZY) {
         u64 T0[IB], T1[IB];
@@ -779,7 +862,7 @@ __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, con
       }
 #pragma unroll
       for (int k2 = 0; k2 < G; ++k2) {
-        const u32 d = __ldg(dm + k2 * gstride + ((size_t)k * nt + t) * a.N + n);
+        const u32 d = __ldg(dm + k2 * gstride + ((size_t)k * nt + t) * N + n);
 #pragma unroll
         for (int i = 0; i < IB; ++i) {
           if (LAZY) {
@@ -798,16 +881,21 @@ __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, con
       if (i < nimg) {
 #pragma unroll
         for (int k2 = 0; k2 < G; ++k2) {
-          const size_t base = ((((size_t)k2 * B + b0 + i) * 2) * nt + t) * a.N + n;
+          const size_t base = ((((size_t)k2 * B + b0 + i) * 2) * nt + t) * N + n;
           out[base] = LAZY ? redc32(acc0[i][k2], q, qi) : (u32)acc0[i][k2];
-          out[base + (size_t)nt * a.N] = LAZY ? redc32(acc1[i][k2], q, qi) : (u32)acc1[i][k2];
+          out[base + (size_t)nt * N] = LAZY ? redc32(acc1[i][k2], q, qi) : (u32)acc1[i][k2];
         }
       }
     }
   }
 }
 
-template <int LC, int G, int IB>
+// NFIX / NPFIX != 0: the ring degree and the key's limb count are compile-time constants (the launch
+// checks a.N == NFIX, a.NP == NPFIX).  Every key row of a baby step (digit j, part p) is then the one
+// 64-bit key pointer plus an immediate, and every staged digit one shared address plus an immediate:
+// the general form spends ~40% of its fmaheavy-pipe cycles on 64-bit address products and adds
+// (IMAD.WIDE x 4 for the row offsets) and spills loop invariants (profiles/r02, SASS of the per-k loop).
+template <int LC, int G, int IB, bool UNIT = false, int NFIX = 0, int NPFIX = 0>
 __global__ void __launch_bounds__(LAZY_SM_T, 1)
 k_vecmat_bsgs_hp(LazyArgs a, int g, int B, const u32* const* __restrict__ keys32, const u32* __restrict__ dm,
                  const PrimeD* __restrict__ primes) {
@@ -815,13 +903,16 @@ k_vecmat_bsgs_hp(LazyArgs a, int g, int B, const u32* const* __restrict__ keys32
   // grid (image pairs, halves, targets): the image pairs vary fastest, so the CTAs resident together
   // share one (target, half) and its key rows / diagonals stay in L2 (round 2; targets fastest
   // re-read them from DRAM, ~2.8x the unique bytes)
+  const u32 N = NFIX ? (u32)NFIX : (u32)a.N, NP = NPFIX ? (u32)NPFIX : (u32)a.NP;
+  constexpr int LOGNFIX = NFIX == 8192 ? 13 : NFIX == 4096 ? 12 : NFIX == 16384 ? 14 : 0;
+  static_assert(NFIX == 0 || LOGNFIX != 0, "fixed ring degree: 2^12, 2^13 or 2^14");
+  const int logN = NFIX ? LOGNFIX : a.logN;
   const int t = blockIdx.z, nt = LC + a.K;
-  const u32 NH = (u32)a.N / 2, h0 = blockIdx.y * NH;
+  const u32 NH = N / 2, h0 = blockIdx.y * NH;
   const int b0 = blockIdx.x * IB, nimg = min(IB, B - b0);
   const int tp = t < LC ? t : a.L + (t - LC);
   const PrimeD P = load_prime(primes, tp);
   const u32 q = (u32)P.q, qi = mont_neg_inv(q);
-  const u32 N = a.N, NP = a.NP;
   const bool data = t < LC;
   const u32 Pm = (u32)((((u64)__ldg(a.P_mod + tp)) << 32) % q);
   u32* c0p = xs + IB * LC * NH;
@@ -852,12 +943,19 @@ k_vecmat_bsgs_hp(LazyArgs a, int g, int B, const u32* const* __restrict__ keys32
   __syncthreads();
   const u32 keyrow = tp * N, kpart = NP * N, kdig = 2 * NP * N;
   const size_t gstride = (size_t)g * nt * N;   // between giant-step groups in dm
-  if ((u64)LC * q < (1ULL << 32) && (u64)g * q < (1ULL << 32))
+  if constexpr (UNIT) {
+    if ((u64)LC * g * q < (1ULL << 32))
+      bsgs_hp_run<LC, G, IB, true, true>(a, g, B, keys32, dm, xs, c0p, t, b0, nimg, nt, data, q, qi, Pm, keyrow,
+                                         kpart, kdig, gstride, h0, NH, N, logN);
+    else
+      bsgs_hp_run<LC, G, IB, false, true>(a, g, B, keys32, dm, xs, c0p, t, b0, nimg, nt, data, q, qi, Pm, keyrow,
+                                          kpart, kdig, gstride, h0, NH, N, logN);
+  } else if ((u64)LC * q < (1ULL << 32) && (u64)g * q < (1ULL << 32))
     bsgs_hp_run<LC, G, IB, true>(a, g, B, keys32, dm, xs, c0p, t, b0, nimg, nt, data, q, qi, Pm, keyrow, kpart,
-                                 kdig, gstride, h0, NH);
+                                 kdig, gstride, h0, NH, N, logN);
   else
     bsgs_hp_run<LC, G, IB, false>(a, g, B, keys32, dm, xs, c0p, t, b0, nimg, nt, data, q, qi, Pm, keyrow, kpart,
-                                  kdig, gstride, h0, NH);
+                                  kdig, gstride, h0, NH, N, logN);
 }
 
 // Fused ModUp + key inner product for small primes (a9 without materialising
@@ -958,6 +1056,26 @@ __global__ void k_to_mont32(const u64* __restrict__ in, u32* __restrict__ out, c
     const u64 q = load_prime(primes, l < lc ? l : L + (l - lc)).q;
     for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
       out[r * N + n] = (u32)((in[r * N + n] << 32) % q);
+  }
+}
+
+// The canonical u64 residues of a Montgomery-form u32 row: out[i] = in[i] 2^-32 mod q (one REDC).
+// Small-prime contexts keep their switching keys as u32 only; the 64-bit forms
+// (key export, the unfused fallback paths) are materialised from them on demand.
+__global__ void k_from_mont32(const u32* __restrict__ in, u64* __restrict__ out, const PrimeD* __restrict__ primes,
+                              int N, int nl, int lc, int L, size_t rows) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int l = (int)(r % nl);
+    const u32 q = (u32)load_prime(primes, l < lc ? l : L + (l - lc)).q;
+    u32 inv = q;   // Newton: q^-1 mod 2^32 (q odd; 3 correct bits double each step)
+    for (int it = 0; it < 5; ++it) inv *= 2u - q * inv;
+    const u32 qneg = 0u - inv;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+      const u64 T = in[r * N + n];
+      const u32 m = (u32)T * qneg;
+      u32 v = (u32)((T + (u64)m * q) >> 32);   // < 2q
+      out[r * N + n] = v >= q ? v - q : v;
+    }
   }
 }
 
@@ -1587,12 +1705,72 @@ static void ks_fused(he_context* c, const u64* dsrc, size_t bs, int B, int Lc, c
   else ks_launch(c, epi);
 }
 
+// Is there a Galois key for this rotation step (in either stored form)?
+bool has_galois_key(he_context* c, int step, u32* gal_out) {
+  const u64 g = galois_element(c->N, step);
+  *gal_out = (u32)g;
+  return c->gk.count(g) || c->gk32.count(g);
+}
+
+// u64 words of a u32-at-rest key: allocated and converted once, on the first caller that needs them
+// (key export, the unfused fallback paths); the hot path of small-prime contexts never does.
+// The conversion and the per-step table update run on a stream of their own and are waited for on
+// the host, so they are never recorded into a CUDA graph when c->stream is capturing (the keys were
+// synchronised at keygen; the consumers on c->stream are enqueued after this returns).
+static cudaStream_t key_aux_stream() {
+  static cudaStream_t s = nullptr;   // one device per process (context_init)
+  if (!s) HE_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+static u64* key64_from32(he_context* c, const u32* k32) {
+  const size_t N = c->N, L = c->L, NP = c->NP, rows = L * 2 * NP;
+  u64* key = nullptr;
+  HE_CK(cudaMalloc(&key, rows * N * 8));
+  cudaStream_t aux = key_aux_stream();
+  k_from_mont32<<<dim3((unsigned)((N + 255) / 256), (unsigned)std::min<size_t>(rows, 65535)), 256, 0, aux>>>(
+      k32, key, c->d_primes, (int)N, (int)NP, (int)NP, (int)L, rows);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFree(key);
+    throw HeError(HE_CUDA_ERROR, std::string("k_from_mont32: ") + cudaGetErrorString(e));
+  }
+  HE_CK(cudaStreamSynchronize(aux));
+  return key;
+}
+
+// The u64 form of a Galois key (null if there is no key for the step).
 const u64* galois_key(he_context* c, int step, u32* gal_out) {
   const u64 g = galois_element(c->N, step);
-  auto it = c->gk.find(g);
-  if (it == c->gk.end()) return nullptr;
   *gal_out = (u32)g;
-  return it->second;
+  auto it = c->gk.find(g);
+  if (it != c->gk.end()) return it->second;
+  auto it32 = c->gk32.find(g);
+  if (it32 == c->gk32.end()) return nullptr;
+  u64* key = key64_from32(c, it32->second);
+  c->gk[g] = key;
+  if (c->d_step_key) {   // every step of the per-step table that maps to this Galois element
+    const int ns = c->N / 2;
+    cudaStream_t aux = key_aux_stream();
+    for (int k = 0; k <= ns; ++k)
+      if (galois_element(c->N, k == 0 ? ns : k) == g)
+        HE_CK(cudaMemcpyAsync(c->d_step_key + k, &key, sizeof(u64*), cudaMemcpyHostToDevice, aux));
+    HE_CK(cudaStreamSynchronize(aux));   // &key is a stack address
+  }
+  return key;
+}
+
+size_t key_bytes(he_context* c) {
+  const size_t N = c->N, L = c->L, NP = c->NP, kw = L * 2 * NP * N;
+  size_t b = c->d_pk ? 2 * L * N * 8 : 0;
+  if (c->d_rlk) b += kw * 8;
+  if (c->d_rlk32) b += kw * 4;
+  return b + c->gk.size() * kw * 8 + c->gk32.size() * kw * 4;
+}
+
+// The u64 form of the relinearisation key (null if there is none).
+const u64* relin_key(he_context* c) {
+  if (!c->d_rlk && c->d_rlk32) c->d_rlk = key64_from32(c, c->d_rlk32);
+  return c->d_rlk;
 }
 
 // Square + relinearize without the tensor: with the fused key switch, d2 = x1^2 is formed where
@@ -1685,7 +1863,7 @@ he_ciphertext* ct_relinearize(he_context* c, const he_ciphertext* a) {
   k.add_bs = 3 * LN;
   k.add_parts = 2;
   try {
-    ks_materialized(c, a->d + 2 * LN, 3 * LN, a->B, Lc, c->d_rlk, 1, k);
+    ks_materialized(c, a->d + 2 * LN, 3 * LN, a->B, Lc, relin_key(c), 1, k);
   } catch (...) {
     ct_free(o);
     throw;
@@ -1698,10 +1876,11 @@ he_ciphertext* ct_rotate(he_context* c, const he_ciphertext* a, int step, bool a
   const int Lc = a->level + 1;
   const size_t LN = (size_t)Lc * c->N;
   u32 g = 0;
-  const u64* key = galois_key(c, step, &g);
-  if (!key) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
-  he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
+  if (!has_galois_key(c, step, &g))
+    throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
   auto it32 = c->gk32.find(g);
+  const u64* key = fused_ks_ok(c) && it32 != c->gk32.end() ? nullptr : galois_key(c, step, &g);
+  he_ciphertext* o = ct_new(c, a->B, 2, a->level, a->scale);
   if (fused_ks_ok(c) && it32 != c->gk32.end()) {
     KsArgs k = ks_base(c, a->B, Lc, nullptr, nullptr, 0);
     k.out = o->d;
@@ -1742,8 +1921,8 @@ static he_ciphertext* ct_rotate_acc(he_context* c, const he_ciphertext* a, int s
   const int Lc = a->level + 1;
   const size_t LN = (size_t)Lc * c->N;
   u32 g = 0;
-  const u64* key = galois_key(c, step, &g);
-  if (!key) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
+  if (!has_galois_key(c, step, &g))
+    throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(step));
   auto it32 = c->gk32.find(g);
   if (!(fused_ks_ok(c) && it32 != c->gk32.end() && acc->level == a->level && acc->B == a->B && acc->size == 2)) {
     he_ciphertext* r = ct_rotate(c, a, step, false);
@@ -1779,8 +1958,7 @@ static he_ciphertext* ct_rotate_acc(he_context* c, const he_ciphertext* a, int s
 // with all rotations hoisted (one ModUp of c1 shared by every k), then one
 // rescale and the bias.
 static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
-                                      const std::vector<const u64*>& keys, const std::vector<u32>& gals,
-                                      int step = 1) {
+                                      const std::vector<u32>& gals, int step = 1) {
   const int Lc = x->level + 1, n = diags->B, B = x->B, nt = Lc + c->K;
   const size_t LN = (size_t)Lc * c->N, N = c->N;
   // steps 1..n-1: the per-step device tables built at keygen (no host copies here)
@@ -1798,6 +1976,11 @@ static he_ciphertext* ct_vec_mat_lazy(he_context* c, const he_ciphertext* x, con
   const u32* gt = c->d_step_gal;
   const bool smem_path = c->small_primes && ((size_t)Lc + 1) * N * 4 <= kMaxSmem && Lc <= 8 &&
                          keys32.size() == (size_t)n && N % (LAZY_SM_T * 4) == 0 && step == 1;
+  if (!smem_path)   // the generic kernel reads the u64 keys through d_step_key: materialise u32-at-rest keys
+    for (int k = 1; k < n; ++k) {
+      u32 gg;
+      galois_key(c, k * step, &gg);
+    }
   u64* ext = (n > 1 && !smem_path) ? modup(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
   u32* ext32 = (n > 1 && smem_path) ? modup32(c, x->d + LN, 2 * LN, B, Lc) : nullptr;
   he_ciphertext* acc = nullptr;
@@ -1871,12 +2054,13 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
   const size_t LN = (size_t)Lc * c->N;
   std::vector<const u64*> keys(n);
   std::vector<u32> gals(n);
-  for (int k = 1; k < n; ++k) {
-    keys[k] = galois_key(c, k, &gals[k]);
-    if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(k));
-  }
+  for (int k = 1; k < n; ++k)
+    if (!has_galois_key(c, k, &gals[k]))
+      throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for rotation step " + std::to_string(k));
+  if (!diags->qp)   // the per-rotation form switches with the u64 keys
+    for (int k = 1; k < n; ++k) keys[k] = galois_key(c, k, &gals[k]);
   if (diags->qp) {
-    he_ciphertext* acc = ct_vec_mat_lazy(c, x, diags, keys, gals);
+    he_ciphertext* acc = ct_vec_mat_lazy(c, x, diags, gals);
     he_ciphertext* res = nullptr;
     try {
       res = ct_rescale(c, acc, bias);   // bias fused into the rescale's store
@@ -1949,6 +2133,10 @@ he_ciphertext* ct_vec_mat(he_context* c, const he_ciphertext* x, const he_plaint
   return res;
 }
 
+__global__ void k_fill_u64(u64* __restrict__ p, size_t n, u64 v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
 // BSGS vec_mat: diags = G groups of g QP diagonals E[k2][k1].
 // Baby-step part: inner[k2] = ModDown(sum_{k1 < g} E[k2][k1] (.) rot(x, k1 step)) for the G
 // groups of diags (unrescaled, scale x.scale * diags.scale).
@@ -1958,14 +2146,17 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
                                               int g, int step, bool rescale = false,
                                               const he_plaintext* bias = nullptr,
                                               const he_plaintext* add_pt = nullptr) {
-  const int Lc = x->level + 1, B = x->B, nt = Lc + c->K, G = diags->B / g;
+  // diags == nullptr: unit diagonals (a rotation sum of g terms, ct_rot_sum): the fused kernel's UNIT form
+  // needs no plaintext; the other paths get the plaintext polynomial 1 (NTT words all 1) g times.
+  const bool unit = diags == nullptr;
+  const int Lc = x->level + 1, B = x->B, nt = Lc + c->K, G = unit ? 1 : diags->B / g;
+  const double dscale = unit ? 1.0 : diags->scale;
+  he_plaintext* ones = nullptr;
   const size_t N = c->N, LN = (size_t)Lc * N;
-  std::vector<const u64*> keys(g);
   std::vector<u32> gals(g, 1);
-  for (int k = 1; k < g; ++k) {
-    keys[k] = galois_key(c, k * step, &gals[k]);
-    if (!keys[k]) throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for baby step " + std::to_string(k * step));
-  }
+  for (int k = 1; k < g; ++k)
+    if (!has_galois_key(c, k * step, &gals[k]))
+      throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for baby step " + std::to_string(k * step));
   std::vector<const u32*> keys32;
   if (c->small_primes) {
     keys32.push_back(nullptr);
@@ -1982,10 +2173,17 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
   std::vector<he_ciphertext*> inner(G, nullptr);
   auto cleanup = [&] {
     for (auto* p : inner) ct_free(p);
+    pt_free(ones);
   };
   try {
+    if (unit && !fused) {
+      ones = pt_new(c, g, x->level, 1.0, 1);
+      k_fill_u64<<<148 * 4, 256, 0, c->stream>>>(ones->d, pt_words(ones), 1);
+      check_launch(c);
+      diags = ones;
+    }
     if (fused) {
-      if (!diags->dm) {
+      if (!unit && !diags->dm) {
         const size_t rows = (size_t)diags->B * nt;
         u32* dmp = dalloc_t<u32>(c, rows * N);
         k_to_mont32<<<dim3((unsigned)((N + 255) / 256), (unsigned)std::min<size_t>(rows, 65535)), 256, 0,
@@ -2003,9 +2201,10 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
         {
           // unique bytes: u32 extended digits (t != j), the u64 own digit (c1) and c0 row, u32 accumulators
           // written, u32 key rows of the g-1 baby steps, u32 diagonals
+          // (a rotation sum - unit diagonals - reads no diagonals and forms no diagonal products)
           const double bytes = 4.0 * N * B * Lc * (nt - 1) + 8.0 * N * 2.0 * B * Lc + 4.0 * N * G * B * 2 * nt +
-                               4.0 * N * ((double)(g - 1) * 2 * Lc * nt + (double)G * g * nt);
-          const double ops = (double)B * (g - 1) * N * (nt * (2.0 * Lc + 2.0 * G) + Lc);
+                               4.0 * N * ((double)(g - 1) * 2 * Lc * nt + (unit ? 0.0 : (double)G * g * nt));
+          const double ops = (double)B * (g - 1) * N * (nt * (2.0 * Lc + (unit ? 0.0 : 2.0 * G)) + Lc);
           static const char* const tags[9] = {"vecmat_bsgs", "vecmat_bsgs_L1", "vecmat_bsgs_L2", "vecmat_bsgs_L3",
                                               "vecmat_bsgs_L4", "vecmat_bsgs_L5", "vecmat_bsgs_L6", "vecmat_bsgs_L7",
                                               "vecmat_bsgs_L8"};
@@ -2016,16 +2215,20 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
           const dim3 grid((unsigned)((B + IBv - 1) / IBv), 2, nt);
           auto launch = [&](auto kern) {
             smem_limit_once((const void*)kern, (int)kMaxSmem);
-            kern<<<grid, LAZY_SM_T, smem_hp, c->stream>>>(la, g, B, kt, diags->dm, c->d_primes);
+            kern<<<grid, LAZY_SM_T, smem_hp, c->stream>>>(la, g, B, kt, unit ? nullptr : diags->dm, c->d_primes);
           };
-#define HE_BSGS_G(LCV, IBV)                                                      \
-    if (G == 1) launch(k_vecmat_bsgs_hp<LCV, 1, IBV>);                           \
-    else if (G == 2) launch(k_vecmat_bsgs_hp<LCV, 2, IBV>);                      \
-    else if (G == 3) launch(k_vecmat_bsgs_hp<LCV, 3, IBV>);                      \
-    else launch(k_vecmat_bsgs_hp<LCV, 4, IBV>);
+          // BASELINE config 4's geometry (N = 2^13, L + K = 8) with image pairs: compile-time strides
+          const bool fixg = N == 8192 && c->NP == 8 && IBv == 2 && HE_BSGS_FIXED;
+#define HE_BSGS_G(LCV, IBV, NF, NPF)                                             \
+    if (unit) launch(k_vecmat_bsgs_hp<LCV, 1, IBV, true, NF, NPF>);              \
+    else if (G == 1) launch(k_vecmat_bsgs_hp<LCV, 1, IBV, false, NF, NPF>);      \
+    else if (G == 2) launch(k_vecmat_bsgs_hp<LCV, 2, IBV, false, NF, NPF>);      \
+    else if (G == 3) launch(k_vecmat_bsgs_hp<LCV, 3, IBV, false, NF, NPF>);      \
+    else launch(k_vecmat_bsgs_hp<LCV, 4, IBV, false, NF, NPF>);
 #define HE_BSGS_CASE(LCV)                                                        \
   case LCV:                                                                      \
-    if (IBv == 2) { HE_BSGS_G(LCV, 2) } else { HE_BSGS_G(LCV, 1) }               \
+    if (fixg) { HE_BSGS_G(LCV, 2, 8192, 8) }                                     \
+    else if (IBv == 2) { HE_BSGS_G(LCV, 2, 0, 0) } else { HE_BSGS_G(LCV, 1, 0, 0) } \
     break;
           switch (Lc) {
             HE_BSGS_CASE(1) HE_BSGS_CASE(2) HE_BSGS_CASE(3) HE_BSGS_CASE(4)
@@ -2049,11 +2252,11 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
             add_pt = nullptr;   // done
           }
           if (rescale && G == 1 && ks_rescale_ok(a)) {
-            inner[k2] = ct_new(c, B, 2, x->level - 1, x->scale * diags->scale / (double)c->hp.q[x->level]);
+            inner[k2] = ct_new(c, B, 2, x->level - 1, x->scale * dscale / (double)c->hp.q[x->level]);
             ks_launch_rescale(c, a, inner[k2]->d, 2 * (LN - N), bias);
             rescale = false;   // done
           } else {
-            inner[k2] = ct_new(c, B, 2, x->level, x->scale * diags->scale);
+            inner[k2] = ct_new(c, B, 2, x->level, x->scale * dscale);
             a.out = inner[k2]->d;
             ks_launch(c, a);
           }
@@ -2066,8 +2269,7 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
     } else {   // generic: one lazy accumulation per giant step (no sharing of the baby-step products)
       for (int k2 = 0; k2 < G; ++k2) {
         he_plaintext view{c, g, diags->level, diags->scale, diags->d + (size_t)k2 * g * nt * N, 1};
-        std::vector<const u64*> kk(keys.begin(), keys.end());
-        inner[k2] = ct_vec_mat_lazy(c, x, &view, kk, gals, step);
+        inner[k2] = ct_vec_mat_lazy(c, x, &view, gals, step);
         dfree(c, view.dm);
       }
     }
@@ -2087,6 +2289,7 @@ static std::vector<he_ciphertext*> bsgs_inner(he_context* c, const he_ciphertext
     cleanup();
     throw;
   }
+  pt_free(ones);
   return inner;
 }
 
@@ -2105,7 +2308,7 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
   const int G = diags->B / g;
   for (int k2 = 1; k2 < G; ++k2) {
     u32 gg;
-    if (!galois_key(c, g * k2, &gg))
+    if (!has_galois_key(c, g * k2, &gg))
       throw HeError(HE_MISSING_GALOIS_KEY, "no Galois key for giant step " + std::to_string(g * k2));
   }
   if (G == 1 && fold_n <= 1) {   // one group, no fold: the rescale (+ bias) merged into the ModDown
@@ -2153,9 +2356,6 @@ he_ciphertext* ct_vec_mat_bsgs(he_context* c, const he_ciphertext* x, const he_p
   }
 }
 
-__global__ void k_fill_u64(u64* __restrict__ p, size_t n, u64 v) {
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
-}
 
 // sum_{k < n} rot(x, k step) with ONE lazy ModDown: the baby-step machinery with unit
 // diagonals (the plaintext polynomial 1, whose NTT words are all 1); scale unchanged.
@@ -2168,18 +2368,7 @@ static he_ciphertext* ct_rot_sum(he_context* c, const he_ciphertext* x, int n, i
     HE_CK(cudaMemcpyAsync(o->d, x->d, ct_words(x) * 8, cudaMemcpyDeviceToDevice, c->stream));
     return o;
   }
-  he_plaintext* ones = pt_new(c, n, x->level, 1.0, 1);
-  std::vector<he_ciphertext*> inner;
-  try {
-    k_fill_u64<<<148 * 4, 256, 0, c->stream>>>(ones->d, pt_words(ones), 1);
-    check_launch(c);
-    inner = bsgs_inner(c, x, ones, n, step, rescale, bias, add_pt);
-  } catch (...) {
-    pt_free(ones);
-    throw;
-  }
-  pt_free(ones);
-  return inner[0];
+  return bsgs_inner(c, x, nullptr, n, step, rescale, bias, add_pt)[0];
 }
 
 // im2col conv on the encrypted side (a15, C18/C19).  fold_n1 = 0: the paper's log2 rotate-and-add
@@ -2357,32 +2546,45 @@ void keygen(he_context* c, const std::vector<int>& steps) {
   c->has_pk = true;
   if (c->K > 0) {
     const size_t kw = (size_t)L * 2 * NP * N;
-    HE_CK(cudaMalloc(&c->d_rlk, kw * 8));
-    make_ksk(c, c->d_rlk, PUR_RLK_A, PUR_RLK_E, 0, 0);
-    c->has_rlk = true;
-    if (c->small_primes) {
-      HE_CK(cudaMalloc(&c->d_rlk32, kw * 4));
-      const size_t rows = (size_t)L * 2 * NP;
+    // Keys at rest: contexts on the fused small-prime key switch keep every switching
+    // key as Montgomery-form u32 words only (4 bytes per residue instead of 8 + 4); the u64 form is
+    // built in one reused scratch block here and, later, only on demand (galois_key / relin_key).
+    const bool u32_only = fused_ks_ok(c);
+    const size_t rows = (size_t)L * 2 * NP;
+    u64* tmp64 = nullptr;
+    if (u32_only) HE_CK(cudaMalloc(&tmp64, kw * 8));
+    auto to32 = [&](const u64* key) {
+      u32* k32 = nullptr;
+      HE_CK(cudaMalloc(&k32, kw * 4));
       k_to_mont32<<<dim3((N + 255) / 256, (unsigned)std::min<size_t>(rows, 65535)), 256, 0, c->stream>>>(
-          c->d_rlk, c->d_rlk32, c->d_primes, N, NP, NP, L, rows);
+          key, k32, c->d_primes, N, NP, NP, L, rows);
       check_launch(c);
-    }
-    for (int st : steps) {
-      const u64 g = galois_element(N, st);
-      if (c->gk.count(g)) continue;
-      u64* key = nullptr;
-      HE_CK(cudaMalloc(&key, kw * 8));
-      c->gk[g] = key;
-      make_ksk(c, key, PUR_GK_A, PUR_GK_E, g << 8, (u32)g);
-      if (c->small_primes) {
-        u32* k32 = nullptr;
-        HE_CK(cudaMalloc(&k32, kw * 4));
-        c->gk32[g] = k32;
-        const size_t rows = (size_t)L * 2 * NP;
-        k_to_mont32<<<dim3((N + 255) / 256, (unsigned)std::min<size_t>(rows, 65535)), 256, 0, c->stream>>>(
-            key, k32, c->d_primes, N, NP, NP, L, rows);
-        check_launch(c);
+      return k32;
+    };
+    try {
+      if (!u32_only) HE_CK(cudaMalloc(&c->d_rlk, kw * 8));
+      u64* rl = u32_only ? tmp64 : c->d_rlk;
+      make_ksk(c, rl, PUR_RLK_A, PUR_RLK_E, 0, 0);
+      c->has_rlk = true;
+      if (c->small_primes) c->d_rlk32 = to32(rl);
+      for (int st : steps) {
+        const u64 g = galois_element(N, st);
+        if (c->gk.count(g) || c->gk32.count(g)) continue;
+        u64* key = tmp64;
+        if (!u32_only) {
+          HE_CK(cudaMalloc(&key, kw * 8));
+          c->gk[g] = key;
+        }
+        make_ksk(c, key, PUR_GK_A, PUR_GK_E, g << 8, (u32)g);
+        if (c->small_primes) c->gk32[g] = to32(key);
       }
+    } catch (...) {
+      if (tmp64) cudaFree(tmp64);
+      throw;
+    }
+    if (tmp64) {
+      HE_CK(cudaStreamSynchronize(c->stream));
+      HE_CK(cudaFree(tmp64));
     }
   }
   build_step_tables(c);

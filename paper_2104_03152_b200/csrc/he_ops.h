@@ -67,7 +67,10 @@ he_ciphertext* ct_conv(he_context* c, const he_ciphertext* x, const he_plaintext
                        const he_plaintext* masks, const he_plaintext* bias, int chunk, int fold_n1 = 0);
 he_ciphertext* ct_conv_bsgs(he_context* c, const he_ciphertext* x, const he_plaintext* diags,
                             const he_plaintext* bias, int chunk, int g);
-const u64* galois_key(he_context* c, int step, u32* gal_out);
+bool has_galois_key(he_context* c, int step, u32* gal_out);       // either stored form
+const u64* galois_key(he_context* c, int step, u32* gal_out);     // u64 form (materialised on demand)
+const u64* relin_key(he_context* c);                              // u64 form (materialised on demand)
+size_t key_bytes(he_context* c);                                  // device bytes held by pk / relin / Galois keys
 size_t wire_payload_bytes(he_context* c, const he_ciphertext* ct);
 void wire_pack(he_context* c, const he_ciphertext* ct, u64* out_dev);
 he_ciphertext* wire_unpack(he_context* c, const u64* in_dev, size_t B, int size, int level, double scale);
