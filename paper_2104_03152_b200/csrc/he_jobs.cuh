@@ -42,6 +42,12 @@ template <class B, class = void>
 struct has_prefetch : std::false_type {};
 template <class B>
 struct has_prefetch<B, std::void_t<decltype(std::declval<const B&>().prefetch(0u))>> : std::true_type {};
+// Pipelined jobs whose input is the staged u32 row combined with a second row read from global memory
+// in the first pass (load_raw_at(staged word, index)): the rescale-fused ModDown (JobKsDataRs).
+template <class B, class = void>
+struct has_load_raw_at : std::false_type {};
+template <class B>
+struct has_load_raw_at<B, std::void_t<decltype(std::declval<const B&>().load_raw_at(0u, 0u))>> : std::true_type {};
 
 template <class J, class = void>
 struct has_gather_src : std::false_type {};
@@ -845,6 +851,21 @@ struct JobKsDataRs {
       const u32 yy = sub32(red32(y[n], q, mu32), hr, q);
       return add32(conv, mulsh32(yy, pm, pmsh, q), q);
     }
+    // pipelined kernel: x is the staged word tb[n]; the y row (shared by the Lc-1 blocks of one
+    // (item, part): L2-resident) is read here, in the transform's first pass
+    __device__ __forceinline__ u64 load_raw_at(u32 x, u32 n) const {
+      const u32 conv = sub32(red32(x, q, mu32), ph, q);
+      const u32 yy = sub32(red32(__ldg(y + n), q, mu32), hr, q);
+      return add32(conv, mulsh32(yy, pm, pmsh, q), q);
+    }
+    __device__ __forceinline__ u64 load_raw(u32 x) const { return x; }   // (interface; load_raw_at is used)
+    __device__ __forceinline__ void prefetch(u32 N) const {
+      prefetch_l2(ax, N * 4);
+      prefetch_l2(e.add, N * 8);
+      prefetch_l2(e.acc, N * 8);
+      prefetch_l2(e.sq0, N * 8);
+      prefetch_l2(e.sq1, N * 8);
+    }
     __device__ __forceinline__ u32 fin(u32 n, u32 v, u32 axv, u32 ev, u32 bv) const {
       const u32 w = add32(axv, mulsh32(ev, pm, pmsh, q), q);
       u32 o = mulsh32(sub32(w, v, q), cinv, cinvsh, q);
@@ -881,6 +902,17 @@ struct JobKsDataRs {
   }
   __device__ u64 load(int blk, u32 n, const PrimeD& P) const { return bind32(blk, P).load(n); }
   __device__ void store(int blk, u32 n, u64 v, const PrimeD& P) const { bind32(blk, P).store(n, v); }
+  // pipelined transform (k_ntt32_pipe): the staged row is the block's tb row, y joins in load_raw_at.
+  // OFF: measured slower than the one-shot kernel on B200 (A/B, the CNN step at batch 512: ks_rescale
+  // 1.11 -> 1.58 ms per step) - the y loads sit on the critical path of every block's first pass and the
+  // wider binding spills in the 40-register persistent kernel; kept for the experiment's record.
+#ifndef HE_KSRS_PIPE
+#define HE_KSRS_PIPE 0
+#endif
+  __host__ __device__ bool pipe_ok() const { return HE_KSRS_PIPE != 0; }
+  __host__ __device__ const u32* raw32(int blk) const {
+    return reinterpret_cast<const u32*>(a.tb) + (size_t)(blk / (a.Lc - 1)) * a.N;
+  }
 };
 
 // Rescale source: row r of x, or (conv, C18) the product ct_b (.) K_c formed on

@@ -636,7 +636,10 @@ __device__ __forceinline__ void ntt32_pipe_block(const JB& jb, u32* sm, const u3
   typedef NttGeomS<LOGN> G;
   constexpr int LO = INV ? 0 : (G::NPASS - 1) * G::R;
   constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-  auto ld = [&](u32 i) { return (u32)jb.load_raw(stage[i]); };
+  auto ld = [&](u32 i) {
+    if constexpr (has_load_raw_at<JB>::value) return (u32)jb.load_raw_at(stage[i], i);
+    else return (u32)jb.load_raw(stage[i]);
+  };
   auto st = [&](u32 i, u32 v) { sm[spad32(i)] = v; };
   ntt_pass32_io<LOGN, INV, LO, NB, LAZY>(tid, tw, q, ld, st);
   __syncthreads();
