@@ -228,8 +228,8 @@ def run_ours(args, rank, world, local_rank):
 
     # --- e2e through the public API from pinned host images ---
     # Every step, through the C-ABI host-buffer calls: client im2col of the step's images into
-    # page-locked memory, he_encode from that HOST buffer (its H2D copy runs on the context stream
-    # inside the call), encrypt, forward, decrypt, he_decode_async into page-locked HOST logits (the
+    # page-locked memory, he_encode_encrypt from that HOST buffer (its H2D copy is issued inside the
+    # call, on the context's copy stream, and the context stream waits for it), encrypt, forward, decrypt, he_decode_async into page-locked HOST logits (the
     # D2H copy is enqueued by the call).  Depth-2 pipeline: the host waits for step i-1's logits only
     # after enqueuing step i, and runs step i+1's im2col while the device computes step i, so the
     # device never drains between steps (each step's inputs and logits still cross PCIe inside the
@@ -386,7 +386,9 @@ def micro_extra(ctx_cnn, stream, dev):
                              "rotation_breakdown": rot_break,
                              "roofline": roofline_block("cfg3_" + top3, (p3[2] / p3[0]) / (p3[1] / p3[0] / 1e3) / 1e9,
                                                         (p3[4] / p3[0]) / (p3[1] / p3[0] / 1e3) / 1e9, peaks,
-                                                        kernel=top3, share=p3[1] / tot3),
+                                                        kernel=top3, share=p3[1] / tot3,
+                                                        # ModUp is transforms only: the butterfly roof applies
+                                                        bfly_peak=BFLY64_GPS if top3 == "ks_modup" else None),
                              "mul_relin_rescale_per_s": round(Bc / s_mul, 1)}
     del c3, ct
     # config 1: one encrypted vec-mat (x 64 values replicated, W 64x10), batch 1: latency

@@ -124,16 +124,28 @@ __device__ __forceinline__ void ntt_pass(u64* sm, u32 tid, u32 gbase, const ulon
 
 // Passes P .. PEND-1 over the local problem: pass P covers bit group GP = INV ? P : NPASS-1-P,
 // local bits [GP R, min(GP R + R, LOGNL)); each ends with a barrier.
+// Two consecutive full passes (NB = R, one group per thread) over bits below 5 + R exchange data inside
+// one warp only (its 32 2^R words; see Pass32 below): __syncwarp() orders them instead of the barrier.
+#ifndef HE_NTT64_WARPSYNC
+#define HE_NTT64_WARPSYNC 1
+#endif
+template <int LOGN, int CL, bool INV, int P>
+struct Pass64 {
+  typedef NttGeom<LOGN, CL> G;
+  static constexpr int GP = INV ? P : G::NPASS - 1 - P;  // forward runs top-down
+  static constexpr int LO = GP * G::R;
+  static constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
+  static constexpr bool WL = HE_NTT64_WARPSYNC && P >= 0 && P < G::NPASS && NB == G::R && LO <= 5 && G::T % 32 == 0;
+};
 template <int LOGN, int CL, bool INV, int P, int PEND = NttGeom<LOGN, CL>::NPASS>
 __device__ __forceinline__ void ntt_passes(u64* sm, u32 tid, u32 gbase, const ulonglong2* tw, u64 q,
                                            u64 two_q) {
-  typedef NttGeom<LOGN, CL> G;
   if constexpr (P < PEND) {
-    constexpr int GP = INV ? P : G::NPASS - 1 - P;  // forward runs top-down
-    constexpr int LO = GP * G::R;
-    constexpr int NB = (LO + G::R <= G::LOGNL) ? G::R : G::LOGNL - LO;
-    ntt_pass<LOGN, CL, INV, LO, NB>(sm, tid, gbase, tw, q, two_q);
-    __syncthreads();
+    typedef Pass64<LOGN, CL, INV, P> PS;
+    ntt_pass<LOGN, CL, INV, PS::LO, PS::NB>(sm, tid, gbase, tw, q, two_q);
+    constexpr bool next_wl = (P + 1 < PEND) && Pass64<LOGN, CL, INV, (P + 1 < PEND ? P + 1 : P)>::WL;
+    if constexpr (PS::WL && next_wl) __syncwarp();
+    else __syncthreads();
     ntt_passes<LOGN, CL, INV, P + 1, PEND>(sm, tid, gbase, tw, q, two_q);
   }
 }

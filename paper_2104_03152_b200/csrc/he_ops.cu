@@ -564,6 +564,9 @@ __global__ void __launch_bounds__(256) k_vecmat_lazy(LazyArgs a, const PrimeD* _
 // are the exact residues, bit-identical to the generic path.  One CTA per
 // (target limb t, item b).
 constexpr int LAZY_SM_T = 1024, LAZY_SM_EPT = 2;
+#ifndef HE_BSGS_UNIT_UNROLL
+#define HE_BSGS_UNIT_UNROLL 2
+#endif
 #ifndef HE_BSGS_FIXED
 #define HE_BSGS_FIXED 1   // 0: always the runtime-geometry BSGS kernels (A/B experiments)
 #endif
@@ -735,6 +738,8 @@ __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, con
         s0[i] = data ? c0p[i * NH + l] : 0u;
         s1[i] = data ? redc32((u64)xs[(i * LC + t) * NH + l] * Pm, q, qi) : 0u;
       }
+      constexpr int kStepsInFlight = HE_BSGS_UNIT_UNROLL;   // the key loads of that many baby steps are issued together
+#pragma unroll kStepsInFlight
       for (int k = 1; k < g; ++k) {
         const u32 gal = __ldg(a.gal + k * a.step);
         const u32* key = keys32[k * a.step] + keyrow + n;
@@ -785,8 +790,7 @@ __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, con
         }
       }
     }
-    return;
-  }
+  } else {
   for (u32 l = threadIdx.x; l < NH; l += LAZY_SM_T) {
     const u32 n = h0 + l;
     acc_t acc0[IB][G], acc1[IB][G];
@@ -888,6 +892,7 @@ __device__ __forceinline__ void bsgs_hp_run(const LazyArgs& a, int g, int B, con
       }
     }
   }
+  }   // !UNIT
 }
 
 // NFIX / NPFIX != 0: the ring degree and the key's limb count are compile-time constants (the launch
