@@ -872,4 +872,78 @@ k_ntt32_pipe(Job job, const PrimeD* __restrict__ primes, const uint2* __restrict
   }
 }
 
+// ---- fused digit INTT + ModUp (small primes, the vec_mat paths' ModUp32) ------------------------
+// One persistent CTA per (item b, digit j): INTT of limb j of the digit source straight into the
+// staging row (u32 coefficients, scaled by N^{-1}), then for every target limb t != j the lift into
+// q_t (C16) and the forward transform from that row, stored as u32 extended digits.  The digit's
+// coefficient row never reaches HBM and the separate INTT launch (one-shot CTAs reading u64 rows)
+// disappears; the words are those of JobLimbsTo32 followed by JobModUp32.
+struct StageRowStore {
+  u32* row;
+  __device__ __forceinline__ void store(u32 n, u64 v) const { row[n] = (u32)v; }
+  __device__ __forceinline__ void store4(u32 n0, u32 st, const u32* v) const {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) row[n0 + u * st] = v[u];
+  }
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttGeomS<LOGN>::T, NttGeom32<LOGN>::MINB)
+k_modup32_fused(const u64* __restrict__ dsrc, size_t bs, u32* __restrict__ ext, const u64* __restrict__ qtab,
+                int Lc, int K, int L, int nitems, const PrimeD* __restrict__ primes,
+                const uint2* __restrict__ tw_all, const uint2* __restrict__ itw_all) {
+  typedef NttGeomS<LOGN> G;
+  extern __shared__ u32 sm32[];
+  u32* stage = sm32 + G::NL + G::NL / 32;
+  const u32 tid = threadIdx.x;
+  const int nt = Lc + K;
+  constexpr int PER = G::NL / G::T, CH = PER < 8 ? PER : 8;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int b = it / Lc, j = it % Lc;
+    {   // INTT of limb j -> stage
+      const PrimeD P = load_prime(primes, j);
+      const u32 q = (u32)P.q;
+      const uint2* itw = itw_all + (size_t)j * G::N;
+      const u64* src = dsrc + (size_t)b * bs + (size_t)j * G::N;
+#pragma unroll 1
+      for (int c = 0; c < PER / CH; ++c) {
+        u32 v[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) v[k] = (u32)src[tid + (c * CH + k) * G::T];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) sm32[spad32(tid + (c * CH + k) * G::T)] = v[k];
+      }
+      __syncthreads();
+      const StageRowStore st{stage};
+      constexpr int NB_LAST = G::LOGNL - (G::NPASS - 1) * G::R;
+      if constexpr (G::NPASS >= 3 && (1 << (G::R - NB_LAST)) % 4 == 0) {
+        if (q < (1u << 30)) {
+          ntt_passes32<LOGN, true, 0, true, G::NPASS - 1>(sm32, tid, itw, q);
+          ntt32_inv_last_store<LOGN, true>(st, sm32, tid, itw, q);
+        } else {
+          ntt_passes32<LOGN, true, 0, false, G::NPASS - 1>(sm32, tid, itw, q);
+          ntt32_inv_last_store<LOGN, false>(st, sm32, tid, itw, q);
+        }
+      } else {
+        ntt_run32<LOGN, true>(sm32, tid, itw, q);
+        ntt32_epilogue<LOGN, true>(st, sm32, tid, __ldg(itw), q);
+      }
+      __syncthreads();   // the coefficient row is complete; sm32 is free
+    }
+    const u32 qj = (u32)__ldg(qtab + j);
+    for (int tt = 0; tt < nt - 1; ++tt) {
+      const int t = tt < j ? tt : tt + 1;
+      const int tp = t < Lc ? t : L + (t - Lc);
+      const PrimeD P = load_prime(primes, tp);
+      const u32 q = (u32)P.q;
+      const uint2* tw = tw_all + (size_t)tp * G::N;
+      const JobModUp32::B32 jb{stage, ext + (((size_t)b * Lc + j) * nt + t) * G::N, qj, q, mu32_of(P)};
+      if (q < (1u << 30)) ntt32_pipe_block<LOGN, false, true>(jb, sm32, stage, tid, tw, q);
+      else ntt32_pipe_block<LOGN, false, false>(jb, sm32, stage, tid, tw, q);
+      ntt32_pipe_rest<LOGN, false>(jb, sm32, tid, tw, q);
+      __syncthreads();   // the (warp-ordered) epilogue is done with sm32 before the next first pass
+    }
+  }
+}
+
 }  // namespace he

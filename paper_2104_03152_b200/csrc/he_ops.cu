@@ -1604,8 +1604,50 @@ static void ks_materialized(he_context* c, const u64* dsrc, size_t bs, int B, in
 }
 
 // Small-prime ModUp: u32 digits and u32 extended digits ([B][Lc][Lc+K][N] u32).
+#ifndef HE_MODUP_FUSED
+#define HE_MODUP_FUSED 1   // 0: digit INTT (JobLimbsTo32) and ModUp32 as two launches
+#endif
+template <int LOGN>
+static void launch_modup32_fused(he_context* c, const u64* dsrc, size_t bs, u32* ext, int B, int Lc) {
+  typedef NttGeomS<LOGN> G;
+  static int grid = 0;   // once per process (one device per process, as launch_ntt32_pipe)
+  auto kern = k_modup32_fused<LOGN>;
+  if (!grid) {
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, NttGeom32Pipe<LOGN>::SMEM));
+    HE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 0, sms = 0;
+    HE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::T, NttGeom32Pipe<LOGN>::SMEM));
+    HE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    grid = std::max(1, per_sm) * sms;
+  }
+  const int nitems = B * Lc, nt = Lc + c->K;
+  // algorithmic bytes: the u64 digit rows read once, the u32 extended digits written once; one
+  // butterfly network per transform (1 inverse + nt - 1 forward per digit)
+  ProfScope ps(c, "ks_modup", c->prof_on ? (double)G::N * nitems * (8.0 + 4.0 * (nt - 1)) : 0.0, nitems * nt,
+               c->prof_on ? 0.5 * G::N * LOGN * (double)nitems * nt : 0.0);
+  int gr = std::min(nitems, grid);
+  if (c->pipe_grid_cap > 0) gr = std::min(gr, c->pipe_grid_cap);
+  kern<<<gr, G::T, NttGeom32Pipe<LOGN>::SMEM, c->stream>>>(dsrc, bs, ext, c->d_q, Lc, c->K, c->L, nitems,
+                                                           c->d_primes, c->d_tw32, c->d_itw32);
+  check_launch(c);
+}
+
 static u32* modup32(he_context* c, const u64* dsrc, size_t bs, int B, int Lc) {
   const size_t N = c->N;
+  if (HE_MODUP_FUSED && c->logN >= 11 && c->logN <= 13) {
+    u32* ext = dalloc_t<u32>(c, (size_t)B * Lc * (Lc + c->K) * N);
+    try {
+      switch (c->logN) {
+        case 11: launch_modup32_fused<11>(c, dsrc, bs, ext, B, Lc); break;
+        case 12: launch_modup32_fused<12>(c, dsrc, bs, ext, B, Lc); break;
+        default: launch_modup32_fused<13>(c, dsrc, bs, ext, B, Lc); break;
+      }
+    } catch (...) {
+      dfree(c, ext);
+      throw;
+    }
+    return ext;
+  }
   Scratch coef(c, (size_t)B * Lc * N * 4);
   {
     JobLimbsTo32 j{dsrc, coef.as<u32>(), c->N, Lc, bs, (size_t)Lc * N};
