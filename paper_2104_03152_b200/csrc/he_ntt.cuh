@@ -930,6 +930,11 @@ k_modup32_fused(const u64* __restrict__ dsrc, size_t bs, u32* __restrict__ ext, 
       }
       __syncthreads();   // the coefficient row is complete; sm32 is free
     }
+    // the next item's digit row -> L2 while this item's nt - 1 forward transforms run
+    if (tid == 0 && it + (int)gridDim.x < nitems) {
+      const int nx = it + (int)gridDim.x;
+      prefetch_l2(dsrc + (size_t)(nx / Lc) * bs + (size_t)(nx % Lc) * G::N, G::N * 8);
+    }
     const u32 qj = (u32)__ldg(qtab + j);
     for (int tt = 0; tt < nt - 1; ++tt) {
       const int t = tt < j ? tt : tt + 1;
