@@ -12,8 +12,10 @@ square -> FC2 -> decrypt -> decode, all in this library's sm_100a kernels.
   library's stream, barrier + synchronize around K steps, max over ranks.
 * e2e: the same metric through the public API from pinned host images:
   host im2col, H2D of the slot vectors inside he_encode, ..., D2H logits.
-* roofline: the dominant kernel (largest share of the step), its algorithmic
-  bytes / CUDA-event time against MEASURED_PEAKS.json HBM GB/s.
+* roofline: the dominant kernel (largest share of the step): bound "alu" — its
+  algorithmic modular ops / CUDA-event time against the modop rate at which the
+  kernel's busiest integer pipe (ncu-measured mix, profiles/r02/pipe_mix.json)
+  saturates; hbm_frac = algorithmic bytes / time against MEASURED_PEAKS.json.
 * cpu_baseline (rank 0, N=1): the CPU oracle (oracle/, test infrastructure)
   timed on a bounded sample of the same workload.
 * extra: key-switch rotations/s (config 3 shape) and NTT GB/s (config 2 shape).

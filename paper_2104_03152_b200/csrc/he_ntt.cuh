@@ -340,7 +340,7 @@ k_ntt_mul_intt(Job job, const PrimeD* __restrict__ primes, const ulonglong2* __r
 // ===================================================== 32-bit arithmetic ===
 // Contexts whose primes are all < 2^31 (BASELINE config 4) run the same
 // network on u32 registers and shared memory (half the smem, 32x32-bit Shoup
-// products); HBM words stay u64.  Strict butterflies: values stay in [0, q)
+// products); ciphertext words in HBM stay u64 (scratch rows, digits and keys are u32).  Strict butterflies: values stay in [0, q)
 // (2q < 2^32, but 4q may not be).  Twiddle table entries are (w, floor(w 2^32 / q));
 // entry 0 of the inverse table holds (N^{-1}, its companion).
 __device__ __forceinline__ u32 spad32(u32 i) { return i + (i >> 5); }
