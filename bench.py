@@ -322,6 +322,14 @@ def run_ours(args, rank, world, local_rank):
                           "(level-0 words), NCCL", "bitwise_equal_single_gpu": bool(torch.equal(rw, words_c))}
 
     extra["communication_cfg4"] = comm
+    # keys at rest: switching keys of this small-prime context are u32 Montgomery words only
+    n_keys = len(rotation_steps(conv_g=CONV_G, fc_bsgs=True, fc1_g=FC1_G))
+    kw = ctx.L * 2 * (ctx.L + ctx.K) * ctx.N
+    extra["key_memory_cfg4"] = {"resident_bytes_after_the_run": ctx.he_key_bytes(), "galois_keys": n_keys,
+                                "u32_at_rest_bytes": 2 * ctx.L * ctx.N * 8 + (1 + n_keys) * kw * 4,
+                                "round1_layout_bytes": 2 * ctx.L * ctx.N * 8 + (1 + n_keys) * kw * 12,
+                                "note": "relin + Galois keys as u32 (4 B / residue); round 1 held u64 + u32 copies "
+                                        "(12 B / residue); u64 forms are materialised only on demand"}
     return dict(value=value, ms=ms, launches=launches, clocks=clk.summary(), roofline=roofline,
                 breakdown=breakdown, e2e=e2e, extra=extra, check=check, cpu=cpu, dist_check=dist_check)
 
